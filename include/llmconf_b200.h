@@ -1,0 +1,210 @@
+/* llmconf_b200 -- C ABI of the B200 configuration-search engine.
+ *
+ * Drop-in boundary.  The reference has no plugin registry: its seam is the
+ * Python function llmconf.search.run_search(db, model, workload, space, jobs,
+ * disagg_constants) (/root/reference/pkg/src/llmconf/search.py:280-358), called
+ * by the CLI (cli.py:239, 286) and the HTTP service (service.py:230).  The
+ * host shim paper_2601_06288_b200.run_search keeps that signature and crosses
+ * into this library through ctypes; the entry points below are what that
+ * binding (or any other FFI) calls.  Plain pointers and sizes only.
+ *
+ *   reference piece                              replaced by
+ *   ------------------------------------------   -----------------------------------
+ *   PerfDatabase._grids (perfdb.py:283-355)      lc_db_upload   (SoA grids in HBM/smem)
+ *   decompose (model.py:271-406) per (tp,pp,ep)  lc_space_upload (host-compiled plan templates)
+ *   enumerate_candidates (search.py:82-113)      K0 inside lc_search_batch
+ *   busiest_shard_tokens (moe_load.py:141-147)   K3 inside lc_search_batch
+ *   get_step_latency / estimate_static /         K2 inside lc_search_batch
+ *     estimate_aggregated / *_candidate
+ *     (estimator.py:71-156, serving_modes.py:231-381)
+ *   _pool_rank top-k, estimate_disaggregated     K5 inside lc_search_batch
+ *     (search.py:276-277, 338-341; serving_modes.py:449-494)
+ *   meets_sla / pareto_filter / select_best /    K4 inside lc_search_batch
+ *     nearest_miss (search.py:129-208)
+ *
+ * Threading: one lc_ctx per host thread (it owns a CUDA stream and workspace).
+ * lc_db / lc_space handles are immutable after upload and may be shared by
+ * contexts on the same device.  Every function returns LC_OK (0) or a negative
+ * code; lc_last_error() describes the last failure on the calling thread.
+ */
+#ifndef LLMCONF_B200_H
+#define LLMCONF_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LC_ABI_VERSION 1
+#define LC_MAX_ENTRIES 16   /* plan entries per (tp, pp, ep) template */
+#define LC_MAX_BUDGETS 16
+#define LC_MAX_EXPERTS 1024
+
+enum { LC_OK = 0, LC_ERR_ARG = -1, LC_ERR_CUDA = -2, LC_ERR_STATE = -3 };
+
+/* extrapolation policy (perfdb.py:46) */
+enum { LC_POLICY_DEFAULT = 0, LC_POLICY_STRICT = 1, LC_POLICY_CLAMP = 2, LC_POLICY_SOL = 3 };
+
+/* operator kinds (perfdb.py:27-39) */
+enum {
+  LC_KIND_GEMM = 0, LC_KIND_ATTN_CTX, LC_KIND_ATTN_GEN, LC_KIND_ALLREDUCE, LC_KIND_ALLGATHER,
+  LC_KIND_ALLTOALL, LC_KIND_P2P, LC_KIND_MOE_DISPATCH, LC_KIND_MOE_COMBINE, LC_KIND_MOE_GEMM,
+  LC_KIND_EMBEDDING
+};
+
+/* plan entry labels, in decompose order (model.py:313-404) */
+enum {
+  LC_LBL_EMBEDDING = 0, LC_LBL_QKV, LC_LBL_CTX_ATTN, LC_LBL_GEN_ATTN, LC_LBL_OUT_PROJ, LC_LBL_MLP_UP,
+  LC_LBL_MLP_DOWN, LC_LBL_ROUTER, LC_LBL_SHARED_UP, LC_LBL_SHARED_DOWN, LC_LBL_EXPERT_FFN,
+  LC_LBL_DISPATCH, LC_LBL_COMBINE, LC_LBL_ATTN_AR, LC_LBL_MLP_AR, LC_LBL_STAGE_BOUNDARY
+};
+
+/* how an entry's interpolated coordinates follow from (n_ctx, n_gen, seq) */
+enum {
+  LC_COORD_TOKENS = 0,  /* d0 = n_ctx + n_gen                              */
+  LC_COORD_MSG = 1,     /* d0 = (n_ctx + n_gen) * hidden * 2               */
+  LC_COORD_CTX = 2,     /* (d0, d1) = (n_ctx/seq, seq) or (1, n_ctx) mixed */
+  LC_COORD_GEN = 3,     /* (d0, d1) = (n_gen, seq)                         */
+  LC_COORD_EXPERT = 4   /* d0 = expert tokens (balanced or skewed)         */
+};
+
+/* per-row status codes; the failing entry's label sits in bits 8..15 */
+enum {
+  LC_ST_OK = 0, LC_ST_MISSING_KEY = 1, LC_ST_EXTRAPOLATION = 2, LC_ST_UNSUPPORTED = 3,
+  LC_ST_INFEASIBLE_CHUNK_OFF = 4, LC_ST_INFEASIBLE_NO_DECODE_SLOT = 5, LC_ST_NOT_EVALUATED = 255
+};
+
+/* ---------------------------------------------------------------- database */
+typedef struct {
+  int32_t n_grids;
+  const int32_t* grid_ndim;      /* [n_grids] 1 or 2 */
+  const int32_t* grid_axis_off;  /* [n_grids*2] offset into axis_val/axis_log */
+  const int32_t* grid_axis_len;  /* [n_grids*2] */
+  const int32_t* grid_cell_off;  /* [n_grids] offset into cell/cell_log, row-major (axis 0 major) */
+  int32_t n_axis;
+  const int64_t* axis_val;       /* sorted per grid */
+  const double* axis_log;        /* math.log(axis_val), computed by the host like the reference */
+  int32_t n_cells;
+  const double* cell;            /* latency_us */
+  const double* cell_log;        /* math.log(cell) */
+  double mem_bandwidth, intra_node_bandwidth, inter_node_bandwidth, gpu_memory;
+  int32_t gpus_per_node;
+  double compute[4];             /* FLOP/s for fp16, fp8, int8, int4; <= 0 = absent */
+  int32_t policy;                /* LC_POLICY_* */
+} lc_db_desc;
+
+/* ------------------------------------------- model x candidate-space plan */
+typedef struct {
+  int32_t label, kind, quant, grid;  /* grid < 0: no grid for this key (MissingKeyError) */
+  int32_t coord, _pad;
+  int64_t repeat;
+  int64_t d[5];                      /* canonical dims; fixed ones filled, axes set on device */
+} lc_entry;
+
+typedef struct {
+  int64_t tp, pp, ep, dp, gpus;
+  int32_t tp_i, ep_i;                /* indices into the sorted tp / ep value lists */
+  int32_t tmpl;                      /* template index */
+  int32_t _pad;
+  double weight_bytes;               /* memory_footprint().weight_bytes (model.py:446) */
+  double kv_token_bytes;             /* memory_footprint().kv_bytes_per_token (model.py:448-452) */
+} lc_combo;
+
+typedef struct {
+  int64_t hidden, topk, n_experts;
+  int32_t is_moe;
+  int32_t n_combos;                  /* consistent (tp,pp,ep,dp) in the reference's nested order */
+  const lc_combo* combos;
+  int32_t n_tmpl;
+  const int32_t* tmpl_n_entries;     /* [n_tmpl] */
+  const lc_entry* entries;           /* [n_tmpl * LC_MAX_ENTRIES] */
+  int32_t n_tp, n_ep;                /* sizes of the tp / ep value lists */
+} lc_space_desc;
+
+/* ------------------------------------------------------------------ search */
+typedef struct {
+  int64_t isl, osl, prefix;
+  int32_t has_ttft, has_floor;
+  double ttft_limit, speed_floor, tpot_cap;   /* tpot_cap = 1000/speed_floor (serving_modes.py:109-111) */
+  int32_t modes;                     /* bit0 static, bit1 aggregated, bit2 disaggregated */
+  int32_t n_budgets;
+  int64_t budgets[LC_MAX_BUDGETS];
+  int32_t b_off, n_b;                /* sorted batch sizes in the shared batch array */
+  int32_t has_ctx_capacity, chunked_prefill;
+  int64_t ctx_capacity;
+  double kv_mem_fraction;
+  int32_t prefill_cap, decode_cap;
+  double ttft_headroom, prefill_util, decode_util;
+  int32_t max_x, max_y;
+  int32_t load;                      /* MoE load vector index (-1 dense) */
+  int32_t _pad;
+} lc_search_desc;
+
+typedef struct {
+  int32_t n_units;                   /* evaluated units (worker set if disaggregated, else candidates) */
+  int32_t unit_off;
+  int32_t n_enumerated;              /* counts.enumerated */
+  int32_t n_rows, n_feasible, n_skipped;
+  int32_t n_front, front_off;
+  int32_t n_plans, plan_off;
+  int64_t best;                      /* row key (mode << 32 | index) or -1 */
+  int64_t nearest;                   /* row key or -1; only when best < 0 */
+  double nearest_violation;
+  double best_thru, best_speed;
+  int64_t queries_1d, queries_2d;    /* reference-equivalent query_latency calls (memoised) */
+} lc_search_result;
+
+typedef struct {
+  int64_t n_units, n_plans, n_front;
+  float kernel_ms[6];                /* K0 enumerate, K3 tails, K2 evaluate, K5a pools, K5b disagg, K4 front */
+  int64_t n_raw;                     /* raw (tp,pp,ep,dp,batch) tuples examined */
+} lc_batch_totals;
+
+/* per-unit / per-plan / front arrays to copy back (any pointer may be NULL) */
+typedef struct {
+  int32_t* unit_search; int32_t* unit_combo; int32_t* unit_batch; uint8_t* unit_in_budget;
+  int32_t* st_status; double* st_ttft; double* st_tpot; double* st_speed; double* st_thru;
+  int32_t* ag_status; double* ag_ttft; double* ag_tpot; double* ag_speed; double* ag_thru;
+  int32_t* pf_status; double* pf_lat; double* pf_rate;
+  int32_t* dc_status; double* dc_lat; double* dc_rate;
+  int64_t* err_c0; int64_t* err_c1;  /* [n_units*4]: failing coords for st, ag, pf, dc */
+  int32_t* plan_p; int32_t* plan_d; int32_t* plan_x; int32_t* plan_y; int64_t* plan_gpus;
+  double* plan_r_sys; double* plan_ttft; double* plan_tpot; double* plan_speed; double* plan_thru;
+  int64_t* front;                    /* row keys */
+} lc_fetch_req;
+
+typedef struct lc_ctx lc_ctx;
+typedef struct lc_db lc_db;
+typedef struct lc_space lc_space;
+
+int lc_abi_version(void);
+const char* lc_last_error(void);
+
+int lc_open(int device, lc_ctx** out);
+int lc_close(lc_ctx* ctx);
+
+int lc_db_upload(lc_ctx* ctx, const lc_db_desc* desc, lc_db** out);
+int lc_db_free(lc_db* db);
+
+int lc_space_upload(lc_ctx* ctx, const lc_space_desc* desc, lc_space** out);
+int lc_space_free(lc_space* sp);
+
+/* Evaluate n_search searches of one (db, model x space) in one pass.
+ * batches: shared sorted batch array; loads: n_loads vectors of n_experts
+ * {q_i = w_i / sum(w)} (numpy) followed by the by-weight order as doubles.
+ * Results stay on the device until lc_fetch / the next batch. */
+int lc_search_batch(lc_ctx* ctx, const lc_db* db, const lc_space* sp, int32_t n_search,
+                    const lc_search_desc* searches, int32_t n_batches, const int64_t* batches,
+                    int32_t n_loads, const double* loads, lc_search_result* results,
+                    lc_batch_totals* totals);
+
+int lc_fetch(lc_ctx* ctx, const lc_fetch_req* req);
+
+/* Kernels only (no H2D/D2H): re-run the last batch's device pipeline
+ * `iters` times and report the mean per-kernel times; for benchmarks. */
+int lc_replay_last(lc_ctx* ctx, int32_t iters, lc_batch_totals* totals);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,30 @@
+"""B200-native configuration-search engine for the llmconf (AIConfigurator) hot path.
+
+Public seam: ``run_search`` -- a drop-in for ``llmconf.search.run_search``
+(/root/reference/pkg/src/llmconf/search.py:280-358) whose arithmetic runs in
+hand-written sm_100a kernels behind the C ABI in include/llmconf_b200.h.
+"""
+
+from .database import PerfDatabase, load_db
+from .engine import Engine, enumerate_candidates, get_engine, run_search
+from .report import SearchReport, csv_from_doc, export_csv
+from .specs import (
+    DEFAULT_DISAGG,
+    CandidateSpace,
+    DisaggConstants,
+    HardwareSpec,
+    ModelSpec,
+    MoESpec,
+    ParallelConfig,
+    PowerLawParams,
+    WorkloadSpec,
+    load_hardware_spec,
+    load_model_spec,
+)
+
+__all__ = [
+    "CandidateSpace", "DEFAULT_DISAGG", "DisaggConstants", "Engine", "HardwareSpec", "ModelSpec", "MoESpec",
+    "ParallelConfig", "PerfDatabase", "PowerLawParams", "SearchReport", "WorkloadSpec", "csv_from_doc",
+    "enumerate_candidates", "export_csv", "get_engine", "load_db", "load_hardware_spec", "load_model_spec",
+    "run_search",
+]

@@ -1,0 +1,412 @@
+// Device-side restatement of the reference's per-operator latency model:
+// grid lookup / log-log interpolation / extrapolation (perfdb.py:431-580),
+// the per-step sum (estimator.py:71-95) and the serving-mode arithmetic
+// (serving_modes.py:161-381).  Everything here is bit-exact with CPython on
+// x86-64: operations are written in Python's left-to-right order and the
+// translation unit is compiled with --fmad=false, so no product is fused
+// unless an explicit fma() says so (only inside glibc_libm.cuh).
+#pragma once
+#include <stdint.h>
+#include <math.h>
+#include "../../include/llmconf_b200.h"
+#include "glibc_libm.cuh"
+
+namespace lc {
+
+__device__ __forceinline__ double quant_bytes(int q) {  // perfdb.py:25
+  return q == 0 ? 2.0 : (q == 3 ? 0.5 : 1.0);
+}
+
+struct DevGrid {
+  int32_t ndim;
+  int32_t ax_off[2];
+  int32_t ax_len[2];
+  int32_t cell_off;
+};
+
+// Read-only view of the flattened database; every array lives in shared
+// memory inside the evaluation kernels (≈35 KB for DeepSeek-V3).
+struct DbView {
+  const DevGrid* grids;
+  const int64_t* axv;
+  const double* axl;
+  const double* cell;
+  const double* clog;
+  const double* logtab;
+  const uint64_t* exptab;
+  double mem_bw, intra_bw, inter_bw, gpu_memory;
+  double compute[4];
+  int32_t gpn, policy;
+};
+
+struct ErrRec {
+  int32_t code;   // LC_ST_*
+  int32_t label;  // failing entry's label
+  int64_t c0, c1; // its interpolated coordinates
+};
+
+// CPython 3.12 builtin sum() over a float sequence with int start 0
+// (bltinmodule.c: Neumaier compensation, compensation added if finite & nonzero).
+struct NeumaierSum {
+  double f, c;
+  int n;
+  __device__ __forceinline__ NeumaierSum() : f(0.0), c(0.0), n(0) {}
+  __device__ __forceinline__ void add(double x) {
+    if (n++ == 0) { f = 0.0 + x; return; }
+    const double t = f + x;
+    if (fabs(f) >= fabs(x)) c += (f - t) + x;
+    else c += (x - t) + f;
+    f = t;
+  }
+  __device__ __forceinline__ double result() const {
+    return (c != 0.0 && isfinite(c)) ? f + c : f;
+  }
+};
+
+__device__ __forceinline__ int lower_bound_i64(const int64_t* v, int n, int64_t x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (v[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// _interp_cells (perfdb.py:509-536) for coordinates inside the box.
+__device__ __forceinline__ double interp_cells(const DbView& D, const DevGrid& G, int64_t c0, int64_t c1,
+                                               int* n_log_calls) {
+  int lo[2], hi[2];
+  double t[2] = {0.0, 0.0};
+  bool exact = true;
+  const int64_t cs[2] = {c0, c1};
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    if (a >= G.ndim) { lo[a] = hi[a] = 0; continue; }
+    const int64_t* v = D.axv + G.ax_off[a];
+    const double* lv = D.axl + G.ax_off[a];
+    const int i = lower_bound_i64(v, G.ax_len[a], cs[a]);
+    if (v[i] == cs[a]) {
+      lo[a] = hi[a] = i;
+    } else {
+      lo[a] = i - 1;
+      hi[a] = i;
+      exact = false;
+      const double lx = glibc::log_fma((double)cs[a], D.logtab);
+      ++*n_log_calls;
+      t[a] = (lx - lv[i - 1]) / (lv[i] - lv[i - 1]);
+    }
+  }
+  const int n1 = G.ndim == 2 ? G.ax_len[1] : 1;
+  const double* cells = D.cell + G.cell_off;
+  const double* clogs = D.clog + G.cell_off;
+  if (exact) return cells[lo[0] * n1 + (G.ndim == 2 ? lo[1] : 0)];
+  // corners: axis-major, lo before hi, zero weights skipped (t < 1.0 / t > 0.0)
+  double w[4];
+  int ci[4];
+  int nc = 1;
+  w[0] = 1.0;
+  ci[0] = 0;
+  for (int a = 0; a < G.ndim; ++a) {
+    double nw[4];
+    int nci[4];
+    int m = 0;
+    const int stride = a == 0 ? n1 : 1;
+    for (int c = 0; c < nc; ++c) {
+      if (lo[a] == hi[a]) {
+        nw[m] = w[c]; nci[m] = ci[c] + lo[a] * stride; ++m;
+      } else {
+        if (t[a] < 1.0) { nw[m] = w[c] * (1.0 - t[a]); nci[m] = ci[c] + lo[a] * stride; ++m; }
+        if (t[a] > 0.0) { nw[m] = w[c] * t[a]; nci[m] = ci[c] + hi[a] * stride; ++m; }
+      }
+    }
+    nc = m;
+    for (int c = 0; c < m; ++c) { w[c] = nw[c]; ci[c] = nci[c]; }
+  }
+  const double v0 = cells[ci[0]];
+  if (nc == 1) return v0;
+  bool same = true;
+  for (int c = 1; c < nc; ++c) same &= cells[ci[c]] == v0;
+  if (same) return v0;  // constant cells stay bit-exact
+  NeumaierSum s;
+  for (int c = 0; c < nc; ++c) s.add(w[c] * clogs[ci[c]]);
+  return glibc::exp_fma(s.result(), D.exptab);
+}
+
+// sol_estimate (perfdb.py:431-484); d is the canonical dim vector.
+__device__ __forceinline__ double sol_us(const DbView& D, int kind, int quant, const int64_t* d, int* st) {
+  const double b = quant_bytes(quant);
+  if (kind >= LC_KIND_ALLREDUCE && kind <= LC_KIND_P2P) {
+    const int64_t n = d[1];
+    const double link = n <= D.gpn ? D.intra_bw : D.inter_bw;
+    double factor;
+    if (kind == LC_KIND_ALLREDUCE) factor = 2.0 * (double)(n - 1) / (double)n;
+    else if (kind == LC_KIND_P2P) factor = 1.0;
+    else factor = (double)(n - 1) / (double)n;
+    const double seconds = (double)d[0] * factor / link;
+    return seconds * 1e6;
+  }
+  const double compute = D.compute[quant];
+  if (!(compute > 0.0)) { *st = LC_ST_UNSUPPORTED; return 0.0; }
+  double flops, bytes_moved;
+  if (kind == LC_KIND_GEMM) {
+    const int64_t m = d[0], n = d[1], k = d[2];
+    flops = 2.0 * (double)m * (double)n * (double)k;
+    bytes_moved = b * (double)(m * k + k * n + m * n);
+  } else if (kind == LC_KIND_ATTN_CTX) {
+    const int64_t B = d[0], s = d[1], H = d[2], KV = d[3], hd = d[4];
+    flops = 2.0 * (double)B * (double)H * (double)s * (double)s * (double)hd;
+    bytes_moved = b * (double)B * (double)s * (double)(2 * H + 2 * KV) * (double)hd;
+  } else if (kind == LC_KIND_ATTN_GEN) {
+    const int64_t B = d[0], kv = d[1], H = d[2], KV = d[3], hd = d[4];
+    flops = 4.0 * (double)B * (double)H * (double)kv * (double)hd;
+    bytes_moved = b * (double)B * (double)kv * 2.0 * (double)KV * (double)hd;
+  } else if (kind == LC_KIND_MOE_GEMM) {
+    const int64_t t = d[0], e = d[1], h = d[3], i = d[4];
+    flops = 3.0 * 2.0 * (double)t * (double)h * (double)i;
+    bytes_moved = b * (3.0 * (double)e * (double)h * (double)i + (double)(t * (h + i)));
+  } else if (kind == LC_KIND_MOE_DISPATCH || kind == LC_KIND_MOE_COMBINE) {
+    const double seconds = b * (double)d[0] * (double)d[2] * (double)d[3] / D.intra_bw;
+    return seconds * 1e6;
+  } else {  // embedding
+    return b * (double)d[0] * (double)d[1] / D.mem_bw * 1e6;
+  }
+  const double a = flops / compute, c = bytes_moved / D.mem_bw;
+  return (c > a ? c : a) * 1e6;
+}
+
+// query_latency (perfdb.py:539-580) for one plan entry with coordinates in d[0..1].
+__device__ __forceinline__ double query(const DbView& D, const lc_entry& e, int64_t* d, int* st, int* n_logs) {
+  if (e.grid < 0) { *st = LC_ST_MISSING_KEY; return 0.0; }
+  const DevGrid G = D.grids[e.grid];
+  bool any_oob = false, any_above = false;
+  int64_t cl[2] = {d[0], d[1]};
+  for (int a = 0; a < G.ndim; ++a) {
+    const int64_t* v = D.axv + G.ax_off[a];
+    const int64_t lo = v[0], hi = v[G.ax_len[a] - 1];
+    if (d[a] < lo) { any_oob = true; cl[a] = lo; }
+    if (d[a] > hi) { any_oob = any_above = true; cl[a] = hi; }
+  }
+  if (!any_oob) return interp_cells(D, G, d[0], d[1], n_logs);
+  if (D.policy == LC_POLICY_STRICT) { *st = LC_ST_EXTRAPOLATION; return 0.0; }
+  const bool use_sol = D.policy == LC_POLICY_SOL || (D.policy == LC_POLICY_DEFAULT && any_above);
+  if (D.policy == LC_POLICY_CLAMP || !use_sol) return interp_cells(D, G, cl[0], cl[1], n_logs);
+  const double edge = interp_cells(D, G, cl[0], cl[1], n_logs);
+  int64_t de[5] = {d[0], d[1], d[2], d[3], d[4]};
+  for (int a = 0; a < G.ndim; ++a) de[a] = cl[a];
+  const double sol_edge = sol_us(D, e.kind, e.quant, de, st);
+  if (*st) return 0.0;
+  const double eff = edge / sol_edge;
+  const double sol_q = sol_us(D, e.kind, e.quant, d, st);
+  if (*st) return 0.0;
+  return sol_q * eff;
+}
+
+enum { PH_PREFILL = 0, PH_DECODE = 1, PH_MIXED = 2 };
+
+struct StepArgs {
+  int phase;
+  int64_t n_ctx, n_gen, seq;
+  int64_t expert_tokens;  // final expert_ffn token count for this step
+};
+
+// Fill the interpolated coordinates of entry e for a step; false if the entry
+// is absent from this step's plan (context attention needs n_ctx > 0,
+// generation attention n_gen > 0: model.py:327-357).
+__device__ __forceinline__ bool entry_coords(const lc_entry& e, const StepArgs& a, int64_t hidden, int64_t* d) {
+  d[0] = e.d[0]; d[1] = e.d[1]; d[2] = e.d[2]; d[3] = e.d[3]; d[4] = e.d[4];
+  const int64_t tokens = a.n_ctx + a.n_gen;
+  switch (e.coord) {
+    case LC_COORD_TOKENS: d[0] = tokens; return true;
+    case LC_COORD_MSG: d[0] = tokens * hidden * 2; return true;
+    case LC_COORD_CTX:
+      if (!a.n_ctx) return false;
+      d[0] = a.phase == PH_MIXED ? 1 : a.n_ctx / a.seq;
+      d[1] = a.phase == PH_MIXED ? a.n_ctx : a.seq;
+      return true;
+    case LC_COORD_GEN:
+      if (!a.n_gen) return false;
+      d[0] = a.n_gen; d[1] = a.seq;
+      return true;
+    default: d[0] = a.expert_tokens; return true;
+  }
+}
+
+struct StepStats {
+  int32_t q1, q2;   // 1-D / 2-D queries issued (reference-equivalent accounting)
+  int32_t logs;
+};
+
+// One forward pass: Σ_entries ((lat * repeat) / 1000.0) * bubble, summed like
+// CPython's sum() in plan order (estimator.py:83-95).  On failure the first
+// failing entry in plan order is recorded.
+__device__ __forceinline__ int step_total(const DbView& D, const lc_entry* E, int n, const StepArgs& a,
+                                          double bubble, int64_t hidden, double* out, ErrRec* err,
+                                          StepStats* ss) {
+  NeumaierSum s;
+  for (int i = 0; i < n; ++i) {
+    const lc_entry& e = E[i];
+    int64_t d[5];
+    if (!entry_coords(e, a, hidden, d)) continue;
+    int st = 0;
+    const double lat = query(D, e, d, &st, &ss->logs);
+    if (e.coord == LC_COORD_CTX || e.coord == LC_COORD_GEN) ++ss->q2; else ++ss->q1;
+    if (st) { err->code = st; err->label = e.label; err->c0 = d[0]; err->c1 = d[1]; return st; }
+    const double ms = lat * (double)e.repeat / 1000.0;
+    s.add(0.0 + ms * bubble);
+  }
+  *out = s.result();
+  return 0;
+}
+
+// Static batching decode loop (serving_modes.py:256-266), stride 32.  Only the
+// generation-attention entry depends on the KV length, so the other entries
+// are priced once and the per-step sum re-run with the new attention term.
+__device__ __forceinline__ int static_decode(const DbView& D, const lc_entry* E, int n, int64_t b, int64_t isl,
+                                             int64_t osl, int64_t expert_tokens, double bubble, int64_t hidden,
+                                             double* tpot, ErrRec* err, StepStats* ss, int32_t* n_steps) {
+  if (osl <= 1) { *tpot = 0.0; return 0; }
+  double term[LC_MAX_ENTRIES];
+  int gi = -1;
+  int m = 0;
+  StepArgs a{PH_DECODE, 0, b, isl + 1, expert_tokens};
+  const lc_entry* ge = nullptr;
+  for (int i = 0; i < n; ++i) {
+    const lc_entry& e = E[i];
+    int64_t d[5];
+    if (!entry_coords(e, a, hidden, d)) continue;
+    int st = 0;
+    const double lat = query(D, e, d, &st, &ss->logs);
+    if (st) { err->code = st; err->label = e.label; err->c0 = d[0]; err->c1 = d[1]; return st; }
+    if (e.coord == LC_COORD_GEN) { gi = m; ge = &e; }
+    const double ms = lat * (double)e.repeat / 1000.0;
+    term[m++] = 0.0 + ms * bubble;
+  }
+  const int per_step_q2 = 1;
+  const int per_step_q1 = m - per_step_q2;
+  double t_gen = 0.0;
+  int64_t k = 0;
+  int steps = 0;
+  while (k < osl - 1) {
+    if (k > 0) {
+      int64_t d[5] = {ge->d[0], ge->d[1], ge->d[2], ge->d[3], ge->d[4]};
+      d[0] = b;
+      d[1] = isl + k + 1;
+      int st = 0;
+      const double lat = query(D, *ge, d, &st, &ss->logs);
+      if (st) { err->code = st; err->label = ge->label; err->c0 = d[0]; err->c1 = d[1]; return st; }
+      const double ms = lat * (double)ge->repeat / 1000.0;
+      term[gi] = 0.0 + ms * bubble;
+    }
+    NeumaierSum s;
+    for (int i = 0; i < m; ++i) s.add(term[i]);
+    const double step = s.result();
+    const int64_t run = (osl - 1 - k) < 32 ? (osl - 1 - k) : 32;
+    t_gen += step * (double)run;
+    k += run;
+    ++steps;
+  }
+  ss->q1 += per_step_q1 * steps;
+  ss->q2 += per_step_q2 * steps;
+  *n_steps = steps;
+  *tpot = t_gen / (double)(osl - 1);
+  return 0;
+}
+
+// derive_metrics (serving_modes.py:161-172)
+__device__ __forceinline__ void derive_metrics(double ttft, double tpot, int64_t batch, int64_t osl, int64_t gpus,
+                                               double* speed, double* thru) {
+  *speed = tpot == 0.0 ? INFINITY : 1000.0 / tpot;
+  const double req = ttft + (double)(osl - 1) * tpot;
+  *thru = 1000.0 / req * (double)batch * (double)osl / (double)gpus;
+}
+
+__device__ __forceinline__ int64_t ceil_div_f(int64_t a, int64_t b) { return (int64_t)ceil((double)a / (double)b); }
+
+// Aggregated-mode schedule (serving_modes.py:292-320): returns status and the
+// mixed-step shape.
+struct AggSched {
+  int32_t st;
+  int64_t c_ctx, chunk_total, T, cpr, chunk_tokens, t_mix, t_gen, n_mix_gen, prefilling;
+};
+
+__device__ __forceinline__ AggSched agg_schedule(const lc_search_desc& S, int64_t b) {
+  AggSched r;
+  r.st = 0;
+  r.chunk_total = S.isl - S.prefix;
+  r.c_ctx = S.has_ctx_capacity ? S.ctx_capacity : (r.chunk_total > 2048 ? r.chunk_total : 2048);
+  r.T = r.cpr = r.chunk_tokens = r.t_mix = r.t_gen = r.n_mix_gen = r.prefilling = 0;
+  if (!S.chunked_prefill && r.chunk_total > r.c_ctx) { r.st = LC_ST_INFEASIBLE_CHUNK_OFF; return r; }
+  r.T = ceil_div_f(r.chunk_total * b, r.c_ctx);
+  r.cpr = ceil_div_f(r.chunk_total, r.c_ctx);
+  r.chunk_tokens = r.c_ctx < r.chunk_total ? r.c_ctx : r.chunk_total;
+  if (b == 1) {
+    r.t_mix = 1; r.t_gen = S.osl - 1; r.n_mix_gen = 0;
+  } else if (r.T >= S.osl) {
+    int64_t n = (int64_t)((double)(b * S.osl) / (double)r.T);
+    r.n_mix_gen = n > 1 ? n : 1;
+    r.t_mix = S.osl; r.t_gen = 0;
+  } else {
+    r.prefilling = ceil_div_f(r.c_ctx, r.chunk_total);
+    r.n_mix_gen = b - r.prefilling;
+    if (r.n_mix_gen < 1) { r.st = LC_ST_INFEASIBLE_NO_DECODE_SLOT; return r; }
+    r.t_mix = r.T; r.t_gen = S.osl - r.T;
+  }
+  return r;
+}
+
+// memory fit for one (combo, batch) (model.py:440-479)
+__device__ __forceinline__ bool fits_memory(const lc_combo& c, const lc_search_desc& S, double gpu_memory,
+                                            int64_t hidden, int64_t batch) {
+  const int64_t cap = S.has_ctx_capacity ? S.ctx_capacity : 2048;
+  const int64_t live = batch > cap ? batch : cap;
+  const int64_t act = 4 * live * hidden * 2;
+  const double overhead = 0.05 * gpu_memory + (double)act;
+  const double stat = c.weight_bytes + overhead;
+  if (stat > gpu_memory) return false;
+  const double kv_budget = S.kv_mem_fraction * (gpu_memory - stat);
+  const double kv_need = c.kv_token_bytes * (double)batch * (double)(S.isl + S.osl);
+  return kv_need <= kv_budget;
+}
+
+__device__ __forceinline__ bool in_budget(const lc_search_desc& S, int64_t g) {
+  if (S.n_budgets == 0) return true;
+  for (int i = 0; i < S.n_budgets; ++i)
+    if (S.budgets[i] == g) return true;
+  return false;
+}
+
+// ---- config key strings (ParallelConfig.key, model.py:205-206) for tie-breaks
+__device__ __forceinline__ int put_int(char* s, int64_t v) {
+  char tmp[24];
+  int n = 0;
+  if (v == 0) tmp[n++] = '0';
+  while (v > 0) { tmp[n++] = (char)('0' + v % 10); v /= 10; }
+  for (int i = 0; i < n; ++i) s[i] = tmp[n - 1 - i];
+  return n;
+}
+
+__device__ __forceinline__ int put_str(char* s, const char* t) {
+  int n = 0;
+  while (t[n]) { s[n] = t[n]; ++n; }
+  return n;
+}
+
+__device__ __forceinline__ int fmt_cfg_key(char* s, const lc_combo& c, int64_t batch) {
+  int n = 0;
+  n += put_str(s + n, "tp"); n += put_int(s + n, c.tp);
+  n += put_str(s + n, "pp"); n += put_int(s + n, c.pp);
+  n += put_str(s + n, "ep"); n += put_int(s + n, c.ep);
+  n += put_str(s + n, "dp"); n += put_int(s + n, c.dp);
+  n += put_str(s + n, "b"); n += put_int(s + n, batch);
+  s[n] = 0;
+  return n;
+}
+
+__device__ __forceinline__ int str_cmp(const char* a, const char* b) {
+  int i = 0;
+  while (a[i] && a[i] == b[i]) ++i;
+  return (int)(unsigned char)a[i] - (int)(unsigned char)b[i];
+}
+
+}  // namespace lc

@@ -1,0 +1,1395 @@
+// llmconf_b200: B200 kernels for the llmconf configuration-search hot path and
+// the C ABI declared in include/llmconf_b200.h.
+//
+// Pipeline for one lc_search_batch (many searches of one model x space):
+//   K0  k_enum_flags / k_scan_* / k_scatter : enumerate_candidates (search.py:82-113)
+//   K3  k_tails                            : MoE busiest-shard tokens (moe_load.py:67-147)
+//   K2  k_eval                             : static / aggregated / pool steps per unit
+//   K5a k_pools                            : pool top-k by (-rate/gpus, key) (search.py:338-339)
+//   K5b k_disagg                           : x*y replica sweep per pairing + plan sort (serving_modes.py:449-494)
+//   K4  k_front                            : SLA, Pareto front, best, nearest miss (search.py:129-208)
+// Build with --fmad=false: bit-exact parity with CPython needs unfused arithmetic.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/llmconf_b200.h"
+#include "glibc_libm.cuh"
+#include "lc_eval.cuh"
+#include "lc_tails.cuh"
+
+using namespace lc;
+
+// ============================================================================ host-side state
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(LC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T>
+  T* get(size_t n, cudaError_t* err) {
+    size_t bytes = n * sizeof(T);
+    if (bytes == 0) bytes = 16;
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      cudaError_t e = cudaMalloc(&p, bytes);
+      if (e != cudaSuccess) { *err = e; return nullptr; }
+      cap = bytes;
+    }
+    return (T*)p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+const double LOG_TAB_H[256] = GLIBC_LOG_TAB_INIT;
+const uint64_t EXP_TAB_H[256] = GLIBC_EXP_TAB_INIT;
+}  // namespace
+
+struct lc_db {
+  int device;
+  int32_t n_grids, n_axis, n_cells;
+  DevGrid* grids;
+  int64_t* axv;
+  double* axl;
+  double* cell;
+  double* clog;
+  double* logtab;
+  uint64_t* exptab;
+  double mem_bw, intra_bw, inter_bw, gpu_memory, compute[4];
+  int32_t gpn, policy;
+  size_t smem_bytes;  // staged size
+};
+
+struct lc_space {
+  int device;
+  int64_t hidden, topk, n_experts;
+  int32_t is_moe, n_combos, n_tmpl, n_tp, n_ep;
+  lc_combo* combos;
+  int32_t* tmpl_n;
+  lc_entry* entries;
+  int64_t* tp_vals;  // [n_tp] from combos
+  int64_t* ep_vals;  // [n_ep]
+  uint8_t* pair_used;  // [n_tp*n_ep]
+};
+
+// per-search bookkeeping computed on the host / device
+struct SearchMeta {
+  int64_t raw_off, n_raw;
+  int64_t tail_off;
+  int32_t unit_off, n_units;
+  int32_t plan_off, plan_cap;
+  int32_t pool_off;  // into pool selection arrays (64 slots per role)
+  int32_t n_pre, n_dec;
+};
+
+struct lc_ctx {
+  int device;
+  cudaStream_t stream;
+  cudaEvent_t ev[8];
+  DBuf searches, batches, loads, meta, results;
+  DBuf flags, pos, block_sums;
+  DBuf u_search, u_combo, u_batch, u_budget;
+  DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
+  DBuf tails, pool_sel, plans_i, plans_d, front, u_queries;
+  // last batch
+  const lc_db* db = nullptr;
+  const lc_space* sp = nullptr;
+  int32_t n_search = 0, n_batches = 0, n_loads = 0;
+  int64_t n_raw = 0, n_units = 0, n_tails = 0, n_plan_slots = 0, n_front_slots = 0;
+  std::vector<SearchMeta> hmeta;
+  std::vector<lc_search_result> hres;
+};
+
+// ============================================================================ device kernels
+namespace {
+
+constexpr int kScanBlock = 1024;
+
+struct EvalParams {
+  // db (global copies; staged to smem)
+  const DevGrid* grids; const int64_t* axv; const double* axl; const double* cell; const double* clog;
+  const double* logtab; const uint64_t* exptab;
+  int32_t n_grids, n_axis, n_cells;
+  double mem_bw, intra_bw, inter_bw, gpu_memory, compute[4];
+  int32_t gpn, policy;
+  // space
+  const lc_combo* combos; const int32_t* tmpl_n; const lc_entry* entries;
+  int64_t hidden, topk, n_experts; int32_t is_moe, n_tp, n_ep;
+  const int64_t* tp_vals; const int64_t* ep_vals; const uint8_t* pair_used;
+  // batch
+  const lc_search_desc* searches; const SearchMeta* meta; int32_t n_search;
+  const int64_t* batches; const double* loads;
+  // units
+  const int32_t* u_search; const int32_t* u_combo; const int32_t* u_batch; const uint8_t* u_budget;
+  int64_t n_units;
+  const int64_t* tails;
+  // outputs
+  int32_t* st_status; double* st_v;  // v: [4][n_units] ttft,tpot,speed,thru
+  int32_t* ag_status; double* ag_v;
+  int32_t* pf_status; double* pf_v;  // [2][n_units] lat, rate
+  int32_t* dc_status; double* dc_v;
+  int64_t* err_c;                    // [8][n_units]: (c0,c1) x (st,ag,pf,dc)
+  int32_t* u_queries;                // q1 | q2 << 16 per unit
+  lc_search_result* results;
+};
+
+__device__ __forceinline__ int find_search(const SearchMeta* meta, int n, int64_t r) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (meta[mid].raw_off <= r) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ---- K0: enumeration flags: bit0 keep (unit), bit1 in budget
+__global__ void k_enum_flags(EvalParams P, int64_t n_raw, uint8_t* flags) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_raw; r += (int64_t)gridDim.x * blockDim.x) {
+    const int s = find_search(P.meta, P.n_search, r);
+    const lc_search_desc& S = P.searches[s];
+    const int64_t rel = r - P.meta[s].raw_off;
+    const int ci = (int)(rel / S.n_b), bi = (int)(rel % S.n_b);
+    const lc_combo c = P.combos[ci];
+    const int64_t b = P.batches[S.b_off + bi];
+    uint8_t f = 0;
+    if (fits_memory(c, S, P.gpu_memory, P.hidden, b)) {
+      const bool inb = in_budget(S, c.gpus);
+      if (inb || (S.modes & 4)) f = 1 | (inb ? 2 : 0);  // workers skip the budget (search.py:323)
+    }
+    flags[r] = f;
+  }
+}
+
+__global__ void k_scan_blocks(const uint8_t* flags, int64_t n, int32_t* block_sums) {
+  const int64_t i = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
+  int v = (i < n) ? (flags[i] & 1) : 0;
+  v = __syncthreads_count(v);
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = v;
+}
+
+__global__ void k_scan_top(int32_t* block_sums, int n) {
+  // single block exclusive scan, in place; block_sums[n] = total
+  __shared__ int32_t carry;
+  __shared__ int32_t warp_tot[32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    const int v = i < n ? block_sums[i] : 0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, t, o);
+        if (lane >= o) t += y;
+      }
+      warp_tot[lane] = t;
+    }
+    __syncthreads();
+    const int excl = x - v + (w ? warp_tot[w - 1] : 0) + carry;
+    if (i < n) block_sums[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) block_sums[n] = carry;
+}
+
+__global__ void k_scatter(EvalParams P, const uint8_t* flags, int64_t n, const int32_t* block_sums, int32_t* pos,
+                          int32_t* u_search, int32_t* u_combo, int32_t* u_batch, uint8_t* u_budget) {
+  __shared__ int32_t warp_tot[32];
+  const int64_t i = blockIdx.x * (int64_t)kScanBlock + threadIdx.x;
+  const uint8_t f = i < n ? flags[i] : 0;
+  const int v = f & 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = warp_tot[lane];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    warp_tot[lane] = t;
+  }
+  __syncthreads();
+  const int p = block_sums[blockIdx.x] + x - v + (w ? warp_tot[w - 1] : 0);
+  if (i < n) {
+    pos[i] = p;
+    if (v) {
+      const int s = find_search(P.meta, P.n_search, i);
+      const lc_search_desc& S = P.searches[s];
+      const int64_t rel = i - P.meta[s].raw_off;
+      u_search[p] = s;
+      u_combo[p] = (int32_t)(rel / S.n_b);
+      u_batch[p] = (int32_t)(rel % S.n_b);
+      u_budget[p] = (f >> 1) & 1;
+    }
+  }
+}
+
+__global__ void k_unit_offsets(SearchMeta* meta, int n_search, const int32_t* pos, int64_t n_raw, int32_t total) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_search) return;
+  const int64_t r0 = meta[s].raw_off, r1 = r0 + meta[s].n_raw;
+  const int32_t a = r0 < n_raw ? pos[r0] : total;
+  const int32_t b = r1 < n_raw ? pos[r1] : total;
+  meta[s].unit_off = a;
+  meta[s].n_units = b - a;
+}
+
+// ---- K3: MoE tails table [type P/D/M][tp_i][ep_i][b_i] per search
+__global__ void k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
+  __shared__ int hist_all[8][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* hist = hist_all[warp];
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; t < n_tails; t += nw) {
+    // locate search by tail offset
+    int lo = 0, hi = P.n_search - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.meta[mid].tail_off <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    const int s = lo;
+    const lc_search_desc& S = P.searches[s];
+    int64_t rel = t - P.meta[s].tail_off;
+    const int bi = (int)(rel % S.n_b); rel /= S.n_b;
+    const int ep_i = (int)(rel % P.n_ep); rel /= P.n_ep;
+    const int tp_i = (int)(rel % P.n_tp); rel /= P.n_tp;
+    const int type = (int)rel;
+    int64_t result = 0;
+    const int64_t tp = P.tp_vals[tp_i], ep = P.ep_vals[ep_i];
+    if (ep > 1 && P.pair_used[tp_i * P.n_ep + ep_i] && S.load >= 0) {
+      const int64_t b = P.batches[S.b_off + bi];
+      const int64_t chunk = S.isl - S.prefix;
+      int64_t tokens = -1;
+      if (type == 0) tokens = b * chunk;
+      else if (type == 1) tokens = b;
+      else {
+        const AggSched a = agg_schedule(S, b);
+        if (!a.st) tokens = a.chunk_tokens + a.n_mix_gen;
+      }
+      if (tokens >= 0) {
+        const int64_t f = ep / tp > 1 ? ep / tp : 1;
+        const int64_t pooled = tokens * f;
+        const int E = (int)P.n_experts;
+        const double* q = P.loads + (int64_t)S.load * 2 * E;
+        if (E <= 256)
+          result = warp_busiest_shard<8>(q, q + E, E, pooled, P.topk, ep, hist);
+        else
+          result = warp_busiest_shard<32>(q, q + E, E, pooled, P.topk, ep, hist);
+      }
+    }
+    if (lane == 0) tails[t] = result;
+  }
+}
+
+// ---- K2: evaluate every unit
+__device__ __forceinline__ void stage_db(const EvalParams& P, unsigned char* smem, DbView* V) {
+  unsigned char* p = smem;
+  uint64_t* exptab = (uint64_t*)p; p += 256 * 8;
+  double* logtab = (double*)p; p += 256 * 8;
+  int64_t* axv = (int64_t*)p; p += (size_t)P.n_axis * 8;
+  double* axl = (double*)p; p += (size_t)P.n_axis * 8;
+  double* cell = (double*)p; p += (size_t)P.n_cells * 8;
+  double* clog = (double*)p; p += (size_t)P.n_cells * 8;
+  DevGrid* grids = (DevGrid*)p;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) { exptab[i] = P.exptab[i]; logtab[i] = P.logtab[i]; }
+  for (int i = threadIdx.x; i < P.n_axis; i += blockDim.x) { axv[i] = P.axv[i]; axl[i] = P.axl[i]; }
+  for (int i = threadIdx.x; i < P.n_cells; i += blockDim.x) { cell[i] = P.cell[i]; clog[i] = P.clog[i]; }
+  for (int i = threadIdx.x; i < P.n_grids; i += blockDim.x) grids[i] = P.grids[i];
+  __syncthreads();
+  V->grids = grids; V->axv = axv; V->axl = axl; V->cell = cell; V->clog = clog;
+  V->logtab = logtab; V->exptab = exptab;
+  V->mem_bw = P.mem_bw; V->intra_bw = P.intra_bw; V->inter_bw = P.inter_bw; V->gpu_memory = P.gpu_memory;
+  for (int i = 0; i < 4; ++i) V->compute[i] = P.compute[i];
+  V->gpn = P.gpn; V->policy = P.policy;
+}
+
+__device__ __forceinline__ int64_t expert_tokens(const EvalParams& P, const lc_combo& c, const SearchMeta& M,
+                                                 const lc_search_desc& S, int type, int bi, int64_t tokens) {
+  if (!P.is_moe) return 0;
+  const int64_t f = c.ep / c.tp > 1 ? c.ep / c.tp : 1;
+  const int64_t pooled = tokens * f;
+  const int64_t balanced = ceil_div_f(pooled * P.topk, c.ep);
+  if (c.ep == 1 || S.load < 0) return balanced;
+  const int64_t tail =
+      P.tails[M.tail_off + (((int64_t)type * P.n_tp + c.tp_i) * P.n_ep + c.ep_i) * S.n_b + bi];
+  return balanced > tail ? balanced : tail;
+}
+
+__device__ __forceinline__ void put_err(const EvalParams& P, int kind, int64_t u, const ErrRec& e) {
+  P.err_c[(int64_t)(2 * kind) * P.n_units + u] = e.c0;
+  P.err_c[(int64_t)(2 * kind + 1) * P.n_units + u] = e.c1;
+}
+
+__global__ void __launch_bounds__(128) k_eval(EvalParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  DbView V;
+  stage_db(P, smem, &V);
+  const int64_t n = P.n_units;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    const int s = P.u_search[u];
+    const lc_search_desc& S = P.searches[s];
+    const SearchMeta& M = P.meta[s];
+    const int bi = P.u_batch[u];
+    const lc_combo c = P.combos[P.u_combo[u]];
+    const lc_entry* E = P.entries + (int64_t)c.tmpl * LC_MAX_ENTRIES;
+    const int ne = P.tmpl_n[c.tmpl];
+    const int64_t b = P.batches[S.b_off + bi];
+    const bool inb = P.u_budget[u] != 0;
+    const bool do_st = (S.modes & 1) && inb, do_ag = (S.modes & 2) && inb, do_dg = (S.modes & 4) != 0;
+    const int64_t mb = b > 1 ? b : 1;
+    const double bubble = (double)(mb + c.pp - 1) / (double)mb;
+    const int64_t chunk = S.isl - S.prefix;
+    const int64_t kv_mid = S.isl + S.osl / 2;
+    StepStats ss{0, 0, 0};
+    int32_t q1 = 0, q2 = 0;
+
+    // prefill step: static TTFT and the prefill pool (estimator memo shares it)
+    double p_total = 0.0;
+    ErrRec p_err{0, 0, 0, 0};
+    if (do_st || do_dg) {
+      StepArgs a{PH_PREFILL, b * chunk, 0, chunk, expert_tokens(P, c, M, S, 0, bi, b * chunk)};
+      step_total(V, E, ne, a, bubble, P.hidden, &p_total, &p_err, &ss);
+      if (!p_err.code) { q1 += ss.q1; q2 += ss.q2; }
+      ss.q1 = ss.q2 = 0;
+    }
+    const int64_t xt_dec = expert_tokens(P, c, M, S, 1, bi, b);
+    int32_t st_steps = 0;
+    if (do_st) {
+      double tpot = 0.0;
+      ErrRec e = p_err;
+      if (!e.code) {
+        static_decode(V, E, ne, b, S.isl, S.osl, xt_dec, bubble, P.hidden, &tpot, &e, &ss, &st_steps);
+        if (!e.code) { q1 += ss.q1; q2 += ss.q2; }
+        ss.q1 = ss.q2 = 0;
+      }
+      P.st_status[u] = e.code | (e.label << 8);
+      if (e.code) {
+        put_err(P, 0, u, e);
+      } else {
+        double speed, thru;
+        derive_metrics(p_total, tpot, b, S.osl, c.gpus, &speed, &thru);
+        P.st_v[u] = p_total; P.st_v[n + u] = tpot; P.st_v[2 * n + u] = speed; P.st_v[3 * n + u] = thru;
+      }
+    }
+    // generation step at the KV midpoint: aggregated l_gen and the decode pool
+    bool g_done = false;
+    double g_total = 0.0;
+    ErrRec g_err{0, 0, 0, 0};
+    auto gen_step = [&]() {
+      if (g_done) return;
+      g_done = true;
+      StepArgs a{PH_DECODE, 0, b, kv_mid, xt_dec};
+      step_total(V, E, ne, a, bubble, P.hidden, &g_total, &g_err, &ss);
+      // memo hit in the reference when a static decode step used the same KV length
+      const int64_t k = kv_mid - S.isl - 1;
+      const bool dup = do_st && S.osl > 1 && k >= 0 && (k % 32) == 0 && (k / 32) < st_steps;
+      if (!g_err.code && !dup) { q1 += ss.q1; q2 += ss.q2; }
+      ss.q1 = ss.q2 = 0;
+    };
+    if (do_ag) {
+      const AggSched sc = agg_schedule(S, b);
+      ErrRec e{sc.st, 0, 0, 0};
+      double ttft = 0.0, tpot = 0.0;
+      if (!sc.st) {
+        double l_mix = 0.0, l_gen = 0.0;
+        StepArgs a{PH_MIXED, sc.chunk_tokens, sc.n_mix_gen, kv_mid,
+                   expert_tokens(P, c, M, S, 2, bi, sc.chunk_tokens + sc.n_mix_gen)};
+        step_total(V, E, ne, a, bubble, P.hidden, &l_mix, &e, &ss);
+        if (!e.code) { q1 += ss.q1; q2 += ss.q2; }
+        ss.q1 = ss.q2 = 0;
+        if (!e.code && (sc.t_gen || b == 1)) {
+          gen_step();
+          e = g_err;
+          l_gen = g_total;
+        }
+        if (!e.code) {
+          const double raw = 2.0 + (double)(sc.T - 3) * (1.0 / 20.0);
+          double F = raw > 2.0 ? raw : 2.0;
+          F = F < 4.0 ? F : 4.0;
+          ttft = l_mix * (double)sc.cpr * F;
+          if (b == 1) tpot = S.osl > 1 ? l_gen : 0.0;
+          else if (S.osl == 1) tpot = 0.0;
+          else if (sc.t_gen == 0) tpot = l_mix;
+          else {
+            const int64_t ms = sc.t_mix - 3 > 1 ? sc.t_mix - 3 : 1;
+            tpot = (l_mix * (double)ms + l_gen * (double)sc.t_gen) / (double)(ms + sc.t_gen);
+          }
+        }
+      }
+      P.ag_status[u] = e.code | (e.label << 8);
+      if (e.code) {
+        put_err(P, 1, u, e);
+      } else {
+        double speed, thru;
+        derive_metrics(ttft, tpot, b, S.osl, c.gpus, &speed, &thru);
+        P.ag_v[u] = ttft; P.ag_v[n + u] = tpot; P.ag_v[2 * n + u] = speed; P.ag_v[3 * n + u] = thru;
+      }
+    }
+    if (do_dg) {
+      P.pf_status[u] = p_err.code | (p_err.label << 8);
+      if (p_err.code) put_err(P, 2, u, p_err);
+      else { P.pf_v[u] = p_total; P.pf_v[n + u] = (double)b * 1000.0 / p_total; }
+      gen_step();
+      P.dc_status[u] = g_err.code | (g_err.label << 8);
+      if (g_err.code) put_err(P, 3, u, g_err);
+      else {
+        P.dc_v[u] = g_total;
+        P.dc_v[n + u] = S.osl == 1 ? INFINITY : (double)b * 1000.0 / ((double)(S.osl - 1) * g_total);
+      }
+    }
+    // reference-equivalent query accounting (summed per search in K4)
+    P.u_queries[u] = (q1 & 0xffff) | (q2 << 16);
+  }
+}
+
+// ---- comparison helpers for top-k / best / nearest
+struct PoolKey {
+  double r;     // -rate / gpus
+  int32_t unit; // global unit index, -1 = none
+};
+
+__device__ __forceinline__ int cfg_cmp(const EvalParams& P, int32_t ua, int32_t ub) {
+  char a[96], b[96];
+  const lc_search_desc& S = P.searches[P.u_search[ua]];
+  fmt_cfg_key(a, P.combos[P.u_combo[ua]], P.batches[S.b_off + P.u_batch[ua]]);
+  fmt_cfg_key(b, P.combos[P.u_combo[ub]], P.batches[S.b_off + P.u_batch[ub]]);
+  return str_cmp(a, b);
+}
+
+__device__ __forceinline__ bool pool_less(const EvalParams& P, const PoolKey& a, const PoolKey& b) {
+  if (a.unit < 0) return false;
+  if (b.unit < 0) return true;
+  if (a.r != b.r) return a.r < b.r;
+  return cfg_cmp(P, a.unit, b.unit) < 0;
+}
+
+// ---- K5a: top-k prefill / decode pool members per search (block per search)
+__global__ void k_pools(EvalParams P, SearchMeta* meta, int32_t* pool_sel) {
+  const int s = blockIdx.x;
+  const lc_search_desc& S = P.searches[s];
+  if (!(S.modes & 4)) return;
+  __shared__ PoolKey red[256];
+  const int32_t u0 = meta[s].unit_off, nu = meta[s].n_units;
+  for (int role = 0; role < 2; ++role) {
+    const int cap = role == 0 ? S.prefill_cap : S.decode_cap;
+    const int32_t* status = role == 0 ? P.pf_status : P.dc_status;
+    const double* v = role == 0 ? P.pf_v : P.dc_v;
+    PoolKey prev{0.0, -1};
+    int got = 0;
+    for (int k = 0; k < cap && k < 64; ++k) {
+      PoolKey best{0.0, -1};
+      for (int i = threadIdx.x; i < nu; i += blockDim.x) {
+        const int32_t u = u0 + i;
+        if (status[u] != 0) continue;
+        const double rate = v[P.n_units + u];
+        PoolKey key{-rate / (double)P.combos[P.u_combo[u]].gpus, u};
+        if (prev.unit >= 0 && !pool_less(P, prev, key)) continue;  // already taken
+        if (pool_less(P, key, best)) best = key;
+      }
+      red[threadIdx.x] = best;
+      __syncthreads();
+      for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w && pool_less(P, red[threadIdx.x + w], red[threadIdx.x])) red[threadIdx.x] = red[threadIdx.x + w];
+        __syncthreads();
+      }
+      const PoolKey sel = red[0];
+      __syncthreads();
+      if (sel.unit < 0) break;
+      if (threadIdx.x == 0) pool_sel[(int64_t)s * 128 + role * 64 + k] = sel.unit;
+      prev = sel;
+      ++got;
+    }
+    if (threadIdx.x == 0) {
+      if (role == 0) meta[s].n_pre = got;
+      else meta[s].n_dec = got;
+    }
+    __syncthreads();
+  }
+}
+
+// ---- K5b: replica sweep per pairing and plan sort (block per search)
+struct PlanRec {
+  int32_t p, d, x, y;  // p/d: global unit index
+  int64_t gpus;
+  double r_sys, ttft, tpot, speed, thru;
+};
+
+__global__ void k_disagg(EvalParams P, SearchMeta* meta, const int32_t* pool_sel, int32_t* plan_i, double* plan_d,
+                         lc_search_result* results) {
+  const int s = blockIdx.x;
+  const lc_search_desc& S = P.searches[s];
+  __shared__ int32_t pre[64], dec[64];
+  __shared__ int npre, ndec;
+  __shared__ PlanRec plans[256];
+  __shared__ int nplan;
+  if (!(S.modes & 4)) {
+    if (threadIdx.x == 0) { meta[s].plan_cap = 0; results[s].n_plans = 0; }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    npre = ndec = 0;
+    for (int k = 0; k < meta[s].n_pre; ++k) {
+      const int32_t u = pool_sel[(int64_t)s * 128 + k];
+      if (!S.has_ttft || P.pf_v[u] * S.ttft_headroom <= S.ttft_limit) pre[npre++] = u;
+    }
+    for (int k = 0; k < meta[s].n_dec; ++k) {
+      const int32_t u = pool_sel[(int64_t)s * 128 + 64 + k];
+      if (!S.has_floor || P.dc_v[u] <= S.tpot_cap) dec[ndec++] = u;
+    }
+    nplan = 0;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  const int npair = npre * ndec;
+  for (int pi = warp; pi < npair && pi < 256; pi += nwarp) {
+    const int32_t up = pre[pi / ndec], ud = dec[pi % ndec];
+    const double rp = P.pf_v[P.n_units + up], rd = P.dc_v[P.n_units + ud];
+    const int64_t gp = P.combos[P.u_combo[up]].gpus, gd = P.combos[P.u_combo[ud]].gpus;
+    bool have = false;
+    double bk = 0.0;
+    int64_t bg = 0;
+    int bx = 0, by = 0;
+    for (int x = 1; x <= S.max_x; ++x) {
+      const double r_pre = rp * (double)x * S.prefill_util;
+      const int64_t g_pre = (int64_t)x * gp;
+      for (int y = 1 + lane; y <= S.max_y; y += 32) {
+        const int64_t gpus = g_pre + (int64_t)y * gd;
+        if (!in_budget(S, gpus)) continue;
+        const double r_dec = rd * (double)y * S.decode_util;
+        const double r_sys = r_dec < r_pre ? r_dec : r_pre;
+        const double k0 = -r_sys * (double)S.osl / (double)gpus;
+        const bool better = !have || k0 < bk ||
+                            (k0 == bk && (gpus < bg || (gpus == bg && (x < bx || (x == bx && y < by)))));
+        if (better) { have = true; bk = k0; bg = gpus; bx = x; by = y; }
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const int oh = __shfl_xor_sync(0xffffffffu, (int)have, o);
+      const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int64_t og = __shfl_xor_sync(0xffffffffu, bg, o);
+      const int ox = __shfl_xor_sync(0xffffffffu, bx, o);
+      const int oy = __shfl_xor_sync(0xffffffffu, by, o);
+      const bool better = oh && (!have || ok < bk ||
+                                 (ok == bk && (og < bg || (og == bg && (ox < bx || (ox == bx && oy < by))))));
+      if (better) { have = true; bk = ok; bg = og; bx = ox; by = oy; }
+    }
+    if (lane == 0 && have) {
+      PlanRec r;
+      r.p = up; r.d = ud; r.x = bx; r.y = by;
+      r.gpus = (int64_t)bx * gp + (int64_t)by * gd;
+      const double r_pre = rp * (double)bx * S.prefill_util;
+      const double r_dec = rd * (double)by * S.decode_util;
+      r.r_sys = r_dec < r_pre ? r_dec : r_pre;
+      r.ttft = P.pf_v[up] * S.ttft_headroom;
+      r.tpot = P.dc_v[ud];
+      r.speed = r.tpot == 0.0 ? INFINITY : 1000.0 / r.tpot;
+      r.thru = r.r_sys * (double)S.osl / (double)r.gpus;
+      // keep pairing order for the stable sort: slot = pairing index
+      plans[pi] = r;
+    }
+    if (lane == 0 && !have) plans[pi].p = -1;
+  }
+  __syncthreads();
+  // compact in pairing order, then stable rank by (-thru, gpus, ttft, x, y)
+  __shared__ int32_t order[256];
+  if (threadIdx.x == 0) {
+    int m = 0;
+    for (int i = 0; i < npair && i < 256; ++i)
+      if (plans[i].p >= 0) order[m++] = i;
+    nplan = m;
+  }
+  __syncthreads();
+  const int32_t off = meta[s].plan_off;
+  for (int i = threadIdx.x; i < nplan; i += blockDim.x) {
+    const PlanRec& a = plans[order[i]];
+    int rank = 0;
+    for (int j = 0; j < nplan; ++j) {
+      if (j == i) continue;
+      const PlanRec& b = plans[order[j]];
+      bool less;
+      if (-b.thru != -a.thru) less = -b.thru < -a.thru;
+      else if (b.gpus != a.gpus) less = b.gpus < a.gpus;
+      else if (b.ttft != a.ttft) less = b.ttft < a.ttft;
+      else if (b.x != a.x) less = b.x < a.x;
+      else if (b.y != a.y) less = b.y < a.y;
+      else less = j < i;
+      rank += less;
+    }
+    const int64_t slot = off + rank;
+    plan_i[slot * 4 + 0] = a.p; plan_i[slot * 4 + 1] = a.d; plan_i[slot * 4 + 2] = a.x; plan_i[slot * 4 + 3] = a.y;
+    plan_d[slot * 6 + 0] = (double)a.gpus; plan_d[slot * 6 + 1] = a.r_sys; plan_d[slot * 6 + 2] = a.ttft;
+    plan_d[slot * 6 + 3] = a.tpot; plan_d[slot * 6 + 4] = a.speed; plan_d[slot * 6 + 5] = a.thru;
+  }
+  if (threadIdx.x == 0) results[s].n_plans = nplan;
+}
+
+// ---- K4: feasibility, Pareto front, best, nearest miss (block per search)
+struct RowView {
+  bool valid;
+  int mode;  // 0 static 1 aggregated 2 disaggregated
+  double ttft, speed, thru;
+  int64_t gpus;
+  int64_t key;  // mode << 32 | index
+};
+
+__device__ __forceinline__ RowView get_row(const EvalParams& P, const SearchMeta& M, const int32_t* plan_i,
+                                           const double* plan_d, int64_t nplan, int64_t r) {
+  RowView v;
+  v.valid = false;
+  const int64_t nu = M.n_units;
+  if (r < 2 * nu) {
+    const int mode = r < nu ? 0 : 1;
+    const int64_t i = mode ? r - nu : r;
+    const int64_t u = M.unit_off + i;
+    if (!P.u_budget[u]) return v;
+    const int32_t* st = mode ? P.ag_status : P.st_status;
+    const double* vv = mode ? P.ag_v : P.st_v;
+    if (st[u] != 0) return v;
+    v.valid = true;
+    v.mode = mode;
+    v.ttft = vv[u];
+    v.speed = vv[2 * P.n_units + u];
+    v.thru = vv[3 * P.n_units + u];
+    v.gpus = P.combos[P.u_combo[u]].gpus;
+    v.key = ((int64_t)mode << 32) | i;
+  } else {
+    const int64_t i = r - 2 * nu;
+    const int64_t slot = M.plan_off + i;
+    v.valid = true;
+    v.mode = 2;
+    v.gpus = (int64_t)plan_d[slot * 6 + 0];
+    v.ttft = plan_d[slot * 6 + 2];
+    v.speed = plan_d[slot * 6 + 4];
+    v.thru = plan_d[slot * 6 + 5];
+    v.key = ((int64_t)2 << 32) | i;
+  }
+  return v;
+}
+
+__device__ __forceinline__ bool feasible(const lc_search_desc& S, const RowView& v) {
+  if (S.has_ttft && v.ttft > S.ttft_limit) return false;
+  return !S.has_floor || v.speed >= S.speed_floor;
+}
+
+__device__ int row_label(const EvalParams& P, const SearchMeta& M, const int32_t* plan_i, int64_t key, char* out) {
+  const int mode = (int)(key >> 32);
+  const int64_t i = key & 0xffffffffll;
+  if (mode < 2) {
+    const int64_t u = M.unit_off + i;
+    const lc_search_desc& S = P.searches[P.u_search[u]];
+    return fmt_cfg_key(out, P.combos[P.u_combo[u]], P.batches[S.b_off + P.u_batch[u]]);
+  }
+  const int64_t slot = M.plan_off + i;
+  const int32_t up = plan_i[slot * 4 + 0], ud = plan_i[slot * 4 + 1];
+  const lc_search_desc& S = P.searches[P.u_search[up]];
+  int n = 0;
+  n += put_str(out + n, "P:"); n += put_int(out + n, plan_i[slot * 4 + 2]); n += put_str(out + n, "x");
+  n += fmt_cfg_key(out + n, P.combos[P.u_combo[up]], P.batches[S.b_off + P.u_batch[up]]);
+  n += put_str(out + n, "|D:"); n += put_int(out + n, plan_i[slot * 4 + 3]); n += put_str(out + n, "x");
+  n += fmt_cfg_key(out + n, P.combos[P.u_combo[ud]], P.batches[S.b_off + P.u_batch[ud]]);
+  return n;
+}
+
+struct BestKey {
+  double nthru, nspeed;
+  int64_t gpus;
+  int mode_rank;  // "aggregated" < "disaggregated" < "static"
+  int64_t key;    // -1 none
+};
+
+__device__ __forceinline__ int mode_rank(int mode) { return mode == 1 ? 0 : (mode == 2 ? 1 : 2); }
+
+__device__ bool best_less(const EvalParams& P, const SearchMeta& M, const int32_t* plan_i, const BestKey& a,
+                          const BestKey& b) {
+  if (a.key < 0) return false;
+  if (b.key < 0) return true;
+  if (a.nthru != b.nthru) return a.nthru < b.nthru;
+  if (a.nspeed != b.nspeed) return a.nspeed < b.nspeed;
+  if (a.gpus != b.gpus) return a.gpus < b.gpus;
+  if (a.mode_rank != b.mode_rank) return a.mode_rank < b.mode_rank;
+  char la[200], lb[200];
+  row_label(P, M, plan_i, a.key, la);
+  row_label(P, M, plan_i, b.key, lb);
+  const int c = str_cmp(la, lb);
+  if (c) return c < 0;
+  return a.key < b.key;
+}
+
+struct MissKey {
+  double viol;
+  int64_t key;
+};
+
+__device__ bool miss_less(const EvalParams& P, const SearchMeta& M, const int32_t* plan_i, const MissKey& a,
+                          const MissKey& b) {
+  if (a.key < 0) return false;
+  if (b.key < 0) return true;
+  if (a.viol != b.viol) return a.viol < b.viol;
+  char la[200], lb[200];
+  row_label(P, M, plan_i, a.key, la);
+  row_label(P, M, plan_i, b.key, lb);
+  const int c = str_cmp(la, lb);
+  if (c) return c < 0;
+  return a.key < b.key;
+}
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double r = -INFINITY;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = fmax(r, red[i]);
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(256) k_front(EvalParams P, const SearchMeta* meta, const int32_t* plan_i,
+                                               const double* plan_d, int64_t* front, lc_search_result* results) {
+  const int s = blockIdx.x;
+  const lc_search_desc& S = P.searches[s];
+  const SearchMeta& M = meta[s];
+  const int64_t nplan = results[s].n_plans;
+  const int64_t nrows_all = 2 * (int64_t)M.n_units + nplan;
+  __shared__ BestKey bred[256];
+  __shared__ MissKey mred[256];
+  __shared__ double dred[32];
+  __shared__ int64_t grp[1024];
+  __shared__ int ngrp, nfront;
+  __shared__ int cnt_feas, cnt_rows, cnt_enum, cnt_skip;
+  if (threadIdx.x == 0) { cnt_feas = cnt_rows = cnt_enum = cnt_skip = 0; nfront = 0; }
+  __syncthreads();
+  // pass 1: counts, best, nearest
+  BestKey best{0, 0, 0, 0, -1};
+  MissKey miss{0, -1};
+  int my_feas = 0, my_rows = 0, my_enum = 0, my_skip = 0;
+  unsigned long long my_q1 = 0, my_q2 = 0;
+  for (int64_t r = threadIdx.x; r < nrows_all; r += blockDim.x) {
+    if (r < M.n_units) {
+      const int64_t u = M.unit_off + r;
+      const int32_t q = P.u_queries[u];
+      my_q1 += (unsigned)(q & 0xffff);
+      my_q2 += (unsigned)(q >> 16);
+      if (P.u_budget[u]) {
+        ++my_enum;
+        if ((S.modes & 1) && P.st_status[u]) ++my_skip;
+        if ((S.modes & 2) && P.ag_status[u]) ++my_skip;
+      }
+      if (S.modes & 4) my_skip += (P.pf_status[u] != 0) + (P.dc_status[u] != 0);
+    }
+    const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+    if (!v.valid) continue;
+    if (v.mode == 0 && !(S.modes & 1)) continue;
+    if (v.mode == 1 && !(S.modes & 2)) continue;
+    ++my_rows;
+    if (feasible(S, v)) {
+      ++my_feas;
+      BestKey k{-v.thru, -v.speed, v.gpus, mode_rank(v.mode), v.key};
+      if (best_less(P, M, plan_i, k, best)) best = k;
+    }
+    double worst = 1.0;
+    if (S.has_ttft && v.ttft > S.ttft_limit) { const double x = v.ttft / S.ttft_limit; if (x > worst) worst = x; }
+    if (S.has_floor && v.speed < S.speed_floor) {
+      const double x = v.speed == 0.0 ? INFINITY : S.speed_floor / v.speed;
+      if (x > worst) worst = x;
+    }
+    MissKey mk{worst, v.key};
+    if (miss_less(P, M, plan_i, mk, miss)) miss = mk;
+  }
+  atomicAdd(&cnt_feas, my_feas); atomicAdd(&cnt_rows, my_rows);
+  atomicAdd(&cnt_enum, my_enum); atomicAdd(&cnt_skip, my_skip);
+  atomicAdd((unsigned long long*)&results[s].queries_1d, my_q1);
+  atomicAdd((unsigned long long*)&results[s].queries_2d, my_q2);
+  bred[threadIdx.x] = best;
+  mred[threadIdx.x] = miss;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      if (best_less(P, M, plan_i, bred[threadIdx.x + w], bred[threadIdx.x])) bred[threadIdx.x] = bred[threadIdx.x + w];
+      if (miss_less(P, M, plan_i, mred[threadIdx.x + w], mred[threadIdx.x])) mred[threadIdx.x] = mred[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    lc_search_result& R = results[s];
+    R.n_enumerated = cnt_enum;
+    R.n_rows = cnt_rows;
+    R.n_feasible = cnt_feas;
+    R.n_skipped = cnt_skip;
+    R.best = bred[0].key;
+    R.best_thru = bred[0].key >= 0 ? -bred[0].nthru : 0.0;
+    R.best_speed = bred[0].key >= 0 ? -bred[0].nspeed : 0.0;
+    R.nearest = bred[0].key >= 0 ? -1 : mred[0].key;
+    R.nearest_violation = bred[0].key >= 0 ? 0.0 : mred[0].viol;
+    R.front_off = (int32_t)(M.unit_off * 2 + M.plan_off);
+  }
+  __syncthreads();
+  // pass 2: staircase (pareto_filter over feasible rows, search.py:156-176)
+  const int64_t foff = (int64_t)M.unit_off * 2 + M.plan_off;
+  double best_thru = -INFINITY;
+  while (true) {
+    double smax = -INFINITY;
+    bool any = false;
+    for (int64_t r = threadIdx.x; r < nrows_all; r += blockDim.x) {
+      const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+      if (!v.valid || !feasible(S, v)) continue;
+      if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
+      if (v.thru > best_thru) { any = true; smax = fmax(smax, v.speed); }
+    }
+    const int any_all = __syncthreads_or(any);
+    if (!any_all) break;
+    const double sp = block_max(any ? smax : -INFINITY, dred);
+    double tmax = -INFINITY;
+    for (int64_t r = threadIdx.x; r < nrows_all; r += blockDim.x) {
+      const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+      if (!v.valid || !feasible(S, v)) continue;
+      if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
+      if (v.speed == sp) tmax = fmax(tmax, v.thru);
+    }
+    const double top = block_max(tmax, dred);
+    if (threadIdx.x == 0) ngrp = 0;
+    __syncthreads();
+    for (int64_t r = threadIdx.x; r < nrows_all; r += blockDim.x) {
+      const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+      if (!v.valid || !feasible(S, v)) continue;
+      if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
+      if (v.speed == sp && v.thru == top) {
+        const int k = atomicAdd(&ngrp, 1);
+        if (k < 1024) grp[k] = v.key;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && ngrp > 1024) {
+      // more ties than the shared buffer holds: ordered sequential scan
+      int m = 0;
+      for (int64_t r = 0; r < nrows_all; ++r) {
+        const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+        if (!v.valid || !feasible(S, v)) continue;
+        if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
+        if (v.speed == sp && v.thru == top) front[foff + nfront + m++] = v.key;
+      }
+      nfront += m;
+    } else if (threadIdx.x == 0) {
+      const int m = ngrp;
+      for (int i = 1; i < m; ++i) {  // row order within the speed group
+        const int64_t x = grp[i];
+        int j = i;
+        while (j > 0 && grp[j - 1] > x) { grp[j] = grp[j - 1]; --j; }
+        grp[j] = x;
+      }
+      for (int i = 0; i < m; ++i) front[foff + nfront + i] = grp[i];
+      nfront += m;
+    }
+    __syncthreads();
+    best_thru = top;
+  }
+  if (threadIdx.x == 0) results[s].n_front = nfront;
+}
+
+}  // namespace
+
+template <class T>
+static int upload(T** dst, const T* src, size_t n, cudaStream_t st) {
+  size_t bytes = n * sizeof(T);
+  CK(cudaMalloc((void**)dst, bytes ? bytes : 16));
+  if (bytes) CK(cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, st));
+  return LC_OK;
+}
+
+// ============================================================================ C ABI
+extern "C" {
+
+int lc_abi_version(void) { return LC_ABI_VERSION; }
+const char* lc_last_error(void) { return g_err.c_str(); }
+
+int lc_open(int device, lc_ctx** out) {
+  if (!out) return fail(LC_ERR_ARG, "lc_open: out is NULL");
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(LC_ERR_ARG, "lc_open: bad device index");
+  CK(cudaSetDevice(device));
+  lc_ctx* c = new lc_ctx();
+  c->device = device;
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  for (auto& e : c->ev) CK(cudaEventCreate(&e));
+  *out = c;
+  return LC_OK;
+}
+
+int lc_close(lc_ctx* c) {
+  if (!c) return LC_OK;
+  cudaSetDevice(c->device);
+  DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
+                  &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
+                  &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
+                  &c->err_c, &c->u_queries, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
+  for (DBuf* b : bufs) b->release();
+  for (auto& e : c->ev) cudaEventDestroy(e);
+  cudaStreamDestroy(c->stream);
+  delete c;
+  return LC_OK;
+}
+
+int lc_db_upload(lc_ctx* c, const lc_db_desc* d, lc_db** out) {
+  if (!c || !d || !out) return fail(LC_ERR_ARG, "lc_db_upload: NULL argument");
+  CK(cudaSetDevice(c->device));
+  lc_db* db = new lc_db();
+  db->device = c->device;
+  db->n_grids = d->n_grids; db->n_axis = d->n_axis; db->n_cells = d->n_cells;
+  std::vector<DevGrid> g(d->n_grids);
+  for (int i = 0; i < d->n_grids; ++i) {
+    g[i].ndim = d->grid_ndim[i];
+    if (g[i].ndim != 1 && g[i].ndim != 2) { delete db; return fail(LC_ERR_ARG, "grid ndim must be 1 or 2"); }
+    for (int a = 0; a < 2; ++a) { g[i].ax_off[a] = d->grid_axis_off[2 * i + a]; g[i].ax_len[a] = d->grid_axis_len[2 * i + a]; }
+    g[i].cell_off = d->grid_cell_off[i];
+  }
+  int rc;
+  if ((rc = upload(&db->grids, g.data(), g.size(), c->stream))) return rc;
+  if ((rc = upload(&db->axv, d->axis_val, d->n_axis, c->stream))) return rc;
+  if ((rc = upload(&db->axl, d->axis_log, d->n_axis, c->stream))) return rc;
+  if ((rc = upload(&db->cell, d->cell, d->n_cells, c->stream))) return rc;
+  if ((rc = upload(&db->clog, d->cell_log, d->n_cells, c->stream))) return rc;
+  if ((rc = upload(&db->logtab, LOG_TAB_H, 256, c->stream))) return rc;
+  if ((rc = upload(&db->exptab, EXP_TAB_H, 256, c->stream))) return rc;
+  db->mem_bw = d->mem_bandwidth; db->intra_bw = d->intra_node_bandwidth; db->inter_bw = d->inter_node_bandwidth;
+  db->gpu_memory = d->gpu_memory;
+  for (int i = 0; i < 4; ++i) db->compute[i] = d->compute[i];
+  db->gpn = d->gpus_per_node; db->policy = d->policy;
+  db->smem_bytes = 256 * 16 + (size_t)d->n_axis * 16 + (size_t)d->n_cells * 16 + (size_t)d->n_grids * sizeof(DevGrid);
+  if (db->smem_bytes > 200 * 1024) { delete db; return fail(LC_ERR_ARG, "database too large for shared-memory staging"); }
+  CK(cudaStreamSynchronize(c->stream));
+  *out = db;
+  return LC_OK;
+}
+
+int lc_db_free(lc_db* db) {
+  if (!db) return LC_OK;
+  cudaSetDevice(db->device);
+  cudaFree(db->grids); cudaFree(db->axv); cudaFree(db->axl); cudaFree(db->cell); cudaFree(db->clog);
+  cudaFree(db->logtab); cudaFree(db->exptab);
+  delete db;
+  return LC_OK;
+}
+
+int lc_space_upload(lc_ctx* c, const lc_space_desc* d, lc_space** out) {
+  if (!c || !d || !out) return fail(LC_ERR_ARG, "lc_space_upload: NULL argument");
+  if (d->n_experts > LC_MAX_EXPERTS) return fail(LC_ERR_ARG, "too many experts");
+  CK(cudaSetDevice(c->device));
+  lc_space* sp = new lc_space();
+  sp->device = c->device;
+  sp->hidden = d->hidden; sp->topk = d->topk; sp->n_experts = d->n_experts; sp->is_moe = d->is_moe;
+  sp->n_combos = d->n_combos; sp->n_tmpl = d->n_tmpl; sp->n_tp = d->n_tp; sp->n_ep = d->n_ep;
+  std::vector<int64_t> tpv(d->n_tp > 0 ? d->n_tp : 1, 1), epv(d->n_ep > 0 ? d->n_ep : 1, 1);
+  std::vector<uint8_t> used((size_t)(d->n_tp > 0 ? d->n_tp : 1) * (d->n_ep > 0 ? d->n_ep : 1), 0);
+  for (int i = 0; i < d->n_combos; ++i) {
+    const lc_combo& k = d->combos[i];
+    if (k.tp_i < 0 || k.tp_i >= d->n_tp || k.ep_i < 0 || k.ep_i >= d->n_ep || k.tmpl < 0 || k.tmpl >= d->n_tmpl)
+      return fail(LC_ERR_ARG, "lc_space_upload: combo index out of range");
+    tpv[k.tp_i] = k.tp; epv[k.ep_i] = k.ep;
+    used[(size_t)k.tp_i * d->n_ep + k.ep_i] = 1;
+  }
+  for (int t = 0; t < d->n_tmpl; ++t)
+    if (d->tmpl_n_entries[t] > LC_MAX_ENTRIES) return fail(LC_ERR_ARG, "template has too many entries");
+  int rc;
+  if ((rc = upload(&sp->combos, d->combos, d->n_combos, c->stream))) return rc;
+  if ((rc = upload(&sp->tmpl_n, d->tmpl_n_entries, d->n_tmpl, c->stream))) return rc;
+  if ((rc = upload(&sp->entries, d->entries, (size_t)d->n_tmpl * LC_MAX_ENTRIES, c->stream))) return rc;
+  if ((rc = upload(&sp->tp_vals, tpv.data(), tpv.size(), c->stream))) return rc;
+  if ((rc = upload(&sp->ep_vals, epv.data(), epv.size(), c->stream))) return rc;
+  if ((rc = upload(&sp->pair_used, used.data(), used.size(), c->stream))) return rc;
+  CK(cudaStreamSynchronize(c->stream));
+  *out = sp;
+  return LC_OK;
+}
+
+int lc_space_free(lc_space* sp) {
+  if (!sp) return LC_OK;
+  cudaSetDevice(sp->device);
+  cudaFree(sp->combos); cudaFree(sp->tmpl_n); cudaFree(sp->entries); cudaFree(sp->tp_vals); cudaFree(sp->ep_vals);
+  cudaFree(sp->pair_used);
+  delete sp;
+  return LC_OK;
+}
+
+static EvalParams make_params(lc_ctx* c) {
+  EvalParams P;
+  memset(&P, 0, sizeof(P));
+  const lc_db* db = c->db;
+  const lc_space* sp = c->sp;
+  P.grids = db->grids; P.axv = db->axv; P.axl = db->axl; P.cell = db->cell; P.clog = db->clog;
+  P.logtab = db->logtab; P.exptab = db->exptab;
+  P.n_grids = db->n_grids; P.n_axis = db->n_axis; P.n_cells = db->n_cells;
+  P.mem_bw = db->mem_bw; P.intra_bw = db->intra_bw; P.inter_bw = db->inter_bw; P.gpu_memory = db->gpu_memory;
+  for (int i = 0; i < 4; ++i) P.compute[i] = db->compute[i];
+  P.gpn = db->gpn; P.policy = db->policy;
+  P.combos = sp->combos; P.tmpl_n = sp->tmpl_n; P.entries = sp->entries;
+  P.hidden = sp->hidden; P.topk = sp->topk; P.n_experts = sp->n_experts; P.is_moe = sp->is_moe;
+  P.n_tp = sp->n_tp; P.n_ep = sp->n_ep; P.tp_vals = sp->tp_vals; P.ep_vals = sp->ep_vals; P.pair_used = sp->pair_used;
+  P.searches = (const lc_search_desc*)c->searches.p;
+  P.meta = (const SearchMeta*)c->meta.p;
+  P.n_search = c->n_search;
+  P.batches = (const int64_t*)c->batches.p;
+  P.loads = (const double*)c->loads.p;
+  P.u_search = (const int32_t*)c->u_search.p; P.u_combo = (const int32_t*)c->u_combo.p;
+  P.u_batch = (const int32_t*)c->u_batch.p; P.u_budget = (const uint8_t*)c->u_budget.p;
+  P.n_units = c->n_units;
+  P.tails = (const int64_t*)c->tails.p;
+  P.st_status = (int32_t*)c->st_status.p; P.st_v = (double*)c->st_v.p;
+  P.ag_status = (int32_t*)c->ag_status.p; P.ag_v = (double*)c->ag_v.p;
+  P.pf_status = (int32_t*)c->pf_status.p; P.pf_v = (double*)c->pf_v.p;
+  P.dc_status = (int32_t*)c->dc_status.p; P.dc_v = (double*)c->dc_v.p;
+  P.err_c = (int64_t*)c->err_c.p;
+  P.u_queries = (int32_t*)c->u_queries.p;
+  P.results = (lc_search_result*)c->results.p;
+  return P;
+}
+
+static int sm_count(int dev) {
+  static int cached[64] = {0};
+  if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (dev >= 0 && dev < 64) cached[dev] = n;
+  return n;
+}
+
+// Everything after the unit list is known: K3, K2, K5a, K5b, K4.
+static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
+  cudaError_t err = cudaSuccess;
+  const int64_t n = c->n_units;
+  // outputs: zero statuses to LC_ST_NOT_EVALUATED semantics by memset to 0 then K2 writes
+  c->st_status.get<int32_t>(n, &err); c->st_v.get<double>(4 * n, &err);
+  c->ag_status.get<int32_t>(n, &err); c->ag_v.get<double>(4 * n, &err);
+  c->pf_status.get<int32_t>(n, &err); c->pf_v.get<double>(2 * n, &err);
+  c->dc_status.get<int32_t>(n, &err); c->dc_v.get<double>(2 * n, &err);
+  c->err_c.get<int64_t>(8 * n, &err);
+  c->u_queries.get<int32_t>(n, &err);
+  c->pool_sel.get<int32_t>((size_t)c->n_search * 128, &err);
+  c->plans_i.get<int32_t>((size_t)c->n_plan_slots * 4, &err);
+  c->plans_d.get<double>((size_t)c->n_plan_slots * 6, &err);
+  c->front.get<int64_t>((size_t)c->n_front_slots, &err);
+  c->tails.get<int64_t>((size_t)(c->n_tails > 0 ? c->n_tails : 1), &err);
+  if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
+  CK(cudaMemsetAsync(c->st_status.p, 0, n * 4, c->stream));
+  CK(cudaMemsetAsync(c->ag_status.p, 0, n * 4, c->stream));
+  CK(cudaMemsetAsync(c->pf_status.p, 0, n * 4, c->stream));
+  CK(cudaMemsetAsync(c->dc_status.p, 0, n * 4, c->stream));
+  // reset per-search result accumulators
+  CK(cudaMemsetAsync(c->results.p, 0, sizeof(lc_search_result) * c->n_search, c->stream));
+  EvalParams P = make_params(c);
+  const int sms = sm_count(c->device);
+  CK(cudaEventRecord(c->ev[1], c->stream));
+  if (c->n_tails > 0) {
+    const int64_t warps = c->n_tails;
+    int blocks = (int)((warps + 7) / 8);
+    if (blocks > sms * 16) blocks = sms * 16;
+    k_tails<<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
+    CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(c->ev[2], c->stream));
+  if (n > 0) {
+    const size_t smem = c->db->smem_bytes;
+    CK(cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval, 128, smem));
+    if (per_sm < 1) per_sm = 1;
+    int64_t blocks = (n + 127) / 128;
+    const int64_t cap = (int64_t)sms * per_sm;
+    if (blocks > cap) blocks = cap;
+    k_eval<<<(int)blocks, 128, smem, c->stream>>>(P);
+    CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(c->ev[3], c->stream));
+  k_pools<<<c->n_search, 256, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, (int32_t*)c->pool_sel.p);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev[4], c->stream));
+  k_disagg<<<c->n_search, 256, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, (const int32_t*)c->pool_sel.p,
+                                                (int32_t*)c->plans_i.p, (double*)c->plans_d.p,
+                                                (lc_search_result*)c->results.p);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev[5], c->stream));
+  k_front<<<c->n_search, 256, 0, c->stream>>>(P, (const SearchMeta*)c->meta.p, (const int32_t*)c->plans_i.p,
+                                               (const double*)c->plans_d.p, (int64_t*)c->front.p,
+                                               (lc_search_result*)c->results.p);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev[6], c->stream));
+  (void)totals;
+  return LC_OK;
+}
+
+static int run_enum(lc_ctx* c) {
+  cudaError_t err = cudaSuccess;
+  const int64_t n_raw = c->n_raw;
+  const int64_t nblk = (n_raw + kScanBlock - 1) / kScanBlock;
+  uint8_t* flags = c->flags.get<uint8_t>(n_raw, &err);
+  int32_t* pos = c->pos.get<int32_t>(n_raw, &err);
+  int32_t* bs = c->block_sums.get<int32_t>(nblk + 1, &err);
+  if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
+  EvalParams P = make_params(c);
+  const int sms = sm_count(c->device);
+  if (n_raw > 0) {
+    int blocks = (int)((n_raw + 255) / 256);
+    if (blocks > sms * 32) blocks = sms * 32;
+    k_enum_flags<<<blocks, 256, 0, c->stream>>>(P, n_raw, flags);
+    k_scan_blocks<<<(int)nblk, kScanBlock, 0, c->stream>>>(flags, n_raw, bs);
+    k_scan_top<<<1, 1024, 0, c->stream>>>(bs, (int)nblk);
+    CK(cudaGetLastError());
+  } else {
+    CK(cudaMemsetAsync(bs, 0, sizeof(int32_t), c->stream));
+  }
+  int32_t total = 0;
+  CK(cudaMemcpyAsync(&total, bs + nblk, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  c->n_units = total;
+  int32_t* us = c->u_search.get<int32_t>(total, &err);
+  int32_t* uc = c->u_combo.get<int32_t>(total, &err);
+  int32_t* ub = c->u_batch.get<int32_t>(total, &err);
+  uint8_t* ubud = c->u_budget.get<uint8_t>(total, &err);
+  if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
+  if (n_raw > 0) {
+    k_scatter<<<(int)nblk, kScanBlock, 0, c->stream>>>(P, flags, n_raw, bs, pos, us, uc, ub, ubud);
+    CK(cudaGetLastError());
+  }
+  k_unit_offsets<<<(c->n_search + 127) / 128, 128, 0, c->stream>>>((SearchMeta*)c->meta.p, c->n_search, pos, n_raw,
+                                                                   total);
+  CK(cudaGetLastError());
+  return LC_OK;
+}
+
+int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_search,
+                    const lc_search_desc* searches, int32_t n_batches, const int64_t* batches, int32_t n_loads,
+                    const double* loads, lc_search_result* results, lc_batch_totals* totals) {
+  if (!c || !db || !sp || (n_search > 0 && !searches) || n_search < 0)
+    return fail(LC_ERR_ARG, "lc_search_batch: bad arguments");
+  CK(cudaSetDevice(c->device));
+  c->db = db;
+  c->sp = sp;
+  c->n_search = n_search;
+  c->n_batches = n_batches;
+  c->n_loads = n_loads;
+  // host bookkeeping: raw tuple, tail and plan offsets
+  c->hmeta.assign(n_search, SearchMeta{});
+  int64_t raw = 0, tails = 0, plans = 0;
+  for (int s = 0; s < n_search; ++s) {
+    const lc_search_desc& S = searches[s];
+    if (S.n_b < 0 || S.b_off < 0 || S.b_off + S.n_b > n_batches) return fail(LC_ERR_ARG, "batch range out of bounds");
+    if (S.n_budgets < 0 || S.n_budgets > LC_MAX_BUDGETS) return fail(LC_ERR_ARG, "too many gpu budgets");
+    if (S.load >= n_loads) return fail(LC_ERR_ARG, "load index out of range");
+    if (S.prefill_cap > 64 || S.decode_cap > 64) return fail(LC_ERR_ARG, "pool caps above 64 are not supported");
+    SearchMeta& M = c->hmeta[s];
+    M.raw_off = raw;
+    M.n_raw = (int64_t)sp->n_combos * S.n_b;
+    raw += M.n_raw;
+    M.tail_off = tails;
+    if (sp->is_moe) tails += 3ll * sp->n_tp * sp->n_ep * S.n_b;
+    M.plan_off = (int32_t)plans;
+    const int pc = (S.modes & 4) ? S.prefill_cap * S.decode_cap : 0;
+    if (pc > 256) return fail(LC_ERR_ARG, "prefill_cap * decode_cap above 256 is not supported");
+    M.plan_cap = pc;
+    plans += pc;
+  }
+  c->n_raw = raw;
+  c->n_tails = tails;
+  c->n_plan_slots = plans;
+  cudaError_t err = cudaSuccess;
+  lc_search_desc* dS = c->searches.get<lc_search_desc>(n_search, &err);
+  int64_t* dB = c->batches.get<int64_t>(n_batches, &err);
+  double* dL = c->loads.get<double>((size_t)n_loads * 2 * (sp->n_experts > 0 ? sp->n_experts : 1), &err);
+  SearchMeta* dM = c->meta.get<SearchMeta>(n_search, &err);
+  c->results.get<lc_search_result>(n_search, &err);
+  if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
+  CK(cudaEventRecord(c->ev[0], c->stream));
+  if (n_search) CK(cudaMemcpyAsync(dS, searches, sizeof(lc_search_desc) * n_search, cudaMemcpyHostToDevice, c->stream));
+  if (n_batches) CK(cudaMemcpyAsync(dB, batches, sizeof(int64_t) * n_batches, cudaMemcpyHostToDevice, c->stream));
+  if (n_loads && sp->n_experts)
+    CK(cudaMemcpyAsync(dL, loads, sizeof(double) * n_loads * 2 * sp->n_experts, cudaMemcpyHostToDevice, c->stream));
+  if (n_search)
+    CK(cudaMemcpyAsync(dM, c->hmeta.data(), sizeof(SearchMeta) * n_search, cudaMemcpyHostToDevice, c->stream));
+  int rc = run_enum(c);
+  if (rc) return rc;
+  c->n_front_slots = 2 * c->n_units + c->n_plan_slots;
+  rc = run_eval_pipeline(c, totals);
+  if (rc) return rc;
+  c->hres.resize(n_search);
+  if (n_search)
+    CK(cudaMemcpyAsync(c->hres.data(), c->results.p, sizeof(lc_search_result) * n_search, cudaMemcpyDeviceToHost,
+                       c->stream));
+  if (n_search)
+    CK(cudaMemcpyAsync(c->hmeta.data(), c->meta.p, sizeof(SearchMeta) * n_search, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  int64_t nfront = 0, nplan = 0;
+  for (int s = 0; s < n_search; ++s) {
+    lc_search_result& R = c->hres[s];
+    R.unit_off = c->hmeta[s].unit_off;
+    R.n_units = c->hmeta[s].n_units;
+    R.plan_off = c->hmeta[s].plan_off;
+    nfront += R.n_front;
+    nplan += R.n_plans;
+  }
+  if (results && n_search) memcpy(results, c->hres.data(), sizeof(lc_search_result) * n_search);
+  if (totals) {
+    memset(totals, 0, sizeof(*totals));
+    totals->n_units = c->n_units;
+    totals->n_plans = nplan;
+    totals->n_front = nfront;
+    totals->n_raw = c->n_raw;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]); totals->kernel_ms[0] = ms;
+    cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]); totals->kernel_ms[1] = ms;
+    cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]); totals->kernel_ms[2] = ms;
+    cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]); totals->kernel_ms[3] = ms;
+    cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]); totals->kernel_ms[4] = ms;
+    cudaEventElapsedTime(&ms, c->ev[5], c->ev[6]); totals->kernel_ms[5] = ms;
+  }
+  return LC_OK;
+}
+
+int lc_replay_last(lc_ctx* c, int32_t iters, lc_batch_totals* totals) {
+  if (!c || !c->db || iters < 1) return fail(LC_ERR_STATE, "lc_replay_last: no previous batch");
+  CK(cudaSetDevice(c->device));
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int it = 0; it < iters; ++it) {
+    // restore the host-side meta (pool counts are rewritten by K5a)
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    int rc = run_eval_pipeline(c, totals);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0;
+    for (int k = 0; k < 6; ++k) {
+      if (k == 0) ms = 0;
+      else cudaEventElapsedTime(&ms, c->ev[k], c->ev[k + 1]);
+      acc[k] += ms;
+    }
+  }
+  if (totals) {
+    for (int k = 0; k < 6; ++k) totals->kernel_ms[k] = (float)(acc[k] / iters);
+    totals->n_units = c->n_units;
+    totals->n_raw = c->n_raw;
+  }
+  return LC_OK;
+}
+
+int lc_fetch(lc_ctx* c, const lc_fetch_req* r) {
+  if (!c || !r) return fail(LC_ERR_ARG, "lc_fetch: NULL argument");
+  CK(cudaSetDevice(c->device));
+  const int64_t n = c->n_units;
+  auto cp = [&](void* dst, const void* src, size_t bytes) -> int {
+    if (!dst || !bytes) return LC_OK;
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+    return LC_OK;
+  };
+  int rc = 0;
+  rc |= cp(r->unit_search, c->u_search.p, n * 4);
+  rc |= cp(r->unit_combo, c->u_combo.p, n * 4);
+  rc |= cp(r->unit_batch, c->u_batch.p, n * 4);
+  rc |= cp(r->unit_in_budget, c->u_budget.p, n);
+  rc |= cp(r->st_status, c->st_status.p, n * 4);
+  rc |= cp(r->ag_status, c->ag_status.p, n * 4);
+  rc |= cp(r->pf_status, c->pf_status.p, n * 4);
+  rc |= cp(r->dc_status, c->dc_status.p, n * 4);
+  const double* stv = (const double*)c->st_v.p;
+  const double* agv = (const double*)c->ag_v.p;
+  const double* pfv = (const double*)c->pf_v.p;
+  const double* dcv = (const double*)c->dc_v.p;
+  rc |= cp(r->st_ttft, stv, n * 8); rc |= cp(r->st_tpot, stv + n, n * 8);
+  rc |= cp(r->st_speed, stv + 2 * n, n * 8); rc |= cp(r->st_thru, stv + 3 * n, n * 8);
+  rc |= cp(r->ag_ttft, agv, n * 8); rc |= cp(r->ag_tpot, agv + n, n * 8);
+  rc |= cp(r->ag_speed, agv + 2 * n, n * 8); rc |= cp(r->ag_thru, agv + 3 * n, n * 8);
+  rc |= cp(r->pf_lat, pfv, n * 8); rc |= cp(r->pf_rate, pfv + n, n * 8);
+  rc |= cp(r->dc_lat, dcv, n * 8); rc |= cp(r->dc_rate, dcv + n, n * 8);
+  if (r->err_c0 || r->err_c1) {
+    std::vector<int64_t> e(8 * n);
+    if (n) CK(cudaMemcpyAsync(e.data(), c->err_c.p, 8 * n * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int k = 0; k < 4; ++k)
+      for (int64_t u = 0; u < n; ++u) {
+        if (r->err_c0) r->err_c0[4 * u + k] = e[(2 * k) * n + u];
+        if (r->err_c1) r->err_c1[4 * u + k] = e[(2 * k + 1) * n + u];
+      }
+  }
+  // plans and fronts are copied compactly per search
+  std::vector<int32_t> pi;
+  std::vector<double> pd;
+  if (c->n_plan_slots && (r->plan_p || r->plan_d || r->plan_x || r->plan_y || r->plan_gpus || r->plan_r_sys ||
+                          r->plan_ttft || r->plan_tpot || r->plan_speed || r->plan_thru)) {
+    pi.resize(c->n_plan_slots * 4);
+    pd.resize(c->n_plan_slots * 6);
+    CK(cudaMemcpyAsync(pi.data(), c->plans_i.p, pi.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(pd.data(), c->plans_d.p, pd.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    int64_t k = 0;
+    for (int s = 0; s < c->n_search; ++s) {
+      const lc_search_result& R = c->hres[s];
+      for (int j = 0; j < R.n_plans; ++j, ++k) {
+        const int64_t slot = R.plan_off + j;
+        if (r->plan_p) r->plan_p[k] = pi[slot * 4 + 0];
+        if (r->plan_d) r->plan_d[k] = pi[slot * 4 + 1];
+        if (r->plan_x) r->plan_x[k] = pi[slot * 4 + 2];
+        if (r->plan_y) r->plan_y[k] = pi[slot * 4 + 3];
+        if (r->plan_gpus) r->plan_gpus[k] = (int64_t)pd[slot * 6 + 0];
+        if (r->plan_r_sys) r->plan_r_sys[k] = pd[slot * 6 + 1];
+        if (r->plan_ttft) r->plan_ttft[k] = pd[slot * 6 + 2];
+        if (r->plan_tpot) r->plan_tpot[k] = pd[slot * 6 + 3];
+        if (r->plan_speed) r->plan_speed[k] = pd[slot * 6 + 4];
+        if (r->plan_thru) r->plan_thru[k] = pd[slot * 6 + 5];
+      }
+    }
+  }
+  if (r->front) {
+    int64_t k = 0;
+    for (int s = 0; s < c->n_search; ++s) {
+      const lc_search_result& R = c->hres[s];
+      if (R.n_front)
+        CK(cudaMemcpyAsync(r->front + k, (const int64_t*)c->front.p + R.front_off, R.n_front * 8,
+                           cudaMemcpyDeviceToHost, c->stream));
+      k += R.n_front;
+    }
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return rc ? LC_ERR_CUDA : LC_OK;
+}
+
+}  // extern "C"

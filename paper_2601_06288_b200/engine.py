@@ -1,0 +1,384 @@
+"""The drop-in search seam on the CUDA engine.
+
+``run_search`` keeps the reference signature and results
+(/root/reference/pkg/src/llmconf/search.py:280-358): it flattens the database
+(once per object), compiles the model x space plan (once per triple), hands one
+search descriptor to ``lc_search_batch`` and materialises the reference's
+``SearchReport`` from the device's per-unit arrays.  ``Engine.sweep`` is the
+columnar path for very large batches of searches: only per-search summaries
+and Pareto fronts come back.
+
+Inputs may be this package's spec objects or the reference's own; only
+attributes are read.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+import time
+import weakref
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .database import FlatDb, flatten
+from .plans import LABELS, SpacePlan, build_space_plan
+from .report import DisaggPlan, PerfEstimate, PoolCandidate, SearchReport, estimate_row, plan_row
+from .specs import (
+    DEFAULT_DISAGG,
+    DEFAULT_MOE_LOAD,
+    CandidateSpace,
+    ParallelConfig,
+    SearchError,
+)
+
+MODE_STATIC, MODE_AGG, MODE_DISAGG = 1, 2, 4
+ST_OK, ST_MISSING, ST_EXTRAP, ST_UNSUPPORTED, ST_CHUNK_OFF, ST_NO_SLOT = range(6)
+
+
+def _moe_q(params, num_experts: int) -> np.ndarray:
+    """[q_i = w_i / sum(w)] + by-weight order, numpy exactly as moe_load.py:51-57, 84, 97."""
+    rng = np.random.default_rng(params.seed)
+    u = rng.random(num_experts)
+    e = 1.0 - params.alpha
+    x = (u * (params.x_max**e - params.x_min**e) + params.x_min**e) ** (1.0 / e)
+    w = np.array(tuple(float(v) for v in x))
+    q = w / w.sum()
+    order = np.lexsort((np.arange(num_experts), -w)).astype(np.float64)
+    return np.concatenate([q, order])
+
+
+@dataclass
+class BatchOutput:
+    """Device results of one lc_search_batch call (summaries on host, the rest on demand)."""
+
+    engine: "Engine"
+    results: np.ndarray           # SEARCH_RESULT_DTYPE per search
+    totals: N.LcBatchTotals
+    plan: SpacePlan
+    flat: FlatDb
+    batches: np.ndarray
+    searches: np.ndarray
+    wall_ms: float
+    units: dict = field(default_factory=dict)
+
+    def fetch_units(self) -> dict:
+        if self.units:
+            return self.units
+        n = int(self.totals.n_units)
+        nplan = int(self.totals.n_plans)
+        nfront = int(self.totals.n_front)
+        out = {}
+        req = N.LcFetchReq()
+        spec = {"unit_search": np.int32, "unit_combo": np.int32, "unit_batch": np.int32, "unit_in_budget": np.uint8,
+                "st_status": np.int32, "st_ttft": np.float64, "st_tpot": np.float64, "st_speed": np.float64,
+                "st_thru": np.float64, "ag_status": np.int32, "ag_ttft": np.float64, "ag_tpot": np.float64,
+                "ag_speed": np.float64, "ag_thru": np.float64, "pf_status": np.int32, "pf_lat": np.float64,
+                "pf_rate": np.float64, "dc_status": np.int32, "dc_lat": np.float64, "dc_rate": np.float64}
+        for name, dt in spec.items():
+            out[name] = np.zeros(max(n, 1), dtype=dt)
+        out["err_c0"] = np.zeros(max(4 * n, 1), dtype=np.int64)
+        out["err_c1"] = np.zeros(max(4 * n, 1), dtype=np.int64)
+        pspec = {"plan_p": np.int32, "plan_d": np.int32, "plan_x": np.int32, "plan_y": np.int32,
+                 "plan_gpus": np.int64, "plan_r_sys": np.float64, "plan_ttft": np.float64,
+                 "plan_tpot": np.float64, "plan_speed": np.float64, "plan_thru": np.float64}
+        for name, dt in pspec.items():
+            out[name] = np.zeros(max(nplan, 1), dtype=dt)
+        out["front"] = np.zeros(max(nfront, 1), dtype=np.int64)
+        for name, ctype in N._FETCH_FIELDS:
+            setattr(req, name, N.ptr(out[name], ctype._type_))
+        self.engine._call(self.engine.lib.lc_fetch, "lc_fetch", self.engine.ctx, C.byref(req))
+        self.units = out
+        return out
+
+
+class Engine:
+    """One CUDA context (device + stream + workspace) with DB / plan handle caches."""
+
+    def __init__(self, device: int = 0):
+        self.lib = N.load_library()
+        self.device = device
+        ctx = C.c_void_p()
+        N.check(self.lib.lc_open(device, C.byref(ctx)), "lc_open")
+        self.ctx = ctx
+        self._dbs: dict[int, tuple] = {}
+        self._spaces: dict[tuple, tuple] = {}
+        self._lock = threading.Lock()
+
+    def _call(self, fn, name, *args):
+        N.check(fn(*args), name)
+
+    def close(self) -> None:
+        for h, _, _ in self._spaces.values():
+            self.lib.lc_space_free(h)
+        for h, _, _ in self._dbs.values():
+            self.lib.lc_db_free(h)
+        self._spaces.clear()
+        self._dbs.clear()
+        if self.ctx:
+            self.lib.lc_close(self.ctx)
+            self.ctx = None
+
+    # ------------------------------------------------------------------ handles
+    def db_handle(self, db) -> tuple[C.c_void_p, FlatDb]:
+        hit = self._dbs.get(id(db))
+        if hit is not None and hit[2]() is db:
+            return hit[0], hit[1]
+        flat = flatten(db)
+        hw = db.hardware
+        d = N.LcDbDesc()
+        d.n_grids = len(flat.keys)
+        d.grid_ndim = N.ptr(flat.grid_ndim, C.c_int32)
+        d.grid_axis_off = N.ptr(flat.grid_axis_off, C.c_int32)
+        d.grid_axis_len = N.ptr(flat.grid_axis_len, C.c_int32)
+        d.grid_cell_off = N.ptr(flat.grid_cell_off, C.c_int32)
+        d.n_axis = len(flat.axis_val)
+        d.axis_val = N.ptr(flat.axis_val, C.c_int64)
+        d.axis_log = N.ptr(flat.axis_log, C.c_double)
+        d.n_cells = len(flat.cell)
+        d.cell = N.ptr(flat.cell, C.c_double)
+        d.cell_log = N.ptr(flat.cell_log, C.c_double)
+        d.mem_bandwidth = float(hw.mem_bandwidth)
+        d.intra_node_bandwidth = float(hw.intra_node_bandwidth)
+        d.inter_node_bandwidth = float(hw.inter_node_bandwidth)
+        d.gpu_memory = float(hw.gpu_memory)
+        d.gpus_per_node = int(hw.gpus_per_node)
+        for i, q in enumerate(("fp16", "fp8", "int8", "int4")):
+            d.compute[i] = float(hw.compute_throughput.get(q, 0.0))
+        d.policy = flat.policy
+        h = C.c_void_p()
+        self._call(self.lib.lc_db_upload, "lc_db_upload", self.ctx, C.byref(d), C.byref(h))
+        self._dbs[id(db)] = (h, flat, weakref.ref(db))
+        return h, flat
+
+    def space_handle(self, db, model, space) -> tuple[C.c_void_p, SpacePlan, FlatDb]:
+        dbh, flat = self.db_handle(db)
+        key = (id(db), model, space)
+        hit = self._spaces.get(key)
+        if hit is not None and hit[2]() is db:
+            return hit[0], hit[1], flat
+        plan = build_space_plan(model, space, flat, db.backend)
+        d = N.LcSpaceDesc()
+        d.hidden, d.topk, d.n_experts, d.is_moe = plan.hidden, plan.topk, plan.n_experts, int(plan.is_moe)
+        d.n_combos = len(plan.combos)
+        d.combos = N.vptr(plan.combos) if len(plan.combos) else None
+        d.n_tmpl = len(plan.infos)
+        d.tmpl_n_entries = N.ptr(plan.tmpl_n, C.c_int32)
+        d.entries = N.vptr(plan.entries)
+        d.n_tp, d.n_ep = len(plan.tp_values), len(plan.ep_values)
+        h = C.c_void_p()
+        self._call(self.lib.lc_space_upload, "lc_space_upload", self.ctx, C.byref(d), C.byref(h))
+        self._spaces[key] = (h, plan, weakref.ref(db))
+        return h, plan, flat
+
+    # ------------------------------------------------------------------ batches
+    def run_batch(self, db, model, space, workloads: Sequence, disagg=DEFAULT_DISAGG, mode_override=None,
+                  enforce_budget: bool = True) -> BatchOutput:
+        t0 = time.perf_counter()
+        sph, plan, flat = self.space_handle(db, model, space)
+        dbh, _ = self.db_handle(db)
+        n = len(workloads)
+        searches = np.zeros(n, dtype=N.SEARCH_DESC_DTYPE)
+        batches: list[int] = []
+        loads: list[np.ndarray] = []
+        load_ix: dict = {}
+        if space.prefill_pool_cap < 0 or space.decode_pool_cap < 0:
+            raise SearchError("pool caps must be >= 0")
+        for i, w in enumerate(workloads):
+            s = searches[i]
+            s["isl"], s["osl"], s["prefix"] = w.isl, w.osl, w.prefix_len
+            if w.ttft_limit_ms is not None:
+                s["has_ttft"], s["ttft_limit"] = 1, float(w.ttft_limit_ms)
+            floor = w.speed_floor()
+            if floor is not None:
+                s["has_floor"], s["speed_floor"] = 1, float(floor)
+                s["tpot_cap"] = float(w.tpot_ceiling())
+            if mode_override is not None:
+                modes = mode_override
+            else:
+                modes = ((MODE_STATIC if "static" in w.modes else 0) | (MODE_AGG if "aggregated" in w.modes else 0)
+                         | (MODE_DISAGG if "disaggregated" in w.modes else 0))
+            s["modes"] = modes
+            budgets = sorted(set(w.gpu_budgets)) if enforce_budget else []
+            if len(budgets) > N.LC_MAX_BUDGETS:
+                raise SearchError(f"at most {N.LC_MAX_BUDGETS} distinct gpu budgets are supported")
+            s["n_budgets"] = len(budgets)
+            s["budgets"][: len(budgets)] = budgets
+            bs = sorted(w.batch_sweep or space.batch_values)
+            s["b_off"], s["n_b"] = len(batches), len(bs)
+            batches.extend(bs)
+            s["has_ctx_capacity"] = space.ctx_capacity is not None
+            s["ctx_capacity"] = space.ctx_capacity or 0
+            s["chunked_prefill"] = int(bool(space.chunked_prefill))
+            s["kv_mem_fraction"] = float(space.kv_mem_fraction)
+            s["prefill_cap"], s["decode_cap"] = space.prefill_pool_cap, space.decode_pool_cap
+            s["ttft_headroom"] = float(disagg.ttft_headroom)
+            s["prefill_util"] = float(disagg.prefill_utilization)
+            s["decode_util"] = float(disagg.decode_utilization)
+            s["max_x"], s["max_y"] = disagg.max_prefill_replicas, disagg.max_decode_replicas
+            s["load"] = -1
+            if plan.is_moe:
+                params = w.moe_load if w.moe_load is not None else DEFAULT_MOE_LOAD
+                lk = (params.alpha, params.x_min, params.x_max, params.seed)
+                if lk not in load_ix:
+                    load_ix[lk] = len(loads)
+                    loads.append(_moe_q(params, plan.n_experts))
+                s["load"] = load_ix[lk]
+        b_arr = np.array(batches if batches else [1], dtype=np.int64)
+        l_arr = np.concatenate(loads) if loads else np.zeros(1)
+        results = np.zeros(n, dtype=N.SEARCH_RESULT_DTYPE)
+        totals = N.LcBatchTotals()
+        self._call(self.lib.lc_search_batch, "lc_search_batch", self.ctx, dbh, sph, n, N.vptr(searches),
+                   len(batches), N.ptr(b_arr, C.c_int64), len(loads), N.ptr(l_arr, C.c_double),
+                   N.vptr(results), C.byref(totals))
+        return BatchOutput(self, results, totals, plan, flat, b_arr, searches,
+                           (time.perf_counter() - t0) * 1000.0)
+
+
+# ------------------------------------------------------------------------------ report building
+def _reason(code_word: int, c0: int, c1: int, plan: SpacePlan, combo, flat: FlatDb, db, workload, space,
+            batch: int) -> str:
+    code, label = code_word & 0xFF, code_word >> 8
+    if code in (ST_MISSING, ST_EXTRAP, ST_UNSUPPORTED):
+        info = next(e for e in plan.infos[int(combo["tmpl"])] if e.label == LABELS[label])
+        if code == ST_MISSING:
+            return f"MissingKeyError: no grid for key {info.key}; database covers kinds {flat.kinds}"
+        if code == ST_UNSUPPORTED:
+            return (f"UnsupportedOperatorError: hardware {db.hardware.name!r} has no compute rate for quant "
+                    f"{info.quant!r}")
+        axes = flat.axes[info.grid]
+        values = flat.axis_values[info.grid]
+        coords = (c0, c1)[: len(axes)]
+        box = {a: (v[0], v[-1]) for a, v in zip(axes, values)}
+        return f"ExtrapolationError: query coords {dict(zip(axes, coords))} outside grid box {box}"
+    chunk_total = workload.isl - workload.prefix_len
+    c_ctx = space.ctx_capacity if space.ctx_capacity is not None else max(chunk_total, 2048)
+    if code == ST_CHUNK_OFF:
+        return f"InfeasibleConfigError: context of {chunk_total} tokens exceeds capacity {c_ctx} and chunking is off"
+    if code == ST_NO_SLOT:
+        prefilling = math.ceil(c_ctx / chunk_total)
+        return f"InfeasibleConfigError: batch {batch} too small to decode alongside {prefilling} prefilling requests"
+    raise SearchError(f"unknown device status {code_word}")
+
+
+def build_report(out: BatchOutput, si: int, db, model, workload, space, wall_ms: float) -> SearchReport:
+    """Materialise the reference SearchReport of search ``si`` from device arrays."""
+    U = out.fetch_units()
+    R = out.results[si]
+    plan, flat = out.plan, out.flat
+    off, n = int(R["unit_off"]), int(R["n_units"])
+    sl = slice(off, off + n)
+    combos = plan.combos[U["unit_combo"][sl]]
+    bidx = U["unit_batch"][sl]
+    s = out.searches[si]
+    batches = out.batches[int(s["b_off"]) + bidx]
+    inb = U["unit_in_budget"][sl].astype(bool)
+    modes = int(s["modes"])
+    cfgs = [space.config(int(c["tp"]), int(c["pp"]), int(c["ep"]), int(c["dp"]), int(b), db.backend)
+            for c, b in zip(combos, batches)]
+    by_key: dict[int, object] = {}
+    rows, skipped = [], []
+    err0, err1 = U["err_c0"], U["err_c1"]
+
+    def add_mode(mode_bit, mode_idx, name, prefix):
+        if not modes & mode_bit:
+            return
+        st = U[f"{prefix}_status"][sl]
+        ttft, tpot, speed, thru = (U[f"{prefix}_{k}"][sl] for k in ("ttft", "tpot", "speed", "thru"))
+        for i in np.nonzero(inb)[0]:
+            i = int(i)
+            cfg = cfgs[i]
+            if st[i] == 0:
+                est = PerfEstimate(name, model.name, cfg, float(ttft[i]), float(tpot[i]), float(speed[i]),
+                                   float(thru[i]), cfg.gpus(), cfg.batch)
+                row = estimate_row(est)
+                rows.append(row)
+                by_key[(mode_idx << 32) | i] = row
+            else:
+                k = 4 * (off + i) + mode_idx
+                skipped.append({"mode": name, "config": cfg.key(),
+                                "reason": _reason(int(st[i]), int(err0[k]), int(err1[k]), plan, combos[i], flat, db,
+                                                  workload, space, cfg.batch)})
+
+    add_mode(MODE_STATIC, 0, "static", "st")
+    add_mode(MODE_AGG, 1, "aggregated", "ag")
+    n_tasks = (int(np.count_nonzero(inb)) * (bool(modes & MODE_STATIC) + bool(modes & MODE_AGG)))
+    if modes & MODE_DISAGG:
+        n_tasks += 2 * n
+        pf_st, dc_st = U["pf_status"][sl], U["dc_status"][sl]
+        for i in range(n):
+            for kind, st, name in ((2, pf_st, "disaggregated/prefill"), (3, dc_st, "disaggregated/decode")):
+                if st[i] != 0:
+                    k = 4 * (off + i) + kind
+                    skipped.append({"mode": name, "config": cfgs[i].key(),
+                                    "reason": _reason(int(st[i]), int(err0[k]), int(err1[k]), plan, combos[i], flat,
+                                                      db, workload, space, cfgs[i].batch)})
+        p0 = int(out.results["n_plans"][:si].sum())
+        for j in range(int(R["n_plans"])):
+            k = p0 + j
+            up, ud = int(U["plan_p"][k]) - off, int(U["plan_d"][k]) - off
+            pc = PoolCandidate("prefill", cfgs[up], float(U["pf_lat"][off + up]), float(U["pf_rate"][off + up]),
+                               cfgs[up].gpus())
+            dc = PoolCandidate("decode", cfgs[ud], float(U["dc_lat"][off + ud]), float(U["dc_rate"][off + ud]),
+                               cfgs[ud].gpus())
+            dp = DisaggPlan(pc, dc, int(U["plan_x"][k]), int(U["plan_y"][k]), int(U["plan_gpus"][k]),
+                            float(U["plan_r_sys"][k]), float(U["plan_ttft"][k]), float(U["plan_tpot"][k]),
+                            float(U["plan_speed"][k]), float(U["plan_thru"][k]))
+            row = plan_row(dp)
+            rows.append(row)
+            by_key[(2 << 32) | j] = row
+    f0 = int(out.results["n_front"][:si].sum())
+    frontier = [by_key[int(k)] for k in U["front"][f0: f0 + int(R["n_front"])]]
+    best = by_key[int(R["best"])] if R["best"] >= 0 else None
+    nearest = by_key[int(R["nearest"])] if (best is None and R["nearest"] >= 0) else None
+    kernel_ms = float(sum(out.totals.kernel_ms))
+    per = [kernel_ms / n_tasks] * n_tasks if n_tasks else []
+    return SearchReport(model=model.name, backend=db.backend, workload=workload, rows=rows, frontier=frontier,
+                        best=best, skipped=skipped, enumerated=int(R["n_enumerated"]), total_ms=wall_ms,
+                        per_candidate_ms=per, nearest=nearest)
+
+
+_ENGINES: dict[int, Engine] = {}
+_ENGINES_LOCK = threading.Lock()
+
+
+def get_engine(device: int = 0) -> Engine:
+    """Process-wide engine per device (one stream; calls are serialised)."""
+    with _ENGINES_LOCK:
+        eng = _ENGINES.get(device)
+        if eng is None:
+            eng = _ENGINES[device] = Engine(device)
+        return eng
+
+
+def run_search(db, model, workload, space=CandidateSpace(), jobs: int = 1, disagg_constants=DEFAULT_DISAGG,
+               device: int = 0) -> SearchReport:
+    """Drop-in for llmconf.search.run_search (search.py:280-358) on the B200 engine.
+
+    ``jobs`` is validated like the reference and otherwise ignored: the search
+    is one batched device pass whatever its value.
+    """
+    if jobs < 1:
+        raise SearchError("jobs must be >= 1")
+    t0 = time.perf_counter()
+    eng = get_engine(device)
+    with eng._lock:
+        out = eng.run_batch(db, model, space, [workload], disagg_constants)
+        return build_report(out, 0, db, model, workload, space, (time.perf_counter() - t0) * 1000.0)
+
+
+def enumerate_candidates(model, space, workload, db, enforce_budget: bool = True, device: int = 0) -> list:
+    """Drop-in for llmconf.search.enumerate_candidates (search.py:82-113), K0 on the device."""
+    eng = get_engine(device)
+    with eng._lock:
+        out = eng.run_batch(db, model, space, [workload], mode_override=0, enforce_budget=enforce_budget)
+        U = out.fetch_units()
+        n = int(out.results[0]["n_units"])
+        combos = out.plan.combos[U["unit_combo"][:n]]
+        bs = out.batches[U["unit_batch"][:n]]
+        return [space.config(int(c["tp"]), int(c["pp"]), int(c["ep"]), int(c["dp"]), int(b), db.backend)
+                for c, b in zip(combos, bs)]
