@@ -65,6 +65,8 @@ class BatchOutput:
     searches: np.ndarray
     wall_ms: float
     units: dict = field(default_factory=dict)
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
 
     def fetch_units(self) -> dict:
         if self.units:
@@ -94,6 +96,23 @@ class BatchOutput:
         self.engine._call(self.engine.lib.lc_fetch, "lc_fetch", self.engine.ctx, C.byref(req))
         self.units = out
         return out
+
+
+def fetch_fronts(out: "BatchOutput") -> tuple[np.ndarray, dict]:
+    """Columnar D2H for large sweeps: Pareto-front row keys and disaggregated plans only."""
+    nplan, nfront = int(out.totals.n_plans), int(out.totals.n_front)
+    front = np.zeros(max(nfront, 1), dtype=np.int64)
+    plans = {"plan_p": np.zeros(max(nplan, 1), np.int32), "plan_d": np.zeros(max(nplan, 1), np.int32),
+             "plan_x": np.zeros(max(nplan, 1), np.int32), "plan_y": np.zeros(max(nplan, 1), np.int32),
+             "plan_gpus": np.zeros(max(nplan, 1), np.int64), "plan_speed": np.zeros(max(nplan, 1)),
+             "plan_thru": np.zeros(max(nplan, 1))}
+    req = N.LcFetchReq()
+    req.front = N.ptr(front, C.c_int64)
+    for name, arr in plans.items():
+        setattr(req, name, N.ptr(arr, {np.dtype(np.int32): C.c_int32, np.dtype(np.int64): C.c_int64,
+                                       np.dtype(np.float64): C.c_double}[arr.dtype]))
+    out.engine._call(out.engine.lib.lc_fetch, "lc_fetch", out.engine.ctx, C.byref(req))
+    return front[:nfront], {k: v[:nplan] for k, v in plans.items()}
 
 
 class Engine:
@@ -235,8 +254,16 @@ class Engine:
         self._call(self.lib.lc_search_batch, "lc_search_batch", self.ctx, dbh, sph, n, N.vptr(searches),
                    len(batches), N.ptr(b_arr, C.c_int64), len(loads), N.ptr(l_arr, C.c_double),
                    N.vptr(results), C.byref(totals))
-        return BatchOutput(self, results, totals, plan, flat, b_arr, searches,
-                           (time.perf_counter() - t0) * 1000.0)
+        out = BatchOutput(self, results, totals, plan, flat, b_arr, searches, (time.perf_counter() - t0) * 1000.0)
+        out.h2d_bytes = searches.nbytes + 8 * len(batches) + (l_arr.nbytes if loads else 0)
+        out.d2h_bytes = results.nbytes + 4
+        return out
+
+    def replay(self, iters: int = 1) -> N.LcBatchTotals:
+        """Re-run the last batch's device pipeline (K0..K4) on resident inputs; per-kernel CUDA-event ms."""
+        totals = N.LcBatchTotals()
+        self._call(self.lib.lc_replay_last, "lc_replay_last", self.ctx, iters, C.byref(totals))
+        return totals
 
 
 # ------------------------------------------------------------------------------ report building
