@@ -74,7 +74,7 @@ __device__ __forceinline__ int lower_bound_i64(const int64_t* v, int n, int64_t 
 }
 
 // _interp_cells (perfdb.py:509-536) for coordinates inside the box.
-__device__ __forceinline__ double interp_cells(const DbView& D, const DevGrid& G, int64_t c0, int64_t c1,
+__device__ __noinline__ double interp_cells(const DbView& D, const DevGrid& G, int64_t c0, int64_t c1,
                                                int* n_log_calls) {
   int lo[2], hi[2];
   double t[2] = {0.0, 0.0};
@@ -134,7 +134,7 @@ __device__ __forceinline__ double interp_cells(const DbView& D, const DevGrid& G
 }
 
 // sol_estimate (perfdb.py:431-484); d is the canonical dim vector.
-__device__ __forceinline__ double sol_us(const DbView& D, int kind, int quant, const int64_t* d, int* st) {
+__device__ __noinline__ double sol_us(const DbView& D, int kind, int quant, const int64_t* d, int* st) {
   const double b = quant_bytes(quant);
   if (kind >= LC_KIND_ALLREDUCE && kind <= LC_KIND_P2P) {
     const int64_t n = d[1];
@@ -176,7 +176,7 @@ __device__ __forceinline__ double sol_us(const DbView& D, int kind, int quant, c
 }
 
 // query_latency (perfdb.py:539-580) for one plan entry with coordinates in d[0..1].
-__device__ __forceinline__ double query(const DbView& D, const lc_entry& e, int64_t* d, int* st, int* n_logs) {
+__device__ __noinline__ double query(const DbView& D, const lc_entry& e, int64_t* d, int* st, int* n_logs) {
   if (e.grid < 0) { *st = LC_ST_MISSING_KEY; return 0.0; }
   const DevGrid G = D.grids[e.grid];
   bool any_oob = false, any_above = false;
@@ -240,7 +240,7 @@ struct StepStats {
 // One forward pass: Σ_entries ((lat * repeat) / 1000.0) * bubble, summed like
 // CPython's sum() in plan order (estimator.py:83-95).  On failure the first
 // failing entry in plan order is recorded.
-__device__ __forceinline__ int step_total(const DbView& D, const lc_entry* E, int n, const StepArgs& a,
+__device__ __noinline__ int step_total(const DbView& D, const lc_entry* E, int n, const StepArgs& a,
                                           double bubble, int64_t hidden, double* out, ErrRec* err,
                                           StepStats* ss) {
   NeumaierSum s;
@@ -262,7 +262,7 @@ __device__ __forceinline__ int step_total(const DbView& D, const lc_entry* E, in
 // Static batching decode loop (serving_modes.py:256-266), stride 32.  Only the
 // generation-attention entry depends on the KV length, so the other entries
 // are priced once and the per-step sum re-run with the new attention term.
-__device__ __forceinline__ int static_decode(const DbView& D, const lc_entry* E, int n, int64_t b, int64_t isl,
+__device__ __noinline__ int static_decode(const DbView& D, const lc_entry* E, int n, int64_t b, int64_t isl,
                                              int64_t osl, int64_t expert_tokens, double bubble, int64_t hidden,
                                              double* tpot, ErrRec* err, StepStats* ss, int32_t* n_steps) {
   if (osl <= 1) { *tpot = 0.0; return 0; }

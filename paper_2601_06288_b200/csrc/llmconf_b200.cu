@@ -854,12 +854,12 @@ struct FrontCand {
   int64_t key;
 };
 
-constexpr int kLocalSamples = 4;   // per-thread dominator sample
-constexpr int kSurvivorCap = 2048; // front candidates kept in shared memory
+constexpr int kSurvivorCap = 2048;  // front candidates kept in shared memory
 constexpr int kFrontThreads = 256;
+constexpr int kSpeedBuckets = 4096;
 
-// Exact staircase over an arbitrary row subset held in shared memory, sorted by
-// (speed desc, row key asc): the reference's group-by-speed / running-max scan.
+// Exact staircase over a row subset sorted by (speed desc, row key asc): the
+// reference's group-by-speed / running-max scan (search.py:156-176).
 __device__ void front_of_sorted(const FrontCand* c, int n, int64_t* out, int* n_out) {
   int m = 0;
   double best_thru = -INFINITY;
@@ -877,18 +877,53 @@ __device__ void front_of_sorted(const FrontCand* c, int n, int64_t* out, int* n_
   *n_out = m;
 }
 
+__device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v, unsigned long long* red) {
+  for (int o = 16; o > 0; o >>= 1) { const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o); v = w < v ? w : v; }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  unsigned long long r = ~0ull;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = red[i] < r ? red[i] : r;
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v, unsigned long long* red) {
+  for (int o = 16; o > 0; o >>= 1) { const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o); v = w > v ? w : v; }
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  unsigned long long r = 0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = red[i] > r ? red[i] : r;
+  __syncthreads();
+  return r;
+}
+
+#define FRONT_ROW_FILTER(v)                                                          \
+  if (!v.valid) continue;                                                            \
+  if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
+
+// K4.  Three passes over the search's rows, one block per search:
+//  1. counts, select_best (search.py:179-187), range of the feasible speeds;
+//  2. per speed-bucket maximum throughput (buckets = top bits of the IEEE
+//     pattern, so bucket order is speed order);
+//  3. a row can only be on the front if it beats the best throughput of every
+//     strictly faster bucket -- those maxima are real rows that would dominate
+//     it -- so only such survivors go through the exact reference scan.
 __global__ void __launch_bounds__(kFrontThreads) k_front(EvalParams P, const SearchMeta* meta, const int32_t* plan_i,
                                                          const double* plan_d, int64_t* front,
                                                          lc_search_result* results) {
   extern __shared__ __align__(16) unsigned char fsm[];
-  FrontCand* samples = (FrontCand*)fsm;                                  // kFrontThreads * kLocalSamples
-  FrontCand* surv = samples + kFrontThreads * kLocalSamples;             // kSurvivorCap
-  FrontCand* sorted = surv + kSurvivorCap;                               // kSurvivorCap
-  int64_t* keys_out = (int64_t*)(sorted + kSurvivorCap);                 // kSurvivorCap
+  unsigned long long* bmax = (unsigned long long*)fsm;         // kSpeedBuckets
+  FrontCand* surv = (FrontCand*)(bmax + kSpeedBuckets);          // kSurvivorCap
+  FrontCand* sorted = surv + kSurvivorCap;                       // kSurvivorCap
+  int64_t* keys_out = (int64_t*)(sorted + kSurvivorCap);         // kSurvivorCap
   __shared__ BestKey bred[kFrontThreads];
   __shared__ MissKey mred[kFrontThreads];
+  __shared__ unsigned long long ured[32];
+  __shared__ unsigned long long tsuf[kFrontThreads];
   __shared__ double dred[32];
-  __shared__ int cnt_feas, cnt_rows, cnt_enum, cnt_skip, n_surv, n_stair, nfront;
+  __shared__ int cnt_feas, cnt_rows, cnt_enum, cnt_skip, n_surv, nfront;
   const int s = blockIdx.x;
   const int tid = threadIdx.x;
   const lc_search_desc& S = P.searches[s];
@@ -897,12 +932,12 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(EvalParams P, const Sea
   const int64_t nrows_all = 2 * (int64_t)M.n_units + nplan;
   const int64_t foff = (int64_t)M.unit_off * 2 + M.plan_off;
   if (tid == 0) { cnt_feas = cnt_rows = cnt_enum = cnt_skip = 0; n_surv = 0; nfront = 0; }
+  for (int i = tid; i < kSpeedBuckets; i += blockDim.x) bmax[i] = 0ull;
   __syncthreads();
 
-  // ---- pass 1: counts, best (select_best), a per-thread dominator sample
+  // ---- pass 1
   BestKey best{0, 0, 0, 0, -1};
-  FrontCand loc[kLocalSamples];
-  int nloc = 0;
+  unsigned long long smin = ~0ull, smax = 0ull;
   int my_feas = 0, my_rows = 0, my_enum = 0, my_skip = 0;
   unsigned long long my_q1 = 0, my_q2 = 0;
   for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
@@ -919,8 +954,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(EvalParams P, const Sea
       if (S.modes & 4) my_skip += (P.pf_status[u] != 0) + (P.dc_status[u] != 0);
     }
     const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-    if (!v.valid) continue;
-    if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
+    FRONT_ROW_FILTER(v)
     ++my_rows;
     if (!feasible(S, v)) continue;
     ++my_feas;
@@ -929,28 +963,14 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(EvalParams P, const Sea
       BestKey k{nt, ns, v.gpus, mode_rank(v.mode), v.key};
       if (best_less(P, M, plan_i, k, best)) best = k;
     }
-    // dominator sample: keep up to kLocalSamples mutually non-dominated rows
-    bool dom = false;
-    for (int j = 0; j < nloc; ++j) dom |= dominates(loc[j].speed, loc[j].thru, v.speed, v.thru);
-    if (!dom) {
-      int m = 0;
-      for (int j = 0; j < nloc; ++j)
-        if (!dominates(v.speed, v.thru, loc[j].speed, loc[j].thru)) loc[m++] = loc[j];
-      nloc = m;
-      if (nloc < kLocalSamples) loc[nloc++] = FrontCand{v.speed, v.thru, v.key};
-      else {
-        int w = 0;  // replace the sample with the least throughput (any real row keeps pruning exact)
-        for (int j = 1; j < nloc; ++j) if (loc[j].thru < loc[w].thru) w = j;
-        loc[w] = FrontCand{v.speed, v.thru, v.key};
-      }
-    }
+    const unsigned long long sb = (unsigned long long)__double_as_longlong(v.speed);
+    smin = sb < smin ? sb : smin;
+    smax = sb > smax ? sb : smax;
   }
   atomicAdd(&cnt_feas, my_feas); atomicAdd(&cnt_rows, my_rows);
   atomicAdd(&cnt_enum, my_enum); atomicAdd(&cnt_skip, my_skip);
   atomicAdd((unsigned long long*)&results[s].queries_1d, my_q1);
   atomicAdd((unsigned long long*)&results[s].queries_2d, my_q2);
-  for (int j = 0; j < kLocalSamples; ++j)
-    samples[tid * kLocalSamples + j] = j < nloc ? loc[j] : FrontCand{-INFINITY, -INFINITY, -1};
   bred[tid] = best;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
@@ -970,15 +990,15 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(EvalParams P, const Sea
     R.nearest_violation = 0.0;
     R.front_off = (int32_t)foff;
   }
-  __syncthreads();
+  const unsigned long long lo = block_min_u64(smin, ured);
+  const unsigned long long hi = block_max_u64(smax, ured);
 
   // ---- nearest miss (search.py:190-208), only when nothing is feasible
   if (cnt_feas == 0) {
     MissKey miss{0, -1};
     for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
       const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-      if (!v.valid) continue;
-      if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
+      FRONT_ROW_FILTER(v)
       double worst = 1.0;
       if (S.has_ttft && v.ttft > S.ttft_limit) { const double x = v.ttft / S.ttft_limit; if (x > worst) worst = x; }
       if (S.has_floor && v.speed < S.speed_floor) {
@@ -996,51 +1016,52 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(EvalParams P, const Sea
       if (tid < w && miss_less(P, M, plan_i, mred[tid + w], mred[tid])) mred[tid] = mred[tid + w];
       __syncthreads();
     }
-    if (tid == 0) { results[s].nearest = mred[0].key; results[s].nearest_violation = mred[0].viol; }
-    if (tid == 0) results[s].n_front = 0;
+    if (tid == 0) {
+      results[s].nearest = mred[0].key;
+      results[s].nearest_violation = mred[0].viol;
+      results[s].n_front = 0;
+    }
     return;
   }
 
-  // ---- staircase of the samples (real rows): sort by speed desc, keep running-max risers
-  const int ns_tot = kFrontThreads * kLocalSamples;
-  for (int i = tid; i < ns_tot; i += blockDim.x) {
-    const FrontCand a = samples[i];
-    int rank = 0;
-    for (int j = 0; j < ns_tot; ++j) {
-      const FrontCand b = samples[j];
-      rank += (b.speed > a.speed) || (b.speed == a.speed && j < i);
-    }
-    surv[rank] = a;  // scratch: sorted samples
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int m = 0;
-    double run = -INFINITY;
-    for (int i = 0; i < ns_tot; ++i) {
-      if (surv[i].key < 0) continue;
-      if (surv[i].thru > run) { samples[m++] = surv[i]; run = surv[i].thru; }
-    }
-    n_stair = m;
-  }
-  __syncthreads();
-  const int nst = n_stair;
-
-  // ---- pass 2: rows not dominated by the staircase sample are the only front candidates
+  // ---- pass 2: bucket maxima (throughput >= 0, so its bit pattern orders like the value)
+  int shift = 0;
+  while (shift < 63 && ((hi >> shift) - (lo >> shift)) >= (unsigned long long)kSpeedBuckets) ++shift;
+  const unsigned long long base = lo >> shift;
   for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
     const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-    if (!v.valid) continue;
-    if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
+    FRONT_ROW_FILTER(v)
     if (!feasible(S, v)) continue;
-    bool dom = false;
-    for (int j = 0; j < nst && !dom; ++j) dom = dominates(samples[j].speed, samples[j].thru, v.speed, v.thru);
-    if (dom) continue;
+    const int b = (int)((((unsigned long long)__double_as_longlong(v.speed)) >> shift) - base);
+    atomicMax(&bmax[b], (unsigned long long)__double_as_longlong(v.thru));
+  }
+  __syncthreads();
+  // exclusive suffix max: bmax[b] <- max over buckets strictly above b
+  constexpr int per = kSpeedBuckets / kFrontThreads;
+  unsigned long long loc[per];
+  unsigned long long run = 0;
+  for (int j = per - 1; j >= 0; --j) { loc[j] = run; const unsigned long long x = bmax[tid * per + j]; run = x > run ? x : run; }
+  tsuf[tid] = run;
+  __syncthreads();
+  unsigned long long above = 0;
+  for (int t = tid + 1; t < kFrontThreads; ++t) above = tsuf[t] > above ? tsuf[t] : above;
+  __syncthreads();
+  for (int j = 0; j < per; ++j) bmax[tid * per + j] = loc[j] > above ? loc[j] : above;
+  __syncthreads();
+
+  // ---- pass 3: survivors
+  for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
+    const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+    FRONT_ROW_FILTER(v)
+    if (!feasible(S, v)) continue;
+    const int b = (int)((((unsigned long long)__double_as_longlong(v.speed)) >> shift) - base);
+    if (v.thru <= __longlong_as_double((long long)bmax[b]) && bmax[b] != 0ull) continue;
     const int k = atomicAdd(&n_surv, 1);
     if (k < kSurvivorCap) surv[k] = FrontCand{v.speed, v.thru, v.key};
   }
   __syncthreads();
   const int nsv = n_surv;
   if (nsv <= kSurvivorCap) {
-    // sort survivors by (speed desc, key asc) and run the exact scan
     for (int i = tid; i < nsv; i += blockDim.x) {
       const FrontCand a = surv[i];
       int rank = 0;
@@ -1059,33 +1080,32 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(EvalParams P, const Sea
     }
     return;
   }
-  // ---- fallback (more than kSurvivorCap candidates): iterative staircase over all rows
+  // ---- fallback (more candidates than shared memory holds): iterative staircase over all rows
   double best_thru = -INFINITY;
   while (true) {
-    double smax = -INFINITY;
+    double sm = -INFINITY;
     bool any = false;
     for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
       const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-      if (!v.valid || !feasible(S, v)) continue;
-      if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
-      if (v.thru > best_thru) { any = true; smax = fmax(smax, v.speed); }
+      FRONT_ROW_FILTER(v)
+      if (!feasible(S, v)) continue;
+      if (v.thru > best_thru) { any = true; sm = fmax(sm, v.speed); }
     }
     if (!__syncthreads_or(any)) break;
-    const double sp = block_max(any ? smax : -INFINITY, dred);
+    const double sp = block_max(any ? sm : -INFINITY, dred);
     double tmax = -INFINITY;
     for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
       const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-      if (!v.valid || !feasible(S, v)) continue;
-      if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
+      FRONT_ROW_FILTER(v)
+      if (!feasible(S, v)) continue;
       if (v.speed == sp) tmax = fmax(tmax, v.thru);
     }
     const double top = block_max(tmax, dred);
     if (tid == 0) {
-      // ordered sequential collection of the group (row order)
       for (int64_t r = 0; r < nrows_all; ++r) {
         const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-        if (!v.valid || !feasible(S, v)) continue;
-        if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
+        FRONT_ROW_FILTER(v)
+        if (!feasible(S, v)) continue;
         if (v.speed == sp && v.thru == top) front[foff + nfront++] = v.key;
       }
     }
@@ -1313,7 +1333,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
                                                 (lc_search_result*)c->results.p);
   CK(cudaGetLastError());
   CK(cudaEventRecord(c->ev[5], c->stream));
-  const size_t fsmem = sizeof(FrontCand) * (kFrontThreads * kLocalSamples + 2 * kSurvivorCap) + 8 * kSurvivorCap;
+  const size_t fsmem = 8 * kSpeedBuckets + sizeof(FrontCand) * 2 * kSurvivorCap + 8 * kSurvivorCap;
   CK(cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
   k_front<<<c->n_search, kFrontThreads, fsmem, c->stream>>>(P, (const SearchMeta*)c->meta.p, (const int32_t*)c->plans_i.p,
                                                (const double*)c->plans_d.p, (int64_t*)c->front.p,
