@@ -14,6 +14,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -94,12 +95,31 @@ struct lc_space {
   int64_t* tp_vals;  // [n_tp] from combos
   int64_t* ep_vals;  // [n_ep]
   uint8_t* pair_used;  // [n_tp*n_ep]
+  int32_t* pair_canon; // [n_tp*n_ep] first pair with the same (max(1, ep/tp), ep): identical tails
+  struct TmplInfo* tmpl_info;  // [n_tmpl]
+};
+
+// One MoE tail table: [tp_i * n_ep + ep_i][b_i].  Prefill-type tables depend on
+// (batch list, load, context length), decode-type on (batch list, load) only,
+// mixed-type on the whole search -- so sweeps share most of them.
+struct TailTable {
+  int64_t off;
+  int32_t type;    // 0 prefill (b * chunk), 1 decode (b), 2 mixed (chunk + n_mix_gen)
+  int32_t search;  // representative search (workload for the mixed schedule)
+  int32_t b_off, n_b, load, _pad;
+  int64_t chunk;
+};
+
+struct TmplInfo {
+  int64_t tp, pp, ep;
+  int32_t tp_i, ep_i;
 };
 
 // per-search bookkeeping computed on the host / device
 struct SearchMeta {
   int64_t raw_off, n_raw;
-  int64_t tail_off;
+  int64_t cell_off;
+  int64_t tail_off[3];  // per tail type
   int32_t unit_off, n_units;
   int32_t plan_off, plan_cap;
   int32_t pool_off;  // into pool selection arrays (64 slots per role)
@@ -114,14 +134,15 @@ struct lc_ctx {
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
-  DBuf tails, pool_sel, plans_i, plans_d, front, u_queries;
+  DBuf tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   // last batch
   const lc_db* db = nullptr;
   const lc_space* sp = nullptr;
   int32_t n_search = 0, n_batches = 0, n_loads = 0;
-  int64_t n_raw = 0, n_cap = 0, n_units = 0, n_tails = 0, n_plan_slots = 0, n_front_slots = 0;
+  int64_t n_raw = 0, n_cap = 0, n_units = 0, n_tails = 0, n_plan_slots = 0, n_front_slots = 0, n_cells = 0;
   int64_t n_total_idx = 0;  // index of the unit total inside block_sums
   std::vector<SearchMeta> hmeta;
+  std::vector<TailTable> htables;
   std::vector<lc_search_result> hres;
 };
 
@@ -140,7 +161,8 @@ struct EvalParams {
   // space
   const lc_combo* combos; const int32_t* tmpl_n; const lc_entry* entries;
   int64_t hidden, topk, n_experts; int32_t is_moe, n_tp, n_ep;
-  const int64_t* tp_vals; const int64_t* ep_vals; const uint8_t* pair_used;
+  const int64_t* tp_vals; const int64_t* ep_vals; const uint8_t* pair_used; const int32_t* pair_canon;
+  const TailTable* tail_tables; int32_t n_tail_tables;
   // batch
   const lc_search_desc* searches; const SearchMeta* meta; int32_t n_search;
   const int64_t* batches; const double* loads;
@@ -156,6 +178,12 @@ struct EvalParams {
   int32_t* dc_status; double* dc_v;
   int64_t* err_c;                    // [8][n_units]: (c0,c1) x (st,ag,pf,dc)
   int32_t* u_queries;                // q1 | q2 << 16 per unit
+  // cells (search x template x batch)
+  const struct TmplInfo* tmpl_info;
+  uint32_t* cell_flags;              // bit0: some candidate in budget, bit1: pool worker
+  struct CellOut* cells;
+  int64_t* cell_err;                 // [cell][8]
+  int64_t n_cells_total;
   lc_search_result* results;
 };
 
@@ -181,7 +209,11 @@ __global__ void k_enum_flags(EvalParams P, int64_t n_raw, uint8_t* flags) {
     uint8_t f = 0;
     if (fits_memory(c, S, P.gpu_memory, P.hidden, b)) {
       const bool inb = in_budget(S, c.gpus);
-      if (inb || (S.modes & 4)) f = 1 | (inb ? 2 : 0);  // workers skip the budget (search.py:323)
+      if (inb || (S.modes & 4)) {  // workers skip the budget (search.py:323)
+        f = 1 | (inb ? 2 : 0);
+        atomicOr(&P.cell_flags[P.meta[s].cell_off + (int64_t)c.tmpl * S.n_b + bi],
+                 (inb ? 1u : 0u) | ((S.modes & 4) ? 2u : 0u));
+      }
     }
     flags[r] = f;
   }
@@ -285,43 +317,40 @@ __global__ void k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* hist = hist_all[warp];
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int npair = P.n_tp * P.n_ep;
   for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; t < n_tails; t += nw) {
-    // locate search by tail offset
-    int lo = 0, hi = P.n_search - 1;
+    int lo = 0, hi = P.n_tail_tables - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (P.meta[mid].tail_off <= t) lo = mid;
+      if (P.tail_tables[mid].off <= t) lo = mid;
       else hi = mid - 1;
     }
-    const int s = lo;
-    const lc_search_desc& S = P.searches[s];
-    int64_t rel = t - P.meta[s].tail_off;
-    const int bi = (int)(rel % S.n_b); rel /= S.n_b;
-    const int ep_i = (int)(rel % P.n_ep); rel /= P.n_ep;
-    const int tp_i = (int)(rel % P.n_tp); rel /= P.n_tp;
-    const int type = (int)rel;
-    int64_t result = 0;
+    const TailTable T = P.tail_tables[lo];
+    const int64_t rel = t - T.off;
+    const int bi = (int)(rel % T.n_b);
+    const int pair = (int)(rel / T.n_b);
+    if (pair >= npair) continue;
+    const int tp_i = pair / P.n_ep, ep_i = pair % P.n_ep;
     const int64_t tp = P.tp_vals[tp_i], ep = P.ep_vals[ep_i];
-    if (ep > 1 && P.pair_used[tp_i * P.n_ep + ep_i] && S.load >= 0) {
-      const int64_t b = P.batches[S.b_off + bi];
-      const int64_t chunk = S.isl - S.prefix;
-      int64_t tokens = -1;
-      if (type == 0) tokens = b * chunk;
-      else if (type == 1) tokens = b;
-      else {
-        const AggSched a = agg_schedule(S, b);
-        if (!a.st) tokens = a.chunk_tokens + a.n_mix_gen;
-      }
-      if (tokens >= 0) {
-        const int64_t f = ep / tp > 1 ? ep / tp : 1;
-        const int64_t pooled = tokens * f;
-        const int E = (int)P.n_experts;
-        const double* q = P.loads + (int64_t)S.load * 2 * E;
-        if (E <= 256)
-          result = warp_busiest_shard<8>(q, q + E, E, pooled, P.topk, ep, hist);
-        else
-          result = warp_busiest_shard<32>(q, q + E, E, pooled, P.topk, ep, hist);
-      }
+    if (!(ep > 1 && P.pair_used[pair] && P.pair_canon[pair] == pair && T.load >= 0)) continue;
+    const int64_t b = P.batches[T.b_off + bi];
+    int64_t tokens = -1;
+    if (T.type == 0) tokens = b * T.chunk;
+    else if (T.type == 1) tokens = b;
+    else {
+      const AggSched a = agg_schedule(P.searches[T.search], b);
+      if (!a.st) tokens = a.chunk_tokens + a.n_mix_gen;
+    }
+    int64_t result = 0;
+    if (tokens >= 0) {
+      const int64_t f = ep / tp > 1 ? ep / tp : 1;
+      const int64_t pooled = tokens * f;
+      const int E = (int)P.n_experts;
+      const double* q = P.loads + (int64_t)T.load * 2 * E;
+      if (E <= 256)
+        result = warp_busiest_shard<8>(q, q + E, E, pooled, P.topk, ep, hist);
+      else
+        result = warp_busiest_shard<32>(q, q + E, E, pooled, P.topk, ep, hist);
     }
     if (lane == 0) tails[t] = result;
   }
@@ -357,7 +386,7 @@ __device__ __forceinline__ int64_t expert_tokens(const EvalParams& P, const lc_c
   const int64_t balanced = ceil_div_f(pooled * P.topk, c.ep);
   if (c.ep == 1 || S.load < 0) return balanced;
   const int64_t tail =
-      P.tails[M.tail_off + (((int64_t)type * P.n_tp + c.tp_i) * P.n_ep + c.ep_i) * S.n_b + bi];
+      P.tails[M.tail_off[type] + (int64_t)P.pair_canon[c.tp_i * P.n_ep + c.ep_i] * S.n_b + bi];
   return balanced > tail ? balanced : tail;
 }
 
@@ -366,73 +395,98 @@ __device__ __forceinline__ void put_err(const EvalParams& P, int kind, int64_t u
   P.err_c[(int64_t)(2 * kind + 1) * P.n_cap + u] = e.c1;
 }
 
-__global__ void __launch_bounds__(128) k_eval(EvalParams P) {
+// Per-cell results.  A cell is (search, (tp,pp,ep) template, batch): every
+// latency of the reference model depends on the parallel config only through
+// tp, pp, ep and the batch (decompose, model.py:271-406; pipeline bubble,
+// estimator.py:45-48), never through dp, so the dp variants of a candidate
+// share one evaluation.  K2b expands cells back to candidates.
+struct CellOut {
+  int32_t st_status, ag_status, pf_status, dc_status;
+  double st_ttft, st_tpot, ag_ttft, ag_tpot, pf_lat, dc_lat;
+  int32_t qP, qSD, qM, qG;  // reference-equivalent query counts per step kind (q1 | q2 << 16)
+  int32_t st_steps, flags;  // flags bit0: aggregated used the generation step
+};
+
+__device__ __forceinline__ void put_cell_err(const EvalParams& P, int kind, int64_t c, const ErrRec& e) {
+  P.cell_err[c * 8 + 2 * kind] = e.c0;
+  P.cell_err[c * 8 + 2 * kind + 1] = e.c1;
+}
+
+__device__ __forceinline__ int find_cell_search(const SearchMeta* meta, int n, int64_t c) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (meta[mid].cell_off <= c) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(128) k_eval_cells(EvalParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   DbView V;
   stage_db(P, smem, &V);
-  const int64_t n = P.n_cap;
-  const int64_t total = *P.d_total;
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
-    const int s = P.u_search[u];
+  const int64_t ncell = P.n_cells_total;
+  for (int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ci < ncell;
+       ci += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t cf = P.cell_flags[ci];
+    if (!cf) continue;
+    const int s = find_cell_search(P.meta, P.n_search, ci);
     const lc_search_desc& S = P.searches[s];
     const SearchMeta& M = P.meta[s];
-    const int bi = P.u_batch[u];
-    const lc_combo c = P.combos[P.u_combo[u]];
-    const lc_entry* E = P.entries + (int64_t)c.tmpl * LC_MAX_ENTRIES;
-    const int ne = P.tmpl_n[c.tmpl];
+    const int64_t rel = ci - M.cell_off;
+    const int tmpl = (int)(rel / S.n_b), bi = (int)(rel % S.n_b);
+    const TmplInfo ti = P.tmpl_info[tmpl];
+    lc_combo c;  // the fields expert_tokens() reads
+    c.tp = ti.tp; c.pp = ti.pp; c.ep = ti.ep; c.tp_i = ti.tp_i; c.ep_i = ti.ep_i;
+    const lc_entry* E = P.entries + (int64_t)tmpl * LC_MAX_ENTRIES;
+    const int ne = P.tmpl_n[tmpl];
     const int64_t b = P.batches[S.b_off + bi];
-    const bool inb = P.u_budget[u] != 0;
-    const bool do_st = (S.modes & 1) && inb, do_ag = (S.modes & 2) && inb, do_dg = (S.modes & 4) != 0;
+    const bool do_st = (cf & 1) && (S.modes & 1), do_ag = (cf & 1) && (S.modes & 2), do_dg = (cf & 2) != 0;
     const int64_t mb = b > 1 ? b : 1;
-    const double bubble = (double)(mb + c.pp - 1) / (double)mb;
+    const double bubble = (double)(mb + ti.pp - 1) / (double)mb;
     const int64_t chunk = S.isl - S.prefix;
     const int64_t kv_mid = S.isl + S.osl / 2;
     StepStats ss{0, 0, 0};
-    int32_t q1 = 0, q2 = 0;
+    CellOut o;
+    o.st_status = o.ag_status = o.pf_status = o.dc_status = LC_ST_NOT_EVALUATED;
+    o.st_ttft = o.st_tpot = o.ag_ttft = o.ag_tpot = o.pf_lat = o.dc_lat = 0.0;
+    o.qP = o.qSD = o.qM = o.qG = 0;
+    o.st_steps = 0;
+    o.flags = 0;
 
-    // prefill step: static TTFT and the prefill pool (estimator memo shares it)
+    // prefill step: static TTFT and the prefill pool (the estimator memo shares it)
     double p_total = 0.0;
     ErrRec p_err{0, 0, 0, 0};
     if (do_st || do_dg) {
       StepArgs a{PH_PREFILL, b * chunk, 0, chunk, expert_tokens(P, c, M, S, 0, bi, b * chunk)};
       step_total(V, E, ne, a, bubble, P.hidden, &p_total, &p_err, &ss);
-      if (!p_err.code) { q1 += ss.q1; q2 += ss.q2; }
+      if (!p_err.code) o.qP = (ss.q1 & 0xffff) | (ss.q2 << 16);
       ss.q1 = ss.q2 = 0;
+      o.pf_status = p_err.code | (p_err.label << 8);
+      o.pf_lat = p_total;
+      if (p_err.code) put_cell_err(P, 2, ci, p_err);
     }
     const int64_t xt_dec = expert_tokens(P, c, M, S, 1, bi, b);
-    int32_t st_steps = 0;
     if (do_st) {
       double tpot = 0.0;
       ErrRec e = p_err;
       if (!e.code) {
-        static_decode(V, E, ne, b, S.isl, S.osl, xt_dec, bubble, P.hidden, &tpot, &e, &ss, &st_steps);
-        if (!e.code) { q1 += ss.q1; q2 += ss.q2; }
+        int32_t steps = 0;
+        static_decode(V, E, ne, b, S.isl, S.osl, xt_dec, bubble, P.hidden, &tpot, &e, &ss, &steps);
+        if (!e.code) o.qSD = (ss.q1 & 0xffff) | (ss.q2 << 16);
         ss.q1 = ss.q2 = 0;
+        o.st_steps = steps;
       }
-      P.st_status[u] = e.code | (e.label << 8);
-      if (e.code) {
-        put_err(P, 0, u, e);
-      } else {
-        double speed, thru;
-        derive_metrics(p_total, tpot, b, S.osl, c.gpus, &speed, &thru);
-        P.st_v[u] = p_total; P.st_v[n + u] = tpot; P.st_v[2 * n + u] = speed; P.st_v[3 * n + u] = thru;
-      }
+      o.st_status = e.code | (e.label << 8);
+      o.st_ttft = p_total;
+      o.st_tpot = tpot;
+      if (e.code) put_cell_err(P, 0, ci, e);
     }
     // generation step at the KV midpoint: aggregated l_gen and the decode pool
     bool g_done = false;
     double g_total = 0.0;
     ErrRec g_err{0, 0, 0, 0};
-    auto gen_step = [&]() {
-      if (g_done) return;
-      g_done = true;
-      StepArgs a{PH_DECODE, 0, b, kv_mid, xt_dec};
-      step_total(V, E, ne, a, bubble, P.hidden, &g_total, &g_err, &ss);
-      // memo hit in the reference when a static decode step used the same KV length
-      const int64_t k = kv_mid - S.isl - 1;
-      const bool dup = do_st && S.osl > 1 && k >= 0 && (k % 32) == 0 && (k / 32) < st_steps;
-      if (!g_err.code && !dup) { q1 += ss.q1; q2 += ss.q2; }
-      ss.q1 = ss.q2 = 0;
-    };
     if (do_ag) {
       const AggSched sc = agg_schedule(S, b);
       ErrRec e{sc.st, 0, 0, 0};
@@ -442,10 +496,15 @@ __global__ void __launch_bounds__(128) k_eval(EvalParams P) {
         StepArgs a{PH_MIXED, sc.chunk_tokens, sc.n_mix_gen, kv_mid,
                    expert_tokens(P, c, M, S, 2, bi, sc.chunk_tokens + sc.n_mix_gen)};
         step_total(V, E, ne, a, bubble, P.hidden, &l_mix, &e, &ss);
-        if (!e.code) { q1 += ss.q1; q2 += ss.q2; }
+        if (!e.code) o.qM = (ss.q1 & 0xffff) | (ss.q2 << 16);
         ss.q1 = ss.q2 = 0;
         if (!e.code && (sc.t_gen || b == 1)) {
-          gen_step();
+          StepArgs g{PH_DECODE, 0, b, kv_mid, xt_dec};
+          step_total(V, E, ne, g, bubble, P.hidden, &g_total, &g_err, &ss);
+          g_done = true;
+          if (!g_err.code) o.qG = (ss.q1 & 0xffff) | (ss.q2 << 16);
+          ss.q1 = ss.q2 = 0;
+          o.flags |= 1;
           e = g_err;
           l_gen = g_total;
         }
@@ -463,29 +522,86 @@ __global__ void __launch_bounds__(128) k_eval(EvalParams P) {
           }
         }
       }
-      P.ag_status[u] = e.code | (e.label << 8);
-      if (e.code) {
-        put_err(P, 1, u, e);
-      } else {
-        double speed, thru;
-        derive_metrics(ttft, tpot, b, S.osl, c.gpus, &speed, &thru);
-        P.ag_v[u] = ttft; P.ag_v[n + u] = tpot; P.ag_v[2 * n + u] = speed; P.ag_v[3 * n + u] = thru;
-      }
+      o.ag_status = e.code | (e.label << 8);
+      o.ag_ttft = ttft;
+      o.ag_tpot = tpot;
+      if (e.code) put_cell_err(P, 1, ci, e);
     }
     if (do_dg) {
-      P.pf_status[u] = p_err.code | (p_err.label << 8);
-      if (p_err.code) put_err(P, 2, u, p_err);
-      else { P.pf_v[u] = p_total; P.pf_v[n + u] = (double)b * 1000.0 / p_total; }
-      gen_step();
-      P.dc_status[u] = g_err.code | (g_err.label << 8);
-      if (g_err.code) put_err(P, 3, u, g_err);
-      else {
-        P.dc_v[u] = g_total;
-        P.dc_v[n + u] = S.osl == 1 ? INFINITY : (double)b * 1000.0 / ((double)(S.osl - 1) * g_total);
+      if (!g_done) {
+        StepArgs g{PH_DECODE, 0, b, kv_mid, xt_dec};
+        step_total(V, E, ne, g, bubble, P.hidden, &g_total, &g_err, &ss);
+        if (!g_err.code) o.qG = (ss.q1 & 0xffff) | (ss.q2 << 16);
+        ss.q1 = ss.q2 = 0;
+      }
+      o.dc_status = g_err.code | (g_err.label << 8);
+      o.dc_lat = g_total;
+      if (g_err.code) put_cell_err(P, 3, ci, g_err);
+    }
+    P.cells[ci] = o;
+  }
+}
+
+// K2b: candidates from their cells -- derive_metrics with the candidate's gpu
+// count (serving_modes.py:161-172) and the pool rates (serving_modes.py:366, 380).
+__global__ void __launch_bounds__(256) k_expand(EvalParams P) {
+  const int64_t n = P.n_cap;
+  const int64_t total = *P.d_total;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
+    const int s = P.u_search[u];
+    const lc_search_desc& S = P.searches[s];
+    const int bi = P.u_batch[u];
+    const lc_combo c = P.combos[P.u_combo[u]];
+    const int64_t ci = P.meta[s].cell_off + (int64_t)c.tmpl * S.n_b + bi;
+    const CellOut o = P.cells[ci];
+    const int64_t b = P.batches[S.b_off + bi];
+    const bool inb = P.u_budget[u] != 0;
+    const bool do_st = (S.modes & 1) && inb, do_ag = (S.modes & 2) && inb, do_dg = (S.modes & 4) != 0;
+    int32_t q = 0;
+    auto add_q = [&](int32_t x) { q += x; };  // packed halves never overflow 16 bits
+    if (do_st) {
+      P.st_status[u] = o.st_status;
+      if (o.st_status) {
+        P.err_c[u] = P.cell_err[ci * 8 + 0]; P.err_c[n + u] = P.cell_err[ci * 8 + 1];
+      } else {
+        double speed, thru;
+        derive_metrics(o.st_ttft, o.st_tpot, b, S.osl, c.gpus, &speed, &thru);
+        P.st_v[u] = o.st_ttft; P.st_v[n + u] = o.st_tpot; P.st_v[2 * n + u] = speed; P.st_v[3 * n + u] = thru;
+        add_q(o.qSD);
       }
     }
-    // reference-equivalent query accounting (summed per search in K4)
-    P.u_queries[u] = (q1 & 0xffff) | (q2 << 16);
+    if (do_ag) {
+      P.ag_status[u] = o.ag_status;
+      if (o.ag_status) {
+        P.err_c[2 * n + u] = P.cell_err[ci * 8 + 2]; P.err_c[3 * n + u] = P.cell_err[ci * 8 + 3];
+      } else {
+        double speed, thru;
+        derive_metrics(o.ag_ttft, o.ag_tpot, b, S.osl, c.gpus, &speed, &thru);
+        P.ag_v[u] = o.ag_ttft; P.ag_v[n + u] = o.ag_tpot; P.ag_v[2 * n + u] = speed; P.ag_v[3 * n + u] = thru;
+      }
+      add_q(o.qM);
+    }
+    if (do_st || do_dg) add_q(o.qP);
+    if (do_dg) {
+      P.pf_status[u] = o.pf_status;
+      if (o.pf_status) {
+        P.err_c[4 * n + u] = P.cell_err[ci * 8 + 4]; P.err_c[5 * n + u] = P.cell_err[ci * 8 + 5];
+      } else {
+        P.pf_v[u] = o.pf_lat; P.pf_v[n + u] = (double)b * 1000.0 / o.pf_lat;
+      }
+      P.dc_status[u] = o.dc_status;
+      if (o.dc_status) {
+        P.err_c[6 * n + u] = P.cell_err[ci * 8 + 6]; P.err_c[7 * n + u] = P.cell_err[ci * 8 + 7];
+      } else {
+        P.dc_v[u] = o.dc_lat;
+        P.dc_v[n + u] = S.osl == 1 ? INFINITY : (double)b * 1000.0 / ((double)(S.osl - 1) * o.dc_lat);
+      }
+    }
+    // the generation step is a memo hit when a static decode step used the same KV length
+    const int64_t k = (S.isl + S.osl / 2) - S.isl - 1;
+    const bool dup = do_st && o.st_status == 0 && S.osl > 1 && k >= 0 && (k % 32) == 0 && (k / 32) < o.st_steps;
+    if (((do_ag && (o.flags & 1)) || do_dg) && !dup) add_q(o.qG);
+    P.u_queries[u] = q;
   }
 }
 
@@ -1151,7 +1267,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
@@ -1210,12 +1326,14 @@ int lc_space_upload(lc_ctx* c, const lc_space_desc* d, lc_space** out) {
   sp->n_combos = d->n_combos; sp->n_tmpl = d->n_tmpl; sp->n_tp = d->n_tp; sp->n_ep = d->n_ep;
   std::vector<int64_t> tpv(d->n_tp > 0 ? d->n_tp : 1, 1), epv(d->n_ep > 0 ? d->n_ep : 1, 1);
   std::vector<uint8_t> used((size_t)(d->n_tp > 0 ? d->n_tp : 1) * (d->n_ep > 0 ? d->n_ep : 1), 0);
+  std::vector<TmplInfo> tinfo(d->n_tmpl > 0 ? d->n_tmpl : 1, TmplInfo{1, 1, 1, 0, 0});
   for (int i = 0; i < d->n_combos; ++i) {
     const lc_combo& k = d->combos[i];
     if (k.tp_i < 0 || k.tp_i >= d->n_tp || k.ep_i < 0 || k.ep_i >= d->n_ep || k.tmpl < 0 || k.tmpl >= d->n_tmpl)
       return fail(LC_ERR_ARG, "lc_space_upload: combo index out of range");
     tpv[k.tp_i] = k.tp; epv[k.ep_i] = k.ep;
     used[(size_t)k.tp_i * d->n_ep + k.ep_i] = 1;
+    tinfo[k.tmpl] = TmplInfo{k.tp, k.pp, k.ep, k.tp_i, k.ep_i};
   }
   for (int t = 0; t < d->n_tmpl; ++t)
     if (d->tmpl_n_entries[t] > LC_MAX_ENTRIES) return fail(LC_ERR_ARG, "template has too many entries");
@@ -1226,6 +1344,19 @@ int lc_space_upload(lc_ctx* c, const lc_space_desc* d, lc_space** out) {
   if ((rc = upload(&sp->tp_vals, tpv.data(), tpv.size(), c->stream))) return rc;
   if ((rc = upload(&sp->ep_vals, epv.data(), epv.size(), c->stream))) return rc;
   if ((rc = upload(&sp->pair_used, used.data(), used.size(), c->stream))) return rc;
+  if ((rc = upload(&sp->tmpl_info, tinfo.data(), tinfo.size(), c->stream))) return rc;
+  std::vector<int32_t> canon(used.size(), 0);
+  for (int a = 0; a < (d->n_tp > 0 ? d->n_tp : 1); ++a)
+    for (int e = 0; e < (d->n_ep > 0 ? d->n_ep : 1); ++e) {
+      const int idx = a * d->n_ep + e;
+      canon[idx] = idx;
+      const int64_t f = epv[e] / tpv[a] > 1 ? epv[e] / tpv[a] : 1;
+      for (int a2 = 0; a2 < a; ++a2) {
+        const int64_t f2 = epv[e] / tpv[a2] > 1 ? epv[e] / tpv[a2] : 1;
+        if (f2 == f && used[a2 * d->n_ep + e]) { canon[idx] = a2 * d->n_ep + e; break; }
+      }
+    }
+  if ((rc = upload(&sp->pair_canon, canon.data(), canon.size(), c->stream))) return rc;
   CK(cudaStreamSynchronize(c->stream));
   *out = sp;
   return LC_OK;
@@ -1236,6 +1367,8 @@ int lc_space_free(lc_space* sp) {
   cudaSetDevice(sp->device);
   cudaFree(sp->combos); cudaFree(sp->tmpl_n); cudaFree(sp->entries); cudaFree(sp->tp_vals); cudaFree(sp->ep_vals);
   cudaFree(sp->pair_used);
+  cudaFree(sp->tmpl_info);
+  cudaFree(sp->pair_canon);
   delete sp;
   return LC_OK;
 }
@@ -1254,6 +1387,9 @@ static EvalParams make_params(lc_ctx* c) {
   P.combos = sp->combos; P.tmpl_n = sp->tmpl_n; P.entries = sp->entries;
   P.hidden = sp->hidden; P.topk = sp->topk; P.n_experts = sp->n_experts; P.is_moe = sp->is_moe;
   P.n_tp = sp->n_tp; P.n_ep = sp->n_ep; P.tp_vals = sp->tp_vals; P.ep_vals = sp->ep_vals; P.pair_used = sp->pair_used;
+  P.pair_canon = sp->pair_canon;
+  P.tail_tables = (const TailTable*)c->tail_tables.p;
+  P.n_tail_tables = (int32_t)c->htables.size();
   P.searches = (const lc_search_desc*)c->searches.p;
   P.meta = (const SearchMeta*)c->meta.p;
   P.n_search = c->n_search;
@@ -1270,6 +1406,11 @@ static EvalParams make_params(lc_ctx* c) {
   P.dc_status = (int32_t*)c->dc_status.p; P.dc_v = (double*)c->dc_v.p;
   P.err_c = (int64_t*)c->err_c.p;
   P.u_queries = (int32_t*)c->u_queries.p;
+  P.tmpl_info = sp->tmpl_info;
+  P.cell_flags = (uint32_t*)c->cell_flags.p;
+  P.cells = (CellOut*)c->cells.p;
+  P.cell_err = (int64_t*)c->cell_err.p;
+  P.n_cells_total = c->n_cells;
   P.results = (lc_search_result*)c->results.p;
   return P;
 }
@@ -1293,6 +1434,8 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   c->dc_status.get<int32_t>(n, &err); c->dc_v.get<double>(2 * n, &err);
   c->err_c.get<int64_t>(8 * n, &err);
   c->u_queries.get<int32_t>(n, &err);
+  c->cells.get<CellOut>(c->n_cells, &err);
+  c->cell_err.get<int64_t>(8 * c->n_cells, &err);
   c->pool_sel.get<int32_t>((size_t)c->n_search * 128, &err);
   c->plans_i.get<int32_t>((size_t)c->n_plan_slots * 4, &err);
   c->plans_d.get<double>((size_t)c->n_plan_slots * 6, &err);
@@ -1312,16 +1455,22 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     CK(cudaGetLastError());
   }
   CK(cudaEventRecord(c->ev[2], c->stream));
-  if (n > 0) {
+  if (c->n_cells > 0) {
     const size_t smem = c->db->smem_bytes;
-    CK(cudaFuncSetAttribute(k_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_eval_cells, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval, 128, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_cells, 128, smem));
     if (per_sm < 1) per_sm = 1;
-    int64_t blocks = (n + 127) / 128;
+    int64_t blocks = (c->n_cells + 127) / 128;
     const int64_t cap = (int64_t)sms * per_sm;
     if (blocks > cap) blocks = cap;
-    k_eval<<<(int)blocks, 128, smem, c->stream>>>(P);
+    k_eval_cells<<<(int)blocks, 128, smem, c->stream>>>(P);
+    CK(cudaGetLastError());
+  }
+  if (n > 0) {
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+    k_expand<<<(int)blocks, 256, 0, c->stream>>>(P);
     CK(cudaGetLastError());
   }
   CK(cudaEventRecord(c->ev[3], c->stream));
@@ -1351,7 +1500,9 @@ static int run_enum(lc_ctx* c) {
   uint8_t* flags = c->flags.get<uint8_t>(n_raw, &err);
   int32_t* pos = c->pos.get<int32_t>(n_raw, &err);
   int32_t* bs = c->block_sums.get<int32_t>(nblk + 1, &err);
+  uint32_t* cflags = c->cell_flags.get<uint32_t>(c->n_cells, &err);
   if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
+  if (c->n_cells) CK(cudaMemsetAsync(cflags, 0, sizeof(uint32_t) * c->n_cells, c->stream));
   EvalParams P = make_params(c);
   const int sms = sm_count(c->device);
   if (n_raw > 0) {
@@ -1394,7 +1545,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   c->n_loads = n_loads;
   // host bookkeeping: raw tuple, tail and plan offsets
   c->hmeta.assign(n_search, SearchMeta{});
-  int64_t raw = 0, tails = 0, plans = 0;
+  int64_t raw = 0, tails = 0, plans = 0, cells = 0;
   for (int s = 0; s < n_search; ++s) {
     const lc_search_desc& S = searches[s];
     if (S.n_b < 0 || S.b_off < 0 || S.b_off + S.n_b > n_batches) return fail(LC_ERR_ARG, "batch range out of bounds");
@@ -1405,15 +1556,47 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     M.raw_off = raw;
     M.n_raw = (int64_t)sp->n_combos * S.n_b;
     raw += M.n_raw;
-    M.tail_off = tails;
-    if (sp->is_moe) tails += 3ll * sp->n_tp * sp->n_ep * S.n_b;
+    M.cell_off = cells;
+    cells += (int64_t)sp->n_tmpl * S.n_b;
+    M.tail_off[0] = M.tail_off[1] = M.tail_off[2] = 0;
     M.plan_off = (int32_t)plans;
     const int pc = (S.modes & 4) ? S.prefill_cap * S.decode_cap : 0;
     if (pc > 256) return fail(LC_ERR_ARG, "prefill_cap * decode_cap above 256 is not supported");
     M.plan_cap = pc;
     plans += pc;
   }
+  // MoE tail tables, shared between searches with the same inputs
+  c->htables.clear();
+  if (sp->is_moe) {
+    std::map<std::vector<int64_t>, int32_t> blist;  // batch list -> canonical offset
+    std::map<std::vector<int64_t>, int32_t> tindex;  // (type, canonical b_off, n_b, load, chunk) -> table
+    const int64_t per_b = (int64_t)sp->n_tp * sp->n_ep;
+    for (int s = 0; s < n_search; ++s) {
+      const lc_search_desc& S = searches[s];
+      std::vector<int64_t> bl(batches + S.b_off, batches + S.b_off + S.n_b);
+      auto it = blist.find(bl);
+      const int32_t cb = it == blist.end() ? (blist[bl] = S.b_off) : it->second;
+      for (int type = 0; type < 3; ++type) {
+        std::vector<int64_t> key = {type, cb, S.n_b, S.load, type == 0 ? S.isl - S.prefix : 0, type == 2 ? s : -1};
+        auto jt = tindex.find(key);
+        int32_t ti;
+        if (jt == tindex.end()) {
+          ti = (int32_t)c->htables.size();
+          tindex[key] = ti;
+          TailTable T;
+          T.off = tails; T.type = type; T.search = s; T.b_off = cb; T.n_b = S.n_b; T.load = S.load; T._pad = 0;
+          T.chunk = S.isl - S.prefix;
+          c->htables.push_back(T);
+          tails += per_b * S.n_b;
+        } else {
+          ti = jt->second;
+        }
+        c->hmeta[s].tail_off[type] = c->htables[ti].off;
+      }
+    }
+  }
   c->n_raw = raw;
+  c->n_cells = cells;
   c->n_tails = tails;
   c->n_plan_slots = plans;
   cudaError_t err = cudaSuccess;
@@ -1421,6 +1604,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   int64_t* dB = c->batches.get<int64_t>(n_batches, &err);
   double* dL = c->loads.get<double>((size_t)n_loads * 2 * (sp->n_experts > 0 ? sp->n_experts : 1), &err);
   SearchMeta* dM = c->meta.get<SearchMeta>(n_search, &err);
+  TailTable* dT = c->tail_tables.get<TailTable>(c->htables.size(), &err);
   c->results.get<lc_search_result>(n_search, &err);
   if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
   if (n_search) CK(cudaMemcpyAsync(dS, searches, sizeof(lc_search_desc) * n_search, cudaMemcpyHostToDevice, c->stream));
@@ -1429,6 +1613,9 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     CK(cudaMemcpyAsync(dL, loads, sizeof(double) * n_loads * 2 * sp->n_experts, cudaMemcpyHostToDevice, c->stream));
   if (n_search)
     CK(cudaMemcpyAsync(dM, c->hmeta.data(), sizeof(SearchMeta) * n_search, cudaMemcpyHostToDevice, c->stream));
+  if (!c->htables.empty())
+    CK(cudaMemcpyAsync(dT, c->htables.data(), sizeof(TailTable) * c->htables.size(), cudaMemcpyHostToDevice,
+                       c->stream));
   CK(cudaEventRecord(c->ev[0], c->stream));
   int rc = run_enum(c);
   if (rc) return rc;
