@@ -178,20 +178,9 @@ def _gather_results(ws, results: np.ndarray) -> np.ndarray:
     """One NCCL all-gather of the packed per-search summaries (fixed-size records)."""
     if ws == 1:
         return results
-    import torch
-    import torch.distributed as dist
+    from paper_2601_06288_b200.dist import gather_records
 
-    raw = np.frombuffer(results.tobytes(), dtype=np.uint8)
-    n = torch.tensor([raw.size], device="cuda")
-    sizes = [torch.zeros_like(n) for _ in range(ws)]
-    dist.all_gather(sizes, n)
-    mx = int(max(int(s) for s in sizes))
-    buf = torch.zeros(mx, dtype=torch.uint8, device="cuda")
-    buf[: raw.size] = torch.from_numpy(raw.copy()).cuda()
-    outs = [torch.zeros(mx, dtype=torch.uint8, device="cuda") for _ in range(ws)]
-    dist.all_gather(outs, buf)
-    parts = [o[: int(s)].cpu().numpy().tobytes() for o, s in zip(outs, sizes)]
-    return np.concatenate([np.frombuffer(p, dtype=results.dtype) for p in parts])
+    return np.concatenate(gather_records(results))
 
 
 # --------------------------------------------------------------------------- main
@@ -247,10 +236,11 @@ def main() -> int:
 
     dev = local if ws > 1 else 0
     # shard searches across ranks: contiguous blocks of each model's workload list
+    from paper_2601_06288_b200.dist import shard_range
+
     my_parts = []
     for p in parts:
-        n = len(p.workloads)
-        lo, hi = n * rank // ws, n * (rank + 1) // ws
+        lo, hi = shard_range(len(p.workloads), rank, ws)
         my_parts.append((p, p.workloads[lo:hi]))
     # one engine (CUDA stream + resident workspace) per model so each keeps its batch resident
     engines = {p.model_name: Engine(dev) for p, w in my_parts if w}
