@@ -110,6 +110,15 @@ typedef struct {
   double kv_token_bytes;             /* memory_footprint().kv_bytes_per_token (model.py:448-452) */
 } lc_combo;
 
+/* a query family priced once per (search, batch): one step kind, one grid, one
+ * coordinate recipe (latency is a pure function of grid and coordinates) */
+enum { LC_STEP_PREFILL = 0, LC_STEP_GEN = 1, LC_STEP_MIXED = 2 };
+typedef struct {
+  lc_entry e;                        /* grid, kind, quant, fixed dims, coordinate recipe */
+  int32_t step;                      /* LC_STEP_* */
+  int32_t pair;                      /* expert recipe: tp_i * n_ep + ep_i, else -1 */
+} lc_slot;
+
 typedef struct {
   int64_t hidden, topk, n_experts;
   int32_t is_moe;
@@ -119,6 +128,12 @@ typedef struct {
   const int32_t* tmpl_n_entries;     /* [n_tmpl] */
   const lc_entry* entries;           /* [n_tmpl * LC_MAX_ENTRIES] */
   int32_t n_tp, n_ep;                /* sizes of the tp / ep value lists */
+  int32_t n_slots;
+  const lc_slot* slots;
+  const int32_t* slot_of;            /* [n_tmpl * LC_MAX_ENTRIES * 3]: slot per (template, entry, step), -1 absent */
+  int32_t n_gen_classes;             /* distinct generation-attention grids (static decode series) */
+  const lc_entry* gen_classes;
+  const int32_t* gclass_of;          /* [n_tmpl] */
 } lc_space_desc;
 
 /* ------------------------------------------------------------------ search */
@@ -156,7 +171,7 @@ typedef struct {
 
 typedef struct {
   int64_t n_units, n_plans, n_front;
-  float kernel_ms[6];                /* K0 enumerate, K3 tails, K2 evaluate, K5a pools, K5b disagg, K4 front */
+  float kernel_ms[6];                /* K0 enumerate, K3 tails, K2 evaluate (tables + cells + expand), K5a pools, K5b disagg, K4 front */
   int64_t n_raw;                     /* raw (tp,pp,ep,dp,batch) tuples examined */
 } lc_batch_totals;
 

@@ -38,7 +38,9 @@ class LcDbDesc(C.Structure):
 class LcSpaceDesc(C.Structure):
     _fields_ = [("hidden", C.c_int64), ("topk", C.c_int64), ("n_experts", C.c_int64), ("is_moe", C.c_int32),
                 ("n_combos", C.c_int32), ("combos", C.c_void_p), ("n_tmpl", C.c_int32),
-                ("tmpl_n_entries", I32P), ("entries", C.c_void_p), ("n_tp", C.c_int32), ("n_ep", C.c_int32)]
+                ("tmpl_n_entries", I32P), ("entries", C.c_void_p), ("n_tp", C.c_int32), ("n_ep", C.c_int32),
+                ("n_slots", C.c_int32), ("slots", C.c_void_p), ("slot_of", I32P), ("n_gen_classes", C.c_int32),
+                ("gen_classes", C.c_void_p), ("gclass_of", I32P)]
 
 
 class LcSearchDesc(C.Structure):

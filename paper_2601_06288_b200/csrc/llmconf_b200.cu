@@ -97,6 +97,18 @@ struct lc_space {
   uint8_t* pair_used;  // [n_tp*n_ep]
   int32_t* pair_canon; // [n_tp*n_ep] first pair with the same (max(1, ep/tp), ep): identical tails
   struct TmplInfo* tmpl_info;  // [n_tmpl]
+  int32_t n_slots, n_gclass;
+  lc_slot* slots;
+  int32_t* slot_of;    // [n_tmpl][16][3]
+  lc_entry* gclasses;
+  int32_t* gclass_of;  // [n_tmpl]
+};
+
+// one priced query (query tables and decode-series tables)
+struct QVal {
+  double lat;
+  int32_t status;
+  int32_t _pad;
 };
 
 // One MoE tail table: [tp_i * n_ep + ep_i][b_i].  Prefill-type tables depend on
@@ -120,6 +132,10 @@ struct SearchMeta {
   int64_t raw_off, n_raw;
   int64_t cell_off;
   int64_t tail_off[3];  // per tail type
+  int64_t qt_off;       // query table [slot][b_i]
+  int64_t ds_off;       // decode-series table [gclass][b_i][step]
+  int32_t n_steps;      // static decode samples (ceil((osl-1)/32), 0 without static mode)
+  int32_t _pad2;
   int32_t unit_off, n_units;
   int32_t plan_off, plan_cap;
   int32_t pool_off;  // into pool selection arrays (64 slots per role)
@@ -134,12 +150,13 @@ struct lc_ctx {
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
-  DBuf tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
+  DBuf qt, ds, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   // last batch
   const lc_db* db = nullptr;
   const lc_space* sp = nullptr;
   int32_t n_search = 0, n_batches = 0, n_loads = 0;
   int64_t n_raw = 0, n_cap = 0, n_units = 0, n_tails = 0, n_plan_slots = 0, n_front_slots = 0, n_cells = 0;
+  int64_t n_qt = 0, n_ds = 0;
   int64_t n_total_idx = 0;  // index of the unit total inside block_sums
   std::vector<SearchMeta> hmeta;
   std::vector<TailTable> htables;
@@ -163,6 +180,10 @@ struct EvalParams {
   int64_t hidden, topk, n_experts; int32_t is_moe, n_tp, n_ep;
   const int64_t* tp_vals; const int64_t* ep_vals; const uint8_t* pair_used; const int32_t* pair_canon;
   const TailTable* tail_tables; int32_t n_tail_tables;
+  const lc_slot* slots; int32_t n_slots; const int32_t* slot_of;
+  const lc_entry* gclasses; int32_t n_gclass; const int32_t* gclass_of;
+  QVal* qt; int64_t n_qt;
+  QVal* ds; int64_t n_ds;
   // batch
   const lc_search_desc* searches; const SearchMeta* meta; int32_t n_search;
   const int64_t* batches; const double* loads;
@@ -422,10 +443,130 @@ __device__ __forceinline__ int find_cell_search(const SearchMeta* meta, int n, i
   return lo;
 }
 
-__global__ void __launch_bounds__(128) k_eval_cells(EvalParams P) {
+__device__ __forceinline__ int find_by_off(const SearchMeta* meta, int n, int64_t x, int which) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    const int64_t o = which == 0 ? meta[mid].qt_off : meta[mid].ds_off;
+    if (o <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ int64_t tail_tokens(const EvalParams& P, const SearchMeta& M, const lc_search_desc& S,
+                                               int type, int pair, int bi, int64_t tokens) {
+  // expert_tokens() for a (tp_i, ep_i) pair index (estimator.py:58-68, model.py:372-373)
+  const int64_t tp = P.tp_vals[pair / P.n_ep], ep = P.ep_vals[pair % P.n_ep];
+  const int64_t f = ep / tp > 1 ? ep / tp : 1;
+  const int64_t pooled = tokens * f;
+  const int64_t balanced = ceil_div_f(pooled * P.topk, ep);
+  if (ep == 1 || S.load < 0) return balanced;
+  const int64_t tail = P.tails[M.tail_off[type] + (int64_t)P.pair_canon[pair] * S.n_b + bi];
+  return balanced > tail ? balanced : tail;
+}
+
+// K2a: query tables.  One thread per (search, slot, batch): the latency every
+// template entry of that slot sees in that step (query_latency, perfdb.py:539-580).
+__global__ void __launch_bounds__(128) k_qtables(EvalParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   DbView V;
   stage_db(P, smem, &V);
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < P.n_qt; x += (int64_t)gridDim.x * blockDim.x) {
+    const int s = find_by_off(P.meta, P.n_search, x, 0);
+    const lc_search_desc& S = P.searches[s];
+    const SearchMeta& M = P.meta[s];
+    const int64_t rel = x - M.qt_off;
+    const int slot = (int)(rel / S.n_b), bi = (int)(rel % S.n_b);
+    const lc_slot SL = P.slots[slot];
+    QVal out{0.0, LC_ST_NOT_EVALUATED, 0};
+    const int64_t b = P.batches[S.b_off + bi];
+    const int64_t chunk = S.isl - S.prefix;
+    const int64_t kv_mid = S.isl + S.osl / 2;
+    bool need = false;
+    StepArgs a{PH_DECODE, 0, b, kv_mid, 0};
+    int type = 1;
+    if (SL.step == LC_STEP_PREFILL) {
+      need = (S.modes & 5) != 0;
+      a = StepArgs{PH_PREFILL, b * chunk, 0, chunk, 0};
+      type = 0;
+    } else if (SL.step == LC_STEP_GEN) {
+      need = (S.modes & 7) != 0;
+    } else {
+      const AggSched sc = agg_schedule(S, b);
+      need = (S.modes & 2) && !sc.st;
+      a = StepArgs{PH_MIXED, sc.chunk_tokens, sc.n_mix_gen, kv_mid, 0};
+      type = 2;
+    }
+    if (need && SL.e.coord == LC_COORD_EXPERT)
+      a.expert_tokens = tail_tokens(P, M, S, type, SL.pair, bi, a.n_ctx + a.n_gen);
+    int64_t d[5];
+    if (need && entry_coords(SL.e, a, P.hidden, d)) {
+      int st = 0, nlog = 0;
+      out.lat = query(V, SL.e, d, &st, &nlog);
+      out.status = st;
+    }
+    P.qt[x] = out;
+  }
+}
+
+// K2a': generation-attention latency at every sampled KV length of the static
+// decode loop (serving_modes.py:258-265): one thread per (search, grid, batch, sample).
+__global__ void __launch_bounds__(128) k_dstables(EvalParams P) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  DbView V;
+  stage_db(P, smem, &V);
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < P.n_ds; x += (int64_t)gridDim.x * blockDim.x) {
+    const int s = find_by_off(P.meta, P.n_search, x, 1);
+    const lc_search_desc& S = P.searches[s];
+    const SearchMeta& M = P.meta[s];
+    int64_t rel = x - M.ds_off;
+    const int k = (int)(rel % M.n_steps);
+    rel /= M.n_steps;
+    const int bi = (int)(rel % S.n_b);
+    const int g = (int)(rel / S.n_b);
+    const lc_entry e = P.gclasses[g];
+    int64_t d[5] = {P.batches[S.b_off + bi], S.isl + 32ll * k + 1, e.d[2], e.d[3], e.d[4]};
+    int st = 0, nlog = 0;
+    QVal out;
+    out.lat = query(V, e, d, &st, &nlog);
+    out.status = st;
+    out._pad = 0;
+    P.ds[x] = out;
+  }
+}
+
+// One step's total from the query table: sum in plan order of
+// ((lat * repeat) / 1000) * bubble, CPython sum() semantics (estimator.py:83-95);
+// the first failing entry in plan order decides the error.
+__device__ __forceinline__ int table_step(const EvalParams& P, const lc_entry* E, int ne, const int32_t* slot_row,
+                                          const QVal* qt, int n_b, int bi, const StepArgs& a, double bubble,
+                                          double* out, ErrRec* err, int* q1, int* q2) {
+  NeumaierSum sum;
+  int c1 = 0, c2 = 0;
+  for (int i = 0; i < ne; ++i) {
+    const lc_entry& e = E[i];
+    if (e.coord == LC_COORD_CTX && !a.n_ctx) continue;
+    if (e.coord == LC_COORD_GEN && !a.n_gen) continue;
+    const QVal q = qt[(int64_t)slot_row[i * 3] * n_b + bi];
+    if (e.coord == LC_COORD_CTX || e.coord == LC_COORD_GEN) ++c2; else ++c1;
+    if (q.status) {
+      int64_t d[5];
+      entry_coords(e, a, P.hidden, d);
+      err->code = q.status; err->label = e.label; err->c0 = d[0]; err->c1 = d[1];
+      return q.status;
+    }
+    const double ms = q.lat * (double)e.repeat / 1000.0;
+    sum.add(0.0 + ms * bubble);
+  }
+  *out = sum.result();
+  *q1 = c1;
+  *q2 = c2;
+  return 0;
+}
+
+// K2: one thread per cell assembles every step from the tables.
+__global__ void __launch_bounds__(128) k_eval_cells(EvalParams P) {
   const int64_t ncell = P.n_cells_total;
   for (int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ci < ncell;
        ci += (int64_t)gridDim.x * blockDim.x) {
@@ -441,42 +582,88 @@ __global__ void __launch_bounds__(128) k_eval_cells(EvalParams P) {
     c.tp = ti.tp; c.pp = ti.pp; c.ep = ti.ep; c.tp_i = ti.tp_i; c.ep_i = ti.ep_i;
     const lc_entry* E = P.entries + (int64_t)tmpl * LC_MAX_ENTRIES;
     const int ne = P.tmpl_n[tmpl];
+    const int32_t* so = P.slot_of + (int64_t)tmpl * LC_MAX_ENTRIES * 3;
+    const QVal* qt = P.qt + M.qt_off;
     const int64_t b = P.batches[S.b_off + bi];
     const bool do_st = (cf & 1) && (S.modes & 1), do_ag = (cf & 1) && (S.modes & 2), do_dg = (cf & 2) != 0;
     const int64_t mb = b > 1 ? b : 1;
     const double bubble = (double)(mb + ti.pp - 1) / (double)mb;
     const int64_t chunk = S.isl - S.prefix;
     const int64_t kv_mid = S.isl + S.osl / 2;
-    StepStats ss{0, 0, 0};
     CellOut o;
     o.st_status = o.ag_status = o.pf_status = o.dc_status = LC_ST_NOT_EVALUATED;
     o.st_ttft = o.st_tpot = o.ag_ttft = o.ag_tpot = o.pf_lat = o.dc_lat = 0.0;
     o.qP = o.qSD = o.qM = o.qG = 0;
     o.st_steps = 0;
     o.flags = 0;
+    int q1 = 0, q2 = 0;
 
-    // prefill step: static TTFT and the prefill pool (the estimator memo shares it)
+    // prefill step: static TTFT and the prefill pool
     double p_total = 0.0;
     ErrRec p_err{0, 0, 0, 0};
     if (do_st || do_dg) {
-      StepArgs a{PH_PREFILL, b * chunk, 0, chunk, expert_tokens(P, c, M, S, 0, bi, b * chunk)};
-      step_total(V, E, ne, a, bubble, P.hidden, &p_total, &p_err, &ss);
-      if (!p_err.code) o.qP = (ss.q1 & 0xffff) | (ss.q2 << 16);
-      ss.q1 = ss.q2 = 0;
+      const StepArgs a{PH_PREFILL, b * chunk, 0, chunk, expert_tokens(P, c, M, S, 0, bi, b * chunk)};
+      table_step(P, E, ne, so + LC_STEP_PREFILL, qt, S.n_b, bi, a, bubble, &p_total, &p_err, &q1, &q2);
+      if (!p_err.code) o.qP = (q1 & 0xffff) | (q2 << 16);
       o.pf_status = p_err.code | (p_err.label << 8);
       o.pf_lat = p_total;
       if (p_err.code) put_cell_err(P, 2, ci, p_err);
     }
     const int64_t xt_dec = expert_tokens(P, c, M, S, 1, bi, b);
+    const StepArgs ga{PH_DECODE, 0, b, kv_mid, xt_dec};
     if (do_st) {
       double tpot = 0.0;
       ErrRec e = p_err;
-      if (!e.code) {
-        int32_t steps = 0;
-        static_decode(V, E, ne, b, S.isl, S.osl, xt_dec, bubble, P.hidden, &tpot, &e, &ss, &steps);
-        if (!e.code) o.qSD = (ss.q1 & 0xffff) | (ss.q2 << 16);
-        ss.q1 = ss.q2 = 0;
-        o.st_steps = steps;
+      if (!e.code && S.osl > 1) {
+        // static decode loop (serving_modes.py:256-266): non-attention terms from the
+        // generation-step slots (same tokens), attention from the decode-series table
+        double term[LC_MAX_ENTRIES];
+        int m = 0, gi = -1;
+        const QVal* ds = P.ds + M.ds_off + ((int64_t)P.gclass_of[tmpl] * S.n_b + bi) * M.n_steps;
+        const lc_entry* ge = nullptr;
+        const StepArgs a0{PH_DECODE, 0, b, S.isl + 1, xt_dec};
+        for (int i = 0; i < ne && !e.code; ++i) {
+          const lc_entry& en = E[i];
+          if (en.coord == LC_COORD_CTX) continue;
+          QVal q;
+          if (en.coord == LC_COORD_GEN) { q = ds[0]; gi = m; ge = &en; }
+          else q = qt[(int64_t)so[i * 3 + LC_STEP_GEN] * S.n_b + bi];
+          if (q.status) {
+            int64_t d[5];
+            entry_coords(en, a0, P.hidden, d);
+            e.code = q.status; e.label = en.label; e.c0 = d[0]; e.c1 = d[1];
+            break;
+          }
+          const double ms = q.lat * (double)en.repeat / 1000.0;
+          term[m++] = 0.0 + ms * bubble;
+        }
+        if (!e.code) {
+          double t_gen = 0.0;
+          int64_t k = 0;
+          int step = 0;
+          while (k < S.osl - 1) {
+            if (step > 0) {
+              const QVal q = ds[step];
+              if (q.status) {
+                e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + k + 1;
+                break;
+              }
+              const double ms = q.lat * (double)ge->repeat / 1000.0;
+              term[gi] = 0.0 + ms * bubble;
+            }
+            NeumaierSum sum;
+            for (int i = 0; i < m; ++i) sum.add(term[i]);
+            const int64_t run = (S.osl - 1 - k) < 32 ? (S.osl - 1 - k) : 32;
+            t_gen += sum.result() * (double)run;
+            k += run;
+            ++step;
+          }
+          if (!e.code) {
+            tpot = t_gen / (double)(S.osl - 1);
+            o.qSD = ((m - 1) * step & 0xffff) | (step << 16);
+            o.st_steps = step;
+          }
+        }
       }
       o.st_status = e.code | (e.label << 8);
       o.st_ttft = p_total;
@@ -493,17 +680,14 @@ __global__ void __launch_bounds__(128) k_eval_cells(EvalParams P) {
       double ttft = 0.0, tpot = 0.0;
       if (!sc.st) {
         double l_mix = 0.0, l_gen = 0.0;
-        StepArgs a{PH_MIXED, sc.chunk_tokens, sc.n_mix_gen, kv_mid,
-                   expert_tokens(P, c, M, S, 2, bi, sc.chunk_tokens + sc.n_mix_gen)};
-        step_total(V, E, ne, a, bubble, P.hidden, &l_mix, &e, &ss);
-        if (!e.code) o.qM = (ss.q1 & 0xffff) | (ss.q2 << 16);
-        ss.q1 = ss.q2 = 0;
+        const StepArgs a{PH_MIXED, sc.chunk_tokens, sc.n_mix_gen, kv_mid,
+                         expert_tokens(P, c, M, S, 2, bi, sc.chunk_tokens + sc.n_mix_gen)};
+        table_step(P, E, ne, so + LC_STEP_MIXED, qt, S.n_b, bi, a, bubble, &l_mix, &e, &q1, &q2);
+        if (!e.code) o.qM = (q1 & 0xffff) | (q2 << 16);
         if (!e.code && (sc.t_gen || b == 1)) {
-          StepArgs g{PH_DECODE, 0, b, kv_mid, xt_dec};
-          step_total(V, E, ne, g, bubble, P.hidden, &g_total, &g_err, &ss);
+          table_step(P, E, ne, so + LC_STEP_GEN, qt, S.n_b, bi, ga, bubble, &g_total, &g_err, &q1, &q2);
           g_done = true;
-          if (!g_err.code) o.qG = (ss.q1 & 0xffff) | (ss.q2 << 16);
-          ss.q1 = ss.q2 = 0;
+          if (!g_err.code) o.qG = (q1 & 0xffff) | (q2 << 16);
           o.flags |= 1;
           e = g_err;
           l_gen = g_total;
@@ -529,10 +713,8 @@ __global__ void __launch_bounds__(128) k_eval_cells(EvalParams P) {
     }
     if (do_dg) {
       if (!g_done) {
-        StepArgs g{PH_DECODE, 0, b, kv_mid, xt_dec};
-        step_total(V, E, ne, g, bubble, P.hidden, &g_total, &g_err, &ss);
-        if (!g_err.code) o.qG = (ss.q1 & 0xffff) | (ss.q2 << 16);
-        ss.q1 = ss.q2 = 0;
+        table_step(P, E, ne, so + LC_STEP_GEN, qt, S.n_b, bi, ga, bubble, &g_total, &g_err, &q1, &q2);
+        if (!g_err.code) o.qG = (q1 & 0xffff) | (q2 << 16);
       }
       o.dc_status = g_err.code | (g_err.label << 8);
       o.dc_lat = g_total;
@@ -1267,7 +1449,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->qt, &c->ds, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
@@ -1357,6 +1539,13 @@ int lc_space_upload(lc_ctx* c, const lc_space_desc* d, lc_space** out) {
       }
     }
   if ((rc = upload(&sp->pair_canon, canon.data(), canon.size(), c->stream))) return rc;
+  sp->n_slots = d->n_slots;
+  sp->n_gclass = d->n_gen_classes;
+  if ((rc = upload(&sp->slots, d->slots, d->n_slots > 0 ? d->n_slots : 0, c->stream))) return rc;
+  if ((rc = upload(&sp->slot_of, d->slot_of, (size_t)(d->n_tmpl > 0 ? d->n_tmpl : 1) * LC_MAX_ENTRIES * 3, c->stream)))
+    return rc;
+  if ((rc = upload(&sp->gclasses, d->gen_classes, d->n_gen_classes > 0 ? d->n_gen_classes : 0, c->stream))) return rc;
+  if ((rc = upload(&sp->gclass_of, d->gclass_of, d->n_tmpl > 0 ? d->n_tmpl : 1, c->stream))) return rc;
   CK(cudaStreamSynchronize(c->stream));
   *out = sp;
   return LC_OK;
@@ -1369,6 +1558,7 @@ int lc_space_free(lc_space* sp) {
   cudaFree(sp->pair_used);
   cudaFree(sp->tmpl_info);
   cudaFree(sp->pair_canon);
+  cudaFree(sp->slots); cudaFree(sp->slot_of); cudaFree(sp->gclasses); cudaFree(sp->gclass_of);
   delete sp;
   return LC_OK;
 }
@@ -1390,6 +1580,10 @@ static EvalParams make_params(lc_ctx* c) {
   P.pair_canon = sp->pair_canon;
   P.tail_tables = (const TailTable*)c->tail_tables.p;
   P.n_tail_tables = (int32_t)c->htables.size();
+  P.slots = sp->slots; P.n_slots = sp->n_slots; P.slot_of = sp->slot_of;
+  P.gclasses = sp->gclasses; P.n_gclass = sp->n_gclass; P.gclass_of = sp->gclass_of;
+  P.qt = (QVal*)c->qt.p; P.n_qt = c->n_qt;
+  P.ds = (QVal*)c->ds.p; P.n_ds = c->n_ds;
   P.searches = (const lc_search_desc*)c->searches.p;
   P.meta = (const SearchMeta*)c->meta.p;
   P.n_search = c->n_search;
@@ -1435,6 +1629,8 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   c->err_c.get<int64_t>(8 * n, &err);
   c->u_queries.get<int32_t>(n, &err);
   c->cells.get<CellOut>(c->n_cells, &err);
+  c->qt.get<QVal>(c->n_qt, &err);
+  c->ds.get<QVal>(c->n_ds, &err);
   c->cell_err.get<int64_t>(8 * c->n_cells, &err);
   c->pool_sel.get<int32_t>((size_t)c->n_search * 128, &err);
   c->plans_i.get<int32_t>((size_t)c->n_plan_slots * 4, &err);
@@ -1455,16 +1651,32 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     CK(cudaGetLastError());
   }
   CK(cudaEventRecord(c->ev[2], c->stream));
-  if (c->n_cells > 0) {
-    const size_t smem = c->db->smem_bytes;
-    CK(cudaFuncSetAttribute(k_eval_cells, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  {
+    EvalParams P2 = make_params(c);  // table pointers are valid only after the allocations above
+    P = P2;
+  }
+  const size_t smem = c->db->smem_bytes;
+  auto launch_tables = [&](auto kern, int64_t n_items) -> int {
+    if (n_items <= 0) return LC_OK;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_eval_cells, 128, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
     if (per_sm < 1) per_sm = 1;
-    int64_t blocks = (c->n_cells + 127) / 128;
+    int64_t blocks = (n_items + 127) / 128;
     const int64_t cap = (int64_t)sms * per_sm;
     if (blocks > cap) blocks = cap;
-    k_eval_cells<<<(int)blocks, 128, smem, c->stream>>>(P);
+    kern<<<(int)blocks, 128, smem, c->stream>>>(P);
+    CK(cudaGetLastError());
+    return LC_OK;
+  };
+  int rc2 = launch_tables(k_qtables, c->n_qt);
+  if (rc2) return rc2;
+  rc2 = launch_tables(k_dstables, c->n_ds);
+  if (rc2) return rc2;
+  if (c->n_cells > 0) {
+    int64_t blocks = (c->n_cells + 127) / 128;
+    if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+    k_eval_cells<<<(int)blocks, 128, 0, c->stream>>>(P);
     CK(cudaGetLastError());
   }
   if (n > 0) {
@@ -1545,7 +1757,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   c->n_loads = n_loads;
   // host bookkeeping: raw tuple, tail and plan offsets
   c->hmeta.assign(n_search, SearchMeta{});
-  int64_t raw = 0, tails = 0, plans = 0, cells = 0;
+  int64_t raw = 0, tails = 0, plans = 0, cells = 0, qts = 0, dss = 0;
   for (int s = 0; s < n_search; ++s) {
     const lc_search_desc& S = searches[s];
     if (S.n_b < 0 || S.b_off < 0 || S.b_off + S.n_b > n_batches) return fail(LC_ERR_ARG, "batch range out of bounds");
@@ -1558,6 +1770,11 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     raw += M.n_raw;
     M.cell_off = cells;
     cells += (int64_t)sp->n_tmpl * S.n_b;
+    M.qt_off = qts;
+    qts += (int64_t)sp->n_slots * S.n_b;
+    M.n_steps = ((S.modes & 1) && S.osl > 1) ? (int32_t)((S.osl - 1 + 31) / 32) : 0;
+    M.ds_off = dss;
+    dss += (int64_t)sp->n_gclass * S.n_b * M.n_steps;
     M.tail_off[0] = M.tail_off[1] = M.tail_off[2] = 0;
     M.plan_off = (int32_t)plans;
     const int pc = (S.modes & 4) ? S.prefill_cap * S.decode_cap : 0;
@@ -1597,6 +1814,8 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   }
   c->n_raw = raw;
   c->n_cells = cells;
+  c->n_qt = qts;
+  c->n_ds = dss;
   c->n_tails = tails;
   c->n_plan_slots = plans;
   cudaError_t err = cudaSuccess;

@@ -189,6 +189,12 @@ class Engine:
         d.tmpl_n_entries = N.ptr(plan.tmpl_n, C.c_int32)
         d.entries = N.vptr(plan.entries)
         d.n_tp, d.n_ep = len(plan.tp_values), len(plan.ep_values)
+        d.n_slots = plan.n_slots
+        d.slots = N.vptr(plan.slots)
+        d.slot_of = N.ptr(plan.slot_of, C.c_int32)
+        d.n_gen_classes = plan.n_gen
+        d.gen_classes = N.vptr(plan.gen_entries)
+        d.gclass_of = N.ptr(plan.gclass_of, C.c_int32)
         h = C.c_void_p()
         self._call(self.lib.lc_space_upload, "lc_space_upload", self.ctx, C.byref(d), C.byref(h))
         self._spaces[key] = (h, plan, weakref.ref(db))

@@ -36,6 +36,8 @@ MAX_ENTRIES = 16
 
 ENTRY_DTYPE = np.dtype([("label", "<i4"), ("kind", "<i4"), ("quant", "<i4"), ("grid", "<i4"), ("coord", "<i4"),
                         ("_pad", "<i4"), ("repeat", "<i8"), ("d", "<i8", (5,))])
+SLOT_DTYPE = np.dtype([("e", ENTRY_DTYPE), ("step", "<i4"), ("pair", "<i4")])
+STEP_P, STEP_G, STEP_M = 0, 1, 2  # prefill (b*chunk), decode at kv midpoint (b), mixed chunk
 COMBO_DTYPE = np.dtype([("tp", "<i8"), ("pp", "<i8"), ("ep", "<i8"), ("dp", "<i8"), ("gpus", "<i8"),
                         ("tp_i", "<i4"), ("ep_i", "<i4"), ("tmpl", "<i4"), ("_pad", "<i4"),
                         ("weight_bytes", "<f8"), ("kv_token_bytes", "<f8")])
@@ -137,6 +139,63 @@ def _template(model, flat: FlatDb, tp: int, pp: int, ep: int) -> tuple[np.ndarra
     return arr[: len(rows)], [info for _, info in rows]
 
 
+def _present(coord: int, step: int) -> bool:
+    """Static presence of an entry in a step's plan (context attention needs n_ctx,
+    generation attention n_gen; the mixed step's n_gen can still be 0 at batch 1)."""
+    if coord == COORD_CTX:
+        return step != STEP_G
+    if coord == COORD_GEN:
+        return step != STEP_P
+    return True
+
+
+def build_slots(entries: np.ndarray, tmpl_n: np.ndarray, combos: np.ndarray, n_ep: int):
+    """Distinct (step, grid, coordinate recipe[, expert (tp,ep) pair]) query families.
+
+    Latency is a pure function of (grid, coordinates) (the grid key fixes kind,
+    quant and every fixed dim), so one slot serves every template entry that
+    shares it; the device prices each slot once per (search, batch).
+    Returns (slots, slot_of[n_tmpl, 16, 3], gen_classes, gclass_of[n_tmpl]).
+    """
+    n_tmpl = len(tmpl_n)
+    pair_of = {}
+    for c in combos:
+        pair_of[int(c["tmpl"])] = (int(c["tp_i"]), int(c["ep_i"]))
+    slots, index = [], {}
+    slot_of = np.full((max(n_tmpl, 1), MAX_ENTRIES, 3), -1, dtype=np.int32)
+    gen, gindex = [], {}
+    gclass_of = np.full(max(n_tmpl, 1), -1, dtype=np.int32)
+    for t in range(n_tmpl):
+        tp_i, ep_i = pair_of.get(t, (0, 0))
+        for i in range(int(tmpl_n[t])):
+            e = entries[t * MAX_ENTRIES + i]
+            coord, grid = int(e["coord"]), int(e["grid"])
+            pair = tp_i * n_ep + ep_i if coord == COORD_EXPERT else -1
+            for step in (STEP_P, STEP_G, STEP_M):
+                if not _present(coord, step):
+                    continue
+                key = (step, grid, coord, pair) if grid >= 0 else (step, -1, coord, pair)
+                if key not in index:
+                    index[key] = len(slots)
+                    slots.append((e, step, pair))
+                slot_of[t, i, step] = index[key]
+            if coord == COORD_GEN:
+                gk = grid
+                if gk not in gindex:
+                    gindex[gk] = len(gen)
+                    gen.append(e)
+                gclass_of[t] = gindex[gk]
+    arr = np.zeros(max(len(slots), 1), dtype=SLOT_DTYPE)
+    for k, (e, step, pair) in enumerate(slots):
+        arr[k]["e"] = e
+        arr[k]["step"] = step
+        arr[k]["pair"] = pair
+    garr = np.zeros(max(len(gen), 1), dtype=ENTRY_DTYPE)
+    for k, e in enumerate(gen):
+        garr[k] = e
+    return arr[: max(len(slots), 1)], len(slots), slot_of, garr, len(gen), gclass_of
+
+
 @dataclass
 class SpacePlan:
     """Everything lc_space_upload needs, plus host lookups for report building."""
@@ -153,6 +212,12 @@ class SpacePlan:
     hidden: int
     topk: int
     n_experts: int
+    slots: np.ndarray = None
+    n_slots: int = 0
+    slot_of: np.ndarray = None
+    gen_entries: np.ndarray = None
+    n_gen: int = 0
+    gclass_of: np.ndarray = None
 
 
 def build_space_plan(model, space, flat: FlatDb, backend: str) -> SpacePlan:
@@ -199,6 +264,8 @@ def build_space_plan(model, space, flat: FlatDb, backend: str) -> SpacePlan:
     combo_arr = np.array(combos, dtype=COMBO_DTYPE) if combos else np.zeros(0, dtype=COMBO_DTYPE)
     ent = np.concatenate(entries) if entries else np.zeros(MAX_ENTRIES, dtype=ENTRY_DTYPE)
     moe = model.moe
-    return SpacePlan(tp_values, pp_values, ep_values, dp_values, combo_arr,
-                     np.array(tmpl_n if tmpl_n else [0], dtype=np.int32), ent, infos, moe is not None,
-                     model.hidden_size, moe.topk if moe else 0, moe.num_experts if moe else 0)
+    tmpl_arr = np.array(tmpl_n if tmpl_n else [0], dtype=np.int32)
+    slots, n_slots, slot_of, gen, n_gen, gclass_of = build_slots(ent, np.array(tmpl_n, dtype=np.int32), combo_arr, len(ep_values))
+    return SpacePlan(tp_values, pp_values, ep_values, dp_values, combo_arr, tmpl_arr, ent, infos, moe is not None,
+                     model.hidden_size, moe.topk if moe else 0, moe.num_experts if moe else 0,
+                     slots, n_slots, slot_of, gen, n_gen, gclass_of)
