@@ -135,6 +135,7 @@ struct SearchMeta {
   int64_t qt_off;       // query table [slot][b_i]
   int64_t ds_off;       // decode-series table [gclass][b_i][step]
   int32_t n_steps;      // static decode samples (ceil((osl-1)/32), 0 without static mode)
+  int64_t mark_off;     // offset of this search's batches in the mixed-token marking pass
   int32_t _pad2;
   int32_t unit_off, n_units;
   int32_t plan_off, plan_cap;
@@ -150,13 +151,13 @@ struct lc_ctx {
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
-  DBuf qt, ds, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
+  DBuf qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   // last batch
   const lc_db* db = nullptr;
   const lc_space* sp = nullptr;
   int32_t n_search = 0, n_batches = 0, n_loads = 0;
   int64_t n_raw = 0, n_cap = 0, n_units = 0, n_tails = 0, n_plan_slots = 0, n_front_slots = 0, n_cells = 0;
-  int64_t n_qt = 0, n_ds = 0;
+  int64_t n_qt = 0, n_ds = 0, n_pd_tails = 0, m_tmax = 0, n_marks = 0;
   int64_t n_total_idx = 0;  // index of the unit total inside block_sums
   std::vector<SearchMeta> hmeta;
   std::vector<TailTable> htables;
@@ -180,6 +181,9 @@ struct EvalParams {
   int64_t hidden, topk, n_experts; int32_t is_moe, n_tp, n_ep;
   const int64_t* tp_vals; const int64_t* ep_vals; const uint8_t* pair_used; const int32_t* pair_canon;
   const TailTable* tail_tables; int32_t n_tail_tables;
+  int64_t n_pd_tails;                // prefill/decode tables; the dense mixed region follows
+  int64_t m_tmax;                    // mixed tokens index range [0, m_tmax]
+  uint8_t* m_used;                   // [n_loads][m_tmax + 1] mixed token counts in use
   const lc_slot* slots; int32_t n_slots; const int32_t* slot_of;
   const lc_entry* gclasses; int32_t n_gclass; const int32_t* gclass_of;
   QVal* qt; int64_t n_qt;
@@ -346,6 +350,26 @@ __global__ void k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
       if (P.tail_tables[mid].off <= t) lo = mid;
       else hi = mid - 1;
     }
+    int64_t result = 0;
+    if (t >= P.n_pd_tails) {
+      // dense mixed region: (load, pair, tokens)
+      int64_t r = t - P.n_pd_tails;
+      const int64_t tok = r % (P.m_tmax + 1);
+      r /= (P.m_tmax + 1);
+      const int pair = (int)(r % npair);
+      const int load = (int)(r / npair);
+      const int tp_i = pair / P.n_ep, ep_i = pair % P.n_ep;
+      const int64_t tp = P.tp_vals[tp_i], ep = P.ep_vals[ep_i];
+      if (ep > 1 && P.pair_used[pair] && P.pair_canon[pair] == pair && P.m_used[(int64_t)load * (P.m_tmax + 1) + tok]) {
+        const int64_t f = ep / tp > 1 ? ep / tp : 1;
+        const int E = (int)P.n_experts;
+        const double* q = P.loads + (int64_t)load * 2 * E;
+        if (E <= 256) result = warp_busiest_shard<8>(q, q + E, E, tok * f, P.topk, ep, hist);
+        else result = warp_busiest_shard<32>(q, q + E, E, tok * f, P.topk, ep, hist);
+        if (lane == 0) tails[t] = result;
+      }
+      continue;
+    }
     const TailTable T = P.tail_tables[lo];
     const int64_t rel = t - T.off;
     const int bi = (int)(rel % T.n_b);
@@ -355,15 +379,8 @@ __global__ void k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
     const int64_t tp = P.tp_vals[tp_i], ep = P.ep_vals[ep_i];
     if (!(ep > 1 && P.pair_used[pair] && P.pair_canon[pair] == pair && T.load >= 0)) continue;
     const int64_t b = P.batches[T.b_off + bi];
-    int64_t tokens = -1;
-    if (T.type == 0) tokens = b * T.chunk;
-    else if (T.type == 1) tokens = b;
-    else {
-      const AggSched a = agg_schedule(P.searches[T.search], b);
-      if (!a.st) tokens = a.chunk_tokens + a.n_mix_gen;
-    }
-    int64_t result = 0;
-    if (tokens >= 0) {
+    const int64_t tokens = T.type == 0 ? b * T.chunk : b;
+    {
       const int64_t f = ep / tp > 1 ? ep / tp : 1;
       const int64_t pooled = tokens * f;
       const int E = (int)P.n_experts;
@@ -374,6 +391,25 @@ __global__ void k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
         result = warp_busiest_shard<32>(q, q + E, E, pooled, P.topk, ep, hist);
     }
     if (lane == 0) tails[t] = result;
+  }
+}
+
+// K3 prologue: mark the mixed-step token counts some (search, batch) will look up
+__global__ void k_mark_mixed(EvalParams P, int64_t n_items) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n_items; x += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = P.n_search - 1;  // items are (search, batch index), searches contiguous by b_off order
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.meta[mid].mark_off <= x) lo = mid;
+      else hi = mid - 1;
+    }
+    const lc_search_desc& S = P.searches[lo];
+    if (S.load < 0 || !(S.modes & 2)) continue;
+    const int bi = (int)(x - P.meta[lo].mark_off);
+    const AggSched a = agg_schedule(S, P.batches[S.b_off + bi]);
+    if (a.st) continue;
+    const int64_t tok = a.chunk_tokens + a.n_mix_gen;
+    if (tok <= P.m_tmax) P.m_used[(int64_t)S.load * (P.m_tmax + 1) + tok] = 1;
   }
 }
 
@@ -399,6 +435,14 @@ __device__ __forceinline__ void stage_db(const EvalParams& P, unsigned char* sme
   V->gpn = P.gpn; V->policy = P.policy;
 }
 
+// tail lookup: prefill/decode tables by batch index, the mixed region by token count
+__device__ __forceinline__ int64_t tail_at(const EvalParams& P, const SearchMeta& M, const lc_search_desc& S, int type,
+                                           int pair, int bi, int64_t tokens) {
+  const int cp = P.pair_canon[pair];
+  if (type < 2) return P.tails[M.tail_off[type] + (int64_t)cp * S.n_b + bi];
+  return P.tails[P.n_pd_tails + ((int64_t)S.load * P.n_tp * P.n_ep + cp) * (P.m_tmax + 1) + tokens];
+}
+
 __device__ __forceinline__ int64_t expert_tokens(const EvalParams& P, const lc_combo& c, const SearchMeta& M,
                                                  const lc_search_desc& S, int type, int bi, int64_t tokens) {
   if (!P.is_moe) return 0;
@@ -406,8 +450,7 @@ __device__ __forceinline__ int64_t expert_tokens(const EvalParams& P, const lc_c
   const int64_t pooled = tokens * f;
   const int64_t balanced = ceil_div_f(pooled * P.topk, c.ep);
   if (c.ep == 1 || S.load < 0) return balanced;
-  const int64_t tail =
-      P.tails[M.tail_off[type] + (int64_t)P.pair_canon[c.tp_i * P.n_ep + c.ep_i] * S.n_b + bi];
+  const int64_t tail = tail_at(P, M, S, type, c.tp_i * P.n_ep + c.ep_i, bi, tokens);
   return balanced > tail ? balanced : tail;
 }
 
@@ -462,7 +505,7 @@ __device__ __forceinline__ int64_t tail_tokens(const EvalParams& P, const Search
   const int64_t pooled = tokens * f;
   const int64_t balanced = ceil_div_f(pooled * P.topk, ep);
   if (ep == 1 || S.load < 0) return balanced;
-  const int64_t tail = P.tails[M.tail_off[type] + (int64_t)P.pair_canon[pair] * S.n_b + bi];
+  const int64_t tail = tail_at(P, M, S, type, pair, bi, tokens);
   return balanced > tail ? balanced : tail;
 }
 
@@ -1449,7 +1492,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->qt, &c->ds, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
@@ -1580,6 +1623,9 @@ static EvalParams make_params(lc_ctx* c) {
   P.pair_canon = sp->pair_canon;
   P.tail_tables = (const TailTable*)c->tail_tables.p;
   P.n_tail_tables = (int32_t)c->htables.size();
+  P.n_pd_tails = c->n_pd_tails;
+  P.m_tmax = c->m_tmax;
+  P.m_used = (uint8_t*)c->m_used.p;
   P.slots = sp->slots; P.n_slots = sp->n_slots; P.slot_of = sp->slot_of;
   P.gclasses = sp->gclasses; P.n_gclass = sp->n_gclass; P.gclass_of = sp->gclass_of;
   P.qt = (QVal*)c->qt.p; P.n_qt = c->n_qt;
@@ -1637,12 +1683,22 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   c->plans_d.get<double>((size_t)c->n_plan_slots * 6, &err);
   c->front.get<int64_t>((size_t)c->n_front_slots, &err);
   c->tails.get<int64_t>((size_t)(c->n_tails > 0 ? c->n_tails : 1), &err);
+  const int64_t n_mark_bytes = (int64_t)(c->n_loads > 0 ? c->n_loads : 1) * (c->m_tmax + 1);
+  c->m_used.get<uint8_t>(n_mark_bytes, &err);
   if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
   // per-search result accumulators (queries are summed by K4)
   CK(cudaMemsetAsync(c->results.p, 0, sizeof(lc_search_result) * c->n_search, c->stream));
   EvalParams P = make_params(c);
   const int sms = sm_count(c->device);
   CK(cudaEventRecord(c->ev[1], c->stream));
+  if (c->n_tails > c->n_pd_tails) {
+    P.m_used = (uint8_t*)c->m_used.p;
+    CK(cudaMemsetAsync(c->m_used.p, 0, n_mark_bytes, c->stream));
+    int blocks = (int)((c->n_marks + 255) / 256);
+    if (blocks < 1) blocks = 1;
+    k_mark_mixed<<<blocks, 256, 0, c->stream>>>(P, c->n_marks);
+    CK(cudaGetLastError());
+  }
   if (c->n_tails > 0) {
     const int64_t warps = c->n_tails;
     int blocks = (int)((warps + 7) / 8);
@@ -1793,8 +1849,8 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
       std::vector<int64_t> bl(batches + S.b_off, batches + S.b_off + S.n_b);
       auto it = blist.find(bl);
       const int32_t cb = it == blist.end() ? (blist[bl] = S.b_off) : it->second;
-      for (int type = 0; type < 3; ++type) {
-        std::vector<int64_t> key = {type, cb, S.n_b, S.load, type == 0 ? S.isl - S.prefix : 0, type == 2 ? s : -1};
+      for (int type = 0; type < 2; ++type) {
+        std::vector<int64_t> key = {type, cb, S.n_b, S.load, type == 0 ? S.isl - S.prefix : 0};
         auto jt = tindex.find(key);
         int32_t ti;
         if (jt == tindex.end()) {
@@ -1812,6 +1868,22 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
       }
     }
   }
+  // dense mixed-step region: tokens = chunk_tokens + n_mix_gen <= context + batch
+  c->n_pd_tails = tails;
+  c->m_tmax = 0;
+  int64_t marks = 0;
+  for (int s = 0; s < n_search; ++s) {
+    const lc_search_desc& S = searches[s];
+    c->hmeta[s].mark_off = marks;
+    marks += S.n_b;
+    if (!sp->is_moe || !(S.modes & 2) || S.n_b == 0) continue;
+    int64_t bmax = 0;
+    for (int j = 0; j < S.n_b; ++j) bmax = batches[S.b_off + j] > bmax ? batches[S.b_off + j] : bmax;
+    const int64_t t = (S.isl - S.prefix) + bmax;
+    c->m_tmax = t > c->m_tmax ? t : c->m_tmax;
+  }
+  c->n_marks = marks;
+  if (sp->is_moe && n_loads > 0 && c->m_tmax > 0) tails += (int64_t)n_loads * sp->n_tp * sp->n_ep * (c->m_tmax + 1);
   c->n_raw = raw;
   c->n_cells = cells;
   c->n_qt = qts;
