@@ -173,6 +173,7 @@ typedef struct {
   int64_t n_units, n_plans, n_front;
   float kernel_ms[6];                /* K0 enumerate, K3 tails, K2 evaluate (tables + cells + expand), K5a pools, K5b disagg, K4 front */
   int64_t n_raw;                     /* raw (tp,pp,ep,dp,batch) tuples examined */
+  int64_t n_launches;                /* kernels launched by the device pipeline (K0..K4) */
 } lc_batch_totals;
 
 /* per-unit / per-plan / front arrays to copy back (any pointer may be NULL) */

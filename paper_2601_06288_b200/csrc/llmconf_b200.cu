@@ -151,13 +151,14 @@ struct lc_ctx {
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
-  DBuf qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
+  DBuf pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   // last batch
   const lc_db* db = nullptr;
   const lc_space* sp = nullptr;
   int32_t n_search = 0, n_batches = 0, n_loads = 0;
   int64_t n_raw = 0, n_cap = 0, n_units = 0, n_tails = 0, n_plan_slots = 0, n_front_slots = 0, n_cells = 0;
   int64_t n_qt = 0, n_ds = 0, n_pd_tails = 0, m_tmax = 0, n_marks = 0;
+  int64_t launches = 0;  // kernels launched by the last pipeline run
   int64_t n_total_idx = 0;  // index of the unit total inside block_sums
   std::vector<SearchMeta> hmeta;
   std::vector<TailTable> htables;
@@ -1456,6 +1457,422 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(EvalParams P, const Sea
   if (tid == 0) results[s].n_front = nfront;
 }
 
+// ---------------------------------------------------------------------------
+// Split versions of K5a and K4: each search's rows are spread over kSplit
+// blocks (grid = kSplit x n_search) and small per-search kernels merge the
+// partials.  Same results as the single-block kernels above (which stay as
+// the fallback for pool caps above kPoolLocal and survivor overflow).
+constexpr int kSplit = 16;
+
+struct PoolPartial {
+  PoolKey k[2][kPoolLocal];
+  int32_t n[2];
+};
+
+__device__ __forceinline__ void slice_of(int64_t n, int parts, int part, int64_t* lo, int64_t* hi) {
+  *lo = n * part / parts;
+  *hi = n * (part + 1) / parts;
+}
+
+// block-wide selection of the `cap` smallest keys among cand[0..m) (destructive)
+__device__ int block_select(const EvalParams& P, PoolKey* cand, int m, int cap, PoolKey* red, PoolKey* out) {
+  const int tid = threadIdx.x;
+  int got = 0;
+  for (int k = 0; k < cap; ++k) {
+    PoolKey best{0.0, -1};
+    int where = -1;
+    for (int j = tid; j < m; j += blockDim.x)
+      if (pool_less(P, cand[j], best)) { best = cand[j]; where = j; }
+    red[tid] = best;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+      if (tid < w && pool_less(P, red[tid + w], red[tid])) red[tid] = red[tid + w];
+      __syncthreads();
+    }
+    const PoolKey sel = red[0];
+    __syncthreads();
+    if (sel.unit < 0) break;
+    if (where >= 0 && best.unit == sel.unit) cand[where].unit = -1;
+    if (tid == 0) out[k] = sel;
+    ++got;
+    __syncthreads();
+  }
+  return got;
+}
+
+__global__ void k_pools_partial(EvalParams P, const SearchMeta* meta, PoolPartial* part) {
+  const int s = blockIdx.y, bx = blockIdx.x, tid = threadIdx.x;
+  const lc_search_desc& S = P.searches[s];
+  if (!(S.modes & 4)) return;
+  __shared__ PoolKey red[kPoolThreads];
+  __shared__ PoolKey cand[kPoolThreads * kPoolLocal];
+  __shared__ PoolKey outk[kPoolLocal];
+  int64_t lo, hi;
+  slice_of(meta[s].n_units, kSplit, bx, &lo, &hi);
+  const int64_t u0 = meta[s].unit_off;
+  PoolPartial* dst = part + (int64_t)s * kSplit + bx;
+  for (int role = 0; role < 2; ++role) {
+    const int cap = role == 0 ? S.prefill_cap : S.decode_cap;
+    if (cap > kPoolLocal) { if (tid == 0) dst->n[role] = 0; continue; }
+    const int32_t* status = role == 0 ? P.pf_status : P.dc_status;
+    const double* v = role == 0 ? P.pf_v : P.dc_v;
+    PoolKey lst[kPoolLocal];
+    int n = 0;
+    for (int64_t i = lo + tid; i < hi; i += blockDim.x) {
+      const int32_t u = (int32_t)(u0 + i);
+      if (status[u] != 0) continue;
+      const PoolKey key{-v[P.n_cap + u] / (double)P.combos[P.u_combo[u]].gpus, u};
+      if (cap > 0) local_insert(P, lst, n, cap, key);
+    }
+    for (int j = 0; j < kPoolLocal; ++j) cand[tid * kPoolLocal + j] = j < n ? lst[j] : PoolKey{0.0, -1};
+    __syncthreads();
+    const int got = block_select(P, cand, kPoolThreads * kPoolLocal, cap, red, outk);
+    if (tid < got) dst->k[role][tid] = outk[tid];
+    if (tid == 0) dst->n[role] = got;
+    __syncthreads();
+  }
+}
+
+__global__ void k_pools_final(EvalParams P, SearchMeta* meta, const PoolPartial* part, int32_t* pool_sel) {
+  const int s = blockIdx.x, tid = threadIdx.x;
+  const lc_search_desc& S = P.searches[s];
+  if (!(S.modes & 4)) return;
+  __shared__ PoolKey red[kPoolThreads];
+  __shared__ PoolKey cand[kSplit * kPoolLocal];
+  __shared__ PoolKey outk[kPoolLocal];
+  for (int role = 0; role < 2; ++role) {
+    const int cap = role == 0 ? S.prefill_cap : S.decode_cap;
+    int got = 0;
+    if (cap <= kPoolLocal) {
+      for (int j = tid; j < kSplit * kPoolLocal; j += blockDim.x) {
+        const PoolPartial& pp = part[(int64_t)s * kSplit + j / kPoolLocal];
+        const int i = j % kPoolLocal;
+        cand[j] = i < pp.n[role] ? pp.k[role][i] : PoolKey{0.0, -1};
+      }
+      __syncthreads();
+      got = block_select(P, cand, kSplit * kPoolLocal, cap, red, outk);
+      if (tid < got) pool_sel[(int64_t)s * 128 + role * 64 + tid] = outk[tid].unit;
+    } else {
+      // large caps: rounds over all units (rare)
+      const int32_t u0 = meta[s].unit_off, nu = meta[s].n_units;
+      const int32_t* status = role == 0 ? P.pf_status : P.dc_status;
+      const double* v = role == 0 ? P.pf_v : P.dc_v;
+      PoolKey prev{0.0, -1};
+      for (int k = 0; k < cap && k < 64; ++k) {
+        PoolKey best{0.0, -1};
+        for (int i = tid; i < nu; i += blockDim.x) {
+          const int32_t u = u0 + i;
+          if (status[u] != 0) continue;
+          const PoolKey key{-v[P.n_cap + u] / (double)P.combos[P.u_combo[u]].gpus, u};
+          if (prev.unit >= 0 && !pool_less(P, prev, key)) continue;
+          if (pool_less(P, key, best)) best = key;
+        }
+        red[tid] = best;
+        __syncthreads();
+        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+          if (tid < w && pool_less(P, red[tid + w], red[tid])) red[tid] = red[tid + w];
+          __syncthreads();
+        }
+        const PoolKey sel = red[0];
+        __syncthreads();
+        if (sel.unit < 0) break;
+        if (tid == 0) pool_sel[(int64_t)s * 128 + role * 64 + k] = sel.unit;
+        prev = sel;
+        ++got;
+      }
+    }
+    if (tid == 0) {
+      if (role == 0) meta[s].n_pre = got;
+      else meta[s].n_dec = got;
+    }
+    __syncthreads();
+  }
+}
+
+struct FrontPartial {
+  BestKey best;
+  unsigned long long smin, smax, q1, q2;
+  int32_t feas, rows, enums, skips;
+};
+
+struct FrontMeta {
+  int32_t shift, any;
+  unsigned long long base;
+};
+
+__global__ void __launch_bounds__(kFrontThreads) k_front_pass1(EvalParams P, const SearchMeta* meta,
+                                                               const int32_t* plan_i, const double* plan_d,
+                                                               const lc_search_result* results, FrontPartial* part) {
+  const int s = blockIdx.y, bx = blockIdx.x, tid = threadIdx.x;
+  const lc_search_desc& S = P.searches[s];
+  const SearchMeta& M = meta[s];
+  const int64_t nplan = results[s].n_plans;
+  const int64_t nrows_all = 2 * (int64_t)M.n_units + nplan;
+  __shared__ BestKey bred[kFrontThreads];
+  __shared__ unsigned long long ured[32];
+  __shared__ int cnt[4];
+  __shared__ unsigned long long qsum[2];
+  if (tid < 4) cnt[tid] = 0;
+  if (tid < 2) qsum[tid] = 0;
+  __syncthreads();
+  int64_t lo, hi;
+  slice_of(nrows_all, kSplit, bx, &lo, &hi);
+  BestKey best{0, 0, 0, 0, -1};
+  unsigned long long smin = ~0ull, smax = 0ull, q1 = 0, q2 = 0;
+  int feas = 0, rows = 0, enums = 0, skips = 0;
+  for (int64_t r = lo + tid; r < hi; r += blockDim.x) {
+    if (r < M.n_units) {
+      const int64_t u = M.unit_off + r;
+      const int32_t q = P.u_queries[u];
+      q1 += (unsigned)(q & 0xffff);
+      q2 += (unsigned)(q >> 16);
+      if (P.u_budget[u]) {
+        ++enums;
+        if ((S.modes & 1) && P.st_status[u]) ++skips;
+        if ((S.modes & 2) && P.ag_status[u]) ++skips;
+      }
+      if (S.modes & 4) skips += (P.pf_status[u] != 0) + (P.dc_status[u] != 0);
+    }
+    const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+    FRONT_ROW_FILTER(v)
+    ++rows;
+    if (!feasible(S, v)) continue;
+    ++feas;
+    const double nt = -v.thru, ns = -v.speed;
+    if (best.key < 0 || nt < best.nthru || (nt == best.nthru && ns <= best.nspeed)) {
+      BestKey k{nt, ns, v.gpus, mode_rank(v.mode), v.key};
+      if (best_less(P, M, plan_i, k, best)) best = k;
+    }
+    const unsigned long long sb = (unsigned long long)__double_as_longlong(v.speed);
+    smin = sb < smin ? sb : smin;
+    smax = sb > smax ? sb : smax;
+  }
+  atomicAdd(&cnt[0], feas); atomicAdd(&cnt[1], rows); atomicAdd(&cnt[2], enums); atomicAdd(&cnt[3], skips);
+  atomicAdd(&qsum[0], q1); atomicAdd(&qsum[1], q2);
+  bred[tid] = best;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (tid < w && best_less(P, M, plan_i, bred[tid + w], bred[tid])) bred[tid] = bred[tid + w];
+    __syncthreads();
+  }
+  const unsigned long long lo_b = block_min_u64(smin, ured);
+  const unsigned long long hi_b = block_max_u64(smax, ured);
+  if (tid == 0) {
+    FrontPartial& o = part[(int64_t)s * kSplit + bx];
+    o.best = bred[0]; o.smin = lo_b; o.smax = hi_b; o.q1 = qsum[0]; o.q2 = qsum[1];
+    o.feas = cnt[0]; o.rows = cnt[1]; o.enums = cnt[2]; o.skips = cnt[3];
+  }
+}
+
+__global__ void __launch_bounds__(kFrontThreads) k_front_mid(EvalParams P, const SearchMeta* meta,
+                                                             const int32_t* plan_i, const double* plan_d,
+                                                             lc_search_result* results, const FrontPartial* part,
+                                                             FrontMeta* fmeta, unsigned long long* buckets,
+                                                             int32_t* n_surv) {
+  const int s = blockIdx.x, tid = threadIdx.x;
+  const lc_search_desc& S = P.searches[s];
+  const SearchMeta& M = meta[s];
+  __shared__ MissKey mred[kFrontThreads];
+  unsigned long long* bk = buckets + (int64_t)s * kSpeedBuckets;
+  for (int i = tid; i < kSpeedBuckets; i += blockDim.x) bk[i] = 0ull;
+  if (tid == 0) {
+    BestKey best{0, 0, 0, 0, -1};
+    unsigned long long lo = ~0ull, hi = 0ull, q1 = 0, q2 = 0;
+    int feas = 0, rows = 0, enums = 0, skips = 0;
+    for (int j = 0; j < kSplit; ++j) {
+      const FrontPartial& p = part[(int64_t)s * kSplit + j];
+      if (best_less(P, M, plan_i, p.best, best)) best = p.best;
+      lo = p.smin < lo ? p.smin : lo;
+      hi = p.smax > hi ? p.smax : hi;
+      q1 += p.q1; q2 += p.q2;
+      feas += p.feas; rows += p.rows; enums += p.enums; skips += p.skips;
+    }
+    lc_search_result& R = results[s];
+    R.n_enumerated = enums; R.n_rows = rows; R.n_feasible = feas; R.n_skipped = skips;
+    R.queries_1d = (int64_t)q1; R.queries_2d = (int64_t)q2;
+    R.best = best.key;
+    R.best_thru = best.key >= 0 ? -best.nthru : 0.0;
+    R.best_speed = best.key >= 0 ? -best.nspeed : 0.0;
+    R.nearest = -1;
+    R.nearest_violation = 0.0;
+    R.front_off = (int32_t)((int64_t)M.unit_off * 2 + M.plan_off);
+    R.n_front = 0;
+    int shift = 0;
+    if (feas) while (shift < 63 && ((hi >> shift) - (lo >> shift)) >= (unsigned long long)kSpeedBuckets) ++shift;
+    fmeta[s].shift = shift;
+    fmeta[s].any = feas > 0;
+    fmeta[s].base = feas ? (lo >> shift) : 0ull;
+    n_surv[s] = 0;
+  }
+  __syncthreads();
+  if (fmeta[s].any) return;
+  // nearest miss (search.py:190-208) when nothing is feasible: rare, one block
+  const int64_t nplan = results[s].n_plans;
+  const int64_t nrows_all = 2 * (int64_t)M.n_units + nplan;
+  MissKey miss{0, -1};
+  for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
+    const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+    FRONT_ROW_FILTER(v)
+    double worst = 1.0;
+    if (S.has_ttft && v.ttft > S.ttft_limit) { const double x = v.ttft / S.ttft_limit; if (x > worst) worst = x; }
+    if (S.has_floor && v.speed < S.speed_floor) {
+      const double x = v.speed == 0.0 ? INFINITY : S.speed_floor / v.speed;
+      if (x > worst) worst = x;
+    }
+    if (miss.key < 0 || worst <= miss.viol) {
+      MissKey mk{worst, v.key};
+      if (miss_less(P, M, plan_i, mk, miss)) miss = mk;
+    }
+  }
+  mred[tid] = miss;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (tid < w && miss_less(P, M, plan_i, mred[tid + w], mred[tid])) mred[tid] = mred[tid + w];
+    __syncthreads();
+  }
+  if (tid == 0) { results[s].nearest = mred[0].key; results[s].nearest_violation = mred[0].viol; }
+}
+
+__global__ void __launch_bounds__(kFrontThreads) k_front_pass2(EvalParams P, const SearchMeta* meta,
+                                                               const int32_t* plan_i, const double* plan_d,
+                                                               const lc_search_result* results, const FrontMeta* fmeta,
+                                                               unsigned long long* buckets) {
+  const int s = blockIdx.y, bx = blockIdx.x, tid = threadIdx.x;
+  const FrontMeta fm = fmeta[s];
+  if (!fm.any) return;
+  const lc_search_desc& S = P.searches[s];
+  const SearchMeta& M = meta[s];
+  const int64_t nplan = results[s].n_plans;
+  const int64_t nrows_all = 2 * (int64_t)M.n_units + nplan;
+  unsigned long long* bk = buckets + (int64_t)s * kSpeedBuckets;
+  int64_t lo, hi;
+  slice_of(nrows_all, kSplit, bx, &lo, &hi);
+  for (int64_t r = lo + tid; r < hi; r += blockDim.x) {
+    const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+    FRONT_ROW_FILTER(v)
+    if (!feasible(S, v)) continue;
+    const int b = (int)((((unsigned long long)__double_as_longlong(v.speed)) >> fm.shift) - fm.base);
+    atomicMax(&bk[b], (unsigned long long)__double_as_longlong(v.thru));
+  }
+}
+
+__global__ void __launch_bounds__(kFrontThreads) k_front_suffix(const FrontMeta* fmeta, unsigned long long* buckets) {
+  const int s = blockIdx.x, tid = threadIdx.x;
+  if (!fmeta[s].any) return;
+  unsigned long long* bk = buckets + (int64_t)s * kSpeedBuckets;
+  __shared__ unsigned long long tsuf[kFrontThreads];
+  constexpr int per = kSpeedBuckets / kFrontThreads;
+  unsigned long long loc[per];
+  unsigned long long run = 0;
+  for (int j = per - 1; j >= 0; --j) { loc[j] = run; const unsigned long long x = bk[tid * per + j]; run = x > run ? x : run; }
+  tsuf[tid] = run;
+  __syncthreads();
+  unsigned long long above = 0;
+  for (int t = tid + 1; t < kFrontThreads; ++t) above = tsuf[t] > above ? tsuf[t] : above;
+  for (int j = 0; j < per; ++j) bk[tid * per + j] = loc[j] > above ? loc[j] : above;
+}
+
+__global__ void __launch_bounds__(kFrontThreads) k_front_pass3(EvalParams P, const SearchMeta* meta,
+                                                               const int32_t* plan_i, const double* plan_d,
+                                                               const lc_search_result* results, const FrontMeta* fmeta,
+                                                               const unsigned long long* buckets, FrontCand* surv,
+                                                               int32_t* n_surv) {
+  const int s = blockIdx.y, bx = blockIdx.x, tid = threadIdx.x;
+  const FrontMeta fm = fmeta[s];
+  if (!fm.any) return;
+  const lc_search_desc& S = P.searches[s];
+  const SearchMeta& M = meta[s];
+  const int64_t nplan = results[s].n_plans;
+  const int64_t nrows_all = 2 * (int64_t)M.n_units + nplan;
+  const unsigned long long* bk = buckets + (int64_t)s * kSpeedBuckets;
+  int64_t lo, hi;
+  slice_of(nrows_all, kSplit, bx, &lo, &hi);
+  for (int64_t r = lo + tid; r < hi; r += blockDim.x) {
+    const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+    FRONT_ROW_FILTER(v)
+    if (!feasible(S, v)) continue;
+    const int b = (int)((((unsigned long long)__double_as_longlong(v.speed)) >> fm.shift) - fm.base);
+    if (bk[b] != 0ull && v.thru <= __longlong_as_double((long long)bk[b])) continue;
+    const int k = atomicAdd(&n_surv[s], 1);
+    if (k < kSurvivorCap) surv[(int64_t)s * kSurvivorCap + k] = FrontCand{v.speed, v.thru, v.key};
+  }
+}
+
+__global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, const SearchMeta* meta,
+                                                               const int32_t* plan_i, const double* plan_d,
+                                                               lc_search_result* results, const FrontMeta* fmeta,
+                                                               const FrontCand* surv, const int32_t* n_surv,
+                                                               int64_t* front) {
+  const int s = blockIdx.x, tid = threadIdx.x;
+  if (!fmeta[s].any) return;
+  extern __shared__ __align__(16) unsigned char fsm2[];
+  FrontCand* sorted = (FrontCand*)fsm2;                     // kSurvivorCap
+  int64_t* keys_out = (int64_t*)(sorted + kSurvivorCap);    // kSurvivorCap
+  __shared__ double dred[32];
+  __shared__ int nfront;
+  const lc_search_desc& S = P.searches[s];
+  const SearchMeta& M = meta[s];
+  const int64_t nplan = results[s].n_plans;
+  const int64_t nrows_all = 2 * (int64_t)M.n_units + nplan;
+  const int64_t foff = (int64_t)M.unit_off * 2 + M.plan_off;
+  const int nsv = n_surv[s];
+  if (nsv <= kSurvivorCap) {
+    const FrontCand* sv = surv + (int64_t)s * kSurvivorCap;
+    for (int i = tid; i < nsv; i += blockDim.x) {
+      const FrontCand a = sv[i];
+      int rank = 0;
+      for (int j = 0; j < nsv; ++j) {
+        const FrontCand b = sv[j];
+        rank += (b.speed > a.speed) || (b.speed == a.speed && b.key < a.key);
+      }
+      sorted[rank] = a;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int m = 0;
+      front_of_sorted(sorted, nsv, keys_out, &m);
+      for (int i = 0; i < m; ++i) front[foff + i] = keys_out[i];
+      results[s].n_front = m;
+    }
+    return;
+  }
+  // survivor overflow: iterative staircase over all rows (one block)
+  if (tid == 0) nfront = 0;
+  __syncthreads();
+  double best_thru = -INFINITY;
+  while (true) {
+    double sm = -INFINITY;
+    bool any = false;
+    for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
+      const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+      FRONT_ROW_FILTER(v)
+      if (!feasible(S, v)) continue;
+      if (v.thru > best_thru) { any = true; sm = fmax(sm, v.speed); }
+    }
+    if (!__syncthreads_or(any)) break;
+    const double sp = block_max(any ? sm : -INFINITY, dred);
+    double tmax = -INFINITY;
+    for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
+      const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+      FRONT_ROW_FILTER(v)
+      if (!feasible(S, v)) continue;
+      if (v.speed == sp) tmax = fmax(tmax, v.thru);
+    }
+    const double top = block_max(tmax, dred);
+    if (tid == 0) {
+      for (int64_t r = 0; r < nrows_all; ++r) {
+        const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+        FRONT_ROW_FILTER(v)
+        if (!feasible(S, v)) continue;
+        if (v.speed == sp && v.thru == top) front[foff + nfront++] = v.key;
+      }
+    }
+    __syncthreads();
+    best_thru = top;
+  }
+  if (tid == 0) results[s].n_front = nfront;
+}
+
 }  // namespace
 
 template <class T>
@@ -1492,7 +1909,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
@@ -1696,6 +2113,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     CK(cudaMemsetAsync(c->m_used.p, 0, n_mark_bytes, c->stream));
     int blocks = (int)((c->n_marks + 255) / 256);
     if (blocks < 1) blocks = 1;
+    ++c->launches;
     k_mark_mixed<<<blocks, 256, 0, c->stream>>>(P, c->n_marks);
     CK(cudaGetLastError());
   }
@@ -1703,6 +2121,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     const int64_t warps = c->n_tails;
     int blocks = (int)((warps + 7) / 8);
     if (blocks > sms * 16) blocks = sms * 16;
+    ++c->launches;
     k_tails<<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
     CK(cudaGetLastError());
   }
@@ -1721,6 +2140,8 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     int64_t blocks = (n_items + 127) / 128;
     const int64_t cap = (int64_t)sms * per_sm;
     if (blocks > cap) blocks = cap;
+    ++c->launches;
+    ++c->launches;
     kern<<<(int)blocks, 128, smem, c->stream>>>(P);
     CK(cudaGetLastError());
     return LC_OK;
@@ -1732,30 +2153,63 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   if (c->n_cells > 0) {
     int64_t blocks = (c->n_cells + 127) / 128;
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+    ++c->launches;
     k_eval_cells<<<(int)blocks, 128, 0, c->stream>>>(P);
     CK(cudaGetLastError());
   }
   if (n > 0) {
     int64_t blocks = (n + 255) / 256;
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+    ++c->launches;
     k_expand<<<(int)blocks, 256, 0, c->stream>>>(P);
     CK(cudaGetLastError());
   }
   CK(cudaEventRecord(c->ev[3], c->stream));
-  k_pools<<<c->n_search, kPoolThreads, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, (int32_t*)c->pool_sel.p);
-  CK(cudaGetLastError());
+  {
+    PoolPartial* pp = c->pool_part.get<PoolPartial>((size_t)c->n_search * kSplit, &err);
+    if (err != cudaSuccess) return fail(LC_ERR_CUDA, "pool partial allocation");
+    ++c->launches;
+    k_pools_partial<<<dim3(kSplit, c->n_search), kPoolThreads, 0, c->stream>>>(P, (const SearchMeta*)c->meta.p, pp);
+    ++c->launches;
+    k_pools_final<<<c->n_search, kPoolThreads, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, pp, (int32_t*)c->pool_sel.p);
+    CK(cudaGetLastError());
+  }
   CK(cudaEventRecord(c->ev[4], c->stream));
+  ++c->launches;
   k_disagg<<<c->n_search, 256, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, (const int32_t*)c->pool_sel.p,
                                                 (int32_t*)c->plans_i.p, (double*)c->plans_d.p,
                                                 (lc_search_result*)c->results.p);
   CK(cudaGetLastError());
   CK(cudaEventRecord(c->ev[5], c->stream));
-  const size_t fsmem = 8 * kSpeedBuckets + sizeof(FrontCand) * 2 * kSurvivorCap + 8 * kSurvivorCap;
-  CK(cudaFuncSetAttribute(k_front, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
-  k_front<<<c->n_search, kFrontThreads, fsmem, c->stream>>>(P, (const SearchMeta*)c->meta.p, (const int32_t*)c->plans_i.p,
-                                               (const double*)c->plans_d.p, (int64_t*)c->front.p,
-                                               (lc_search_result*)c->results.p);
-  CK(cudaGetLastError());
+  {
+    FrontPartial* fp = c->front_part.get<FrontPartial>((size_t)c->n_search * kSplit, &err);
+    FrontMeta* fm = c->front_meta.get<FrontMeta>(c->n_search, &err);
+    unsigned long long* bk = c->buckets.get<unsigned long long>((size_t)c->n_search * kSpeedBuckets, &err);
+    FrontCand* sv = c->surv.get<FrontCand>((size_t)c->n_search * kSurvivorCap, &err);
+    int32_t* ns = c->n_surv.get<int32_t>(c->n_search, &err);
+    if (err != cudaSuccess) return fail(LC_ERR_CUDA, "front workspace allocation");
+    const SearchMeta* meta = (const SearchMeta*)c->meta.p;
+    const int32_t* pi = (const int32_t*)c->plans_i.p;
+    const double* pd = (const double*)c->plans_d.p;
+    lc_search_result* res = (lc_search_result*)c->results.p;
+    const dim3 g(kSplit, c->n_search);
+    ++c->launches;
+    k_front_pass1<<<g, kFrontThreads, 0, c->stream>>>(P, meta, pi, pd, res, fp);
+    ++c->launches;
+    k_front_mid<<<c->n_search, kFrontThreads, 0, c->stream>>>(P, meta, pi, pd, res, fp, fm, bk, ns);
+    ++c->launches;
+    k_front_pass2<<<g, kFrontThreads, 0, c->stream>>>(P, meta, pi, pd, res, fm, bk);
+    ++c->launches;
+    k_front_suffix<<<c->n_search, kFrontThreads, 0, c->stream>>>(fm, bk);
+    ++c->launches;
+    k_front_pass3<<<g, kFrontThreads, 0, c->stream>>>(P, meta, pi, pd, res, fm, bk, sv, ns);
+    const size_t fsmem = (sizeof(FrontCand) + 8) * kSurvivorCap;
+    CK(cudaFuncSetAttribute(k_front_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
+    ++c->launches;
+    k_front_final<<<c->n_search, kFrontThreads, fsmem, c->stream>>>(P, meta, pi, pd, res, fm, sv, ns,
+                                                                      (int64_t*)c->front.p);
+    CK(cudaGetLastError());
+  }
   CK(cudaEventRecord(c->ev[6], c->stream));
   (void)totals;
   return LC_OK;
@@ -1776,8 +2230,11 @@ static int run_enum(lc_ctx* c) {
   if (n_raw > 0) {
     int blocks = (int)((n_raw + 255) / 256);
     if (blocks > sms * 32) blocks = sms * 32;
+    ++c->launches;
     k_enum_flags<<<blocks, 256, 0, c->stream>>>(P, n_raw, flags);
+    ++c->launches;
     k_scan_blocks<<<(int)nblk, kScanBlock, 0, c->stream>>>(flags, n_raw, bs);
+    ++c->launches;
     k_scan_top<<<1, 1024, 0, c->stream>>>(bs, (int)nblk);
     CK(cudaGetLastError());
   } else {
@@ -1791,9 +2248,11 @@ static int run_enum(lc_ctx* c) {
   uint8_t* ubud = c->u_budget.get<uint8_t>(n_raw, &err);
   if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
   if (n_raw > 0) {
+    ++c->launches;
     k_scatter<<<(int)nblk, kScanBlock, 0, c->stream>>>(P, flags, n_raw, bs, pos, us, uc, ub, ubud);
     CK(cudaGetLastError());
   }
+  ++c->launches;
   k_unit_offsets<<<(c->n_search + 127) / 128, 128, 0, c->stream>>>((SearchMeta*)c->meta.p, c->n_search, pos, n_raw,
                                                                    bs + nblk);
   CK(cudaGetLastError());
@@ -1908,6 +2367,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     CK(cudaMemcpyAsync(dT, c->htables.data(), sizeof(TailTable) * c->htables.size(), cudaMemcpyHostToDevice,
                        c->stream));
   CK(cudaEventRecord(c->ev[0], c->stream));
+  c->launches = 0;
   int rc = run_enum(c);
   if (rc) return rc;
   c->n_front_slots = 2 * c->n_cap + c->n_plan_slots;
@@ -1940,6 +2400,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     totals->n_plans = nplan;
     totals->n_front = nfront;
     totals->n_raw = c->n_raw;
+    totals->n_launches = c->launches;
     float ms = 0;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]); totals->kernel_ms[0] = ms;
     cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]); totals->kernel_ms[1] = ms;
@@ -1958,6 +2419,7 @@ int lc_replay_last(lc_ctx* c, int32_t iters, lc_batch_totals* totals) {
   for (int it = 0; it < iters; ++it) {
     // inputs (descriptors, batches, loads, DB, plan) are resident: K0 .. K4 only
     CK(cudaEventRecord(c->ev[0], c->stream));
+    c->launches = 0;
     int rc = run_enum(c);
     if (rc) return rc;
     rc = run_eval_pipeline(c, totals);
@@ -1973,6 +2435,7 @@ int lc_replay_last(lc_ctx* c, int32_t iters, lc_batch_totals* totals) {
     for (int k = 0; k < 6; ++k) totals->kernel_ms[k] = (float)(acc[k] / iters);
     totals->n_units = c->n_units;
     totals->n_raw = c->n_raw;
+    totals->n_launches = c->launches;
   }
   return LC_OK;
 }
