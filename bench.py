@@ -187,7 +187,7 @@ def _gather_results(ws, results: np.ndarray) -> np.ndarray:
 def main() -> int:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--sweep", default="config5")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
@@ -245,19 +245,21 @@ def main() -> int:
     # one engine (CUDA stream + resident workspace) per model so each keeps its batch resident
     engines = {p.model_name: Engine(dev) for p, w in my_parts if w}
 
-    def e2e_step():
-        cands, h2d, d2h, res = 0, 0, 0, []
-        for p, wls in my_parts:
-            if not wls:
-                continue
-            out = engines[p.model_name].run_batch(p.db, p.model, p.space, wls)
-            front, plans = fetch_fronts(out)
-            cands += int(out.results["n_enumerated"].sum())
-            h2d += out.h2d_bytes
-            d2h += out.d2h_bytes + front.nbytes + sum(v.nbytes for v in plans.values())
-            res.append(out.results)
-        return cands, h2d, d2h, res
+    pool = ThreadPoolExecutor(max_workers=max(1, len(engines)))
 
+    def one_model(pw):
+        p, wls = pw
+        out = engines[p.model_name].run_batch(p.db, p.model, p.space, wls)
+        front, plans = fetch_fronts(out)
+        return (int(out.results["n_enumerated"].sum()), out.h2d_bytes,
+                out.d2h_bytes + front.nbytes + sum(v.nbytes for v in plans.values()), out.results)
+
+    def e2e_step():
+        outs = list(pool.map(one_model, [pw for pw in my_parts if pw[1]]))
+        return (sum(o[0] for o in outs), sum(o[1] for o in outs), sum(o[2] for o in outs), [o[3] for o in outs])
+
+    clocks = ClockSampler(dev)
+    clocks.start()
     # warm-up (also uploads DBs / plans and sizes the workspace)
     for _ in range(max(args.warmup, 1)):
         e2e_step()
@@ -270,32 +272,41 @@ def main() -> int:
     cands_local = sum(int(o.results["n_enumerated"].sum()) for o in outs.values())
     q1 = sum(int(o.results["queries_1d"].sum()) for o in outs.values())
     q2 = sum(int(o.results["queries_2d"].sum()) for o in outs.values())
-    clocks = ClockSampler(dev)
+    # per-kernel breakdown (sequential, untimed) for the roofline of the dominant kernel
     kernel_ms = np.zeros(6)
-    step_ms = []
-    launches = 0
-    _barrier(ws)
-    clocks.start()
-    t_wall0 = time.perf_counter()
-    for step in range(args.steps):
-        ms = 0.0
-        for p, wls in my_parts:
-            if not wls:
-                continue
+    launches_per_step = 0
+    for p, wls in my_parts:
+        if wls:
             tot = engines[p.model_name].replay(1)
-            launches += int(tot.n_launches)
-            k = np.array(list(tot.kernel_ms), dtype=np.float64)
-            kernel_ms += k
-            ms += float(k.sum())
-        step_ms.append(ms)
+            kernel_ms += np.array(list(tot.kernel_ms), dtype=np.float64)
+            launches_per_step += int(tot.n_launches)
+    # timed steps: every model's pipeline enqueued at once on its own stream; one
+    # CUDA-event span on the current stream covers all of them
+    streams = {m: torch.cuda.ExternalStream(e.stream_ptr()) for m, e in engines.items()}
+    cur = torch.cuda.current_stream()
+    step_ms = []
     _barrier(ws)
-    wall_s = time.perf_counter() - t_wall0
-    clk = clocks.stop()
+    for step in range(args.steps):
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        start.record(cur)
+        for m, st in streams.items():
+            st.wait_event(start)
+        for m, e in engines.items():
+            e.replay_async()
+        for m, st in streams.items():
+            done = torch.cuda.Event()
+            done.record(st)
+            cur.wait_event(done)
+        stop.record(cur)
+        stop.synchronize()
+        step_ms.append(start.elapsed_time(stop))
+    _barrier(ws)
+    launches = launches_per_step * args.steps
     dev_s_local = sum(step_ms) / 1000.0
     dev_s = _max_over_ranks(ws, dev_s_local)
     cands_total = _sum_over_ranks(ws, float(cands_local))
     value = cands_total * args.steps / dev_s
-    kernel_ms /= args.steps
 
     # ---- end-to-end through the public API (host objects -> summaries + fronts on host)
     _barrier(ws)
@@ -307,6 +318,7 @@ def main() -> int:
         e2e_d2h += d2h
     torch.cuda.synchronize()
     e2e_s = _max_over_ranks(ws, time.perf_counter() - t0)
+    clk = clocks.stop()
     merged = _gather_results(ws, np.concatenate(res) if res else np.zeros(0))
     e2e_value = cands_total * args.steps / e2e_s
 
@@ -341,7 +353,8 @@ def main() -> int:
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": dict(workload_desc, candidates=int(cands_total), parallelism=f"searches sharded over {ws} GPU(s)",
                        l2="per-step unit arrays exceed L2 (~2 GB written per step)"),
-        "search_wall_ms": {"device": dev_s * 1000 / args.steps, "e2e": e2e_s * 1000 / args.steps},
+        "search_wall_ms": {"device": dev_s * 1000 / args.steps, "e2e": e2e_s * 1000 / args.steps,
+                           "per_model_sequential_device": float(kernel_ms.sum())},
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_h2d // args.steps,

@@ -220,6 +220,14 @@ int lc_fetch(lc_ctx* ctx, const lc_fetch_req* req);
  * `iters` times and report the mean per-kernel times; for benchmarks. */
 int lc_replay_last(lc_ctx* ctx, int32_t iters, lc_batch_totals* totals);
 
+/* Asynchronous variant: enqueue the last batch's device pipeline (K0..K4) on the
+ * context's stream and return immediately (no per-kernel timing). */
+int lc_replay_async(lc_ctx* ctx);
+
+/* The context's CUDA stream (cudaStream_t), for callers that order or time work
+ * against it (e.g. CUDA events across several contexts). */
+int lc_stream(lc_ctx* ctx, void** stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -100,7 +100,8 @@ SEARCH_DESC_DTYPE = np.dtype([("isl", "<i8"), ("osl", "<i8"), ("prefix", "<i8"),
 assert SEARCH_DESC_DTYPE.itemsize == C.sizeof(LcSearchDesc), (SEARCH_DESC_DTYPE.itemsize, C.sizeof(LcSearchDesc))
 
 EXPORTED = ("lc_abi_version", "lc_last_error", "lc_open", "lc_close", "lc_db_upload", "lc_db_free",
-            "lc_space_upload", "lc_space_free", "lc_search_batch", "lc_fetch", "lc_replay_last")
+            "lc_space_upload", "lc_space_free", "lc_search_batch", "lc_fetch", "lc_replay_last", "lc_replay_async",
+            "lc_stream")
 
 _LIB = None
 
@@ -126,6 +127,8 @@ def load_library(path: str | os.PathLike | None = None):
                                     C.c_int32, F64P, C.c_void_p, C.POINTER(LcBatchTotals)]
     lib.lc_fetch.argtypes = [C.c_void_p, C.POINTER(LcFetchReq)]
     lib.lc_replay_last.argtypes = [C.c_void_p, C.c_int32, C.POINTER(LcBatchTotals)]
+    lib.lc_replay_async.argtypes = [C.c_void_p]
+    lib.lc_stream.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
     if path is None:
         _LIB = lib
     return lib

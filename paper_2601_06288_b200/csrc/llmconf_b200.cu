@@ -151,7 +151,7 @@ struct lc_ctx {
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
-  DBuf pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
+  DBuf front_compact, pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   // last batch
   const lc_db* db = nullptr;
   const lc_space* sp = nullptr;
@@ -455,10 +455,6 @@ __device__ __forceinline__ int64_t expert_tokens(const EvalParams& P, const lc_c
   return balanced > tail ? balanced : tail;
 }
 
-__device__ __forceinline__ void put_err(const EvalParams& P, int kind, int64_t u, const ErrRec& e) {
-  P.err_c[(int64_t)(2 * kind) * P.n_cap + u] = e.c0;
-  P.err_c[(int64_t)(2 * kind + 1) * P.n_cap + u] = e.c1;
-}
 
 // Per-cell results.  A cell is (search, (tp,pp,ep) template, batch): every
 // latency of the reference model depends on the parallel config only through
@@ -863,87 +859,6 @@ __device__ __forceinline__ void local_insert(const EvalParams& P, PoolKey* lst, 
   lst[j] = k;
 }
 
-__global__ void k_pools(EvalParams P, SearchMeta* meta, int32_t* pool_sel) {
-  const int s = blockIdx.x;
-  const lc_search_desc& S = P.searches[s];
-  if (!(S.modes & 4)) return;
-  __shared__ PoolKey red[kPoolThreads];
-  __shared__ PoolKey cand[kPoolThreads * kPoolLocal];
-  const int tid = threadIdx.x;
-  const int32_t u0 = meta[s].unit_off, nu = meta[s].n_units;
-  for (int role = 0; role < 2; ++role) {
-    const int cap = role == 0 ? S.prefill_cap : S.decode_cap;
-    const int32_t* status = role == 0 ? P.pf_status : P.dc_status;
-    const double* v = role == 0 ? P.pf_v : P.dc_v;
-    int got = 0;
-    if (cap <= kPoolLocal) {
-      // one pass: per-thread top-cap by (-rate/gpus, key) (search.py:276-277, 338-339) ...
-      PoolKey lst[kPoolLocal];
-      int n = 0;
-      for (int i = tid; i < nu; i += blockDim.x) {
-        const int32_t u = u0 + i;
-        if (status[u] != 0) continue;
-        const double rate = v[P.n_cap + u];
-        const PoolKey key{-rate / (double)P.combos[P.u_combo[u]].gpus, u};
-        if (cap > 0) local_insert(P, lst, n, cap, key);
-      }
-      for (int j = 0; j < kPoolLocal; ++j) cand[tid * kPoolLocal + j] = j < n ? lst[j] : PoolKey{0.0, -1};
-      __syncthreads();
-      // ... then cap rounds of a block argmin over the 256 local lists in shared memory
-      for (int k = 0; k < cap; ++k) {
-        PoolKey best{0.0, -1};
-        int where = -1;
-        for (int j = tid; j < kPoolThreads * kPoolLocal; j += blockDim.x)
-          if (pool_less(P, cand[j], best)) { best = cand[j]; where = j; }
-        red[tid] = best;
-        __syncthreads();
-        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-          if (tid < w && pool_less(P, red[tid + w], red[tid])) red[tid] = red[tid + w];
-          __syncthreads();
-        }
-        const PoolKey sel = red[0];
-        __syncthreads();
-        if (sel.unit < 0) break;
-        if (where >= 0 && best.unit == sel.unit) cand[where].unit = -1;
-        if (tid == 0) pool_sel[(int64_t)s * 128 + role * 64 + k] = sel.unit;
-        ++got;
-        __syncthreads();
-      }
-    } else {
-      // large caps: cap rounds over all units, each taking the next key above the previous one
-      PoolKey prev{0.0, -1};
-      for (int k = 0; k < cap && k < 64; ++k) {
-        PoolKey best{0.0, -1};
-        for (int i = tid; i < nu; i += blockDim.x) {
-          const int32_t u = u0 + i;
-          if (status[u] != 0) continue;
-          const double rate = v[P.n_cap + u];
-          const PoolKey key{-rate / (double)P.combos[P.u_combo[u]].gpus, u};
-          if (prev.unit >= 0 && !pool_less(P, prev, key)) continue;
-          if (pool_less(P, key, best)) best = key;
-        }
-        red[tid] = best;
-        __syncthreads();
-        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-          if (tid < w && pool_less(P, red[tid + w], red[tid])) red[tid] = red[tid + w];
-          __syncthreads();
-        }
-        const PoolKey sel = red[0];
-        __syncthreads();
-        if (sel.unit < 0) break;
-        if (tid == 0) pool_sel[(int64_t)s * 128 + role * 64 + k] = sel.unit;
-        prev = sel;
-        ++got;
-      }
-    }
-    if (tid == 0) {
-      if (role == 0) meta[s].n_pre = got;
-      else meta[s].n_dec = got;
-    }
-    __syncthreads();
-  }
-}
-
 // ---- K5b: replica sweep per pairing and plan sort (block per search)
 struct PlanRec {
   int32_t p, d, x, y;  // p/d: global unit index
@@ -1185,12 +1100,6 @@ __device__ __forceinline__ double block_max(double v, double* red) {
   return r;
 }
 
-__device__ __forceinline__ bool dominates(double s1, double t1, double s2, double t2) {
-  // row 1 keeps row 2 off the front (pareto_filter, search.py:156-176): same speed and more
-  // throughput, or faster with at least the same throughput
-  return (s1 == s2 && t1 > t2) || (s1 > s2 && t1 >= t2);
-}
-
 struct FrontCand {
   double speed, thru;
   int64_t key;
@@ -1245,224 +1154,17 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
   if (!v.valid) continue;                                                            \
   if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
 
-// K4.  Three passes over the search's rows, one block per search:
-//  1. counts, select_best (search.py:179-187), range of the feasible speeds;
-//  2. per speed-bucket maximum throughput (buckets = top bits of the IEEE
-//     pattern, so bucket order is speed order);
-//  3. a row can only be on the front if it beats the best throughput of every
-//     strictly faster bucket -- those maxima are real rows that would dominate
-//     it -- so only such survivors go through the exact reference scan.
-__global__ void __launch_bounds__(kFrontThreads) k_front(EvalParams P, const SearchMeta* meta, const int32_t* plan_i,
-                                                         const double* plan_d, int64_t* front,
-                                                         lc_search_result* results) {
-  extern __shared__ __align__(16) unsigned char fsm[];
-  unsigned long long* bmax = (unsigned long long*)fsm;         // kSpeedBuckets
-  FrontCand* surv = (FrontCand*)(bmax + kSpeedBuckets);          // kSurvivorCap
-  FrontCand* sorted = surv + kSurvivorCap;                       // kSurvivorCap
-  int64_t* keys_out = (int64_t*)(sorted + kSurvivorCap);         // kSurvivorCap
-  __shared__ BestKey bred[kFrontThreads];
-  __shared__ MissKey mred[kFrontThreads];
-  __shared__ unsigned long long ured[32];
-  __shared__ unsigned long long tsuf[kFrontThreads];
-  __shared__ double dred[32];
-  __shared__ int cnt_feas, cnt_rows, cnt_enum, cnt_skip, n_surv, nfront;
-  const int s = blockIdx.x;
-  const int tid = threadIdx.x;
-  const lc_search_desc& S = P.searches[s];
-  const SearchMeta& M = meta[s];
-  const int64_t nplan = results[s].n_plans;
-  const int64_t nrows_all = 2 * (int64_t)M.n_units + nplan;
-  const int64_t foff = (int64_t)M.unit_off * 2 + M.plan_off;
-  if (tid == 0) { cnt_feas = cnt_rows = cnt_enum = cnt_skip = 0; n_surv = 0; nfront = 0; }
-  for (int i = tid; i < kSpeedBuckets; i += blockDim.x) bmax[i] = 0ull;
-  __syncthreads();
-
-  // ---- pass 1
-  BestKey best{0, 0, 0, 0, -1};
-  unsigned long long smin = ~0ull, smax = 0ull;
-  int my_feas = 0, my_rows = 0, my_enum = 0, my_skip = 0;
-  unsigned long long my_q1 = 0, my_q2 = 0;
-  for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
-    if (r < M.n_units) {
-      const int64_t u = M.unit_off + r;
-      const int32_t q = P.u_queries[u];
-      my_q1 += (unsigned)(q & 0xffff);
-      my_q2 += (unsigned)(q >> 16);
-      if (P.u_budget[u]) {
-        ++my_enum;
-        if ((S.modes & 1) && P.st_status[u]) ++my_skip;
-        if ((S.modes & 2) && P.ag_status[u]) ++my_skip;
-      }
-      if (S.modes & 4) my_skip += (P.pf_status[u] != 0) + (P.dc_status[u] != 0);
-    }
-    const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-    FRONT_ROW_FILTER(v)
-    ++my_rows;
-    if (!feasible(S, v)) continue;
-    ++my_feas;
-    const double nt = -v.thru, ns = -v.speed;
-    if (best.key < 0 || nt < best.nthru || (nt == best.nthru && ns <= best.nspeed)) {
-      BestKey k{nt, ns, v.gpus, mode_rank(v.mode), v.key};
-      if (best_less(P, M, plan_i, k, best)) best = k;
-    }
-    const unsigned long long sb = (unsigned long long)__double_as_longlong(v.speed);
-    smin = sb < smin ? sb : smin;
-    smax = sb > smax ? sb : smax;
-  }
-  atomicAdd(&cnt_feas, my_feas); atomicAdd(&cnt_rows, my_rows);
-  atomicAdd(&cnt_enum, my_enum); atomicAdd(&cnt_skip, my_skip);
-  atomicAdd((unsigned long long*)&results[s].queries_1d, my_q1);
-  atomicAdd((unsigned long long*)&results[s].queries_2d, my_q2);
-  bred[tid] = best;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (tid < w && best_less(P, M, plan_i, bred[tid + w], bred[tid])) bred[tid] = bred[tid + w];
-    __syncthreads();
-  }
-  if (tid == 0) {
-    lc_search_result& R = results[s];
-    R.n_enumerated = cnt_enum;
-    R.n_rows = cnt_rows;
-    R.n_feasible = cnt_feas;
-    R.n_skipped = cnt_skip;
-    R.best = bred[0].key;
-    R.best_thru = bred[0].key >= 0 ? -bred[0].nthru : 0.0;
-    R.best_speed = bred[0].key >= 0 ? -bred[0].nspeed : 0.0;
-    R.nearest = -1;
-    R.nearest_violation = 0.0;
-    R.front_off = (int32_t)foff;
-  }
-  const unsigned long long lo = block_min_u64(smin, ured);
-  const unsigned long long hi = block_max_u64(smax, ured);
-
-  // ---- nearest miss (search.py:190-208), only when nothing is feasible
-  if (cnt_feas == 0) {
-    MissKey miss{0, -1};
-    for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
-      const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-      FRONT_ROW_FILTER(v)
-      double worst = 1.0;
-      if (S.has_ttft && v.ttft > S.ttft_limit) { const double x = v.ttft / S.ttft_limit; if (x > worst) worst = x; }
-      if (S.has_floor && v.speed < S.speed_floor) {
-        const double x = v.speed == 0.0 ? INFINITY : S.speed_floor / v.speed;
-        if (x > worst) worst = x;
-      }
-      if (miss.key < 0 || worst <= miss.viol) {
-        MissKey mk{worst, v.key};
-        if (miss_less(P, M, plan_i, mk, miss)) miss = mk;
-      }
-    }
-    mred[tid] = miss;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-      if (tid < w && miss_less(P, M, plan_i, mred[tid + w], mred[tid])) mred[tid] = mred[tid + w];
-      __syncthreads();
-    }
-    if (tid == 0) {
-      results[s].nearest = mred[0].key;
-      results[s].nearest_violation = mred[0].viol;
-      results[s].n_front = 0;
-    }
-    return;
-  }
-
-  // ---- pass 2: bucket maxima (throughput >= 0, so its bit pattern orders like the value)
-  int shift = 0;
-  while (shift < 63 && ((hi >> shift) - (lo >> shift)) >= (unsigned long long)kSpeedBuckets) ++shift;
-  const unsigned long long base = lo >> shift;
-  for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
-    const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-    FRONT_ROW_FILTER(v)
-    if (!feasible(S, v)) continue;
-    const int b = (int)((((unsigned long long)__double_as_longlong(v.speed)) >> shift) - base);
-    atomicMax(&bmax[b], (unsigned long long)__double_as_longlong(v.thru));
-  }
-  __syncthreads();
-  // exclusive suffix max: bmax[b] <- max over buckets strictly above b
-  constexpr int per = kSpeedBuckets / kFrontThreads;
-  unsigned long long loc[per];
-  unsigned long long run = 0;
-  for (int j = per - 1; j >= 0; --j) { loc[j] = run; const unsigned long long x = bmax[tid * per + j]; run = x > run ? x : run; }
-  tsuf[tid] = run;
-  __syncthreads();
-  unsigned long long above = 0;
-  for (int t = tid + 1; t < kFrontThreads; ++t) above = tsuf[t] > above ? tsuf[t] : above;
-  __syncthreads();
-  for (int j = 0; j < per; ++j) bmax[tid * per + j] = loc[j] > above ? loc[j] : above;
-  __syncthreads();
-
-  // ---- pass 3: survivors
-  for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
-    const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-    FRONT_ROW_FILTER(v)
-    if (!feasible(S, v)) continue;
-    const int b = (int)((((unsigned long long)__double_as_longlong(v.speed)) >> shift) - base);
-    if (v.thru <= __longlong_as_double((long long)bmax[b]) && bmax[b] != 0ull) continue;
-    const int k = atomicAdd(&n_surv, 1);
-    if (k < kSurvivorCap) surv[k] = FrontCand{v.speed, v.thru, v.key};
-  }
-  __syncthreads();
-  const int nsv = n_surv;
-  if (nsv <= kSurvivorCap) {
-    for (int i = tid; i < nsv; i += blockDim.x) {
-      const FrontCand a = surv[i];
-      int rank = 0;
-      for (int j = 0; j < nsv; ++j) {
-        const FrontCand b = surv[j];
-        rank += (b.speed > a.speed) || (b.speed == a.speed && b.key < a.key);
-      }
-      sorted[rank] = a;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int m = 0;
-      front_of_sorted(sorted, nsv, keys_out, &m);
-      for (int i = 0; i < m; ++i) front[foff + i] = keys_out[i];
-      results[s].n_front = m;
-    }
-    return;
-  }
-  // ---- fallback (more candidates than shared memory holds): iterative staircase over all rows
-  double best_thru = -INFINITY;
-  while (true) {
-    double sm = -INFINITY;
-    bool any = false;
-    for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
-      const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-      FRONT_ROW_FILTER(v)
-      if (!feasible(S, v)) continue;
-      if (v.thru > best_thru) { any = true; sm = fmax(sm, v.speed); }
-    }
-    if (!__syncthreads_or(any)) break;
-    const double sp = block_max(any ? sm : -INFINITY, dred);
-    double tmax = -INFINITY;
-    for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
-      const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-      FRONT_ROW_FILTER(v)
-      if (!feasible(S, v)) continue;
-      if (v.speed == sp) tmax = fmax(tmax, v.thru);
-    }
-    const double top = block_max(tmax, dred);
-    if (tid == 0) {
-      for (int64_t r = 0; r < nrows_all; ++r) {
-        const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-        FRONT_ROW_FILTER(v)
-        if (!feasible(S, v)) continue;
-        if (v.speed == sp && v.thru == top) front[foff + nfront++] = v.key;
-      }
-    }
-    __syncthreads();
-    best_thru = top;
-  }
-  if (tid == 0) results[s].n_front = nfront;
-}
-
 // ---------------------------------------------------------------------------
-// Split versions of K5a and K4: each search's rows are spread over kSplit
-// blocks (grid = kSplit x n_search) and small per-search kernels merge the
-// partials.  Same results as the single-block kernels above (which stay as
-// the fallback for pool caps above kPoolLocal and survivor overflow).
+// K5a and K4.  Each search's rows are spread over kSplit blocks (grid =
+// kSplit x n_search) and small per-search kernels merge the partials.
+// K4: (1) counts, select_best (search.py:179-187) and the range of feasible
+// speeds; (2) per speed-bucket maximum throughput (buckets = top bits of the
+// IEEE pattern, so bucket order is speed order); (3) a row can only be on the
+// front if it beats the best throughput of every strictly faster bucket --
+// those maxima are real rows that would dominate it -- so only such
+// survivors go through the exact reference scan (search.py:156-176).
 constexpr int kSplit = 16;
+constexpr int kCompactFront = 256;  // fixed-stride copy of each front for one-shot D2H
 
 struct PoolPartial {
   PoolKey k[2][kPoolLocal];
@@ -1802,7 +1504,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, con
                                                                const int32_t* plan_i, const double* plan_d,
                                                                lc_search_result* results, const FrontMeta* fmeta,
                                                                const FrontCand* surv, const int32_t* n_surv,
-                                                               int64_t* front) {
+                                                               int64_t* front, int64_t* compact) {
   const int s = blockIdx.x, tid = threadIdx.x;
   if (!fmeta[s].any) return;
   extern __shared__ __align__(16) unsigned char fsm2[];
@@ -1832,6 +1534,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, con
       int m = 0;
       front_of_sorted(sorted, nsv, keys_out, &m);
       for (int i = 0; i < m; ++i) front[foff + i] = keys_out[i];
+      for (int i = 0; i < m && i < kCompactFront; ++i) compact[(int64_t)s * kCompactFront + i] = keys_out[i];
       results[s].n_front = m;
     }
     return;
@@ -1864,7 +1567,10 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, con
         const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
         FRONT_ROW_FILTER(v)
         if (!feasible(S, v)) continue;
-        if (v.speed == sp && v.thru == top) front[foff + nfront++] = v.key;
+        if (v.speed == sp && v.thru == top) {
+          if (nfront < kCompactFront) compact[(int64_t)s * kCompactFront + nfront] = v.key;
+          front[foff + nfront++] = v.key;
+        }
       }
     }
     __syncthreads();
@@ -1895,6 +1601,21 @@ int lc_open(int device, lc_ctx** out) {
   CK(cudaGetDeviceCount(&n));
   if (device < 0 || device >= n) return fail(LC_ERR_ARG, "lc_open: bad device index");
   CK(cudaSetDevice(device));
+  // kernel attributes are per process and device: set them once, to the largest
+  // shared-memory staging any database may need, so concurrent contexts never race
+  {
+    static std::mutex mu;
+    static bool done[64] = {false};
+    std::lock_guard<std::mutex> lock(mu);
+    if (device < 64 && !done[device]) {
+      const int big = 200 * 1024;
+      CK(cudaFuncSetAttribute(k_qtables, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+      CK(cudaFuncSetAttribute(k_dstables, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+      CK(cudaFuncSetAttribute(k_front_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)((sizeof(FrontCand) + 8) * kSurvivorCap)));
+      done[device] = true;
+    }
+  }
   lc_ctx* c = new lc_ctx();
   c->device = device;
   CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -1909,7 +1630,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
@@ -2133,7 +1854,6 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   const size_t smem = c->db->smem_bytes;
   auto launch_tables = [&](auto kern, int64_t n_items) -> int {
     if (n_items <= 0) return LC_OK;
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
     if (per_sm < 1) per_sm = 1;
@@ -2204,10 +1924,11 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     ++c->launches;
     k_front_pass3<<<g, kFrontThreads, 0, c->stream>>>(P, meta, pi, pd, res, fm, bk, sv, ns);
     const size_t fsmem = (sizeof(FrontCand) + 8) * kSurvivorCap;
-    CK(cudaFuncSetAttribute(k_front_final, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsmem));
     ++c->launches;
+    int64_t* fc = c->front_compact.get<int64_t>((size_t)c->n_search * kCompactFront, &err);
+    if (err != cudaSuccess) return fail(LC_ERR_CUDA, "front workspace allocation");
     k_front_final<<<c->n_search, kFrontThreads, fsmem, c->stream>>>(P, meta, pi, pd, res, fm, sv, ns,
-                                                                      (int64_t*)c->front.p);
+                                                                      (int64_t*)c->front.p, fc);
     CK(cudaGetLastError());
   }
   CK(cudaEventRecord(c->ev[6], c->stream));
@@ -2440,6 +2161,22 @@ int lc_replay_last(lc_ctx* c, int32_t iters, lc_batch_totals* totals) {
   return LC_OK;
 }
 
+int lc_replay_async(lc_ctx* c) {
+  if (!c || !c->db) return fail(LC_ERR_STATE, "lc_replay_async: no previous batch");
+  CK(cudaSetDevice(c->device));
+  CK(cudaEventRecord(c->ev[0], c->stream));
+  c->launches = 0;
+  int rc = run_enum(c);
+  if (rc) return rc;
+  return run_eval_pipeline(c, nullptr);
+}
+
+int lc_stream(lc_ctx* c, void** stream) {
+  if (!c || !stream) return fail(LC_ERR_ARG, "lc_stream: NULL argument");
+  *stream = (void*)c->stream;
+  return LC_OK;
+}
+
 int lc_fetch(lc_ctx* c, const lc_fetch_req* r) {
   if (!c || !r) return fail(LC_ERR_ARG, "lc_fetch: NULL argument");
   CK(cudaSetDevice(c->device));
@@ -2508,13 +2245,26 @@ int lc_fetch(lc_ctx* c, const lc_fetch_req* r) {
     }
   }
   if (r->front) {
-    int64_t k = 0;
-    for (int s = 0; s < c->n_search; ++s) {
-      const lc_search_result& R = c->hres[s];
-      if (R.n_front)
-        CK(cudaMemcpyAsync(r->front + k, (const int64_t*)c->front.p + R.front_off, R.n_front * 8,
-                           cudaMemcpyDeviceToHost, c->stream));
-      k += R.n_front;
+    bool fits = true;
+    for (int s = 0; s < c->n_search; ++s) fits &= c->hres[s].n_front <= kCompactFront;
+    if (fits && c->n_search) {
+      std::vector<int64_t> cf((size_t)c->n_search * kCompactFront);
+      CK(cudaMemcpyAsync(cf.data(), c->front_compact.p, cf.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      int64_t k = 0;
+      for (int s = 0; s < c->n_search; ++s) {
+        memcpy(r->front + k, cf.data() + (size_t)s * kCompactFront, 8 * (size_t)c->hres[s].n_front);
+        k += c->hres[s].n_front;
+      }
+    } else {
+      int64_t k = 0;
+      for (int s = 0; s < c->n_search; ++s) {
+        const lc_search_result& R = c->hres[s];
+        if (R.n_front)
+          CK(cudaMemcpyAsync(r->front + k, (const int64_t*)c->front.p + R.front_off, R.n_front * 8,
+                             cudaMemcpyDeviceToHost, c->stream));
+        k += R.n_front;
+      }
     }
   }
   CK(cudaStreamSynchronize(c->stream));

@@ -209,6 +209,7 @@ class Engine:
         n = len(workloads)
         searches = np.zeros(n, dtype=N.SEARCH_DESC_DTYPE)
         batches: list[int] = []
+        b_index: dict[tuple, int] = {}  # identical batch lists share one copy
         loads: list[np.ndarray] = []
         load_ix: dict = {}
         if space.prefill_pool_cap < 0 or space.decode_pool_cap < 0:
@@ -233,9 +234,12 @@ class Engine:
                 raise SearchError(f"at most {N.LC_MAX_BUDGETS} distinct gpu budgets are supported")
             s["n_budgets"] = len(budgets)
             s["budgets"][: len(budgets)] = budgets
-            bs = sorted(w.batch_sweep or space.batch_values)
-            s["b_off"], s["n_b"] = len(batches), len(bs)
-            batches.extend(bs)
+            bs = tuple(sorted(w.batch_sweep or space.batch_values))
+            off = b_index.get(bs)
+            if off is None:
+                off = b_index[bs] = len(batches)
+                batches.extend(bs)
+            s["b_off"], s["n_b"] = off, len(bs)
             s["has_ctx_capacity"] = space.ctx_capacity is not None
             s["ctx_capacity"] = space.ctx_capacity or 0
             s["chunked_prefill"] = int(bool(space.chunked_prefill))
@@ -264,6 +268,16 @@ class Engine:
         out.h2d_bytes = searches.nbytes + 8 * len(batches) + (l_arr.nbytes if loads else 0)
         out.d2h_bytes = results.nbytes + 4
         return out
+
+    def replay_async(self) -> None:
+        """Enqueue the last batch's device pipeline on this engine's stream (no sync)."""
+        self._call(self.lib.lc_replay_async, "lc_replay_async", self.ctx)
+
+    def stream_ptr(self) -> int:
+        """cudaStream_t of this engine (for torch.cuda.ExternalStream)."""
+        h = C.c_void_p()
+        self._call(self.lib.lc_stream, "lc_stream", self.ctx, C.byref(h))
+        return int(h.value or 0)
 
     def replay(self, iters: int = 1) -> N.LcBatchTotals:
         """Re-run the last batch's device pipeline (K0..K4) on resident inputs; per-kernel CUDA-event ms."""
