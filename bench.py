@@ -130,6 +130,8 @@ def cpu_reference(parts, sample_every: int, threads: int) -> dict:
 
 # --------------------------------------------------------------------------- distributed helpers
 def _dist_init():
+    """One process per GPU (torchrun env).  BENCH_DIST_BACKEND=gloo runs the same
+    sharding / all-gather logic with CPU collectives (e.g. several ranks on one GPU)."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -137,9 +139,20 @@ def _dist_init():
         import torch
         import torch.distributed as dist
 
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        local = local % max(1, torch.cuda.device_count())
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return ws, rank, local
+
+
+def _coll_device() -> str:
+    import torch.distributed as dist
+
+    return "cuda" if dist.get_backend() == "nccl" else "cpu"
 
 
 def _barrier(ws):
@@ -158,7 +171,7 @@ def _max_over_ranks(ws, x: float) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -169,7 +182,7 @@ def _sum_over_ranks(ws, x: float) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t)
     return float(t.item())
 

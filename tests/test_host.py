@@ -1,0 +1,130 @@
+"""Host-side logic that needs no GPU: DB ingest, the device image, plan
+templates, skip-reason formatting and report documents."""
+
+from __future__ import annotations
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+import paper_2601_06288_b200 as pkg
+from golden_io import BY_NAME, CASES, db_path, golden_report, model_doc
+from paper_2601_06288_b200.database import KIND_DIMS, flatten, grid_key
+from paper_2601_06288_b200.engine import _reason
+from paper_2601_06288_b200.plans import LABEL_CODE, build_space_plan
+from product_cases import case_objects
+
+
+def test_load_db_rebuilds_reference_grids():
+    from oracle import oracle
+
+    header, recs = oracle.read_db_records(db_path(BY_NAME["cfg4_dsv3"]))
+    db = pkg.load_db(db_path(BY_NAME["cfg4_dsv3"]))
+    assert len(db.records) == len(recs) == 1390
+    assert len(db._grids) == 41
+    for r in recs[:200]:
+        key = grid_key(r["kind"], r["quant"], r["shape"])
+        g = db._grids[key]
+        coords = tuple(int(r["shape"][a]) for a in KIND_DIMS[r["kind"]][1])
+        assert g.cells[coords] == r["latency_us"]
+
+
+def test_flat_image_matches_grid_index():
+    db = pkg.load_db(db_path(BY_NAME["a1_qwen_small"]))
+    flat = flatten(db)
+    assert flatten(db) is flat  # cached per object
+    for gid, key in enumerate(flat.keys):
+        g = db._grids[key]
+        off, n = flat.grid_axis_off[2 * gid], flat.grid_axis_len[2 * gid]
+        assert tuple(flat.axis_val[off: off + n]) == g.axis_values[0]
+        assert all(flat.axis_log[off + i] == math.log(v) for i, v in enumerate(g.axis_values[0]))
+        c0 = flat.grid_cell_off[gid]
+        first = tuple(v[0] for v in g.axis_values)
+        assert flat.cell[c0] == g.cells[first]
+        assert flat.cell_log[c0] == math.log(g.cells[first])
+
+
+@pytest.mark.parametrize("name", ["cfg4_dsv3", "gptoss_all_default", "a1_qwen_small", "moe_small_all"])
+def test_templates_resolve_every_grid_of_a_complete_db(name):
+    db, model, workload, space, dc = case_objects(BY_NAME[name])
+    plan = build_space_plan(model, space, flatten(db), db.backend)
+    assert all(e.grid >= 0 for infos in plan.infos for e in infos)
+    # one template per distinct (tp, pp, ep); slots cover every present entry of every step
+    assert len({(int(c["tp"]), int(c["pp"]), int(c["ep"])) for c in plan.combos}) == len(plan.infos)
+    for t, n in enumerate(plan.tmpl_n):
+        for i in range(int(n)):
+            coord = int(plan.entries[t * 16 + i]["coord"])
+            steps = [s for s in range(3) if plan.slot_of[t, i, s] >= 0]
+            assert steps == ([0, 2] if coord == 2 else [1, 2] if coord == 3 else [0, 1, 2])
+
+
+def _combo_for(plan, cfg_key):
+    for c in plan.combos:
+        tp, pp, ep, dp = (int(c[k]) for k in ("tp", "pp", "ep", "dp"))
+        if cfg_key.startswith(f"tp{tp}pp{pp}ep{ep}dp{dp}b"):
+            return c
+    raise KeyError(cfg_key)
+
+
+@pytest.mark.parametrize("name", ["missing_allreduce", "missing_tp16", "unsupported_quant_a100", "strict_long_isl",
+                                  "no_chunking", "batch_too_small"])
+def test_skip_reasons_format_like_the_reference(name):
+    """Rebuild each golden skip reason from the status word the device emits."""
+    case = BY_NAME[name]
+    db, model, workload, space, dc = case_objects(case)
+    flat = flatten(db)
+    plan = build_space_plan(model, space, flat, db.backend)
+    golden = golden_report(name)["skipped"]
+    assert golden
+    for sk in golden:
+        reason = sk["reason"]
+        combo = _combo_for(plan, sk["config"])
+        batch = int(sk["config"].rsplit("b", 1)[1])
+        kind = reason.split(":", 1)[0]
+        if kind == "InfeasibleConfigError":
+            code = 4 if "chunking is off" in reason else 5
+            got = _reason(code, 0, 0, plan, combo, flat, db, workload, space, batch)
+            assert got == reason
+            continue
+        code = {"MissingKeyError": 1, "ExtrapolationError": 2, "UnsupportedOperatorError": 3}[kind]
+        # find the entry whose message matches (labels are unique per template)
+        ok = False
+        for info in plan.infos[int(combo["tmpl"])]:
+            c0 = c1 = 0
+            if code == 2:
+                coords = reason.split("{", 1)[1].split("}", 1)[0]
+                vals = [int(x.split(":")[1]) for x in coords.split(",")]
+                c0, c1 = (vals + [0])[:2]
+            got = _reason(code | (LABEL_CODE[info.label] << 8), c0, c1, plan, combo, flat, db, workload, space,
+                          batch)
+            ok |= got == reason
+        assert ok, reason
+
+
+def test_report_document_shape():
+    from paper_2601_06288_b200.report import PerfEstimate, SearchReport, estimate_row
+
+    w = pkg.WorkloadSpec(isl=100, osl=10, ttft_limit_ms=50.0, min_speed=1.0)
+    cfg = pkg.ParallelConfig(tp=2, batch=4)
+    est = PerfEstimate("static", "m", cfg, 10.0, 2.0, 500.0, 123.0, cfg.gpus(), 4)
+    row = estimate_row(est)
+    rep = SearchReport("m", "trtllm", w, [row], [row], row, [], 1, 1.0, [1.0])
+    doc = json.loads(rep.to_json())
+    assert doc["counts"] == {"enumerated": 1, "evaluated": 1, "feasible": 1, "frontier": 1, "skipped": 0}
+    assert doc["best"]["config"] == "tp2pp1ep1dp1b4"
+    assert doc["schema"] == "llmconf-report/1" and doc["version"] == "0.1.0"
+    assert set(doc["rows"][0]) == {"mode", "model", "parallel", "batch", "runtime", "gpus", "ttft_ms", "tpot_ms",
+                                   "speed", "throughput_per_gpu", "config", "feasible", "frontier"}
+
+
+def test_spec_validation_mirrors_reference():
+    with pytest.raises(pkg.specs.WorkloadError):
+        pkg.WorkloadSpec(isl=10, osl=1, min_speed=1.0, tpot_limit_ms=1.0)
+    with pytest.raises(pkg.specs.ParallelConfigError):
+        pkg.ParallelConfig(tp=0)
+    with pytest.raises(pkg.specs.ModelConfigError):
+        pkg.ModelSpec.from_doc(dict(model_doc("qwen-small"), kv_heads=7))
+    with pytest.raises(pkg.specs.SearchError):
+        pkg.run_search(None, None, None, jobs=0)
