@@ -100,22 +100,38 @@ def _oracle_inputs(part):
     return header, recs, mdoc, space
 
 
-def cpu_reference(parts, sample_every: int, threads: int) -> dict:
-    """Time the oracle over every ``sample_every``-th search (all models), one search per thread."""
+def cpu_reference(parts, step: int, threads: int, jobs_per_step: int | None = None, batch_slice: int = 32) -> dict:
+    """Time the reference algorithm (C oracle) on a bounded, rotating sample of the sweep.
+
+    One job = one sweep workload restricted to a contiguous slice of ``batch_slice``
+    batch sizes (a smaller search of the same kind; per-candidate cost does not
+    depend on the slice), one job per host thread.  Successive steps walk
+    through (workload, slice) pairs of every model so the sample covers the
+    sweep.  Returns candidates evaluated / wall time.
+    """
     from oracle import oracle
 
     oracle.build()
+    jobs_per_step = jobs_per_step or 4 * threads
+    inputs = [_oracle_inputs(p) for p in parts]
+    pairs = []
+    for mi, part in enumerate(parts):
+        bl = list(part.space.batch_values)
+        slices = [bl[i: i + batch_slice] for i in range(0, len(bl), batch_slice)]
+        for wi in range(len(part.workloads)):
+            for si in range(len(slices)):
+                pairs.append((mi, wi, si, slices))
+    # deterministic stride through all (model, workload, slice) triples
+    stride = 7919
+    chosen = [pairs[((step * jobs_per_step + j) * stride) % len(pairs)] for j in range(jobs_per_step)]
     jobs = []
-    for part in parts:
-        header, recs, mdoc, space = _oracle_inputs(part)
-        for i, w in enumerate(part.workloads):
-            if i % sample_every == sample_every // 2:
-                jobs.append((header, recs, mdoc, w.to_doc(), space))
+    for mi, wi, si, slices in chosen:
+        header, recs, mdoc, _ = inputs[mi]
+        jobs.append((header, recs, mdoc, parts[mi].workloads[wi].to_doc(), {"batch_values": slices[si]}))
 
     def one(job):
         header, recs, mdoc, wdoc, space = job
-        doc = oracle.run_search(header, recs, mdoc, wdoc, space)
-        return doc["counts"]["enumerated"]
+        return oracle.run_search(header, recs, mdoc, wdoc, space)["counts"]["enumerated"]
 
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=threads) as ex:
@@ -123,8 +139,9 @@ def cpu_reference(parts, sample_every: int, threads: int) -> dict:
     dt = time.perf_counter() - t0
     cands = int(sum(counts))
     return {"value": cands / dt, "unit": UNIT, "cores": min(threads, len(jobs)), "kind": "port",
-            "sample": f"{len(jobs)} of {sum(len(p.workloads) for p in parts)} searches (every {sample_every}th), "
-                      f"{cands} candidates in {dt:.2f}s, oracle/oracle.c (C restatement of the reference)",
+            "sample": f"{len(jobs)} sweep workloads x {batch_slice}-batch slices per step (rotating), "
+                      f"{cands} candidates in {dt:.2f}s on {min(threads, len(jobs))} threads; "
+                      f"oracle/oracle.c (C restatement of the reference)",
             "seconds": dt, "candidates": cands}
 
 
@@ -204,7 +221,7 @@ def main() -> int:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--sweep", default="config5")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--cpu-sample-every", type=int, default=25)
+    ap.add_argument("--cpu-steps", type=int, default=6, help="reference-oracle sample steps for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
@@ -226,10 +243,10 @@ def main() -> int:
             return 0
         threads = os.cpu_count() or 1
         vals, secs = [], []
-        for _ in range(args.warmup):
-            cpu_reference(parts, args.cpu_sample_every * 3, threads)
-        for _ in range(args.steps):
-            r = cpu_reference(parts, args.cpu_sample_every, threads)
+        for i in range(args.warmup):
+            cpu_reference(parts, 10_000 + i, threads)
+        for i in range(args.steps):
+            r = cpu_reference(parts, i, threads)
             vals.append(r["value"])
             secs.append(r["seconds"])
         value = float(np.median(vals))
@@ -357,8 +374,12 @@ def main() -> int:
 
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
-        cpu = cpu_reference(parts, args.cpu_sample_every, os.cpu_count() or 1)
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        runs = [cpu_reference(parts, i, os.cpu_count() or 1) for i in range(args.cpu_steps)]
+        cands = sum(r["candidates"] for r in runs)
+        secs = sum(r["seconds"] for r in runs)
+        cpu = {"value": cands / secs, "unit": UNIT, "cores": runs[0]["cores"], "kind": "port",
+               "sample": f"{args.cpu_steps} steps of: " + runs[0]["sample"].split(", ", 1)[0]
+                         + f"; {cands} candidates in {secs:.2f}s total"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
