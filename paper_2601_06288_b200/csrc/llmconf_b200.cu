@@ -104,6 +104,12 @@ struct lc_space {
   int32_t* gclass_of;  // [n_tmpl]
 };
 
+// a decode-series table shared by the searches with the same (isl, batch list)
+struct DsGroup {
+  int64_t off, isl;
+  int32_t b_off, n_b, n_steps, _pad;
+};
+
 // one priced query (query tables and decode-series tables)
 struct QVal {
   double lat;
@@ -133,8 +139,9 @@ struct SearchMeta {
   int64_t cell_off;
   int64_t tail_off[3];  // per tail type
   int64_t qt_off;       // query table [slot][b_i]
-  int64_t ds_off;       // decode-series table [gclass][b_i][step]
+  int64_t ds_off;       // decode-series table [gclass][b_i][step], shared by searches with equal (isl, batches)
   int32_t n_steps;      // static decode samples (ceil((osl-1)/32), 0 without static mode)
+  int32_t ds_stride;    // steps stored per (gclass, batch) in the shared table (max over its searches)
   int64_t mark_off;     // offset of this search's batches in the mixed-token marking pass
   int32_t _pad2;
   int32_t unit_off, n_units;
@@ -151,7 +158,7 @@ struct lc_ctx {
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
-  DBuf front_compact, pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
+  DBuf ds_groups, front_compact, pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   // last batch
   const lc_db* db = nullptr;
   const lc_space* sp = nullptr;
@@ -162,6 +169,7 @@ struct lc_ctx {
   int64_t n_total_idx = 0;  // index of the unit total inside block_sums
   std::vector<SearchMeta> hmeta;
   std::vector<TailTable> htables;
+  std::vector<DsGroup> hds;
   std::vector<lc_search_result> hres;
 };
 
@@ -189,6 +197,7 @@ struct EvalParams {
   const lc_entry* gclasses; int32_t n_gclass; const int32_t* gclass_of;
   QVal* qt; int64_t n_qt;
   QVal* ds; int64_t n_ds;
+  const DsGroup* ds_groups; int32_t n_ds_groups;
   // batch
   const lc_search_desc* searches; const SearchMeta* meta; int32_t n_search;
   const int64_t* batches; const double* loads;
@@ -557,16 +566,20 @@ __global__ void __launch_bounds__(128) k_dstables(EvalParams P) {
   DbView V;
   stage_db(P, smem, &V);
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < P.n_ds; x += (int64_t)gridDim.x * blockDim.x) {
-    const int s = find_by_off(P.meta, P.n_search, x, 1);
-    const lc_search_desc& S = P.searches[s];
-    const SearchMeta& M = P.meta[s];
-    int64_t rel = x - M.ds_off;
-    const int k = (int)(rel % M.n_steps);
-    rel /= M.n_steps;
-    const int bi = (int)(rel % S.n_b);
-    const int g = (int)(rel / S.n_b);
+    int lo = 0, hi = P.n_ds_groups - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.ds_groups[mid].off <= x) lo = mid;
+      else hi = mid - 1;
+    }
+    const DsGroup G = P.ds_groups[lo];
+    int64_t rel = x - G.off;
+    const int k = (int)(rel % G.n_steps);
+    rel /= G.n_steps;
+    const int bi = (int)(rel % G.n_b);
+    const int g = (int)(rel / G.n_b);
     const lc_entry e = P.gclasses[g];
-    int64_t d[5] = {P.batches[S.b_off + bi], S.isl + 32ll * k + 1, e.d[2], e.d[3], e.d[4]};
+    int64_t d[5] = {P.batches[G.b_off + bi], G.isl + 32ll * k + 1, e.d[2], e.d[3], e.d[4]};
     int st = 0, nlog = 0;
     QVal out;
     out.lat = query(V, e, d, &st, &nlog);
@@ -659,7 +672,7 @@ __global__ void __launch_bounds__(128) k_eval_cells(EvalParams P) {
         // generation-step slots (same tokens), attention from the decode-series table
         double term[LC_MAX_ENTRIES];
         int m = 0, gi = -1;
-        const QVal* ds = P.ds + M.ds_off + ((int64_t)P.gclass_of[tmpl] * S.n_b + bi) * M.n_steps;
+        const QVal* ds = P.ds + M.ds_off + ((int64_t)P.gclass_of[tmpl] * S.n_b + bi) * M.ds_stride;
         const lc_entry* ge = nullptr;
         const StepArgs a0{PH_DECODE, 0, b, S.isl + 1, xt_dec};
         for (int i = 0; i < ne && !e.code; ++i) {
@@ -1630,7 +1643,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
@@ -1768,6 +1781,7 @@ static EvalParams make_params(lc_ctx* c) {
   P.gclasses = sp->gclasses; P.n_gclass = sp->n_gclass; P.gclass_of = sp->gclass_of;
   P.qt = (QVal*)c->qt.p; P.n_qt = c->n_qt;
   P.ds = (QVal*)c->ds.p; P.n_ds = c->n_ds;
+  P.ds_groups = (const DsGroup*)c->ds_groups.p; P.n_ds_groups = (int32_t)c->hds.size();
   P.searches = (const lc_search_desc*)c->searches.p;
   P.meta = (const SearchMeta*)c->meta.p;
   P.n_search = c->n_search;
@@ -2009,8 +2023,6 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     M.qt_off = qts;
     qts += (int64_t)sp->n_slots * S.n_b;
     M.n_steps = ((S.modes & 1) && S.osl > 1) ? (int32_t)((S.osl - 1 + 31) / 32) : 0;
-    M.ds_off = dss;
-    dss += (int64_t)sp->n_gclass * S.n_b * M.n_steps;
     M.tail_off[0] = M.tail_off[1] = M.tail_off[2] = 0;
     M.plan_off = (int32_t)plans;
     const int pc = (S.modes & 4) ? S.prefill_cap * S.decode_cap : 0;
@@ -2048,6 +2060,42 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
       }
     }
   }
+  // decode-series groups: the KV samples isl + 32k + 1 do not depend on osl
+  c->hds.clear();
+  {
+    std::map<std::vector<int64_t>, int32_t> blist, gidx;
+    for (int s = 0; s < n_search; ++s) {
+      const lc_search_desc& S = searches[s];
+      SearchMeta& M = c->hmeta[s];
+      M.ds_off = 0;
+      M.ds_stride = 0;
+      if (!M.n_steps || !sp->n_gclass) continue;
+      std::vector<int64_t> bl(batches + S.b_off, batches + S.b_off + S.n_b);
+      auto it = blist.find(bl);
+      const int32_t cb = it == blist.end() ? (blist[bl] = S.b_off) : it->second;
+      const std::vector<int64_t> key = {S.isl, cb, S.n_b};
+      auto jt = gidx.find(key);
+      int32_t gi;
+      if (jt == gidx.end()) {
+        gi = gidx[key] = (int32_t)c->hds.size();
+        c->hds.push_back(DsGroup{0, S.isl, cb, S.n_b, 0, 0});
+      } else {
+        gi = jt->second;
+      }
+      if (M.n_steps > c->hds[gi].n_steps) c->hds[gi].n_steps = M.n_steps;
+      M._pad2 = gi;  // group index until offsets are known
+    }
+    for (auto& g : c->hds) {
+      g.off = dss;
+      dss += (int64_t)sp->n_gclass * g.n_b * g.n_steps;
+    }
+    for (int s = 0; s < n_search; ++s) {
+      SearchMeta& M = c->hmeta[s];
+      if (!M.n_steps || !sp->n_gclass) continue;
+      M.ds_off = c->hds[M._pad2].off;
+      M.ds_stride = c->hds[M._pad2].n_steps;
+    }
+  }
   // dense mixed-step region: tokens = chunk_tokens + n_mix_gen <= context + batch
   c->n_pd_tails = tails;
   c->m_tmax = 0;
@@ -2076,6 +2124,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   double* dL = c->loads.get<double>((size_t)n_loads * 2 * (sp->n_experts > 0 ? sp->n_experts : 1), &err);
   SearchMeta* dM = c->meta.get<SearchMeta>(n_search, &err);
   TailTable* dT = c->tail_tables.get<TailTable>(c->htables.size(), &err);
+  DsGroup* dG = c->ds_groups.get<DsGroup>(c->hds.size(), &err);
   c->results.get<lc_search_result>(n_search, &err);
   if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
   if (n_search) CK(cudaMemcpyAsync(dS, searches, sizeof(lc_search_desc) * n_search, cudaMemcpyHostToDevice, c->stream));
@@ -2087,6 +2136,8 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   if (!c->htables.empty())
     CK(cudaMemcpyAsync(dT, c->htables.data(), sizeof(TailTable) * c->htables.size(), cudaMemcpyHostToDevice,
                        c->stream));
+  if (!c->hds.empty())
+    CK(cudaMemcpyAsync(dG, c->hds.data(), sizeof(DsGroup) * c->hds.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaEventRecord(c->ev[0], c->stream));
   c->launches = 0;
   int rc = run_enum(c);
