@@ -99,9 +99,23 @@ struct lc_space {
   struct TmplInfo* tmpl_info;  // [n_tmpl]
   int32_t n_slots, n_gclass;
   lc_slot* slots;
-  int32_t* slot_of;    // [n_tmpl][16][3]
+  int32_t* slot_of;    // [n_tmpl][16][3]: class << 16 | index within class
+  int32_t* class_slots;  // global slot id per (class, index), class c at class_off[c]
+  int32_t class_n[4], class_off[4];
   lc_entry* gclasses;
   int32_t* gclass_of;  // [n_tmpl]
+};
+
+// Query-table sharing.  A slot's inputs are (grid, coordinates); which search
+// inputs the coordinates depend on splits slots into four classes:
+//   0 prefill steps:            (context length, batch list, MoE load)
+//   1 decode, non-attention:    (batch list, MoE load)
+//   2 decode, attention:        (KV midpoint isl + osl/2, batch list)
+//   3 mixed steps:              the whole search
+// Searches that agree on a class's inputs share one table for that class.
+struct QtGroup {
+  int64_t off;
+  int32_t cls, search, n_slots, _pad;
 };
 
 // a decode-series table shared by the searches with the same (isl, batch list)
@@ -138,7 +152,7 @@ struct SearchMeta {
   int64_t raw_off, n_raw;
   int64_t cell_off;
   int64_t tail_off[3];  // per tail type
-  int64_t qt_off;       // query table [slot][b_i]
+  int64_t qt_off[4];    // query tables per slot class [slot-in-class][b_i] (classes in QtGroup)
   int64_t ds_off;       // decode-series table [gclass][b_i][step], shared by searches with equal (isl, batches)
   int32_t n_steps;      // static decode samples (ceil((osl-1)/32), 0 without static mode)
   int32_t ds_stride;    // steps stored per (gclass, batch) in the shared table (max over its searches)
@@ -158,7 +172,7 @@ struct lc_ctx {
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
-  DBuf ds_groups, front_compact, pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
+  DBuf qt_groups, ds_groups, front_compact, pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   // last batch
   const lc_db* db = nullptr;
   const lc_space* sp = nullptr;
@@ -170,6 +184,7 @@ struct lc_ctx {
   std::vector<SearchMeta> hmeta;
   std::vector<TailTable> htables;
   std::vector<DsGroup> hds;
+  std::vector<QtGroup> hqt;
   std::vector<lc_search_result> hres;
 };
 
@@ -194,6 +209,8 @@ struct EvalParams {
   int64_t m_tmax;                    // mixed tokens index range [0, m_tmax]
   uint8_t* m_used;                   // [n_loads][m_tmax + 1] mixed token counts in use
   const lc_slot* slots; int32_t n_slots; const int32_t* slot_of;
+  const int32_t* class_slots; int32_t class_off[4];
+  const QtGroup* qt_groups; int32_t n_qt_groups;
   const lc_entry* gclasses; int32_t n_gclass; const int32_t* gclass_of;
   QVal* qt; int64_t n_qt;
   QVal* ds; int64_t n_ds;
@@ -347,6 +364,7 @@ __global__ void k_unit_offsets(SearchMeta* meta, int n_search, const int32_t* po
 }
 
 // ---- K3: MoE tails table [type P/D/M][tp_i][ep_i][b_i] per search
+template <int PER>
 __global__ void k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
   __shared__ int hist_all[8][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -374,8 +392,7 @@ __global__ void k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
         const int64_t f = ep / tp > 1 ? ep / tp : 1;
         const int E = (int)P.n_experts;
         const double* q = P.loads + (int64_t)load * 2 * E;
-        if (E <= 256) result = warp_busiest_shard<8>(q, q + E, E, tok * f, P.topk, ep, hist);
-        else result = warp_busiest_shard<32>(q, q + E, E, tok * f, P.topk, ep, hist);
+        result = warp_busiest_shard<PER>(q, q + E, E, tok * f, P.topk, ep, hist);
         if (lane == 0) tails[t] = result;
       }
       continue;
@@ -395,10 +412,7 @@ __global__ void k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
       const int64_t pooled = tokens * f;
       const int E = (int)P.n_experts;
       const double* q = P.loads + (int64_t)T.load * 2 * E;
-      if (E <= 256)
-        result = warp_busiest_shard<8>(q, q + E, E, pooled, P.topk, ep, hist);
-      else
-        result = warp_busiest_shard<32>(q, q + E, E, pooled, P.topk, ep, hist);
+      result = warp_busiest_shard<PER>(q, q + E, E, pooled, P.topk, ep, hist);
     }
     if (lane == 0) tails[t] = result;
   }
@@ -492,16 +506,6 @@ __device__ __forceinline__ int find_cell_search(const SearchMeta* meta, int n, i
   return lo;
 }
 
-__device__ __forceinline__ int find_by_off(const SearchMeta* meta, int n, int64_t x, int which) {
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    const int64_t o = which == 0 ? meta[mid].qt_off : meta[mid].ds_off;
-    if (o <= x) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
 
 __device__ __forceinline__ int64_t tail_tokens(const EvalParams& P, const SearchMeta& M, const lc_search_desc& S,
                                                int type, int pair, int bi, int64_t tokens) {
@@ -522,28 +526,32 @@ __global__ void __launch_bounds__(128) k_qtables(EvalParams P) {
   DbView V;
   stage_db(P, smem, &V);
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < P.n_qt; x += (int64_t)gridDim.x * blockDim.x) {
-    const int s = find_by_off(P.meta, P.n_search, x, 0);
+    int lo = 0, hi = P.n_qt_groups - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.qt_groups[mid].off <= x) lo = mid;
+      else hi = mid - 1;
+    }
+    const QtGroup Gq = P.qt_groups[lo];
+    const int s = Gq.search;  // representative: every member agrees on this class's inputs
     const lc_search_desc& S = P.searches[s];
     const SearchMeta& M = P.meta[s];
-    const int64_t rel = x - M.qt_off;
-    const int slot = (int)(rel / S.n_b), bi = (int)(rel % S.n_b);
-    const lc_slot SL = P.slots[slot];
+    const int64_t rel = x - Gq.off;
+    const int j = (int)(rel / S.n_b), bi = (int)(rel % S.n_b);
+    const lc_slot SL = P.slots[P.class_slots[P.class_off[Gq.cls] + j]];
     QVal out{0.0, LC_ST_NOT_EVALUATED, 0};
     const int64_t b = P.batches[S.b_off + bi];
     const int64_t chunk = S.isl - S.prefix;
     const int64_t kv_mid = S.isl + S.osl / 2;
-    bool need = false;
+    bool need = true;
     StepArgs a{PH_DECODE, 0, b, kv_mid, 0};
     int type = 1;
     if (SL.step == LC_STEP_PREFILL) {
-      need = (S.modes & 5) != 0;
       a = StepArgs{PH_PREFILL, b * chunk, 0, chunk, 0};
       type = 0;
-    } else if (SL.step == LC_STEP_GEN) {
-      need = (S.modes & 7) != 0;
-    } else {
+    } else if (SL.step == LC_STEP_MIXED) {
       const AggSched sc = agg_schedule(S, b);
-      need = (S.modes & 2) && !sc.st;
+      need = !sc.st;
       a = StepArgs{PH_MIXED, sc.chunk_tokens, sc.n_mix_gen, kv_mid, 0};
       type = 2;
     }
@@ -592,8 +600,12 @@ __global__ void __launch_bounds__(128) k_dstables(EvalParams P) {
 // One step's total from the query table: sum in plan order of
 // ((lat * repeat) / 1000) * bubble, CPython sum() semantics (estimator.py:83-95);
 // the first failing entry in plan order decides the error.
-__device__ __forceinline__ int table_step(const EvalParams& P, const lc_entry* E, int ne, const int32_t* slot_row,
-                                          const QVal* qt, int n_b, int bi, const StepArgs& a, double bubble,
+__device__ __forceinline__ QVal qt_at(const EvalParams& P, const SearchMeta& M, int32_t so, int n_b, int bi) {
+  return P.qt[M.qt_off[so >> 16] + (int64_t)(so & 0xffff) * n_b + bi];
+}
+
+__device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta& M, const lc_entry* E, int ne,
+                                          const int32_t* slot_row, int n_b, int bi, const StepArgs& a, double bubble,
                                           double* out, ErrRec* err, int* q1, int* q2) {
   NeumaierSum sum;
   int c1 = 0, c2 = 0;
@@ -601,7 +613,7 @@ __device__ __forceinline__ int table_step(const EvalParams& P, const lc_entry* E
     const lc_entry& e = E[i];
     if (e.coord == LC_COORD_CTX && !a.n_ctx) continue;
     if (e.coord == LC_COORD_GEN && !a.n_gen) continue;
-    const QVal q = qt[(int64_t)slot_row[i * 3] * n_b + bi];
+    const QVal q = qt_at(P, M, slot_row[i * 3], n_b, bi);
     if (e.coord == LC_COORD_CTX || e.coord == LC_COORD_GEN) ++c2; else ++c1;
     if (q.status) {
       int64_t d[5];
@@ -636,7 +648,6 @@ __global__ void __launch_bounds__(128) k_eval_cells(EvalParams P) {
     const lc_entry* E = P.entries + (int64_t)tmpl * LC_MAX_ENTRIES;
     const int ne = P.tmpl_n[tmpl];
     const int32_t* so = P.slot_of + (int64_t)tmpl * LC_MAX_ENTRIES * 3;
-    const QVal* qt = P.qt + M.qt_off;
     const int64_t b = P.batches[S.b_off + bi];
     const bool do_st = (cf & 1) && (S.modes & 1), do_ag = (cf & 1) && (S.modes & 2), do_dg = (cf & 2) != 0;
     const int64_t mb = b > 1 ? b : 1;
@@ -656,7 +667,7 @@ __global__ void __launch_bounds__(128) k_eval_cells(EvalParams P) {
     ErrRec p_err{0, 0, 0, 0};
     if (do_st || do_dg) {
       const StepArgs a{PH_PREFILL, b * chunk, 0, chunk, expert_tokens(P, c, M, S, 0, bi, b * chunk)};
-      table_step(P, E, ne, so + LC_STEP_PREFILL, qt, S.n_b, bi, a, bubble, &p_total, &p_err, &q1, &q2);
+      table_step(P, M, E, ne, so + LC_STEP_PREFILL, S.n_b, bi, a, bubble, &p_total, &p_err, &q1, &q2);
       if (!p_err.code) o.qP = (q1 & 0xffff) | (q2 << 16);
       o.pf_status = p_err.code | (p_err.label << 8);
       o.pf_lat = p_total;
@@ -680,7 +691,7 @@ __global__ void __launch_bounds__(128) k_eval_cells(EvalParams P) {
           if (en.coord == LC_COORD_CTX) continue;
           QVal q;
           if (en.coord == LC_COORD_GEN) { q = ds[0]; gi = m; ge = &en; }
-          else q = qt[(int64_t)so[i * 3 + LC_STEP_GEN] * S.n_b + bi];
+          else q = qt_at(P, M, so[i * 3 + LC_STEP_GEN], S.n_b, bi);
           if (q.status) {
             int64_t d[5];
             entry_coords(en, a0, P.hidden, d);
@@ -735,10 +746,10 @@ __global__ void __launch_bounds__(128) k_eval_cells(EvalParams P) {
         double l_mix = 0.0, l_gen = 0.0;
         const StepArgs a{PH_MIXED, sc.chunk_tokens, sc.n_mix_gen, kv_mid,
                          expert_tokens(P, c, M, S, 2, bi, sc.chunk_tokens + sc.n_mix_gen)};
-        table_step(P, E, ne, so + LC_STEP_MIXED, qt, S.n_b, bi, a, bubble, &l_mix, &e, &q1, &q2);
+        table_step(P, M, E, ne, so + LC_STEP_MIXED, S.n_b, bi, a, bubble, &l_mix, &e, &q1, &q2);
         if (!e.code) o.qM = (q1 & 0xffff) | (q2 << 16);
         if (!e.code && (sc.t_gen || b == 1)) {
-          table_step(P, E, ne, so + LC_STEP_GEN, qt, S.n_b, bi, ga, bubble, &g_total, &g_err, &q1, &q2);
+          table_step(P, M, E, ne, so + LC_STEP_GEN, S.n_b, bi, ga, bubble, &g_total, &g_err, &q1, &q2);
           g_done = true;
           if (!g_err.code) o.qG = (q1 & 0xffff) | (q2 << 16);
           o.flags |= 1;
@@ -766,7 +777,7 @@ __global__ void __launch_bounds__(128) k_eval_cells(EvalParams P) {
     }
     if (do_dg) {
       if (!g_done) {
-        table_step(P, E, ne, so + LC_STEP_GEN, qt, S.n_b, bi, ga, bubble, &g_total, &g_err, &q1, &q2);
+        table_step(P, M, E, ne, so + LC_STEP_GEN, S.n_b, bi, ga, bubble, &g_total, &g_err, &q1, &q2);
         if (!g_err.code) o.qG = (q1 & 0xffff) | (q2 << 16);
       }
       o.dc_status = g_err.code | (g_err.label << 8);
@@ -1643,7 +1654,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
@@ -1736,8 +1747,31 @@ int lc_space_upload(lc_ctx* c, const lc_space_desc* d, lc_space** out) {
   sp->n_slots = d->n_slots;
   sp->n_gclass = d->n_gen_classes;
   if ((rc = upload(&sp->slots, d->slots, d->n_slots > 0 ? d->n_slots : 0, c->stream))) return rc;
-  if ((rc = upload(&sp->slot_of, d->slot_of, (size_t)(d->n_tmpl > 0 ? d->n_tmpl : 1) * LC_MAX_ENTRIES * 3, c->stream)))
-    return rc;
+  {
+    std::vector<int32_t> cls(d->n_slots > 0 ? d->n_slots : 1, 0), idx(d->n_slots > 0 ? d->n_slots : 1, 0);
+    std::vector<int32_t> lists[4];
+    for (int k = 0; k < d->n_slots; ++k) {
+      const lc_slot& sl = d->slots[k];
+      const int c0 = sl.step == LC_STEP_PREFILL ? 0 : sl.step == LC_STEP_MIXED ? 3 : (sl.e.coord == LC_COORD_GEN ? 2 : 1);
+      cls[k] = c0;
+      idx[k] = (int32_t)lists[c0].size();
+      lists[c0].push_back(k);
+    }
+    std::vector<int32_t> all;
+    for (int c0 = 0; c0 < 4; ++c0) {
+      sp->class_off[c0] = (int32_t)all.size();
+      sp->class_n[c0] = (int32_t)lists[c0].size();
+      all.insert(all.end(), lists[c0].begin(), lists[c0].end());
+    }
+    const size_t n_so = (size_t)(d->n_tmpl > 0 ? d->n_tmpl : 1) * LC_MAX_ENTRIES * 3;
+    std::vector<int32_t> so(n_so, -1);
+    for (size_t i = 0; i < n_so && d->n_tmpl > 0; ++i) {
+      const int32_t g = d->slot_of[i];
+      so[i] = g < 0 ? -1 : ((cls[g] << 16) | idx[g]);
+    }
+    if ((rc = upload(&sp->slot_of, so.data(), so.size(), c->stream))) return rc;
+    if ((rc = upload(&sp->class_slots, all.data(), all.size(), c->stream))) return rc;
+  }
   if ((rc = upload(&sp->gclasses, d->gen_classes, d->n_gen_classes > 0 ? d->n_gen_classes : 0, c->stream))) return rc;
   if ((rc = upload(&sp->gclass_of, d->gclass_of, d->n_tmpl > 0 ? d->n_tmpl : 1, c->stream))) return rc;
   CK(cudaStreamSynchronize(c->stream));
@@ -1752,7 +1786,7 @@ int lc_space_free(lc_space* sp) {
   cudaFree(sp->pair_used);
   cudaFree(sp->tmpl_info);
   cudaFree(sp->pair_canon);
-  cudaFree(sp->slots); cudaFree(sp->slot_of); cudaFree(sp->gclasses); cudaFree(sp->gclass_of);
+  cudaFree(sp->slots); cudaFree(sp->slot_of); cudaFree(sp->class_slots); cudaFree(sp->gclasses); cudaFree(sp->gclass_of);
   delete sp;
   return LC_OK;
 }
@@ -1778,6 +1812,9 @@ static EvalParams make_params(lc_ctx* c) {
   P.m_tmax = c->m_tmax;
   P.m_used = (uint8_t*)c->m_used.p;
   P.slots = sp->slots; P.n_slots = sp->n_slots; P.slot_of = sp->slot_of;
+  P.class_slots = sp->class_slots;
+  for (int k = 0; k < 4; ++k) P.class_off[k] = sp->class_off[k];
+  P.qt_groups = (const QtGroup*)c->qt_groups.p; P.n_qt_groups = (int32_t)c->hqt.size();
   P.gclasses = sp->gclasses; P.n_gclass = sp->n_gclass; P.gclass_of = sp->gclass_of;
   P.qt = (QVal*)c->qt.p; P.n_qt = c->n_qt;
   P.ds = (QVal*)c->ds.p; P.n_ds = c->n_ds;
@@ -1857,7 +1894,9 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     int blocks = (int)((warps + 7) / 8);
     if (blocks > sms * 16) blocks = sms * 16;
     ++c->launches;
-    k_tails<<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
+    // experts per lane: 8 covers E <= 256 (DeepSeek-V3, GPT-OSS) at a quarter of the registers
+    if (c->sp->n_experts <= 256) k_tails<8><<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
+    else k_tails<32><<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
     CK(cudaGetLastError());
   }
   CK(cudaEventRecord(c->ev[2], c->stream));
@@ -1874,7 +1913,6 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     int64_t blocks = (n_items + 127) / 128;
     const int64_t cap = (int64_t)sms * per_sm;
     if (blocks > cap) blocks = cap;
-    ++c->launches;
     ++c->launches;
     kern<<<(int)blocks, 128, smem, c->stream>>>(P);
     CK(cudaGetLastError());
@@ -2020,8 +2058,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     raw += M.n_raw;
     M.cell_off = cells;
     cells += (int64_t)sp->n_tmpl * S.n_b;
-    M.qt_off = qts;
-    qts += (int64_t)sp->n_slots * S.n_b;
+    M.qt_off[0] = M.qt_off[1] = M.qt_off[2] = M.qt_off[3] = 0;
     M.n_steps = ((S.modes & 1) && S.osl > 1) ? (int32_t)((S.osl - 1 + 31) / 32) : 0;
     M.tail_off[0] = M.tail_off[1] = M.tail_off[2] = 0;
     M.plan_off = (int32_t)plans;
@@ -2057,6 +2094,35 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
           ti = jt->second;
         }
         c->hmeta[s].tail_off[type] = c->htables[ti].off;
+      }
+    }
+  }
+  // query-table groups per slot class (see QtGroup)
+  c->hqt.clear();
+  {
+    std::map<std::vector<int64_t>, int32_t> blist, gidx;
+    for (int s = 0; s < n_search; ++s) {
+      const lc_search_desc& S = searches[s];
+      std::vector<int64_t> bl(batches + S.b_off, batches + S.b_off + S.n_b);
+      auto it = blist.find(bl);
+      const int64_t cb = it == blist.end() ? (blist[bl] = S.b_off) : it->second;
+      const bool need[4] = {(S.modes & 5) != 0, (S.modes & 7) != 0, (S.modes & 6) != 0, (S.modes & 2) != 0};
+      for (int cl = 0; cl < 4; ++cl) {
+        if (!need[cl] || !sp->class_n[cl]) continue;
+        std::vector<int64_t> key;
+        if (cl == 0) key = {0, S.isl - S.prefix, cb, S.n_b, S.load};
+        else if (cl == 1) key = {1, cb, S.n_b, S.load};
+        else if (cl == 2) key = {2, S.isl + S.osl / 2, cb, S.n_b};
+        else key = {3, s};
+        auto jt = gidx.find(key);
+        if (jt == gidx.end()) {
+          gidx[key] = (int32_t)c->hqt.size();
+          c->hqt.push_back(QtGroup{qts, cl, s, sp->class_n[cl], 0});
+          c->hmeta[s].qt_off[cl] = qts;
+          qts += (int64_t)sp->class_n[cl] * S.n_b;
+        } else {
+          c->hmeta[s].qt_off[cl] = c->hqt[jt->second].off;
+        }
       }
     }
   }
@@ -2125,6 +2191,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   SearchMeta* dM = c->meta.get<SearchMeta>(n_search, &err);
   TailTable* dT = c->tail_tables.get<TailTable>(c->htables.size(), &err);
   DsGroup* dG = c->ds_groups.get<DsGroup>(c->hds.size(), &err);
+  QtGroup* dQ = c->qt_groups.get<QtGroup>(c->hqt.size(), &err);
   c->results.get<lc_search_result>(n_search, &err);
   if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
   if (n_search) CK(cudaMemcpyAsync(dS, searches, sizeof(lc_search_desc) * n_search, cudaMemcpyHostToDevice, c->stream));
@@ -2138,6 +2205,8 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
                        c->stream));
   if (!c->hds.empty())
     CK(cudaMemcpyAsync(dG, c->hds.data(), sizeof(DsGroup) * c->hds.size(), cudaMemcpyHostToDevice, c->stream));
+  if (!c->hqt.empty())
+    CK(cudaMemcpyAsync(dQ, c->hqt.data(), sizeof(QtGroup) * c->hqt.size(), cudaMemcpyHostToDevice, c->stream));
   CK(cudaEventRecord(c->ev[0], c->stream));
   c->launches = 0;
   int rc = run_enum(c);
