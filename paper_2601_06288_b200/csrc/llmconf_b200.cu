@@ -172,7 +172,7 @@ struct lc_ctx {
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
-  DBuf qt_groups, ds_groups, front_compact, pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
+  DBuf pool_key, qt_groups, ds_groups, front_compact, pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   // last batch
   const lc_db* db = nullptr;
   const lc_space* sp = nullptr;
@@ -230,6 +230,7 @@ struct EvalParams {
   int32_t* dc_status; double* dc_v;
   int64_t* err_c;                    // [8][n_units]: (c0,c1) x (st,ag,pf,dc)
   int32_t* u_queries;                // q1 | q2 << 16 per unit
+  double* pool_key;                  // [2][n_cap]: (-rate)/gpus per pool role (search.py:276-277), +inf if skipped
   // cells (search x template x batch)
   const struct TmplInfo* tmpl_info;
   uint32_t* cell_flags;              // bit0: some candidate in budget, bit1: pool worker
@@ -832,15 +833,21 @@ __global__ void __launch_bounds__(256) k_expand(EvalParams P) {
       P.pf_status[u] = o.pf_status;
       if (o.pf_status) {
         P.err_c[4 * n + u] = P.cell_err[ci * 8 + 4]; P.err_c[5 * n + u] = P.cell_err[ci * 8 + 5];
+        P.pool_key[u] = INFINITY;
       } else {
-        P.pf_v[u] = o.pf_lat; P.pf_v[n + u] = (double)b * 1000.0 / o.pf_lat;
+        const double rate = (double)b * 1000.0 / o.pf_lat;
+        P.pf_v[u] = o.pf_lat; P.pf_v[n + u] = rate;
+        P.pool_key[u] = -rate / (double)c.gpus;
       }
       P.dc_status[u] = o.dc_status;
       if (o.dc_status) {
         P.err_c[6 * n + u] = P.cell_err[ci * 8 + 6]; P.err_c[7 * n + u] = P.cell_err[ci * 8 + 7];
+        P.pool_key[n + u] = INFINITY;
       } else {
+        const double rate = S.osl == 1 ? INFINITY : (double)b * 1000.0 / ((double)(S.osl - 1) * o.dc_lat);
         P.dc_v[u] = o.dc_lat;
-        P.dc_v[n + u] = S.osl == 1 ? INFINITY : (double)b * 1000.0 / ((double)(S.osl - 1) * o.dc_lat);
+        P.dc_v[n + u] = rate;
+        P.pool_key[n + u] = -rate / (double)c.gpus;
       }
     }
     // the generation step is a memo hit when a static decode step used the same KV length
@@ -1187,7 +1194,8 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
 // front if it beats the best throughput of every strictly faster bucket --
 // those maxima are real rows that would dominate it -- so only such
 // survivors go through the exact reference scan (search.py:156-176).
-constexpr int kSplit = 16;
+constexpr int kSplit = 64;      // blocks per search for the Pareto passes
+constexpr int kPoolSplit = 16;  // blocks per search for the pool top-k
 constexpr int kCompactFront = 256;  // fixed-stride copy of each front for one-shot D2H
 
 struct PoolPartial {
@@ -1200,61 +1208,66 @@ __device__ __forceinline__ void slice_of(int64_t n, int parts, int part, int64_t
   *hi = n * (part + 1) / parts;
 }
 
-// block-wide selection of the `cap` smallest keys among cand[0..m) (destructive)
-__device__ int block_select(const EvalParams& P, PoolKey* cand, int m, int cap, PoolKey* red, PoolKey* out) {
-  const int tid = threadIdx.x;
-  int got = 0;
+// k-way merge across a warp: lane l holds a sorted list lst[0..n) (n <= cap);
+// writes the warp's `cap` smallest keys, in order, to out[] and returns how many.
+__device__ int warp_merge(const EvalParams& P, const PoolKey* lst, int n, int cap, PoolKey* out) {
+  const int lane = threadIdx.x & 31;
+  int head = 0, got = 0;
   for (int k = 0; k < cap; ++k) {
-    PoolKey best{0.0, -1};
-    int where = -1;
-    for (int j = tid; j < m; j += blockDim.x)
-      if (pool_less(P, cand[j], best)) { best = cand[j]; where = j; }
-    red[tid] = best;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-      if (tid < w && pool_less(P, red[tid + w], red[tid])) red[tid] = red[tid + w];
-      __syncthreads();
+    PoolKey best = head < n ? lst[head] : PoolKey{0.0, -1};
+    int src = lane;
+    for (int o = 16; o > 0; o >>= 1) {
+      PoolKey other;
+      other.r = __shfl_xor_sync(0xffffffffu, best.r, o);
+      other.unit = __shfl_xor_sync(0xffffffffu, best.unit, o);
+      const int osrc = __shfl_xor_sync(0xffffffffu, src, o);
+      if (pool_less(P, other, best) || (other.unit == best.unit && osrc < src)) { best = other; src = osrc; }
     }
-    const PoolKey sel = red[0];
-    __syncthreads();
-    if (sel.unit < 0) break;
-    if (where >= 0 && best.unit == sel.unit) cand[where].unit = -1;
-    if (tid == 0) out[k] = sel;
+    if (best.unit < 0) break;
+    if (lane == src) ++head;
+    if (lane == 0) out[k] = best;
     ++got;
-    __syncthreads();
   }
   return got;
 }
 
 __global__ void k_pools_partial(EvalParams P, const SearchMeta* meta, PoolPartial* part) {
-  const int s = blockIdx.y, bx = blockIdx.x, tid = threadIdx.x;
+  const int s = blockIdx.y, bx = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const lc_search_desc& S = P.searches[s];
   if (!(S.modes & 4)) return;
-  __shared__ PoolKey red[kPoolThreads];
-  __shared__ PoolKey cand[kPoolThreads * kPoolLocal];
-  __shared__ PoolKey outk[kPoolLocal];
+  constexpr int kWarps = kPoolThreads / 32;
+  __shared__ PoolKey wout[kWarps][kPoolLocal];
+  __shared__ int wn[kWarps];
   int64_t lo, hi;
-  slice_of(meta[s].n_units, kSplit, bx, &lo, &hi);
+  slice_of(meta[s].n_units, kPoolSplit, bx, &lo, &hi);
   const int64_t u0 = meta[s].unit_off;
-  PoolPartial* dst = part + (int64_t)s * kSplit + bx;
+  PoolPartial* dst = part + (int64_t)s * kPoolSplit + bx;
   for (int role = 0; role < 2; ++role) {
     const int cap = role == 0 ? S.prefill_cap : S.decode_cap;
-    if (cap > kPoolLocal) { if (tid == 0) dst->n[role] = 0; continue; }
-    const int32_t* status = role == 0 ? P.pf_status : P.dc_status;
-    const double* v = role == 0 ? P.pf_v : P.dc_v;
+    if (cap > kPoolLocal || cap <= 0) { if (tid == 0) dst->n[role] = 0; continue; }
+    const double* keys = P.pool_key + (int64_t)role * P.n_cap;
     PoolKey lst[kPoolLocal];
     int n = 0;
     for (int64_t i = lo + tid; i < hi; i += blockDim.x) {
       const int32_t u = (int32_t)(u0 + i);
-      if (status[u] != 0) continue;
-      const PoolKey key{-v[P.n_cap + u] / (double)P.combos[P.u_combo[u]].gpus, u};
-      if (cap > 0) local_insert(P, lst, n, cap, key);
+      const double r = keys[u];
+      if (r == INFINITY) continue;  // pool candidate skipped
+      local_insert(P, lst, n, cap, PoolKey{r, u});
     }
-    for (int j = 0; j < kPoolLocal; ++j) cand[tid * kPoolLocal + j] = j < n ? lst[j] : PoolKey{0.0, -1};
+    const int got = warp_merge(P, lst, n, cap, wout[warp]);
+    if (lane == 0) wn[warp] = got;
     __syncthreads();
-    const int got = block_select(P, cand, kPoolThreads * kPoolLocal, cap, red, outk);
-    if (tid < got) dst->k[role][tid] = outk[tid];
-    if (tid == 0) dst->n[role] = got;
+    if (warp == 0) {
+      PoolKey l2[kPoolLocal];
+      int n2 = 0;
+      if (lane < kWarps) {
+        n2 = wn[lane];
+        for (int j = 0; j < n2; ++j) l2[j] = wout[lane][j];
+      }
+      PoolKey* o = dst->k[role];
+      const int g2 = warp_merge(P, l2, n2, cap, o);
+      if (lane == 0) dst->n[role] = g2;
+    }
     __syncthreads();
   }
 }
@@ -1264,48 +1277,57 @@ __global__ void k_pools_final(EvalParams P, SearchMeta* meta, const PoolPartial*
   const lc_search_desc& S = P.searches[s];
   if (!(S.modes & 4)) return;
   __shared__ PoolKey red[kPoolThreads];
-  __shared__ PoolKey cand[kSplit * kPoolLocal];
   __shared__ PoolKey outk[kPoolLocal];
   for (int role = 0; role < 2; ++role) {
     const int cap = role == 0 ? S.prefill_cap : S.decode_cap;
     int got = 0;
     if (cap <= kPoolLocal) {
-      for (int j = tid; j < kSplit * kPoolLocal; j += blockDim.x) {
-        const PoolPartial& pp = part[(int64_t)s * kSplit + j / kPoolLocal];
-        const int i = j % kPoolLocal;
-        cand[j] = i < pp.n[role] ? pp.k[role][i] : PoolKey{0.0, -1};
+      if (tid < 32) {
+        PoolKey l[kPoolLocal];
+        int n = 0;
+        if (tid < kPoolSplit) {
+          const PoolPartial& pp = part[(int64_t)s * kPoolSplit + tid];
+          n = pp.n[role];
+          for (int j = 0; j < n; ++j) l[j] = pp.k[role][j];
+        }
+        got = warp_merge(P, l, n, cap, outk);
+        __syncwarp();
+        if (tid < got) pool_sel[(int64_t)s * 128 + role * 64 + tid] = outk[tid].unit;
+      }
+      got = __shfl_sync(0xffffffffu, got, 0);  // warp 0's count, broadcast within warp 0 only
+      if (tid == 0) {
+        if (role == 0) meta[s].n_pre = got;
+        else meta[s].n_dec = got;
       }
       __syncthreads();
-      got = block_select(P, cand, kSplit * kPoolLocal, cap, red, outk);
-      if (tid < got) pool_sel[(int64_t)s * 128 + role * 64 + tid] = outk[tid].unit;
-    } else {
-      // large caps: rounds over all units (rare)
-      const int32_t u0 = meta[s].unit_off, nu = meta[s].n_units;
-      const int32_t* status = role == 0 ? P.pf_status : P.dc_status;
-      const double* v = role == 0 ? P.pf_v : P.dc_v;
-      PoolKey prev{0.0, -1};
-      for (int k = 0; k < cap && k < 64; ++k) {
-        PoolKey best{0.0, -1};
-        for (int i = tid; i < nu; i += blockDim.x) {
-          const int32_t u = u0 + i;
-          if (status[u] != 0) continue;
-          const PoolKey key{-v[P.n_cap + u] / (double)P.combos[P.u_combo[u]].gpus, u};
-          if (prev.unit >= 0 && !pool_less(P, prev, key)) continue;
-          if (pool_less(P, key, best)) best = key;
-        }
-        red[tid] = best;
-        __syncthreads();
-        for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-          if (tid < w && pool_less(P, red[tid + w], red[tid])) red[tid] = red[tid + w];
-          __syncthreads();
-        }
-        const PoolKey sel = red[0];
-        __syncthreads();
-        if (sel.unit < 0) break;
-        if (tid == 0) pool_sel[(int64_t)s * 128 + role * 64 + k] = sel.unit;
-        prev = sel;
-        ++got;
+      continue;
+    }
+    // large caps: rounds over all units (rare)
+    const int32_t u0 = meta[s].unit_off, nu = meta[s].n_units;
+    const double* keys = P.pool_key + (int64_t)role * P.n_cap;
+    PoolKey prev{0.0, -1};
+    for (int k = 0; k < cap && k < 64; ++k) {
+      PoolKey best{0.0, -1};
+      for (int i = tid; i < nu; i += blockDim.x) {
+        const int32_t u = u0 + i;
+        const double r = keys[u];
+        if (r == INFINITY) continue;
+        const PoolKey key{r, u};
+        if (prev.unit >= 0 && !pool_less(P, prev, key)) continue;
+        if (pool_less(P, key, best)) best = key;
       }
+      red[tid] = best;
+      __syncthreads();
+      for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (tid < w && pool_less(P, red[tid + w], red[tid])) red[tid] = red[tid + w];
+        __syncthreads();
+      }
+      const PoolKey sel = red[0];
+      __syncthreads();
+      if (sel.unit < 0) break;
+      if (tid == 0) pool_sel[(int64_t)s * 128 + role * 64 + k] = sel.unit;
+      prev = sel;
+      ++got;
     }
     if (tid == 0) {
       if (role == 0) meta[s].n_pre = got;
@@ -1533,7 +1555,8 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, con
   if (!fmeta[s].any) return;
   extern __shared__ __align__(16) unsigned char fsm2[];
   FrontCand* sorted = (FrontCand*)fsm2;                     // kSurvivorCap
-  int64_t* keys_out = (int64_t*)(sorted + kSurvivorCap);    // kSurvivorCap
+  FrontCand* staged = sorted + kSurvivorCap;                // kSurvivorCap
+  int64_t* keys_out = (int64_t*)(staged + kSurvivorCap);    // kSurvivorCap
   __shared__ double dred[32];
   __shared__ int nfront;
   const lc_search_desc& S = P.searches[s];
@@ -1543,7 +1566,10 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, con
   const int64_t foff = (int64_t)M.unit_off * 2 + M.plan_off;
   const int nsv = n_surv[s];
   if (nsv <= kSurvivorCap) {
-    const FrontCand* sv = surv + (int64_t)s * kSurvivorCap;
+    const FrontCand* svg = surv + (int64_t)s * kSurvivorCap;
+    for (int i = tid; i < nsv; i += blockDim.x) staged[i] = svg[i];
+    __syncthreads();
+    const FrontCand* sv = staged;
     for (int i = tid; i < nsv; i += blockDim.x) {
       const FrontCand a = sv[i];
       int rank = 0;
@@ -1636,7 +1662,7 @@ int lc_open(int device, lc_ctx** out) {
       CK(cudaFuncSetAttribute(k_qtables, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
       CK(cudaFuncSetAttribute(k_dstables, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
       CK(cudaFuncSetAttribute(k_front_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)((sizeof(FrontCand) + 8) * kSurvivorCap)));
+                              (int)((2 * sizeof(FrontCand) + 8) * kSurvivorCap)));
       done[device] = true;
     }
   }
@@ -1654,7 +1680,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaStreamDestroy(c->stream);
@@ -1835,6 +1861,7 @@ static EvalParams make_params(lc_ctx* c) {
   P.dc_status = (int32_t*)c->dc_status.p; P.dc_v = (double*)c->dc_v.p;
   P.err_c = (int64_t*)c->err_c.p;
   P.u_queries = (int32_t*)c->u_queries.p;
+  P.pool_key = (double*)c->pool_key.p;
   P.tmpl_info = sp->tmpl_info;
   P.cell_flags = (uint32_t*)c->cell_flags.p;
   P.cells = (CellOut*)c->cells.p;
@@ -1863,6 +1890,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   c->dc_status.get<int32_t>(n, &err); c->dc_v.get<double>(2 * n, &err);
   c->err_c.get<int64_t>(8 * n, &err);
   c->u_queries.get<int32_t>(n, &err);
+  c->pool_key.get<double>(2 * n, &err);
   c->cells.get<CellOut>(c->n_cells, &err);
   c->qt.get<QVal>(c->n_qt, &err);
   c->ds.get<QVal>(c->n_ds, &err);
@@ -1938,10 +1966,10 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   }
   CK(cudaEventRecord(c->ev[3], c->stream));
   {
-    PoolPartial* pp = c->pool_part.get<PoolPartial>((size_t)c->n_search * kSplit, &err);
+    PoolPartial* pp = c->pool_part.get<PoolPartial>((size_t)c->n_search * kPoolSplit, &err);
     if (err != cudaSuccess) return fail(LC_ERR_CUDA, "pool partial allocation");
     ++c->launches;
-    k_pools_partial<<<dim3(kSplit, c->n_search), kPoolThreads, 0, c->stream>>>(P, (const SearchMeta*)c->meta.p, pp);
+    k_pools_partial<<<dim3(kPoolSplit, c->n_search), kPoolThreads, 0, c->stream>>>(P, (const SearchMeta*)c->meta.p, pp);
     ++c->launches;
     k_pools_final<<<c->n_search, kPoolThreads, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, pp, (int32_t*)c->pool_sel.p);
     CK(cudaGetLastError());
@@ -1975,7 +2003,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     k_front_suffix<<<c->n_search, kFrontThreads, 0, c->stream>>>(fm, bk);
     ++c->launches;
     k_front_pass3<<<g, kFrontThreads, 0, c->stream>>>(P, meta, pi, pd, res, fm, bk, sv, ns);
-    const size_t fsmem = (sizeof(FrontCand) + 8) * kSurvivorCap;
+    const size_t fsmem = (2 * sizeof(FrontCand) + 8) * kSurvivorCap;
     ++c->launches;
     int64_t* fc = c->front_compact.get<int64_t>((size_t)c->n_search * kCompactFront, &err);
     if (err != cudaSuccess) return fail(LC_ERR_CUDA, "front workspace allocation");
