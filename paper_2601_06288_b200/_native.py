@@ -111,7 +111,7 @@ def load_library(path: str | os.PathLike | None = None):
     global _LIB
     if _LIB is not None and path is None:
         return _LIB
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("LC_B200_LIB", LIB_PATH))
     if not p.exists():
         raise NativeUnavailable(f"{p} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = C.CDLL(str(p))

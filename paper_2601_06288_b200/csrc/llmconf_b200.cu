@@ -632,7 +632,10 @@ __device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta&
 }
 
 // K2: one thread per cell assembles every step from the tables.
-__global__ void __launch_bounds__(128) k_eval_cells(EvalParams P) {
+#ifndef LC_CELL_MIN_BLOCKS
+#define LC_CELL_MIN_BLOCKS 8  // 64 registers: occupancy beats the few spills (measured)
+#endif
+__global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalParams P) {
   const int64_t ncell = P.n_cells_total;
   for (int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ci < ncell;
        ci += (int64_t)gridDim.x * blockDim.x) {
@@ -897,7 +900,7 @@ struct PlanRec {
   double r_sys, ttft, tpot, speed, thru;
 };
 
-__global__ void k_disagg(EvalParams P, SearchMeta* meta, const int32_t* pool_sel, int32_t* plan_i, double* plan_d,
+__global__ void __launch_bounds__(1024) k_disagg(EvalParams P, SearchMeta* meta, const int32_t* pool_sel, int32_t* plan_i, double* plan_d,
                          lc_search_result* results) {
   const int s = blockIdx.x;
   const lc_search_desc& S = P.searches[s];
@@ -1976,7 +1979,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   }
   CK(cudaEventRecord(c->ev[4], c->stream));
   ++c->launches;
-  k_disagg<<<c->n_search, 256, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, (const int32_t*)c->pool_sel.p,
+  k_disagg<<<c->n_search, 1024, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, (const int32_t*)c->pool_sel.p,
                                                 (int32_t*)c->plans_i.p, (double*)c->plans_d.p,
                                                 (lc_search_result*)c->results.p);
   CK(cudaGetLastError());
