@@ -305,11 +305,15 @@ def main() -> int:
     # per-kernel breakdown (sequential, untimed) for the roofline of the dominant kernel
     kernel_ms = np.zeros(6)
     launches_per_step = 0
+    tq = tq2 = n_cells = 0
     for p, wls in my_parts:
         if wls:
             tot = engines[p.model_name].replay(1)
             kernel_ms += np.array(list(tot.kernel_ms), dtype=np.float64)
             launches_per_step += int(tot.n_launches)
+            tq += int(tot.n_table_queries)
+            tq2 += int(tot.n_table_queries_2d)
+            n_cells += int(tot.n_cells)
     # timed steps: every model's pipeline enqueued at once on its own stream; one
     # CUDA-event span on the current stream covers all of them
     streams = {m: torch.cuda.ExternalStream(e.stream_ptr()) for m, e in engines.items()}
@@ -365,10 +369,11 @@ def main() -> int:
             "algorithmic_bytes_per_launch": alg_bytes, "queries_1d": q1, "queries_2d": q2,
             "kernel_ms": {"K0_enumerate": kernel_ms[0], "K3_moe_tails": kernel_ms[1], "K2_evaluate": kernel_ms[2],
                           "K5a_pools": kernel_ms[3], "K5b_disagg": kernel_ms[4], "K4_front": kernel_ms[5]}}
-    prof = ROOT / "profiles" / "ncu_k_eval_traffic.json"
+    prof = ROOT / "profiles" / "ncu_k2_traffic.json"
     if prof.exists():
         try:
-            roof["traffic"] = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            roof["traffic"] = json.loads(prof.read_text()).get("dram_bytes_per_step")
+            roof["traffic_source"] = "profiles/ncu_k2_traffic.json"
         except Exception:
             pass
 

@@ -174,6 +174,9 @@ typedef struct {
   float kernel_ms[6];                /* K0 enumerate, K3 tails, K2 evaluate (tables + cells + expand), K5a pools, K5b disagg, K4 front */
   int64_t n_raw;                     /* raw (tp,pp,ep,dp,batch) tuples examined */
   int64_t n_launches;                /* kernels launched by the device pipeline (K0..K4) */
+  int64_t n_table_queries;           /* distinct queries priced: query-table + decode-series entries */
+  int64_t n_table_queries_2d;        /* of which 2-D (attention) */
+  int64_t n_cells;                   /* (search, template, batch) cells */
 } lc_batch_totals;
 
 /* per-unit / per-plan / front arrays to copy back (any pointer may be NULL) */

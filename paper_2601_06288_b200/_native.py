@@ -65,7 +65,8 @@ class LcSearchResult(C.Structure):
 
 class LcBatchTotals(C.Structure):
     _fields_ = [("n_units", C.c_int64), ("n_plans", C.c_int64), ("n_front", C.c_int64),
-                ("kernel_ms", C.c_float * 6), ("n_raw", C.c_int64), ("n_launches", C.c_int64)]
+                ("kernel_ms", C.c_float * 6), ("n_raw", C.c_int64), ("n_launches", C.c_int64),
+                ("n_table_queries", C.c_int64), ("n_table_queries_2d", C.c_int64), ("n_cells", C.c_int64)]
 
 
 _FETCH_FIELDS = [

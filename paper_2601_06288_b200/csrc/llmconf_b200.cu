@@ -101,7 +101,7 @@ struct lc_space {
   lc_slot* slots;
   int32_t* slot_of;    // [n_tmpl][16][3]: class << 16 | index within class
   int32_t* class_slots;  // global slot id per (class, index), class c at class_off[c]
-  int32_t class_n[4], class_off[4];
+  int32_t class_n[4], class_off[4], class_n2d[4];
   lc_entry* gclasses;
   int32_t* gclass_of;  // [n_tmpl]
 };
@@ -180,6 +180,7 @@ struct lc_ctx {
   int64_t n_raw = 0, n_cap = 0, n_units = 0, n_tails = 0, n_plan_slots = 0, n_front_slots = 0, n_cells = 0;
   int64_t n_qt = 0, n_ds = 0, n_pd_tails = 0, m_tmax = 0, n_marks = 0;
   int64_t launches = 0;  // kernels launched by the last pipeline run
+  int64_t n_qt_2d = 0;   // 2-D entries among the query tables
   int64_t n_total_idx = 0;  // index of the unit total inside block_sums
   std::vector<SearchMeta> hmeta;
   std::vector<TailTable> htables;
@@ -1779,17 +1780,20 @@ int lc_space_upload(lc_ctx* c, const lc_space_desc* d, lc_space** out) {
   {
     std::vector<int32_t> cls(d->n_slots > 0 ? d->n_slots : 1, 0), idx(d->n_slots > 0 ? d->n_slots : 1, 0);
     std::vector<int32_t> lists[4];
+    int32_t n2d[4] = {0, 0, 0, 0};
     for (int k = 0; k < d->n_slots; ++k) {
       const lc_slot& sl = d->slots[k];
       const int c0 = sl.step == LC_STEP_PREFILL ? 0 : sl.step == LC_STEP_MIXED ? 3 : (sl.e.coord == LC_COORD_GEN ? 2 : 1);
       cls[k] = c0;
       idx[k] = (int32_t)lists[c0].size();
+      if (sl.e.coord == LC_COORD_CTX || sl.e.coord == LC_COORD_GEN) ++n2d[c0];
       lists[c0].push_back(k);
     }
     std::vector<int32_t> all;
     for (int c0 = 0; c0 < 4; ++c0) {
       sp->class_off[c0] = (int32_t)all.size();
       sp->class_n[c0] = (int32_t)lists[c0].size();
+      sp->class_n2d[c0] = n2d[c0];
       all.insert(all.end(), lists[c0].begin(), lists[c0].end());
     }
     const size_t n_so = (size_t)(d->n_tmpl > 0 ? d->n_tmpl : 1) * LC_MAX_ENTRIES * 3;
@@ -2130,6 +2134,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   }
   // query-table groups per slot class (see QtGroup)
   c->hqt.clear();
+  c->n_qt_2d = 0;
   {
     std::map<std::vector<int64_t>, int32_t> blist, gidx;
     for (int s = 0; s < n_search; ++s) {
@@ -2149,6 +2154,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
         if (jt == gidx.end()) {
           gidx[key] = (int32_t)c->hqt.size();
           c->hqt.push_back(QtGroup{qts, cl, s, sp->class_n[cl], 0});
+          c->n_qt_2d += (int64_t)sp->class_n2d[cl] * S.n_b;
           c->hmeta[s].qt_off[cl] = qts;
           qts += (int64_t)sp->class_n[cl] * S.n_b;
         } else {
@@ -2273,6 +2279,9 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     totals->n_front = nfront;
     totals->n_raw = c->n_raw;
     totals->n_launches = c->launches;
+    totals->n_table_queries = c->n_qt + c->n_ds;
+    totals->n_table_queries_2d = c->n_qt_2d + c->n_ds;
+    totals->n_cells = c->n_cells;
     float ms = 0;
     cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]); totals->kernel_ms[0] = ms;
     cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]); totals->kernel_ms[1] = ms;
@@ -2308,6 +2317,9 @@ int lc_replay_last(lc_ctx* c, int32_t iters, lc_batch_totals* totals) {
     totals->n_units = c->n_units;
     totals->n_raw = c->n_raw;
     totals->n_launches = c->launches;
+    totals->n_table_queries = c->n_qt + c->n_ds;
+    totals->n_table_queries_2d = c->n_qt_2d + c->n_ds;
+    totals->n_cells = c->n_cells;
   }
   return LC_OK;
 }
