@@ -2105,14 +2105,13 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   // MoE tail tables, shared between searches with the same inputs
   c->htables.clear();
   if (sp->is_moe) {
-    std::map<std::vector<int64_t>, int32_t> blist;  // batch list -> canonical offset
-    std::map<std::vector<int64_t>, int32_t> tindex;  // (type, canonical b_off, n_b, load, chunk) -> table
+    // batch lists are identified by (b_off, n_b): callers that pass one copy per
+    // distinct list (the Python engine does) get full sharing
+    std::map<std::vector<int64_t>, int32_t> tindex;  // (type, b_off, n_b, load, chunk) -> table
     const int64_t per_b = (int64_t)sp->n_tp * sp->n_ep;
     for (int s = 0; s < n_search; ++s) {
       const lc_search_desc& S = searches[s];
-      std::vector<int64_t> bl(batches + S.b_off, batches + S.b_off + S.n_b);
-      auto it = blist.find(bl);
-      const int32_t cb = it == blist.end() ? (blist[bl] = S.b_off) : it->second;
+      const int32_t cb = S.b_off;
       for (int type = 0; type < 2; ++type) {
         std::vector<int64_t> key = {type, cb, S.n_b, S.load, type == 0 ? S.isl - S.prefix : 0};
         auto jt = tindex.find(key);
@@ -2136,12 +2135,10 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   c->hqt.clear();
   c->n_qt_2d = 0;
   {
-    std::map<std::vector<int64_t>, int32_t> blist, gidx;
+    std::map<std::vector<int64_t>, int32_t> gidx;
     for (int s = 0; s < n_search; ++s) {
       const lc_search_desc& S = searches[s];
-      std::vector<int64_t> bl(batches + S.b_off, batches + S.b_off + S.n_b);
-      auto it = blist.find(bl);
-      const int64_t cb = it == blist.end() ? (blist[bl] = S.b_off) : it->second;
+      const int64_t cb = S.b_off;
       const bool need[4] = {(S.modes & 5) != 0, (S.modes & 7) != 0, (S.modes & 6) != 0, (S.modes & 2) != 0};
       for (int cl = 0; cl < 4; ++cl) {
         if (!need[cl] || !sp->class_n[cl]) continue;
@@ -2166,16 +2163,14 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   // decode-series groups: the KV samples isl + 32k + 1 do not depend on osl
   c->hds.clear();
   {
-    std::map<std::vector<int64_t>, int32_t> blist, gidx;
+    std::map<std::vector<int64_t>, int32_t> gidx;
     for (int s = 0; s < n_search; ++s) {
       const lc_search_desc& S = searches[s];
       SearchMeta& M = c->hmeta[s];
       M.ds_off = 0;
       M.ds_stride = 0;
       if (!M.n_steps || !sp->n_gclass) continue;
-      std::vector<int64_t> bl(batches + S.b_off, batches + S.b_off + S.n_b);
-      auto it = blist.find(bl);
-      const int32_t cb = it == blist.end() ? (blist[bl] = S.b_off) : it->second;
+      const int32_t cb = S.b_off;
       const std::vector<int64_t> key = {S.isl, cb, S.n_b};
       auto jt = gidx.find(key);
       int32_t gi;
