@@ -185,6 +185,8 @@ struct lc_ctx {
   std::vector<SearchMeta> hmeta;
   std::vector<TailTable> htables;
   std::vector<DsGroup> hds;
+  int64_t* pinned_front = nullptr;  // page-locked staging for front D2H
+  size_t pinned_front_cap = 0;
   std::vector<QtGroup> hqt;
   std::vector<lc_search_result> hres;
 };
@@ -1200,7 +1202,7 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
 // survivors go through the exact reference scan (search.py:156-176).
 constexpr int kSplit = 64;      // blocks per search for the Pareto passes
 constexpr int kPoolSplit = 16;  // blocks per search for the pool top-k
-constexpr int kCompactFront = 256;  // fixed-stride copy of each front for one-shot D2H
+constexpr int kCompactFront = 2048;  // fixed-stride copy of each front for one-shot D2H (= survivor cap)
 
 struct PoolPartial {
   PoolKey k[2][kPoolLocal];
@@ -1687,6 +1689,7 @@ int lc_close(lc_ctx* c) {
                   &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
+  if (c->pinned_front) cudaFreeHost(c->pinned_front);
   cudaStreamDestroy(c->stream);
   delete c;
   return LC_OK;
@@ -2406,12 +2409,22 @@ int lc_fetch(lc_ctx* c, const lc_fetch_req* r) {
     bool fits = true;
     for (int s = 0; s < c->n_search; ++s) fits &= c->hres[s].n_front <= kCompactFront;
     if (fits && c->n_search) {
-      std::vector<int64_t> cf((size_t)c->n_search * kCompactFront);
-      CK(cudaMemcpyAsync(cf.data(), c->front_compact.p, cf.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+      // copy only up to the longest front of each search row: rows are kCompactFront apart
+      int32_t maxf = 0;
+      for (int s = 0; s < c->n_search; ++s) maxf = c->hres[s].n_front > maxf ? c->hres[s].n_front : maxf;
+      const size_t need = (size_t)c->n_search * kCompactFront;
+      if (c->pinned_front_cap < need) {
+        if (c->pinned_front) cudaFreeHost(c->pinned_front);
+        CK(cudaHostAlloc((void**)&c->pinned_front, need * 8, cudaHostAllocDefault));
+        c->pinned_front_cap = need;
+      }
+      if (maxf > 0)
+        CK(cudaMemcpy2DAsync(c->pinned_front, kCompactFront * 8, c->front_compact.p, kCompactFront * 8,
+                             (size_t)maxf * 8, c->n_search, cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       int64_t k = 0;
       for (int s = 0; s < c->n_search; ++s) {
-        memcpy(r->front + k, cf.data() + (size_t)s * kCompactFront, 8 * (size_t)c->hres[s].n_front);
+        memcpy(r->front + k, c->pinned_front + (size_t)s * kCompactFront, 8 * (size_t)c->hres[s].n_front);
         k += c->hres[s].n_front;
       }
     } else {

@@ -15,6 +15,7 @@ attributes are read.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import math
 import threading
 import time
@@ -40,6 +41,7 @@ MODE_STATIC, MODE_AGG, MODE_DISAGG = 1, 2, 4
 ST_OK, ST_MISSING, ST_EXTRAP, ST_UNSUPPORTED, ST_CHUNK_OFF, ST_NO_SLOT = range(6)
 
 
+@functools.lru_cache(maxsize=256)
 def _moe_q(params, num_experts: int) -> np.ndarray:
     """[q_i = w_i / sum(w)] + by-weight order, numpy exactly as moe_load.py:51-57, 84, 97."""
     rng = np.random.default_rng(params.seed)
@@ -214,49 +216,71 @@ class Engine:
         load_ix: dict = {}
         if space.prefill_pool_cap < 0 or space.decode_pool_cap < 0:
             raise SearchError("pool caps must be >= 0")
+        # per-search fields gathered in lists, written column-wise
+        isl, osl, prefix, has_ttft, ttft, has_floor, floor_v, cap_v = [], [], [], [], [], [], [], []
+        modes_v, b_off, n_b, load_v = [], [], [], []
+        budget_rows = np.zeros((n, N.LC_MAX_BUDGETS), dtype=np.int64)
+        n_budgets = np.zeros(n, dtype=np.int32)
         for i, w in enumerate(workloads):
-            s = searches[i]
-            s["isl"], s["osl"], s["prefix"] = w.isl, w.osl, w.prefix_len
-            if w.ttft_limit_ms is not None:
-                s["has_ttft"], s["ttft_limit"] = 1, float(w.ttft_limit_ms)
-            floor = w.speed_floor()
-            if floor is not None:
-                s["has_floor"], s["speed_floor"] = 1, float(floor)
-                s["tpot_cap"] = float(w.tpot_ceiling())
+            isl.append(w.isl)
+            osl.append(w.osl)
+            prefix.append(w.prefix_len)
+            has_ttft.append(w.ttft_limit_ms is not None)
+            ttft.append(float(w.ttft_limit_ms) if w.ttft_limit_ms is not None else 0.0)
+            fl = w.speed_floor()
+            has_floor.append(fl is not None)
+            floor_v.append(float(fl) if fl is not None else 0.0)
+            cap_v.append(float(w.tpot_ceiling()) if fl is not None else 0.0)
             if mode_override is not None:
-                modes = mode_override
+                modes_v.append(mode_override)
             else:
-                modes = ((MODE_STATIC if "static" in w.modes else 0) | (MODE_AGG if "aggregated" in w.modes else 0)
-                         | (MODE_DISAGG if "disaggregated" in w.modes else 0))
-            s["modes"] = modes
-            budgets = sorted(set(w.gpu_budgets)) if enforce_budget else []
-            if len(budgets) > N.LC_MAX_BUDGETS:
-                raise SearchError(f"at most {N.LC_MAX_BUDGETS} distinct gpu budgets are supported")
-            s["n_budgets"] = len(budgets)
-            s["budgets"][: len(budgets)] = budgets
-            bs = tuple(sorted(w.batch_sweep or space.batch_values))
-            off = b_index.get(bs)
+                modes_v.append((MODE_STATIC if "static" in w.modes else 0) | (MODE_AGG if "aggregated" in w.modes else 0)
+                               | (MODE_DISAGG if "disaggregated" in w.modes else 0))
+            if enforce_budget and w.gpu_budgets:
+                budgets = sorted(set(w.gpu_budgets))
+                if len(budgets) > N.LC_MAX_BUDGETS:
+                    raise SearchError(f"at most {N.LC_MAX_BUDGETS} distinct gpu budgets are supported")
+                n_budgets[i] = len(budgets)
+                budget_rows[i, : len(budgets)] = budgets
+            src = w.batch_sweep or space.batch_values
+            key = (id(src), len(src)) if isinstance(src, tuple) else tuple(src)
+            off = b_index.get(key)
             if off is None:
-                off = b_index[bs] = len(batches)
-                batches.extend(bs)
-            s["b_off"], s["n_b"] = off, len(bs)
-            s["has_ctx_capacity"] = space.ctx_capacity is not None
-            s["ctx_capacity"] = space.ctx_capacity or 0
-            s["chunked_prefill"] = int(bool(space.chunked_prefill))
-            s["kv_mem_fraction"] = float(space.kv_mem_fraction)
-            s["prefill_cap"], s["decode_cap"] = space.prefill_pool_cap, space.decode_pool_cap
-            s["ttft_headroom"] = float(disagg.ttft_headroom)
-            s["prefill_util"] = float(disagg.prefill_utilization)
-            s["decode_util"] = float(disagg.decode_utilization)
-            s["max_x"], s["max_y"] = disagg.max_prefill_replicas, disagg.max_decode_replicas
-            s["load"] = -1
+                bs = tuple(sorted(src))
+                off = b_index.get(bs)
+                if off is None:
+                    off = len(batches)
+                    batches.extend(bs)
+                    b_index[bs] = off
+                b_index[key] = off
+            b_off.append(off)
+            n_b.append(len(src))
+            ld = -1
             if plan.is_moe:
                 params = w.moe_load if w.moe_load is not None else DEFAULT_MOE_LOAD
                 lk = (params.alpha, params.x_min, params.x_max, params.seed)
                 if lk not in load_ix:
                     load_ix[lk] = len(loads)
                     loads.append(_moe_q(params, plan.n_experts))
-                s["load"] = load_ix[lk]
+                ld = load_ix[lk]
+            load_v.append(ld)
+        searches["isl"], searches["osl"], searches["prefix"] = isl, osl, prefix
+        searches["has_ttft"], searches["ttft_limit"] = has_ttft, ttft
+        searches["has_floor"], searches["speed_floor"], searches["tpot_cap"] = has_floor, floor_v, cap_v
+        searches["modes"] = modes_v
+        searches["n_budgets"] = n_budgets
+        searches["budgets"] = budget_rows
+        searches["b_off"], searches["n_b"] = b_off, n_b
+        searches["has_ctx_capacity"] = space.ctx_capacity is not None
+        searches["ctx_capacity"] = space.ctx_capacity or 0
+        searches["chunked_prefill"] = int(bool(space.chunked_prefill))
+        searches["kv_mem_fraction"] = float(space.kv_mem_fraction)
+        searches["prefill_cap"], searches["decode_cap"] = space.prefill_pool_cap, space.decode_pool_cap
+        searches["ttft_headroom"] = float(disagg.ttft_headroom)
+        searches["prefill_util"] = float(disagg.prefill_utilization)
+        searches["decode_util"] = float(disagg.decode_utilization)
+        searches["max_x"], searches["max_y"] = disagg.max_prefill_replicas, disagg.max_decode_replicas
+        searches["load"] = load_v
         b_arr = np.array(batches if batches else [1], dtype=np.int64)
         l_arr = np.concatenate(loads) if loads else np.zeros(1)
         results = np.zeros(n, dtype=N.SEARCH_RESULT_DTYPE)

@@ -25,3 +25,11 @@ p = parts[0]
 pr = cProfile.Profile(); pr.enable()
 out = engs[p.model_name].run_batch(p.db, p.model, p.space, p.workloads); fetch_fronts(out)
 pr.disable(); pstats.Stats(pr).sort_stats("cumulative").print_stats(14)
+
+# front / plan statistics of the sweep
+for p in parts:
+    out = engs[p.model_name].run_batch(p.db, p.model, p.space, p.workloads)
+    r = out.results
+    print(p.model_name, "n_front max/mean", int(r["n_front"].max()), float(r["n_front"].mean()),
+          "n_plans max", int(r["n_plans"].max()), "units/search max", int(r["n_units"].max()),
+          "feasible mean", float(r["n_feasible"].mean()))
