@@ -6,7 +6,7 @@ hand-written sm_100a kernels behind the C ABI in include/llmconf_b200.h.
 """
 
 from .database import PerfDatabase, load_db
-from .engine import Engine, enumerate_candidates, get_engine, run_search
+from .engine import Engine, enumerate_candidates, get_engine, run_search, run_search_json
 from .report import SearchReport, csv_from_doc, export_csv
 from .specs import (
     DEFAULT_DISAGG,
@@ -26,5 +26,5 @@ __all__ = [
     "CandidateSpace", "DEFAULT_DISAGG", "DisaggConstants", "Engine", "HardwareSpec", "ModelSpec", "MoESpec",
     "ParallelConfig", "PerfDatabase", "PowerLawParams", "SearchReport", "WorkloadSpec", "csv_from_doc",
     "enumerate_candidates", "export_csv", "get_engine", "load_db", "load_hardware_spec", "load_model_spec",
-    "run_search",
+    "run_search", "run_search_json",
 ]

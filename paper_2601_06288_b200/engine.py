@@ -453,3 +453,23 @@ def enumerate_candidates(model, space, workload, db, enforce_budget: bool = True
         bs = out.batches[U["unit_batch"][:n]]
         return [space.config(int(c["tp"]), int(c["pp"]), int(c["ep"]), int(c["dp"]), int(b), db.backend)
                 for c, b in zip(combos, bs)]
+
+
+def run_search_json(db, model, workload, space=CandidateSpace(), jobs: int = 1,
+                    disagg_constants=DEFAULT_DISAGG, device: int = 0) -> str:
+    """``run_search(...).to_json()`` without materialising per-row objects.
+
+    Same bytes as the reference's report JSON (search.py:262-264); rows are
+    written from the device's column arrays (fastreport.report_json).
+    """
+    from .fastreport import columns_from_batch, report_json
+
+    if jobs < 1:
+        raise SearchError("jobs must be >= 1")
+    t0 = time.perf_counter()
+    eng = get_engine(device)
+    with eng._lock:
+        out = eng.run_batch(db, model, space, [workload], disagg_constants)
+        cols = columns_from_batch(out, 0, db, model, workload, space, 0.0)
+    cols.total_ms = (time.perf_counter() - t0) * 1000.0
+    return report_json(cols)

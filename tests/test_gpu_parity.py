@@ -60,3 +60,25 @@ def test_enumerate_candidates_matches_reference_counts(pkg):
         db, model, workload, space, dc = case_objects(case)
         cands = pkg.enumerate_candidates(model, space, workload, db)
         assert len(cands) == golden_report(name)["counts"]["enumerated"]
+
+
+@pytest.mark.parametrize("name", ["cfg2_qwen3_disagg", "cfg4_dsv3", "missing_tp16", "unmeetable_sla", "flat_ties_moe",
+                                  "gptoss_all_default"])
+def test_columnar_json_matches_object_report(pkg, name):
+    from golden_io import BY_NAME
+    from paper_2601_06288_b200.engine import build_report, get_engine
+    from paper_2601_06288_b200.fastreport import columns_from_batch, report_json
+
+    case = BY_NAME[name]
+    db, model, workload, space, dc = case_objects(case)
+    eng = get_engine(0)
+    with eng._lock:
+        out = eng.run_batch(db, model, space, [workload], dc)
+        slow = build_report(out, 0, db, model, workload, space, 7.25).to_json()
+        fast = report_json(columns_from_batch(out, 0, db, model, workload, space, 7.25))
+    assert fast == slow
+    doc = json.loads(fast)
+    doc.pop("timing")
+    golden = golden_report(name)
+    golden.pop("_meta")
+    assert json.dumps(doc, sort_keys=True) == json.dumps(golden, sort_keys=True)
