@@ -709,26 +709,50 @@ __global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalPara
           term[m++] = 0.0 + ms * bubble;
         }
         if (!e.code) {
+          // terms before the attention entry give a fixed partial state; two samples
+          // are then summed as independent chains (ILP), in plan order
+          NeumaierSum pre;
+          for (int i = 0; i < gi; ++i) pre.add(term[i]);
           double t_gen = 0.0;
-          int64_t k = 0;
+          const int nsteps = M.n_steps;
           int step = 0;
-          while (k < S.osl - 1) {
+          for (; step < nsteps && !e.code; step += 2) {
+            const bool two = step + 1 < nsteps;
+            double g0 = term[gi], g1 = 0.0;
             if (step > 0) {
               const QVal q = ds[step];
               if (q.status) {
-                e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + k + 1;
+                e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + 32ll * step + 1;
                 break;
               }
-              const double ms = q.lat * (double)ge->repeat / 1000.0;
-              term[gi] = 0.0 + ms * bubble;
+              g0 = 0.0 + (q.lat * (double)ge->repeat / 1000.0) * bubble;
             }
-            NeumaierSum sum;
-            for (int i = 0; i < m; ++i) sum.add(term[i]);
-            const int64_t run = (S.osl - 1 - k) < 32 ? (S.osl - 1 - k) : 32;
-            t_gen += sum.result() * (double)run;
-            k += run;
-            ++step;
+            if (two) {
+              const QVal q = ds[step + 1];
+              if (q.status) {
+                e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + 32ll * (step + 1) + 1;
+                break;
+              }
+              g1 = 0.0 + (q.lat * (double)ge->repeat / 1000.0) * bubble;
+            }
+            NeumaierSum s0 = pre, s1 = pre;
+            s0.add(g0);
+            s1.add(g1);
+            for (int i = gi + 1; i < m; ++i) {
+              const double x = term[i];
+              s0.add(x);
+              s1.add(x);
+            }
+            const int64_t k0 = 32ll * step;
+            const int64_t run0 = (S.osl - 1 - k0) < 32 ? (S.osl - 1 - k0) : 32;
+            t_gen += s0.result() * (double)run0;
+            if (two) {
+              const int64_t k1 = k0 + 32;
+              const int64_t run1 = (S.osl - 1 - k1) < 32 ? (S.osl - 1 - k1) : 32;
+              t_gen += s1.result() * (double)run1;
+            }
           }
+          step = step < nsteps ? step : nsteps;
           if (!e.code) {
             tpot = t_gen / (double)(S.osl - 1);
             o.qSD = ((m - 1) * step & 0xffff) | (step << 16);
