@@ -167,6 +167,8 @@ typedef struct {
   double nearest_violation;
   double best_thru, best_speed;
   int64_t queries_1d, queries_2d;    /* reference-equivalent query_latency calls (memoised) */
+  int32_t n_survivors;               /* rows left for the exact Pareto scan after bucket pruning */
+  int32_t _pad;
 } lc_search_result;
 
 typedef struct {

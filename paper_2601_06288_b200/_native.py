@@ -60,7 +60,7 @@ class LcSearchResult(C.Structure):
                 ("n_front", C.c_int32), ("front_off", C.c_int32), ("n_plans", C.c_int32), ("plan_off", C.c_int32),
                 ("best", C.c_int64), ("nearest", C.c_int64), ("nearest_violation", C.c_double),
                 ("best_thru", C.c_double), ("best_speed", C.c_double), ("queries_1d", C.c_int64),
-                ("queries_2d", C.c_int64)]
+                ("queries_2d", C.c_int64), ("n_survivors", C.c_int32), ("_pad", C.c_int32)]
 
 
 class LcBatchTotals(C.Structure):

@@ -1595,26 +1595,63 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, con
   const int64_t nrows_all = 2 * (int64_t)M.n_units + nplan;
   const int64_t foff = (int64_t)M.unit_off * 2 + M.plan_off;
   const int nsv = n_surv[s];
+  if (tid == 0) results[s].n_survivors = nsv;
   if (nsv <= kSurvivorCap) {
+    // bitonic sort of the survivors by (speed desc, row key asc), padded to a power of two
     const FrontCand* svg = surv + (int64_t)s * kSurvivorCap;
-    for (int i = tid; i < nsv; i += blockDim.x) staged[i] = svg[i];
+    int np2 = 1;
+    while (np2 < nsv) np2 <<= 1;
+    for (int i = tid; i < np2; i += blockDim.x)
+      sorted[i] = i < nsv ? svg[i] : FrontCand{-INFINITY, 0.0, INT64_MAX};
     __syncthreads();
-    const FrontCand* sv = staged;
-    for (int i = tid; i < nsv; i += blockDim.x) {
-      const FrontCand a = sv[i];
-      int rank = 0;
-      for (int j = 0; j < nsv; ++j) {
-        const FrontCand b = sv[j];
-        rank += (b.speed > a.speed) || (b.speed == a.speed && b.key < a.key);
+    for (int k = 2; k <= np2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = tid; i < np2; i += blockDim.x) {
+          const int l = i ^ j;
+          if (l > i) {
+            const FrontCand a = sorted[i], b = sorted[l];
+            const bool a_first = (a.speed > b.speed) || (a.speed == b.speed && a.key < b.key);
+            const bool up = (i & k) == 0;
+            if (up != a_first) { sorted[i] = b; sorted[l] = a; }
+          }
+        }
+        __syncthreads();
       }
-      sorted[rank] = a;
+    }
+    // group maxima and the running maximum of all faster rows, in parallel
+    double* pm = (double*)staged;  // inclusive prefix max of thru over sorted order
+    for (int i = tid; i < nsv; i += blockDim.x) pm[i] = sorted[i].thru;
+    __syncthreads();
+    for (int off = 1; off < nsv; off <<= 1) {
+      double v[8];
+      int c = 0;
+      for (int i = tid; i < nsv; i += blockDim.x, ++c) v[c & 7] = (i >= off) ? fmax(pm[i], pm[i - off]) : pm[i];
+      __syncthreads();
+      c = 0;
+      for (int i = tid; i < nsv; i += blockDim.x, ++c) pm[i] = v[c & 7];
+      __syncthreads();
+    }
+    int* flag = (int*)keys_out;  // front membership, then output positions
+    for (int i = tid; i < nsv; i += blockDim.x) {
+      int g0 = i;
+      while (g0 > 0 && sorted[g0 - 1].speed == sorted[i].speed) --g0;
+      int g1 = i;
+      while (g1 + 1 < nsv && sorted[g1 + 1].speed == sorted[i].speed) ++g1;
+      double top = -INFINITY;
+      for (int j = g0; j <= g1; ++j) top = fmax(top, sorted[j].thru);
+      const double faster = g0 > 0 ? pm[g0 - 1] : -INFINITY;
+      flag[i] = (sorted[i].thru == top && top > faster) ? 1 : 0;
     }
     __syncthreads();
     if (tid == 0) {
       int m = 0;
-      front_of_sorted(sorted, nsv, keys_out, &m);
-      for (int i = 0; i < m; ++i) front[foff + i] = keys_out[i];
-      for (int i = 0; i < m && i < kCompactFront; ++i) compact[(int64_t)s * kCompactFront + i] = keys_out[i];
+      for (int i = 0; i < nsv; ++i) {
+        if (!flag[i]) continue;
+        const int64_t key = sorted[i].key;
+        front[foff + m] = key;
+        compact[(int64_t)s * kCompactFront + m] = key;
+        ++m;
+      }
       results[s].n_front = m;
     }
     return;

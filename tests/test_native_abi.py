@@ -21,7 +21,7 @@ def test_library_exports_header_symbols():
 def test_struct_layouts_match_header_sizes():
     # sizes fixed by the header's field lists (no implicit padding by construction)
     assert ctypes.sizeof(_native.LcSearchDesc) == 272
-    assert ctypes.sizeof(_native.LcSearchResult) == 96
+    assert ctypes.sizeof(_native.LcSearchResult) == 104
     assert ctypes.sizeof(_native.LcBatchTotals) == 88
     assert _native.SEARCH_DESC_DTYPE.itemsize == 272
 
