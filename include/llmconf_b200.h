@@ -68,6 +68,10 @@ enum {
   LC_COORD_EXPERT = 4   /* d0 = expert tokens (balanced or skewed)         */
 };
 
+/* lc_search_desc.modes bits */
+enum { LC_MODE_STATIC = 1, LC_MODE_AGGREGATED = 2, LC_MODE_DISAGGREGATED = 4,
+       LC_MODE_FORCE = 16 /* skip the memory-fit and budget filters (single-config estimates) */ };
+
 /* per-row status codes; the failing entry's label sits in bits 8..15 */
 enum {
   LC_ST_OK = 0, LC_ST_MISSING_KEY = 1, LC_ST_EXTRAPOLATION = 2, LC_ST_UNSUPPORTED = 3,
@@ -141,7 +145,7 @@ typedef struct {
   int64_t isl, osl, prefix;
   int32_t has_ttft, has_floor;
   double ttft_limit, speed_floor, tpot_cap;   /* tpot_cap = 1000/speed_floor (serving_modes.py:109-111) */
-  int32_t modes;                     /* bit0 static, bit1 aggregated, bit2 disaggregated */
+  int32_t modes;                     /* bit0 static, bit1 aggregated, bit2 disaggregated, LC_MODE_FORCE */
   int32_t n_budgets;
   int64_t budgets[LC_MAX_BUDGETS];
   int32_t b_off, n_b;                /* sorted batch sizes in the shared batch array */

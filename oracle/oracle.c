@@ -1052,3 +1052,18 @@ void or_free(or_result* r) {
   free(r->cand); free(r->work); free(r->rows); free(r->skip); free(r->front);
   memset(r, 0, sizeof(*r));
 }
+
+int or_estimate(const or_db* db, const or_model* m, const or_search* s, const or_cfg* cfg, int mode, double* out,
+                char* reason, int reason_len) {
+  gridset gs;
+  build_grids(db, &gs);
+  ctx_t X = {&gs, m, s, 0};
+  cfg_t c = {cfg->tp, cfg->pp, cfg->ep, cfg->dp, cfg->batch};
+  est_t e = {0, 0, 0, 0};
+  err_t err = {0, {0}};
+  const int st = mode == 0 ? estimate_static(&X, &c, &e, &err) : estimate_aggregated(&X, &c, &e, &err);
+  if (st) snprintf(reason, (size_t)reason_len, "%s", err.msg);
+  else { out[0] = e.ttft; out[1] = e.tpot; out[2] = e.speed; out[3] = e.thru; }
+  free_grids(&gs);
+  return st;
+}

@@ -109,6 +109,12 @@ typedef struct {
 } or_result;
 
 int or_run_search(const or_db* db, const or_model* m, const or_search* s, or_result* out);
+
+/* estimate_static / estimate_aggregated for one config (serving_modes.py:231-341):
+ * mode 0 static, 1 aggregated; returns 0 and fills out[4] = ttft, tpot, speed, thru,
+ * or a nonzero status with the reference's "Type: message" in reason. */
+int or_estimate(const or_db* db, const or_model* m, const or_search* s, const or_cfg* cfg, int mode, double* out,
+                char* reason, int reason_len);
 void or_free(or_result* r);
 
 /* pieces exposed for unit KATs */

@@ -132,6 +132,8 @@ def lib():
         _LIB.or_neumaier_sum.restype = C.c_double
         _LIB.or_busiest_shard.argtypes = [F64P, C.c_int, C.c_int64, C.c_int64, C.c_int64, I64P]
         _LIB.or_busiest_shard.restype = C.c_int64
+        _LIB.or_estimate.argtypes = [C.POINTER(OrDb), C.POINTER(OrModel), C.POINTER(OrSearch), C.POINTER(OrCfg),
+                                     C.c_int, F64P, C.c_char_p, C.c_int]
     return _LIB
 
 
@@ -208,7 +210,7 @@ class _Keep:
 
 
 def run_search(header: dict, records: list[dict], model: dict, workload: dict, space: dict | None = None,
-               disagg: dict | None = None, extrapolation: str = "default") -> dict:
+               disagg: dict | None = None, extrapolation: str = "default", _estimate=None) -> dict:
     """Evaluate one search on the CPU oracle; returns a report-like document."""
     space = dict(space or {})
     disagg = dict(disagg or {})
@@ -304,6 +306,12 @@ def run_search(header: dict, records: list[dict], model: dict, workload: dict, s
     s.max_x = disagg.get("max_prefill_replicas", 32)
     s.max_y = disagg.get("max_decode_replicas", 64)
 
+    if _estimate is not None:
+        cfg = OrCfg(*_estimate[0])
+        out = (C.c_double * 4)()
+        reason = C.create_string_buffer(512)
+        st = lib().or_estimate(C.byref(db), C.byref(mm), C.byref(s), C.byref(cfg), _estimate[1], out, reason, 512)
+        return {"status": st, "values": list(out), "reason": reason.value.decode()}
     res = OrResult()
     lib().or_run_search(C.byref(db), C.byref(mm), C.byref(s), C.byref(res))
     try:
@@ -375,3 +383,10 @@ def busiest_shard(weights, total: int, topk: int, ep: int) -> tuple[int, list[in
     out = (C.c_int64 * len(weights))()
     tail = lib().or_busiest_shard(w, len(weights), total, topk, ep, out)
     return tail, list(out)
+
+
+def estimate(header: dict, records: list[dict], model: dict, workload: dict, cfg: tuple, mode: str,
+             space: dict | None = None, extrapolation: str = "default") -> dict:
+    """estimate_static / estimate_aggregated of one (tp, pp, ep, dp, batch) config."""
+    return run_search(header, records, model, workload, space, None, extrapolation,
+                      _estimate=(cfg, 0 if mode == "static" else 1))

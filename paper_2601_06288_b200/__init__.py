@@ -6,7 +6,15 @@ hand-written sm_100a kernels behind the C ABI in include/llmconf_b200.h.
 """
 
 from .database import PerfDatabase, load_db
-from .engine import Engine, enumerate_candidates, get_engine, run_search, run_search_json
+from .engine import (
+    Engine,
+    enumerate_candidates,
+    estimate_aggregated,
+    estimate_static,
+    get_engine,
+    run_search,
+    run_search_json,
+)
 from .report import SearchReport, csv_from_doc, export_csv
 from .specs import (
     DEFAULT_DISAGG,
@@ -25,6 +33,6 @@ from .specs import (
 __all__ = [
     "CandidateSpace", "DEFAULT_DISAGG", "DisaggConstants", "Engine", "HardwareSpec", "ModelSpec", "MoESpec",
     "ParallelConfig", "PerfDatabase", "PowerLawParams", "SearchReport", "WorkloadSpec", "csv_from_doc",
-    "enumerate_candidates", "export_csv", "get_engine", "load_db", "load_hardware_spec", "load_model_spec",
+    "enumerate_candidates", "estimate_aggregated", "estimate_static", "export_csv", "get_engine", "load_db", "load_hardware_spec", "load_model_spec",
     "run_search", "run_search_json",
 ]

@@ -263,8 +263,11 @@ __global__ void k_enum_flags(EvalParams P, int64_t n_raw, uint8_t* flags) {
     const lc_combo c = P.combos[ci];
     const int64_t b = P.batches[S.b_off + bi];
     uint8_t f = 0;
-    if (fits_memory(c, S, P.gpu_memory, P.hidden, b)) {
-      const bool inb = in_budget(S, c.gpus);
+    // LC_MODE_FORCE: evaluate every consistent tuple (single-config estimates,
+    // serving_modes.estimate_static / estimate_aggregated apply no memory or budget filter)
+    const bool force = (S.modes & LC_MODE_FORCE) != 0;
+    if (force || fits_memory(c, S, P.gpu_memory, P.hidden, b)) {
+      const bool inb = force || in_budget(S, c.gpus);
       if (inb || (S.modes & 4)) {  // workers skip the budget (search.py:323)
         f = 1 | (inb ? 2 : 0);
         atomicOr(&P.cell_flags[P.meta[s].cell_off + (int64_t)c.tmpl * S.n_b + bi],
@@ -716,40 +719,44 @@ __global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalPara
           double t_gen = 0.0;
           const int nsteps = M.n_steps;
           int step = 0;
-          for (; step < nsteps && !e.code; step += 2) {
-            const bool two = step + 1 < nsteps;
-            double g0 = term[gi], g1 = 0.0;
-            if (step > 0) {
-              const QVal q = ds[step];
+#ifndef LC_DECODE_CHAINS
+#define LC_DECODE_CHAINS 2
+#endif
+          for (; step < nsteps && !e.code; step += LC_DECODE_CHAINS) {
+            double g[LC_DECODE_CHAINS];
+#pragma unroll
+            for (int j = 0; j < LC_DECODE_CHAINS; ++j) {
+              const int sj = step + j;
+              g[j] = 0.0;
+              if (sj >= nsteps || e.code) continue;
+              if (sj == 0) { g[j] = term[gi]; continue; }
+              const QVal q = ds[sj];
               if (q.status) {
-                e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + 32ll * step + 1;
-                break;
+                e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + 32ll * sj + 1;
+                continue;
               }
-              g0 = 0.0 + (q.lat * (double)ge->repeat / 1000.0) * bubble;
+              g[j] = 0.0 + (q.lat * (double)ge->repeat / 1000.0) * bubble;
             }
-            if (two) {
-              const QVal q = ds[step + 1];
-              if (q.status) {
-                e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + 32ll * (step + 1) + 1;
-                break;
-              }
-              g1 = 0.0 + (q.lat * (double)ge->repeat / 1000.0) * bubble;
+            if (e.code) break;
+            NeumaierSum sc[LC_DECODE_CHAINS];
+#pragma unroll
+            for (int j = 0; j < LC_DECODE_CHAINS; ++j) {
+              sc[j] = pre;
+              sc[j].add(g[j]);
             }
-            NeumaierSum s0 = pre, s1 = pre;
-            s0.add(g0);
-            s1.add(g1);
             for (int i = gi + 1; i < m; ++i) {
               const double x = term[i];
-              s0.add(x);
-              s1.add(x);
+#pragma unroll
+              for (int j = 0; j < LC_DECODE_CHAINS; ++j) sc[j].add(x);
             }
-            const int64_t k0 = 32ll * step;
-            const int64_t run0 = (S.osl - 1 - k0) < 32 ? (S.osl - 1 - k0) : 32;
-            t_gen += s0.result() * (double)run0;
-            if (two) {
-              const int64_t k1 = k0 + 32;
-              const int64_t run1 = (S.osl - 1 - k1) < 32 ? (S.osl - 1 - k1) : 32;
-              t_gen += s1.result() * (double)run1;
+#pragma unroll
+            for (int j = 0; j < LC_DECODE_CHAINS; ++j) {
+              const int sj = step + j;
+              if (sj < nsteps) {
+                const int64_t kk = 32ll * sj;
+                const int64_t run = (S.osl - 1 - kk) < 32 ? (S.osl - 1 - kk) : 32;
+                t_gen += sc[j].result() * (double)run;
+              }
             }
           }
           step = step < nsteps ? step : nsteps;

@@ -473,3 +473,85 @@ def run_search_json(db, model, workload, space=CandidateSpace(), jobs: int = 1,
         cols = columns_from_batch(out, 0, db, model, workload, space, 0.0)
     cols.total_ms = (time.perf_counter() - t0) * 1000.0
     return report_json(cols)
+
+
+MODE_FORCE = 16  # LC_MODE_FORCE: no memory-fit / budget filter
+
+
+def consistency_problems(model, cfg) -> list[str]:
+    """check_consistency messages (model.py:209-236)."""
+    out = []
+    if model.num_heads % cfg.tp:
+        out.append(f"tp={cfg.tp} does not divide num_heads={model.num_heads}")
+    if cfg.pp > model.num_layers:
+        out.append(f"pp={cfg.pp} exceeds num_layers={model.num_layers}")
+    moe = model.moe
+    if moe is None:
+        if cfg.ep != 1:
+            out.append("ep > 1 requires a mixture-of-experts model")
+        if cfg.tp <= model.intermediate_size and model.intermediate_size % cfg.tp:
+            out.append(f"tp={cfg.tp} does not divide intermediate_size={model.intermediate_size}")
+    else:
+        if moe.num_experts % cfg.ep:
+            out.append(f"ep={cfg.ep} does not divide num_experts={moe.num_experts}")
+        if cfg.ep > cfg.tp * cfg.dp:
+            out.append(f"ep={cfg.ep} exceeds tp*dp={cfg.tp * cfg.dp}")
+        hi, lo = max(cfg.ep, cfg.tp), min(cfg.ep, cfg.tp)
+        if hi % lo:
+            out.append(f"ep={cfg.ep} and tp={cfg.tp} must nest (one divides the other)")
+        elif cfg.tp > cfg.ep and moe.expert_intermediate % (cfg.tp // cfg.ep):
+            out.append(f"tp/ep={cfg.tp // cfg.ep} does not divide expert_intermediate={moe.expert_intermediate}")
+        if moe.shared_intermediate and cfg.tp <= moe.shared_intermediate and moe.shared_intermediate % cfg.tp:
+            out.append(f"tp={cfg.tp} does not divide shared_intermediate={moe.shared_intermediate}")
+    return out
+
+
+def _estimate(mode_bit: int, name: str, db, model, cfg, workload, device: int):
+    import dataclasses
+
+    from . import specs as S
+
+    problems = consistency_problems(model, cfg)
+    if problems:
+        raise S.ParallelConfigError("; ".join(problems))
+    space = CandidateSpace(tp_values=(cfg.tp,), pp_values=(cfg.pp,), ep_values=(cfg.ep,), dp_values=(cfg.dp,),
+                           batch_values=(cfg.batch,), ctx_capacity=cfg.ctx_capacity,
+                           chunked_prefill=cfg.chunked_prefill, kv_mem_fraction=cfg.kv_mem_fraction,
+                           cuda_graph=cfg.cuda_graph)
+    wl = dataclasses.replace(workload, batch_sweep=())
+    eng = get_engine(device)
+    with eng._lock:
+        out = eng.run_batch(db, model, space, [wl], mode_override=mode_bit | MODE_FORCE, enforce_budget=False)
+        U = out.fetch_units()
+        if int(out.results[0]["n_units"]) != 1:
+            raise SearchError("single-config estimate did not produce exactly one unit")
+        pre = "st" if mode_bit == MODE_STATIC else "ag"
+        st = int(U[f"{pre}_status"][0])
+        if st:
+            k = 0 if mode_bit == MODE_STATIC else 1
+            msg = _reason(st, int(U["err_c0"][k]), int(U["err_c1"][k]), out.plan, out.plan.combos[U["unit_combo"][0]],
+                          out.flat, db, workload, space, cfg.batch)
+            kind, text = msg.split(": ", 1)
+            raise getattr(S, kind)(text)
+        return PerfEstimate(name, model.name, cfg, float(U[f"{pre}_ttft"][0]), float(U[f"{pre}_tpot"][0]),
+                            float(U[f"{pre}_speed"][0]), float(U[f"{pre}_thru"][0]), cfg.gpus(), cfg.batch)
+
+
+def estimate_static(db, model, cfg, workload, stride: int = 32, device: int = 0) -> PerfEstimate:
+    """Drop-in for serving_modes.estimate_static (serving_modes.py:231-267) for one config.
+
+    Raises like the reference (ParallelConfigError, PerfDbError subclasses).  Only
+    the reference's default decode stride (32) is implemented on the device.
+    """
+    from .specs import WorkloadError
+
+    if stride < 1:
+        raise WorkloadError("stride must be >= 1")
+    if stride != 32:
+        raise NotImplementedError("the device evaluates the default decode stride (32) only")
+    return _estimate(MODE_STATIC, "static", db, model, cfg, workload, device)
+
+
+def estimate_aggregated(db, model, cfg, workload, device: int = 0) -> PerfEstimate:
+    """Drop-in for serving_modes.estimate_aggregated (serving_modes.py:279-341) for one config."""
+    return _estimate(MODE_AGG, "aggregated", db, model, cfg, workload, device)
