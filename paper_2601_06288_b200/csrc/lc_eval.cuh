@@ -232,87 +232,6 @@ __device__ __forceinline__ bool entry_coords(const lc_entry& e, const StepArgs& 
   }
 }
 
-struct StepStats {
-  int32_t q1, q2;   // 1-D / 2-D queries issued (reference-equivalent accounting)
-  int32_t logs;
-};
-
-// One forward pass: Σ_entries ((lat * repeat) / 1000.0) * bubble, summed like
-// CPython's sum() in plan order (estimator.py:83-95).  On failure the first
-// failing entry in plan order is recorded.
-__device__ __noinline__ int step_total(const DbView& D, const lc_entry* E, int n, const StepArgs& a,
-                                          double bubble, int64_t hidden, double* out, ErrRec* err,
-                                          StepStats* ss) {
-  NeumaierSum s;
-  for (int i = 0; i < n; ++i) {
-    const lc_entry& e = E[i];
-    int64_t d[5];
-    if (!entry_coords(e, a, hidden, d)) continue;
-    int st = 0;
-    const double lat = query(D, e, d, &st, &ss->logs);
-    if (e.coord == LC_COORD_CTX || e.coord == LC_COORD_GEN) ++ss->q2; else ++ss->q1;
-    if (st) { err->code = st; err->label = e.label; err->c0 = d[0]; err->c1 = d[1]; return st; }
-    const double ms = lat * (double)e.repeat / 1000.0;
-    s.add(0.0 + ms * bubble);
-  }
-  *out = s.result();
-  return 0;
-}
-
-// Static batching decode loop (serving_modes.py:256-266), stride 32.  Only the
-// generation-attention entry depends on the KV length, so the other entries
-// are priced once and the per-step sum re-run with the new attention term.
-__device__ __noinline__ int static_decode(const DbView& D, const lc_entry* E, int n, int64_t b, int64_t isl,
-                                             int64_t osl, int64_t expert_tokens, double bubble, int64_t hidden,
-                                             double* tpot, ErrRec* err, StepStats* ss, int32_t* n_steps) {
-  if (osl <= 1) { *tpot = 0.0; return 0; }
-  double term[LC_MAX_ENTRIES];
-  int gi = -1;
-  int m = 0;
-  StepArgs a{PH_DECODE, 0, b, isl + 1, expert_tokens};
-  const lc_entry* ge = nullptr;
-  for (int i = 0; i < n; ++i) {
-    const lc_entry& e = E[i];
-    int64_t d[5];
-    if (!entry_coords(e, a, hidden, d)) continue;
-    int st = 0;
-    const double lat = query(D, e, d, &st, &ss->logs);
-    if (st) { err->code = st; err->label = e.label; err->c0 = d[0]; err->c1 = d[1]; return st; }
-    if (e.coord == LC_COORD_GEN) { gi = m; ge = &e; }
-    const double ms = lat * (double)e.repeat / 1000.0;
-    term[m++] = 0.0 + ms * bubble;
-  }
-  const int per_step_q2 = 1;
-  const int per_step_q1 = m - per_step_q2;
-  double t_gen = 0.0;
-  int64_t k = 0;
-  int steps = 0;
-  while (k < osl - 1) {
-    if (k > 0) {
-      int64_t d[5] = {ge->d[0], ge->d[1], ge->d[2], ge->d[3], ge->d[4]};
-      d[0] = b;
-      d[1] = isl + k + 1;
-      int st = 0;
-      const double lat = query(D, *ge, d, &st, &ss->logs);
-      if (st) { err->code = st; err->label = ge->label; err->c0 = d[0]; err->c1 = d[1]; return st; }
-      const double ms = lat * (double)ge->repeat / 1000.0;
-      term[gi] = 0.0 + ms * bubble;
-    }
-    NeumaierSum s;
-    for (int i = 0; i < m; ++i) s.add(term[i]);
-    const double step = s.result();
-    const int64_t run = (osl - 1 - k) < 32 ? (osl - 1 - k) : 32;
-    t_gen += step * (double)run;
-    k += run;
-    ++steps;
-  }
-  ss->q1 += per_step_q1 * steps;
-  ss->q2 += per_step_q2 * steps;
-  *n_steps = steps;
-  *tpot = t_gen / (double)(osl - 1);
-  return 0;
-}
-
 // derive_metrics (serving_modes.py:161-172)
 __device__ __forceinline__ void derive_metrics(double ttft, double tpot, int64_t batch, int64_t osl, int64_t gpus,
                                                double* speed, double* thru) {
