@@ -379,6 +379,16 @@ def main() -> int:
             "unique_achieved": uniq_achieved, "unique_frac": uniq_achieved / peak,
             "kernel_ms": {"K0_enumerate": kernel_ms[0], "K3_moe_tails": kernel_ms[1], "K2_evaluate": kernel_ms[2],
                           "K5a_pools": kernel_ms[3], "K5b_disagg": kernel_ms[4], "K4_front": kernel_ms[5]}}
+    # FP64 context: measured DFMA peak (tools/cuda/fp64_peak.cu) and the ncu FP64-pipe activity of
+    # the K2 kernels (profiles/r1_ncu_v7.json) -- the stage is FP64/latency bound, not HBM bound
+    try:
+        roof["fp64_peak_gflops_measured"] = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())[
+            "fp64_fma_gflops"]
+        ncu = json.loads((ROOT / "profiles" / "r1_ncu_v7.json").read_text())["kernels"]
+        roof["ncu_fp64_pipe_active_pct"] = {k: ncu[k].get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+                                            for k in ("k_qtables", "k_dstables", "k_eval_cells", "k_expand") if k in ncu}
+    except Exception:
+        pass
     prof = ROOT / "profiles" / "ncu_k2_traffic.json"
     if prof.exists():
         try:
