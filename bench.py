@@ -385,8 +385,9 @@ def main() -> int:
         roof["fp64_peak_gflops_measured"] = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())[
             "fp64_fma_gflops"]
         ncu = json.loads((ROOT / "profiles" / "r1_ncu_v7.json").read_text())["kernels"]
-        roof["ncu_fp64_pipe_active_pct"] = {k: ncu[k].get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
-                                            for k in ("k_qtables", "k_dstables", "k_eval_cells", "k_expand") if k in ncu}
+        roof["ncu_fp64_pipe_active_pct"] = {
+            k: float(str(ncu[k].get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")).split()[0])
+            for k in ("k_qtables", "k_dstables", "k_eval_cells", "k_expand") if k in ncu}
     except Exception:
         pass
     prof = ROOT / "profiles" / "ncu_k2_traffic.json"

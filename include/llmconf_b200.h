@@ -237,6 +237,26 @@ int lc_replay_async(lc_ctx* ctx);
  * against it (e.g. CUDA events across several contexts). */
 int lc_stream(lc_ctx* ctx, void** stream);
 
+/* ------------------------------------------------ single-operator queries */
+/* One query_latency(db, query, policy) call (perfdb.py:539-580).  The host
+ * resolves the query's grid key (OperatorQuery.grid_key, perfdb.py:239-244) to a
+ * grid id of the uploaded database and writes the shape in canonical order. */
+typedef struct {
+  int32_t grid;                      /* grid id; < 0: no grid for the key (MissingKeyError) */
+  int32_t kind, quant;               /* LC_KIND_*, index into fp16/fp8/int8/int4 */
+  int32_t policy;                    /* LC_POLICY_*, or -1: the database's policy */
+  int64_t d[5];                      /* required dims in _KIND_DIMS order (perfdb.py:51-69) */
+  int64_t kv_len;                    /* attention_generation: shape kv_len, or -1 = seq_len */
+} lc_query;                          /* 64 bytes */
+
+/* Price n queries: latency_us[i] in microseconds and status[i] = LC_ST_OK,
+ * LC_ST_MISSING_KEY, LC_ST_EXTRAPOLATION or LC_ST_UNSUPPORTED.  Host arrays in
+ * and out; returns after the results are copied back.
+ * Replaces query_latency (perfdb.py:539-580) and, for in-grid coordinates,
+ * _interp_cells (perfdb.py:509-536); sol_estimate (perfdb.py:431-484) above the grid. */
+int lc_query_batch(lc_ctx* ctx, const lc_db* db, int32_t n, const lc_query* queries, double* latency_us,
+                   int32_t* status);
+
 #ifdef __cplusplus
 }
 #endif

@@ -175,6 +175,7 @@ static void free_grids(gridset* gs) {
 typedef struct {
   int kind, quant, attn;
   int64_t d[5]; /* canonical order */
+  int64_t kv_len; /* attention_generation shape kv_len; <= 0: seq_len (OperatorQuery.kv_len, perfdb.py:232-234) */
 } query;
 
 enum { ST_OK = 0, ST_MISSING = 1, ST_EXTRAP = 2, ST_UNSUPPORTED = 3 };
@@ -235,7 +236,7 @@ static int sol_estimate(const or_db* db, const query* q, double* out, err_t* err
     flops = 2.0 * (double)B * (double)H * (double)s * (double)s * (double)hd;
     bytes_moved = b * (double)B * (double)s * (double)(2 * H + 2 * KV) * (double)hd;
   } else if (kind == OK_KIND_ATTN_GEN) {
-    int64_t B = d[0], kv = d[1], H = d[2], KV = d[3], hd = d[4]; /* kv_len defaults to seq_len */
+    int64_t B = d[0], kv = q->kv_len > 0 ? q->kv_len : d[1], H = d[2], KV = d[3], hd = d[4];
     flops = 4.0 * (double)B * (double)H * (double)kv * (double)hd;
     bytes_moved = b * (double)B * (double)kv * 2.0 * (double)KV * (double)hd;
   } else if (kind == OK_KIND_MOE_GEMM) {
@@ -327,7 +328,7 @@ static double interp_cells(const grid* G, const int64_t* coords) {
 }
 
 /* query_latency, perfdb.py:539-580 */
-static int query_latency(const gridset* gs, const query* q, double* out, err_t* err) {
+static int query_latency_p(const gridset* gs, const query* q, int policy, double* out, err_t* err) {
   const or_db* db = gs->db;
   const kind_info* ki = &KINFO[q->kind];
   int64_t fixed[4] = {0, 0, 0, 0};
@@ -365,7 +366,7 @@ static int query_latency(const gridset* gs, const query* q, double* out, err_t* 
     *out = interp_cells(G, coords);
     return ST_OK;
   }
-  if (db->policy == 1) { /* strict */
+  if (policy == 1) { /* strict */
     err->st = ST_EXTRAP;
     int w = snprintf(err->msg, sizeof(err->msg), "ExtrapolationError: query coords {");
     for (int a = 0; a < G->n_axes; ++a)
@@ -385,8 +386,8 @@ static int query_latency(const gridset* gs, const query* q, double* out, err_t* 
     c = c > lo ? c : lo;
     clamped[a] = c < hi ? c : hi;
   }
-  int use_sol = db->policy == 3 || (db->policy == 0 && any_above);
-  if (db->policy == 2 || !use_sol) {
+  int use_sol = policy == 3 || (policy == 0 && any_above);
+  if (policy == 2 || !use_sol) {
     *out = interp_cells(G, clamped);
     return ST_OK;
   }
@@ -399,6 +400,31 @@ static int query_latency(const gridset* gs, const query* q, double* out, err_t* 
   if (sol_estimate(db, q, &sol_q, err)) return err->st;
   *out = sol_q * eff;
   return ST_OK;
+}
+
+static int query_latency(const gridset* gs, const query* q, double* out, err_t* err) {
+  return query_latency_p(gs, q, gs->db->policy, out, err);
+}
+
+int or_query_batch(const or_db* db, int32_t n, const int32_t* kind, const int32_t* quant, const int32_t* attn,
+                   const int64_t* dims, const int64_t* kv_len, int32_t policy, double* out, int32_t* status,
+                   char* msgs, int32_t msg_len) {
+  gridset gs;
+  build_grids(db, &gs);
+  for (int32_t i = 0; i < n; ++i) {
+    query q;
+    memset(&q, 0, sizeof(q));
+    q.kind = kind[i]; q.quant = quant[i]; q.attn = attn[i];
+    for (int k = 0; k < 5; ++k) q.d[k] = dims[(size_t)i * 5 + k];
+    q.kv_len = kv_len ? kv_len[i] : 0;
+    err_t err;
+    err.st = 0; err.msg[0] = 0;
+    out[i] = 0.0;
+    status[i] = query_latency_p(&gs, &q, policy >= 0 ? policy : db->policy, &out[i], &err);
+    if (msgs && msg_len > 0) snprintf(msgs + (size_t)i * msg_len, (size_t)msg_len, "%s", status[i] ? err.msg : "");
+  }
+  free_grids(&gs);
+  return 0;
 }
 
 /* ------------------------------------------------------------------------- */
@@ -528,7 +554,7 @@ static int decompose(const or_model* m, const cfg_t* c, int phase /*0 prefill 1 
 #define ADD(K, QN, LBL, REP, D0, D1, D2, D3, D4)                                              \
   do {                                                                                      \
     entry* e_ = &out[n++];                                                                  \
-    e_->q.kind = (K); e_->q.quant = (QN); e_->q.attn = m->attn;                             \
+    e_->q.kind = (K); e_->q.quant = (QN); e_->q.attn = m->attn; e_->q.kv_len = 0;          \
     e_->q.d[0] = (D0); e_->q.d[1] = (D1); e_->q.d[2] = (D2); e_->q.d[3] = (D3); e_->q.d[4] = (D4); \
     e_->repeat = (REP); e_->label = (LBL);                                                  \
   } while (0)

@@ -117,6 +117,13 @@ int or_estimate(const or_db* db, const or_model* m, const or_search* s, const or
                 char* reason, int reason_len);
 void or_free(or_result* r);
 
+/* query_latency (perfdb.py:539-580) for n queries: dims [n][5] in canonical order,
+ * kv_len NULL or [n] (<= 0: seq_len), policy -1 = the database's; status 0 ok,
+ * 1 missing key, 2 extrapolation, 3 unsupported; msgs NULL or [n][msg_len]. */
+int or_query_batch(const or_db* db, int32_t n, const int32_t* kind, const int32_t* quant, const int32_t* attn,
+                   const int64_t* dims, const int64_t* kv_len, int32_t policy, double* out, int32_t* status,
+                   char* msgs, int32_t msg_len);
+
 /* pieces exposed for unit KATs */
 double or_neumaier_sum(const double* xs, int n);
 int64_t or_busiest_shard(const double* weights, int e, int64_t total, int64_t topk, int64_t ep,

@@ -134,6 +134,8 @@ def lib():
         _LIB.or_busiest_shard.restype = C.c_int64
         _LIB.or_estimate.argtypes = [C.POINTER(OrDb), C.POINTER(OrModel), C.POINTER(OrSearch), C.POINTER(OrCfg),
                                      C.c_int, F64P, C.c_char_p, C.c_int]
+        _LIB.or_query_batch.argtypes = [C.POINTER(OrDb), C.c_int32, I32P, I32P, I32P, I64P, I64P, C.c_int32,
+                                        F64P, I32P, C.c_char_p, C.c_int32]
     return _LIB
 
 
@@ -209,12 +211,7 @@ class _Keep:
         return C.cast(a, C.POINTER(ctype))
 
 
-def run_search(header: dict, records: list[dict], model: dict, workload: dict, space: dict | None = None,
-               disagg: dict | None = None, extrapolation: str = "default", _estimate=None) -> dict:
-    """Evaluate one search on the CPU oracle; returns a report-like document."""
-    space = dict(space or {})
-    disagg = dict(disagg or {})
-    keep = _Keep()
+def _db(header: dict, records: list[dict], extrapolation: str, keep: "_Keep") -> OrDb:
     hw = header["hardware"]
     n = len(records)
     kinds, quants, attns, dims, lats = [], [], [], [], []
@@ -242,6 +239,46 @@ def run_search(header: dict, records: list[dict], model: dict, workload: dict, s
         db.compute[i] = float(hw["compute_throughput"].get(q, 0.0))
     db.policy = POLICIES.index(extrapolation)
     db.backend = header["backend"].encode()
+    return db
+
+
+def query_batch(header: dict, records: list[dict], queries: list[dict], policy: str | None = None,
+                extrapolation: str = "default") -> list[tuple[float | None, str]]:
+    """query_latency (perfdb.py:539-580) of each {kind, quant, shape} query:
+    (latency_us, "") or (None, "Type: message")."""
+    keep = _Keep()
+    db = _db(header, records, extrapolation, keep)
+    n = len(queries)
+    kinds, quants, attns, dims, kv = [], [], [], [], []
+    for q in queries:
+        kinds.append(KINDS.index(q["kind"]))
+        quants.append(QUANTS.index(q["quant"]))
+        attns.append(ATTN[q["shape"].get("attn_kind")])
+        d = [int(q["shape"][name]) for name in KIND_DIMS[q["kind"]]]
+        dims.extend(d + [0] * (5 - len(d)))
+        kv.append(int(q["shape"].get("kv_len", 0)))
+    out = (C.c_double * max(n, 1))()
+    st = (C.c_int32 * max(n, 1))()
+    msgs = C.create_string_buffer(512 * max(n, 1))
+    lib().or_query_batch(C.byref(db), n, keep.arr(kinds, C.c_int32), keep.arr(quants, C.c_int32),
+                         keep.arr(attns, C.c_int32), keep.arr(dims, C.c_int64), keep.arr(kv, C.c_int64),
+                         -1 if policy is None else POLICIES.index(policy), out, st, msgs, 512)
+    res = []
+    for i in range(n):
+        if st[i]:
+            res.append((None, msgs.raw[i * 512:(i + 1) * 512].split(b"\0", 1)[0].decode()))
+        else:
+            res.append((out[i], ""))
+    return res
+
+
+def run_search(header: dict, records: list[dict], model: dict, workload: dict, space: dict | None = None,
+               disagg: dict | None = None, extrapolation: str = "default", _estimate=None) -> dict:
+    """Evaluate one search on the CPU oracle; returns a report-like document."""
+    space = dict(space or {})
+    disagg = dict(disagg or {})
+    keep = _Keep()
+    db = _db(header, records, extrapolation, keep)
 
     moe = model.get("moe")
     mm = OrModel()

@@ -15,6 +15,7 @@ from .engine import (
     run_search,
     run_search_json,
 )
+from .queries import OperatorQuery, query_latency, query_latency_batch
 from .report import SearchReport, csv_from_doc, export_csv
 from .specs import (
     DEFAULT_DISAGG,
@@ -34,5 +35,5 @@ __all__ = [
     "CandidateSpace", "DEFAULT_DISAGG", "DisaggConstants", "Engine", "HardwareSpec", "ModelSpec", "MoESpec",
     "ParallelConfig", "PerfDatabase", "PowerLawParams", "SearchReport", "WorkloadSpec", "csv_from_doc",
     "enumerate_candidates", "estimate_aggregated", "estimate_static", "export_csv", "get_engine", "load_db", "load_hardware_spec", "load_model_spec",
-    "run_search", "run_search_json",
+    "OperatorQuery", "query_latency", "query_latency_batch", "run_search", "run_search_json",
 ]

@@ -100,9 +100,13 @@ SEARCH_DESC_DTYPE = np.dtype([("isl", "<i8"), ("osl", "<i8"), ("prefix", "<i8"),
                               ("max_x", "<i4"), ("max_y", "<i4"), ("load", "<i4"), ("_pad", "<i4")])
 assert SEARCH_DESC_DTYPE.itemsize == C.sizeof(LcSearchDesc), (SEARCH_DESC_DTYPE.itemsize, C.sizeof(LcSearchDesc))
 
+QUERY_DTYPE = np.dtype([("grid", "<i4"), ("kind", "<i4"), ("quant", "<i4"), ("policy", "<i4"), ("d", "<i8", (5,)),
+                        ("kv_len", "<i8")])
+assert QUERY_DTYPE.itemsize == 64
+
 EXPORTED = ("lc_abi_version", "lc_last_error", "lc_open", "lc_close", "lc_db_upload", "lc_db_free",
             "lc_space_upload", "lc_space_free", "lc_search_batch", "lc_fetch", "lc_replay_last", "lc_replay_async",
-            "lc_stream")
+            "lc_stream", "lc_query_batch")
 
 _LIB = None
 
@@ -130,6 +134,7 @@ def load_library(path: str | os.PathLike | None = None):
     lib.lc_replay_last.argtypes = [C.c_void_p, C.c_int32, C.POINTER(LcBatchTotals)]
     lib.lc_replay_async.argtypes = [C.c_void_p]
     lib.lc_stream.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.lc_query_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, F64P, I32P]
     if path is None:
         _LIB = lib
     return lib

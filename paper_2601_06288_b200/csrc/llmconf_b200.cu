@@ -173,6 +173,7 @@ struct lc_ctx {
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
   DBuf pool_key, qt_groups, ds_groups, front_compact, pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
+  DBuf q_in, q_lat, q_st;  // lc_query_batch
   // last batch
   const lc_db* db = nullptr;
   const lc_space* sp = nullptr;
@@ -441,6 +442,58 @@ __global__ void k_mark_mixed(EvalParams P, int64_t n_items) {
     if (a.st) continue;
     const int64_t tok = a.chunk_tokens + a.n_mix_gen;
     if (tok <= P.m_tmax) P.m_used[(int64_t)S.load * (P.m_tmax + 1) + tok] = 1;
+  }
+}
+
+// ---- single-operator queries (lc_query_batch): query_latency (perfdb.py:539-580)
+// for arbitrary shapes, one thread per query.  The database is read from global
+// memory (a few tens of KB, L1/L2 resident after the first touch).
+__global__ void k_query(DbView D, int32_t n, const lc_query* __restrict__ qs, double* __restrict__ out,
+                        int32_t* __restrict__ status) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const lc_query q = qs[i];
+    const int policy = q.policy >= 0 ? q.policy : D.policy;
+    int st = LC_ST_OK, n_logs = 0;
+    double r = 0.0;
+    if (q.grid < 0) {
+      st = LC_ST_MISSING_KEY;
+    } else {
+      const DevGrid G = D.grids[q.grid];
+      bool any_oob = false, any_above = false;
+      int64_t cl[2] = {q.d[0], q.d[1]};
+      for (int a = 0; a < G.ndim; ++a) {  // _axis_position out-of-bounds flags (perfdb.py:490-506)
+        const int64_t* v = D.axv + G.ax_off[a];
+        const int64_t lo = v[0], hi = v[G.ax_len[a] - 1];
+        if (q.d[a] < lo) { any_oob = true; cl[a] = lo; }
+        if (q.d[a] > hi) { any_oob = any_above = true; cl[a] = hi; }
+      }
+      if (!any_oob) {
+        r = interp_cells(D, G, q.d[0], q.d[1], &n_logs);
+      } else if (policy == LC_POLICY_STRICT) {
+        st = LC_ST_EXTRAPOLATION;
+      } else {
+        const bool use_sol = policy == LC_POLICY_SOL || (policy == LC_POLICY_DEFAULT && any_above);
+        const double edge = interp_cells(D, G, cl[0], cl[1], &n_logs);
+        if (policy == LC_POLICY_CLAMP || !use_sol) {
+          r = edge;
+        } else {
+          // edge query = query.with_coords(clamped); generation attention streams
+          // kv_len (default seq_len) keys, which with_coords leaves as given
+          int64_t de[5], dq[5];
+          for (int k = 0; k < 5; ++k) de[k] = dq[k] = q.d[k];
+          for (int a = 0; a < G.ndim; ++a) de[a] = cl[a];
+          if (q.kind == LC_KIND_ATTN_GEN && q.kv_len > 0) de[1] = dq[1] = q.kv_len;
+          const double sol_edge = sol_us(D, q.kind, q.quant, de, &st);
+          if (!st) {
+            const double eff = edge / sol_edge;
+            const double sol_q = sol_us(D, q.kind, q.quant, dq, &st);
+            if (!st) r = sol_q * eff;
+          }
+        }
+      }
+    }
+    out[i] = st ? 0.0 : r;
+    status[i] = st;
   }
 }
 
@@ -1754,7 +1807,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->pinned_front) cudaFreeHost(c->pinned_front);
@@ -2398,6 +2451,40 @@ int lc_replay_async(lc_ctx* c) {
   int rc = run_enum(c);
   if (rc) return rc;
   return run_eval_pipeline(c, nullptr);
+}
+
+int lc_query_batch(lc_ctx* c, const lc_db* db, int32_t n, const lc_query* queries, double* latency_us,
+                   int32_t* status) {
+  if (!c || !db || n < 0 || (n > 0 && (!queries || !latency_us || !status)))
+    return fail(LC_ERR_ARG, "lc_query_batch: bad argument");
+  if (n == 0) return LC_OK;
+  CK(cudaSetDevice(c->device));
+  for (int32_t i = 0; i < n; ++i) {
+    const lc_query& q = queries[i];
+    if (q.grid >= db->n_grids || q.kind < 0 || q.kind > LC_KIND_EMBEDDING || q.quant < 0 || q.quant > 3 ||
+        q.policy < -1 || q.policy > LC_POLICY_SOL)
+      return fail(LC_ERR_ARG, "lc_query_batch: query " + std::to_string(i) + " out of range");
+  }
+  cudaError_t e = cudaSuccess;
+  lc_query* dq = c->q_in.get<lc_query>(n, &e);
+  double* dlat = c->q_lat.get<double>(n, &e);
+  int32_t* dst = c->q_st.get<int32_t>(n, &e);
+  if (e != cudaSuccess) return fail(LC_ERR_CUDA, std::string("lc_query_batch: ") + cudaGetErrorString(e));
+  CK(cudaMemcpyAsync(dq, queries, sizeof(lc_query) * (size_t)n, cudaMemcpyHostToDevice, c->stream));
+  DbView V;
+  V.grids = db->grids; V.axv = db->axv; V.axl = db->axl; V.cell = db->cell; V.clog = db->clog;
+  V.logtab = db->logtab; V.exptab = db->exptab;
+  V.mem_bw = db->mem_bw; V.intra_bw = db->intra_bw; V.inter_bw = db->inter_bw; V.gpu_memory = db->gpu_memory;
+  for (int i = 0; i < 4; ++i) V.compute[i] = db->compute[i];
+  V.gpn = db->gpn; V.policy = db->policy;
+  const int threads = 128;
+  const int blocks = (int)std::min<int64_t>(((int64_t)n + threads - 1) / threads, 148 * 16);
+  k_query<<<blocks, threads, 0, c->stream>>>(V, n, dq, dlat, dst);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(latency_us, dlat, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(status, dst, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return LC_OK;
 }
 
 int lc_stream(lc_ctx* c, void** stream) {

@@ -110,3 +110,16 @@ def max_rel_err(a: dict, b: dict) -> float:
             if x != y:
                 worst = max(worst, abs(x - y) / max(abs(x), abs(y)))
     return worst
+
+
+def query_goldens() -> dict:
+    """Single-query vectors from the reference (tests/golden/make_query_golden.py)."""
+    return json.loads(gzip.decompress((GOLDEN / "queries.json.gz").read_bytes()))
+
+
+def query_groups(doc: dict) -> dict:
+    """Vectors grouped by (database, policy), in file order."""
+    groups: dict = {}
+    for v in doc["vectors"]:
+        groups.setdefault((v["db"], v["policy"]), []).append(v)
+    return groups
