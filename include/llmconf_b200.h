@@ -257,6 +257,38 @@ typedef struct {
 int lc_query_batch(lc_ctx* ctx, const lc_db* db, int32_t n, const lc_query* queries, double* latency_us,
                    int32_t* status);
 
+/* ------------------------------------------------ synthetic database generation */
+/* One grid of generate_synthetic_db (perfdb.py:641-666): GridAxes (perfdb.py:586-614)
+ * with its per-key hash constants already evaluated by the host. */
+typedef struct {
+  int32_t kind, quant;               /* LC_KIND_*, quant index */
+  int32_t n_axes, _pad;              /* 1 or 2 interpolated axes */
+  int32_t axis_dim[2];               /* canonical dim index each axis fills */
+  int32_t axis_off[2], axis_len[2];  /* into axis_val / axis_term */
+  int64_t cell_off;                  /* first cell; grids are contiguous and in order */
+  int64_t d[5];                      /* fixed dims in canonical order (axis slots ignored) */
+  double offset;                     /* (_hash_unit(seed, key, "offset") - 0.5) * 0.3 */
+} lc_gen_grid;                       /* 96 bytes */
+
+typedef struct {
+  int32_t n_grids;
+  const lc_gen_grid* grids;
+  int32_t n_axis;
+  const int64_t* axis_val;           /* axis values */
+  const double* axis_term;           /* math.sin(omega * math.log2(value) + phase) per value (perfdb.py:637) */
+  int64_t n_cells;
+  double amplitude;                  /* efficiency_amplitude */
+  double mem_bandwidth, intra_node_bandwidth, inter_node_bandwidth;
+  int32_t gpus_per_node;
+  double compute[4];                 /* FLOP/s for fp16, fp8, int8, int4; <= 0 = absent */
+} lc_dbgen_desc;
+
+/* Fill latency_us[n_cells] (roofline x efficiency, row-major per grid, axis 0
+ * major) and latency_log[n_cells] (natural log; NaN where glibc's near-1 path
+ * applies, for the host to recompute).  status[n_grids] = LC_ST_UNSUPPORTED for
+ * a grid whose quant has no compute rate (UnsupportedOperatorError). */
+int lc_dbgen(lc_ctx* ctx, const lc_dbgen_desc* desc, double* latency_us, double* latency_log, int32_t* status);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,8 @@ from .engine import (
     run_search,
     run_search_json,
 )
+from .dbgen import GridAxes, generate_synthetic_db, grid_spec_for_model, save_db
+from .soa import load_soa, save_soa
 from .queries import OperatorQuery, query_latency, query_latency_batch
 from .report import SearchReport, csv_from_doc, export_csv
 from .specs import (
@@ -35,5 +37,6 @@ __all__ = [
     "CandidateSpace", "DEFAULT_DISAGG", "DisaggConstants", "Engine", "HardwareSpec", "ModelSpec", "MoESpec",
     "ParallelConfig", "PerfDatabase", "PowerLawParams", "SearchReport", "WorkloadSpec", "csv_from_doc",
     "enumerate_candidates", "estimate_aggregated", "estimate_static", "export_csv", "get_engine", "load_db", "load_hardware_spec", "load_model_spec",
+    "GridAxes", "generate_synthetic_db", "load_soa", "save_soa", "grid_spec_for_model", "save_db",
     "OperatorQuery", "query_latency", "query_latency_batch", "run_search", "run_search_json",
 ]

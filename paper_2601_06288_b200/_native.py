@@ -100,13 +100,26 @@ SEARCH_DESC_DTYPE = np.dtype([("isl", "<i8"), ("osl", "<i8"), ("prefix", "<i8"),
                               ("max_x", "<i4"), ("max_y", "<i4"), ("load", "<i4"), ("_pad", "<i4")])
 assert SEARCH_DESC_DTYPE.itemsize == C.sizeof(LcSearchDesc), (SEARCH_DESC_DTYPE.itemsize, C.sizeof(LcSearchDesc))
 
+GEN_GRID_DTYPE = np.dtype([("kind", "<i4"), ("quant", "<i4"), ("n_axes", "<i4"), ("_pad", "<i4"),
+                           ("axis_dim", "<i4", (2,)), ("axis_off", "<i4", (2,)), ("axis_len", "<i4", (2,)),
+                           ("cell_off", "<i8"), ("d", "<i8", (5,)), ("offset", "<f8")])
+assert GEN_GRID_DTYPE.itemsize == 96
+
+
+class LcDbgenDesc(C.Structure):
+    _fields_ = [("n_grids", C.c_int32), ("grids", C.c_void_p), ("n_axis", C.c_int32), ("axis_val", I64P),
+                ("axis_term", F64P), ("n_cells", C.c_int64), ("amplitude", C.c_double),
+                ("mem_bandwidth", C.c_double), ("intra_node_bandwidth", C.c_double),
+                ("inter_node_bandwidth", C.c_double), ("gpus_per_node", C.c_int32), ("compute", C.c_double * 4)]
+
+
 QUERY_DTYPE = np.dtype([("grid", "<i4"), ("kind", "<i4"), ("quant", "<i4"), ("policy", "<i4"), ("d", "<i8", (5,)),
                         ("kv_len", "<i8")])
 assert QUERY_DTYPE.itemsize == 64
 
 EXPORTED = ("lc_abi_version", "lc_last_error", "lc_open", "lc_close", "lc_db_upload", "lc_db_free",
             "lc_space_upload", "lc_space_free", "lc_search_batch", "lc_fetch", "lc_replay_last", "lc_replay_async",
-            "lc_stream", "lc_query_batch")
+            "lc_stream", "lc_query_batch", "lc_dbgen")
 
 _LIB = None
 
@@ -134,6 +147,7 @@ def load_library(path: str | os.PathLike | None = None):
     lib.lc_replay_last.argtypes = [C.c_void_p, C.c_int32, C.POINTER(LcBatchTotals)]
     lib.lc_replay_async.argtypes = [C.c_void_p]
     lib.lc_stream.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.lc_dbgen.argtypes = [C.c_void_p, C.POINTER(LcDbgenDesc), F64P, F64P, I32P]
     lib.lc_query_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, F64P, I32P]
     if path is None:
         _LIB = lib

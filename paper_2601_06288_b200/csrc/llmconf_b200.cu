@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <map>
@@ -41,6 +42,9 @@ int fail(int code, const std::string& msg) {
     if (e_ != cudaSuccess)                                                             \
       return fail(LC_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));    \
   } while (0)
+
+// largest database image staged into shared memory; larger ones are read from global memory
+constexpr size_t kDbStageMax = 200 * 1024;
 
 struct DBuf {
   void* p = nullptr;
@@ -83,6 +87,7 @@ struct lc_db {
   double mem_bw, intra_bw, inter_bw, gpu_memory, compute[4];
   int32_t gpn, policy;
   size_t smem_bytes;  // staged size
+  int32_t staged;     // 1: fits the shared-memory staging budget; 0: kernels read it from global memory
 };
 
 struct lc_space {
@@ -204,6 +209,7 @@ struct EvalParams {
   int32_t n_grids, n_axis, n_cells;
   double mem_bw, intra_bw, inter_bw, gpu_memory, compute[4];
   int32_t gpn, policy;
+  int32_t db_global;                 // database too large to stage: read it from global memory (L1/L2)
   // space
   const lc_combo* combos; const int32_t* tmpl_n; const lc_entry* entries;
   int64_t hidden, topk, n_experts; int32_t is_moe, n_tp, n_ep;
@@ -497,8 +503,56 @@ __global__ void k_query(DbView D, int32_t n, const lc_query* __restrict__ qs, do
   }
 }
 
+// ---- synthetic database generation (lc_dbgen): generate_synthetic_db
+// (perfdb.py:641-666).  One thread per grid cell: roofline latency of the cell's
+// query (sol_estimate, perfdb.py:431-484) times the smooth efficiency factor
+// (perfdb.py:625-638), whose per-axis sine terms the host evaluates once per
+// axis value with CPython's math (they depend on one coordinate each).  The
+// cell's natural log is taken here too (glibc __log_fma restated); the few
+// latencies on glibc's near-1 path come back NaN and the host recomputes them.
+__global__ void k_dbgen(DbView D, const lc_gen_grid* __restrict__ grids, int32_t n_grids,
+                        const int64_t* __restrict__ axv, const double* __restrict__ term, int64_t n_cells,
+                        double amplitude, double* __restrict__ lat, double* __restrict__ lat_log,
+                        int32_t* __restrict__ status) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n_cells; x += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = n_grids - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (grids[mid].cell_off <= x) lo = mid;
+      else hi = mid - 1;
+    }
+    const lc_gen_grid& G = grids[lo];
+    const int64_t rel = x - G.cell_off;
+    int idx[2] = {0, 0};
+    if (G.n_axes == 2) { idx[0] = (int)(rel / G.axis_len[1]); idx[1] = (int)(rel % G.axis_len[1]); }
+    else idx[0] = (int)rel;
+    int64_t d[5] = {G.d[0], G.d[1], G.d[2], G.d[3], G.d[4]};
+    double total = 0.0;
+    for (int a = 0; a < G.n_axes; ++a) {
+      d[G.axis_dim[a]] = axv[G.axis_off[a] + idx[a]];
+      total += term[G.axis_off[a] + idx[a]];
+    }
+    int st = 0;
+    const double base = sol_us(D, G.kind, G.quant, d, &st);
+    double eff = 2.0;
+    if (amplitude != 0.0) eff = 2.0 + G.offset + amplitude * total / (double)G.n_axes;
+    const double v = base * eff;
+    lat[x] = v;
+    lat_log[x] = st ? 0.0 : glibc::log_fma(v, D.logtab);
+    if (st) status[lo] = st;  // benign race: every failing cell of a grid writes the same code
+  }
+}
+
 // ---- K2: evaluate every unit
 __device__ __forceinline__ void stage_db(const EvalParams& P, unsigned char* smem, DbView* V) {
+  V->mem_bw = P.mem_bw; V->intra_bw = P.intra_bw; V->inter_bw = P.inter_bw; V->gpu_memory = P.gpu_memory;
+  for (int i = 0; i < 4; ++i) V->compute[i] = P.compute[i];
+  V->gpn = P.gpn; V->policy = P.policy;
+  if (P.db_global) {
+    V->grids = P.grids; V->axv = P.axv; V->axl = P.axl; V->cell = P.cell; V->clog = P.clog;
+    V->logtab = P.logtab; V->exptab = P.exptab;
+    return;
+  }
   unsigned char* p = smem;
   uint64_t* exptab = (uint64_t*)p; p += 256 * 8;
   double* logtab = (double*)p; p += 256 * 8;
@@ -514,9 +568,6 @@ __device__ __forceinline__ void stage_db(const EvalParams& P, unsigned char* sme
   __syncthreads();
   V->grids = grids; V->axv = axv; V->axl = axl; V->cell = cell; V->clog = clog;
   V->logtab = logtab; V->exptab = exptab;
-  V->mem_bw = P.mem_bw; V->intra_bw = P.intra_bw; V->inter_bw = P.inter_bw; V->gpu_memory = P.gpu_memory;
-  for (int i = 0; i < 4; ++i) V->compute[i] = P.compute[i];
-  V->gpn = P.gpn; V->policy = P.policy;
 }
 
 // tail lookup: prefill/decode tables by batch index, the mixed region by token count
@@ -1785,7 +1836,7 @@ int lc_open(int device, lc_ctx** out) {
     static bool done[64] = {false};
     std::lock_guard<std::mutex> lock(mu);
     if (device < 64 && !done[device]) {
-      const int big = 200 * 1024;
+      const int big = (int)kDbStageMax;
       CK(cudaFuncSetAttribute(k_qtables, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
       CK(cudaFuncSetAttribute(k_dstables, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
       CK(cudaFuncSetAttribute(k_front_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1842,7 +1893,7 @@ int lc_db_upload(lc_ctx* c, const lc_db_desc* d, lc_db** out) {
   for (int i = 0; i < 4; ++i) db->compute[i] = d->compute[i];
   db->gpn = d->gpus_per_node; db->policy = d->policy;
   db->smem_bytes = 256 * 16 + (size_t)d->n_axis * 16 + (size_t)d->n_cells * 16 + (size_t)d->n_grids * sizeof(DevGrid);
-  if (db->smem_bytes > 200 * 1024) { delete db; return fail(LC_ERR_ARG, "database too large for shared-memory staging"); }
+  db->staged = db->smem_bytes <= (size_t)kDbStageMax && !getenv("LC_DB_GLOBAL");
   CK(cudaStreamSynchronize(c->stream));
   *out = db;
   return LC_OK;
@@ -1959,6 +2010,7 @@ static EvalParams make_params(lc_ctx* c) {
   P.mem_bw = db->mem_bw; P.intra_bw = db->intra_bw; P.inter_bw = db->inter_bw; P.gpu_memory = db->gpu_memory;
   for (int i = 0; i < 4; ++i) P.compute[i] = db->compute[i];
   P.gpn = db->gpn; P.policy = db->policy;
+  P.db_global = db->staged ? 0 : 1;
   P.combos = sp->combos; P.tmpl_n = sp->tmpl_n; P.entries = sp->entries;
   P.hidden = sp->hidden; P.topk = sp->topk; P.n_experts = sp->n_experts; P.is_moe = sp->is_moe;
   P.n_tp = sp->n_tp; P.n_ep = sp->n_ep; P.tp_vals = sp->tp_vals; P.ep_vals = sp->ep_vals; P.pair_used = sp->pair_used;
@@ -2063,7 +2115,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     EvalParams P2 = make_params(c);  // table pointers are valid only after the allocations above
     P = P2;
   }
-  const size_t smem = c->db->smem_bytes;
+  const size_t smem = c->db->staged ? c->db->smem_bytes : 0;
   auto launch_tables = [&](auto kern, int64_t n_items) -> int {
     if (n_items <= 0) return LC_OK;
     int per_sm = 0;
@@ -2484,6 +2536,61 @@ int lc_query_batch(lc_ctx* c, const lc_db* db, int32_t n, const lc_query* querie
   CK(cudaMemcpyAsync(latency_us, dlat, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(status, dst, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  return LC_OK;
+}
+
+int lc_dbgen(lc_ctx* c, const lc_dbgen_desc* g, double* latency_us, double* latency_log, int32_t* status) {
+  if (!c || !g || !latency_us || !latency_log || !status || g->n_grids < 0 || g->n_cells < 0)
+    return fail(LC_ERR_ARG, "lc_dbgen: bad argument");
+  for (int32_t i = 0; i < g->n_grids; ++i) status[i] = 0;
+  if (g->n_cells == 0 || g->n_grids == 0) return LC_OK;
+  int64_t expect = 0;
+  for (int32_t i = 0; i < g->n_grids; ++i) {
+    const lc_gen_grid& G = g->grids[i];
+    if (G.n_axes < 1 || G.n_axes > 2 || G.kind < 0 || G.kind > LC_KIND_EMBEDDING || G.quant < 0 || G.quant > 3 ||
+        G.cell_off != expect)
+      return fail(LC_ERR_ARG, "lc_dbgen: grid " + std::to_string(i) + " malformed");
+    int64_t cells = 1;
+    for (int a = 0; a < G.n_axes; ++a) {
+      if (G.axis_len[a] < 1 || G.axis_off[a] < 0 || G.axis_off[a] + G.axis_len[a] > g->n_axis ||
+          G.axis_dim[a] < 0 || G.axis_dim[a] > 4)
+        return fail(LC_ERR_ARG, "lc_dbgen: grid " + std::to_string(i) + " axis out of range");
+      cells *= G.axis_len[a];
+    }
+    expect += cells;
+  }
+  if (expect != g->n_cells) return fail(LC_ERR_ARG, "lc_dbgen: n_cells does not match the grids");
+  CK(cudaSetDevice(c->device));
+  lc_gen_grid* dg = nullptr; int64_t* dax = nullptr; double* dterm = nullptr; double* dlogtab = nullptr;
+  double* dlat = nullptr; double* dlog = nullptr; int32_t* dst = nullptr;
+  int rc = 0;
+  if ((rc = upload(&dg, g->grids, (size_t)g->n_grids, c->stream)) || (rc = upload(&dax, g->axis_val, (size_t)g->n_axis, c->stream)) ||
+      (rc = upload(&dterm, g->axis_term, (size_t)g->n_axis, c->stream)) ||
+      (rc = upload(&dlogtab, LOG_TAB_H, 256, c->stream))) {
+    cudaFree(dg); cudaFree(dax); cudaFree(dterm); cudaFree(dlogtab);
+    return rc;
+  }
+  cudaError_t e = cudaMalloc(&dlat, sizeof(double) * (size_t)g->n_cells);
+  if (e == cudaSuccess) e = cudaMalloc(&dlog, sizeof(double) * (size_t)g->n_cells);
+  if (e == cudaSuccess) e = cudaMalloc(&dst, sizeof(int32_t) * (size_t)g->n_grids);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dst, 0, sizeof(int32_t) * (size_t)g->n_grids, c->stream);
+  if (e == cudaSuccess) {
+    DbView V;
+    memset(&V, 0, sizeof(V));
+    V.logtab = dlogtab;
+    V.mem_bw = g->mem_bandwidth; V.intra_bw = g->intra_node_bandwidth; V.inter_bw = g->inter_node_bandwidth;
+    for (int i = 0; i < 4; ++i) V.compute[i] = g->compute[i];
+    V.gpn = g->gpus_per_node;
+    const int64_t blocks = std::min<int64_t>((g->n_cells + 255) / 256, 148 * 16);
+    k_dbgen<<<(int)blocks, 256, 0, c->stream>>>(V, dg, g->n_grids, dax, dterm, g->n_cells, g->amplitude, dlat, dlog, dst);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(latency_us, dlat, sizeof(double) * (size_t)g->n_cells, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(latency_log, dlog, sizeof(double) * (size_t)g->n_cells, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(status, dst, sizeof(int32_t) * (size_t)g->n_grids, cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(dg); cudaFree(dax); cudaFree(dterm); cudaFree(dlogtab); cudaFree(dlat); cudaFree(dlog); cudaFree(dst);
+  if (e != cudaSuccess) return fail(LC_ERR_CUDA, std::string("lc_dbgen: ") + cudaGetErrorString(e));
   return LC_OK;
 }
 

@@ -183,8 +183,16 @@ class PerfDatabase:
         return {k[0] for k in self._grids}
 
 
-def load_db(path: str | Path, extrapolation: str = "default") -> PerfDatabase:
-    """Load a JSON-lines database (optionally gzip-compressed)."""
+def load_db(path: str | Path, extrapolation: str = "default", soa_cache: bool | str | Path = False) -> PerfDatabase:
+    """Load a JSON-lines database (optionally gzip-compressed).
+
+    ``soa_cache``: True (``<path>.soa.npz``) or a cache path -- reuse the binary
+    structure-of-arrays image while the source file is unchanged (soa.py).
+    """
+    if soa_cache:
+        from .soa import load_db_cached
+
+        return load_db_cached(path, extrapolation, None if soa_cache is True else soa_cache)
     path = Path(path)
     raw = path.read_bytes()
     if path.suffix == ".gz":

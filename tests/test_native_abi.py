@@ -42,3 +42,52 @@ def test_open_without_device_fails_loudly():
     else:
         assert rc != 0
         assert lib.lc_last_error()
+
+
+def test_ctypes_and_numpy_layouts_match_the_c_compiler(tmp_path):
+    """Compile a probe against include/llmconf_b200.h with gcc and compare every
+    struct size and key field offset with the ctypes / numpy mirrors."""
+    import json
+    import subprocess
+
+    import numpy as np
+
+    from paper_2601_06288_b200.plans import COMBO_DTYPE, ENTRY_DTYPE, SLOT_DTYPE
+
+    exe = tmp_path / "abi_layout"
+    src = Path(__file__).resolve().parent / "native" / "abi_layout.c"
+    subprocess.run(["gcc", "-O0", "-o", str(exe), str(src)], check=True)
+    c = json.loads(subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout)
+
+    def off(dt: np.dtype, name: str) -> int:
+        return dt.fields[name][1]
+
+    N = _native
+    sizes = {"lc_db_desc": ctypes.sizeof(N.LcDbDesc), "lc_space_desc": ctypes.sizeof(N.LcSpaceDesc),
+             "lc_search_desc": N.SEARCH_DESC_DTYPE.itemsize, "lc_search_result": ctypes.sizeof(N.LcSearchResult),
+             "lc_batch_totals": ctypes.sizeof(N.LcBatchTotals), "lc_fetch_req": ctypes.sizeof(N.LcFetchReq),
+             "lc_entry": ENTRY_DTYPE.itemsize, "lc_combo": COMBO_DTYPE.itemsize, "lc_slot": SLOT_DTYPE.itemsize,
+             "lc_query": N.QUERY_DTYPE.itemsize, "lc_gen_grid": N.GEN_GRID_DTYPE.itemsize,
+             "lc_dbgen_desc": ctypes.sizeof(N.LcDbgenDesc)}
+    for k, v in sizes.items():
+        assert c[k] == v, (k, c[k], v)
+    fields = {
+        "lc_entry.repeat": off(ENTRY_DTYPE, "repeat"), "lc_entry.d": off(ENTRY_DTYPE, "d"),
+        "lc_combo.weight_bytes": off(COMBO_DTYPE, "weight_bytes"), "lc_slot.step": off(SLOT_DTYPE, "step"),
+        "lc_slot.pair": off(SLOT_DTYPE, "pair"), "lc_search_desc.budgets": off(N.SEARCH_DESC_DTYPE, "budgets"),
+        "lc_search_desc.ctx_capacity": off(N.SEARCH_DESC_DTYPE, "ctx_capacity"),
+        "lc_search_desc.load": off(N.SEARCH_DESC_DTYPE, "load"),
+        "lc_search_result.best": N.LcSearchResult.best.offset,
+        "lc_search_result.n_survivors": N.LcSearchResult.n_survivors.offset,
+        "lc_batch_totals.kernel_ms": N.LcBatchTotals.kernel_ms.offset,
+        "lc_batch_totals.n_cells": N.LcBatchTotals.n_cells.offset,
+        "lc_query.d": off(N.QUERY_DTYPE, "d"), "lc_query.kv_len": off(N.QUERY_DTYPE, "kv_len"),
+        "lc_gen_grid.cell_off": off(N.GEN_GRID_DTYPE, "cell_off"), "lc_gen_grid.d": off(N.GEN_GRID_DTYPE, "d"),
+        "lc_gen_grid.offset": off(N.GEN_GRID_DTYPE, "offset"),
+        "lc_dbgen_desc.amplitude": N.LcDbgenDesc.amplitude.offset,
+        "lc_dbgen_desc.compute": N.LcDbgenDesc.compute.offset,
+        "lc_db_desc.compute": N.LcDbDesc.compute.offset, "lc_db_desc.policy": N.LcDbDesc.policy.offset,
+        "lc_space_desc.gclass_of": N.LcSpaceDesc.gclass_of.offset,
+    }
+    for k, v in fields.items():
+        assert c[k] == v, (k, c[k], v)
