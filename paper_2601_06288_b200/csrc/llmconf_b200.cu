@@ -15,6 +15,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <string>
@@ -129,6 +130,27 @@ struct DsGroup {
   int32_t b_off, n_b, n_steps, _pad;
 };
 
+// Static decode loops shared across output lengths.  The KV samples isl + 32k + 1
+// and the decode step terms depend on (isl, batch list, MoE load), not on osl, and
+// the loop accumulates t_gen in sample order, so a search with a shorter osl sees a
+// prefix of a longer one's partial sums: one thread per (group, template, batch)
+// walks the samples once and hands every member its own total.
+struct SeriesGroup {
+  int64_t off;                    // first thread index
+  int32_t rep;                    // representative search (query / decode-series table offsets)
+  int32_t m_off, n_m;             // members, sorted by n_steps
+  int32_t _pad;
+};
+struct SeriesMember {
+  int32_t search, n_steps;
+};
+struct SdOut {
+  double t_gen;                   // sum of step * run over the member's samples
+  int32_t status;                 // code | label << 8
+  int32_t qsd;                    // reference-equivalent query counts (q1 | q2 << 16)
+  int64_t c0, c1;                 // failing query coordinates
+};
+
 // one priced query (query tables and decode-series tables)
 struct QVal {
   double lat;
@@ -179,6 +201,10 @@ struct lc_ctx {
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
   DBuf pool_key, qt_groups, ds_groups, front_compact, pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   DBuf q_in, q_lat, q_st;  // lc_query_batch
+  DBuf sgroups, smembers, sd;  // shared static decode loops
+  std::vector<SeriesGroup> hsg;
+  std::vector<SeriesMember> hsm;
+  int64_t n_series = 0;
   // last batch
   const lc_db* db = nullptr;
   const lc_space* sp = nullptr;
@@ -225,6 +251,7 @@ struct EvalParams {
   QVal* qt; int64_t n_qt;
   QVal* ds; int64_t n_ds;
   const DsGroup* ds_groups; int32_t n_ds_groups;
+  const SeriesGroup* sgroups; int32_t n_sgroups; const SeriesMember* smembers; SdOut* sd; int64_t n_series;
   // batch
   const lc_search_desc* searches; const SearchMeta* meta; int32_t n_search;
   const int64_t* batches; const double* loads;
@@ -741,10 +768,129 @@ __device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta&
   return 0;
 }
 
-// K2: one thread per cell assembles every step from the tables.
 #ifndef LC_CELL_MIN_BLOCKS
 #define LC_CELL_MIN_BLOCKS 8  // 64 registers: occupancy beats the few spills (measured)
 #endif
+// K2b: static decode loops (serving_modes.py:256-266), one thread per
+// (series group, template, batch) shared by the group's output lengths (SeriesGroup).
+// Non-attention terms come from the decode-step query slots (same tokens at every
+// sample), attention from the decode-series table.  For each member the result is
+// its partial sum after n_steps - 1 samples plus the last sample times its run.
+__global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_dseries(EvalParams P) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < P.n_series;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = P.n_sgroups - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.sgroups[mid].off <= x) lo = mid;
+      else hi = mid - 1;
+    }
+    const SeriesGroup G = P.sgroups[lo];
+    const lc_search_desc& S = P.searches[G.rep];
+    const SearchMeta& M = P.meta[G.rep];
+    const int64_t rel = x - G.off;
+    const int tmpl = (int)(rel / S.n_b), bi = (int)(rel % S.n_b);
+    const SeriesMember* mem = P.smembers + G.m_off;
+    // samples needed: the longest member whose cell is evaluated
+    int K = 0;
+    for (int j = 0; j < G.n_m; ++j) {
+      const int64_t ci = P.meta[mem[j].search].cell_off + (int64_t)tmpl * S.n_b + bi;
+      if ((P.cell_flags[ci] & 1) && mem[j].n_steps > K) K = mem[j].n_steps;
+    }
+    if (!K) continue;
+    const TmplInfo ti = P.tmpl_info[tmpl];
+    lc_combo c;
+    c.tp = ti.tp; c.pp = ti.pp; c.ep = ti.ep; c.tp_i = ti.tp_i; c.ep_i = ti.ep_i;
+    const lc_entry* E = P.entries + (int64_t)tmpl * LC_MAX_ENTRIES;
+    const int ne = P.tmpl_n[tmpl];
+    const int32_t* so = P.slot_of + (int64_t)tmpl * LC_MAX_ENTRIES * 3;
+    const int64_t b = P.batches[S.b_off + bi];
+    const int64_t mb = b > 1 ? b : 1;
+    const double bubble = (double)(mb + ti.pp - 1) / (double)mb;
+    const int64_t xt_dec = expert_tokens(P, c, M, S, 1, bi, b);
+    const QVal* ds = P.ds + M.ds_off + ((int64_t)P.gclass_of[tmpl] * S.n_b + bi) * M.ds_stride;
+    const StepArgs a0{PH_DECODE, 0, b, S.isl + 1, xt_dec};
+    double term[LC_MAX_ENTRIES];
+    int m = 0, gi = -1;
+    const lc_entry* ge = nullptr;
+    ErrRec e{0, 0, 0, 0};
+    for (int i = 0; i < ne && !e.code; ++i) {
+      const lc_entry& en = E[i];
+      if (en.coord == LC_COORD_CTX) continue;
+      QVal q;
+      if (en.coord == LC_COORD_GEN) { q = ds[0]; gi = m; ge = &en; }
+      else q = qt_at(P, M, so[i * 3 + LC_STEP_GEN], S.n_b, bi);
+      if (q.status) {
+        int64_t d[5];
+        entry_coords(en, a0, P.hidden, d);
+        e.code = q.status; e.label = en.label; e.c0 = d[0]; e.c1 = d[1];
+        break;
+      }
+      const double ms = q.lat * (double)en.repeat / 1000.0;
+      term[m++] = 0.0 + ms * bubble;
+    }
+    int mi = 0;  // next member to receive its total (members ascend in n_steps)
+    auto put = [&](int j, double t_gen, int32_t status, int steps, int64_t c0, int64_t c1) {
+      const int64_t ci = P.meta[mem[j].search].cell_off + (int64_t)tmpl * S.n_b + bi;
+      SdOut o;
+      o.t_gen = t_gen;
+      o.status = status;
+      o.qsd = ((m - 1) * steps & 0xffff) | (steps << 16);
+      o.c0 = c0; o.c1 = c1;
+      P.sd[ci] = o;
+    };
+    if (!e.code) {
+      NeumaierSum pre;
+      for (int i = 0; i < gi; ++i) pre.add(term[i]);
+      double t_gen = 0.0;
+#ifndef LC_DECODE_CHAINS
+#define LC_DECODE_CHAINS 2
+#endif
+      for (int step = 0; step < K && !e.code; step += LC_DECODE_CHAINS) {
+        double g[LC_DECODE_CHAINS];
+        int bad = -1;
+#pragma unroll
+        for (int j = 0; j < LC_DECODE_CHAINS; ++j) {
+          const int sj = step + j;
+          g[j] = 0.0;
+          if (sj >= K || bad >= 0) continue;
+          if (sj == 0) { g[j] = term[gi]; continue; }
+          const QVal q = ds[sj];
+          if (q.status) { bad = j; e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + 32ll * sj + 1; continue; }
+          g[j] = 0.0 + (q.lat * (double)ge->repeat / 1000.0) * bubble;
+        }
+        NeumaierSum sc[LC_DECODE_CHAINS];
+#pragma unroll
+        for (int j = 0; j < LC_DECODE_CHAINS; ++j) {
+          sc[j] = pre;
+          sc[j].add(g[j]);
+        }
+        for (int i = gi + 1; i < m; ++i) {
+          const double xv = term[i];
+#pragma unroll
+          for (int j = 0; j < LC_DECODE_CHAINS; ++j) sc[j].add(xv);
+        }
+#pragma unroll
+        for (int j = 0; j < LC_DECODE_CHAINS; ++j) {
+          const int sj = step + j;
+          if (sj >= K || (bad >= 0 && j >= bad)) continue;
+          const double st = sc[j].result();
+          // members whose last sample is sj: t_gen + st * run, run = osl - 1 - 32 sj
+          while (mi < G.n_m && mem[mi].n_steps - 1 == sj) {
+            const int64_t run = P.searches[mem[mi].search].osl - 1 - 32ll * sj;
+            put(mi, t_gen + st * (double)run, 0, mem[mi].n_steps, 0, 0);
+            ++mi;
+          }
+          t_gen += st * 32.0;
+        }
+      }
+    }
+    // members not reached: the first failing query decides
+    for (; mi < G.n_m; ++mi) put(mi, 0.0, e.code | (e.label << 8), 0, e.c0, e.c1);
+  }
+}
+
+// K2: one thread per cell assembles every step from the tables.
 __global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalParams P) {
   const int64_t ncell = P.n_cells_total;
   for (int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ci < ncell;
@@ -793,82 +939,13 @@ __global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalPara
       double tpot = 0.0;
       ErrRec e = p_err;
       if (!e.code && S.osl > 1) {
-        // static decode loop (serving_modes.py:256-266): non-attention terms from the
-        // generation-step slots (same tokens), attention from the decode-series table
-        double term[LC_MAX_ENTRIES];
-        int m = 0, gi = -1;
-        const QVal* ds = P.ds + M.ds_off + ((int64_t)P.gclass_of[tmpl] * S.n_b + bi) * M.ds_stride;
-        const lc_entry* ge = nullptr;
-        const StepArgs a0{PH_DECODE, 0, b, S.isl + 1, xt_dec};
-        for (int i = 0; i < ne && !e.code; ++i) {
-          const lc_entry& en = E[i];
-          if (en.coord == LC_COORD_CTX) continue;
-          QVal q;
-          if (en.coord == LC_COORD_GEN) { q = ds[0]; gi = m; ge = &en; }
-          else q = qt_at(P, M, so[i * 3 + LC_STEP_GEN], S.n_b, bi);
-          if (q.status) {
-            int64_t d[5];
-            entry_coords(en, a0, P.hidden, d);
-            e.code = q.status; e.label = en.label; e.c0 = d[0]; e.c1 = d[1];
-            break;
-          }
-          const double ms = q.lat * (double)en.repeat / 1000.0;
-          term[m++] = 0.0 + ms * bubble;
-        }
-        if (!e.code) {
-          // terms before the attention entry give a fixed partial state; two samples
-          // are then summed as independent chains (ILP), in plan order
-          NeumaierSum pre;
-          for (int i = 0; i < gi; ++i) pre.add(term[i]);
-          double t_gen = 0.0;
-          const int nsteps = M.n_steps;
-          int step = 0;
-#ifndef LC_DECODE_CHAINS
-#define LC_DECODE_CHAINS 2
-#endif
-          for (; step < nsteps && !e.code; step += LC_DECODE_CHAINS) {
-            double g[LC_DECODE_CHAINS];
-#pragma unroll
-            for (int j = 0; j < LC_DECODE_CHAINS; ++j) {
-              const int sj = step + j;
-              g[j] = 0.0;
-              if (sj >= nsteps || e.code) continue;
-              if (sj == 0) { g[j] = term[gi]; continue; }
-              const QVal q = ds[sj];
-              if (q.status) {
-                e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + 32ll * sj + 1;
-                continue;
-              }
-              g[j] = 0.0 + (q.lat * (double)ge->repeat / 1000.0) * bubble;
-            }
-            if (e.code) break;
-            NeumaierSum sc[LC_DECODE_CHAINS];
-#pragma unroll
-            for (int j = 0; j < LC_DECODE_CHAINS; ++j) {
-              sc[j] = pre;
-              sc[j].add(g[j]);
-            }
-            for (int i = gi + 1; i < m; ++i) {
-              const double x = term[i];
-#pragma unroll
-              for (int j = 0; j < LC_DECODE_CHAINS; ++j) sc[j].add(x);
-            }
-#pragma unroll
-            for (int j = 0; j < LC_DECODE_CHAINS; ++j) {
-              const int sj = step + j;
-              if (sj < nsteps) {
-                const int64_t kk = 32ll * sj;
-                const int64_t run = (S.osl - 1 - kk) < 32 ? (S.osl - 1 - kk) : 32;
-                t_gen += sc[j].result() * (double)run;
-              }
-            }
-          }
-          step = step < nsteps ? step : nsteps;
-          if (!e.code) {
-            tpot = t_gen / (double)(S.osl - 1);
-            o.qSD = ((m - 1) * step & 0xffff) | (step << 16);
-            o.st_steps = step;
-          }
+        const SdOut sd = P.sd[ci];  // k_dseries
+        if (sd.status) {
+          e.code = sd.status & 0xff; e.label = sd.status >> 8; e.c0 = sd.c0; e.c1 = sd.c1;
+        } else {
+          tpot = sd.t_gen / (double)(S.osl - 1);
+          o.qSD = sd.qsd;
+          o.st_steps = M.n_steps;
         }
       }
       o.st_status = e.code | (e.label << 8);
@@ -1858,7 +1935,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->pinned_front) cudaFreeHost(c->pinned_front);
@@ -2028,6 +2105,8 @@ static EvalParams make_params(lc_ctx* c) {
   P.qt = (QVal*)c->qt.p; P.n_qt = c->n_qt;
   P.ds = (QVal*)c->ds.p; P.n_ds = c->n_ds;
   P.ds_groups = (const DsGroup*)c->ds_groups.p; P.n_ds_groups = (int32_t)c->hds.size();
+  P.sgroups = (const SeriesGroup*)c->sgroups.p; P.n_sgroups = (int32_t)c->hsg.size();
+  P.smembers = (const SeriesMember*)c->smembers.p; P.sd = (SdOut*)c->sd.p; P.n_series = c->n_series;
   P.searches = (const lc_search_desc*)c->searches.p;
   P.meta = (const SearchMeta*)c->meta.p;
   P.n_search = c->n_search;
@@ -2133,6 +2212,13 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   if (rc2) return rc2;
   rc2 = launch_tables(k_dstables, c->n_ds);
   if (rc2) return rc2;
+  if (c->n_series > 0) {
+    int64_t blocks = (c->n_series + 127) / 128;
+    if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+    ++c->launches;
+    k_dseries<<<(int)blocks, 128, 0, c->stream>>>(P);
+    CK(cudaGetLastError());
+  }
   if (c->n_cells > 0) {
     int64_t blocks = (c->n_cells + 127) / 128;
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
@@ -2370,6 +2456,35 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
       M.ds_stride = c->hds[M._pad2].n_steps;
     }
   }
+  // static decode series: searches that differ only in osl share one loop (SeriesGroup)
+  c->hsg.clear();
+  c->hsm.clear();
+  c->n_series = 0;
+  if (sp->n_gclass) {
+    std::map<std::vector<int64_t>, std::vector<int32_t>> members;
+    std::vector<std::vector<int64_t>> order;
+    for (int s = 0; s < n_search; ++s) {
+      const lc_search_desc& S = searches[s];
+      if (!c->hmeta[s].n_steps) continue;
+      std::vector<int64_t> key = {S.isl, S.b_off, S.n_b, S.load};
+      auto it = members.find(key);
+      if (it == members.end()) { order.push_back(key); members[key] = {s}; }
+      else it->second.push_back(s);
+    }
+    for (const auto& key : order) {
+      std::vector<int32_t>& ms = members[key];
+      std::stable_sort(ms.begin(), ms.end(), [&](int32_t a, int32_t b) { return c->hmeta[a].n_steps < c->hmeta[b].n_steps; });
+      SeriesGroup g;
+      g.off = c->n_series;
+      g.rep = ms[0];
+      g.m_off = (int32_t)c->hsm.size();
+      g.n_m = (int32_t)ms.size();
+      g._pad = 0;
+      for (int32_t s : ms) c->hsm.push_back(SeriesMember{s, c->hmeta[s].n_steps});
+      c->hsg.push_back(g);
+      c->n_series += (int64_t)sp->n_tmpl * searches[ms[0]].n_b;
+    }
+  }
   // dense mixed-step region: tokens = chunk_tokens + n_mix_gen <= context + batch
   c->n_pd_tails = tails;
   c->m_tmax = 0;
@@ -2400,6 +2515,9 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   TailTable* dT = c->tail_tables.get<TailTable>(c->htables.size(), &err);
   DsGroup* dG = c->ds_groups.get<DsGroup>(c->hds.size(), &err);
   QtGroup* dQ = c->qt_groups.get<QtGroup>(c->hqt.size(), &err);
+  SeriesGroup* dSG = c->sgroups.get<SeriesGroup>(c->hsg.size(), &err);
+  SeriesMember* dSM = c->smembers.get<SeriesMember>(c->hsm.size(), &err);
+  c->sd.get<SdOut>(c->n_series ? (size_t)cells : 0, &err);
   c->results.get<lc_search_result>(n_search, &err);
   if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
   if (n_search) CK(cudaMemcpyAsync(dS, searches, sizeof(lc_search_desc) * n_search, cudaMemcpyHostToDevice, c->stream));
@@ -2415,6 +2533,10 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     CK(cudaMemcpyAsync(dG, c->hds.data(), sizeof(DsGroup) * c->hds.size(), cudaMemcpyHostToDevice, c->stream));
   if (!c->hqt.empty())
     CK(cudaMemcpyAsync(dQ, c->hqt.data(), sizeof(QtGroup) * c->hqt.size(), cudaMemcpyHostToDevice, c->stream));
+  if (!c->hsg.empty()) {
+    CK(cudaMemcpyAsync(dSG, c->hsg.data(), sizeof(SeriesGroup) * c->hsg.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(dSM, c->hsm.data(), sizeof(SeriesMember) * c->hsm.size(), cudaMemcpyHostToDevice, c->stream));
+  }
   CK(cudaEventRecord(c->ev[0], c->stream));
   c->launches = 0;
   int rc = run_enum(c);
