@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define LC_ABI_VERSION 1
+#define LC_ABI_VERSION 2
 #define LC_MAX_ENTRIES 16   /* plan entries per (tp, pp, ep) template */
 #define LC_MAX_BUDGETS 16
 #define LC_MAX_EXPERTS 1024
@@ -70,7 +70,9 @@ enum {
 
 /* lc_search_desc.modes bits */
 enum { LC_MODE_STATIC = 1, LC_MODE_AGGREGATED = 2, LC_MODE_DISAGGREGATED = 4,
-       LC_MODE_FORCE = 16 /* skip the memory-fit and budget filters (single-config estimates) */ };
+       LC_MODE_FORCE = 16 /* skip the memory-fit and budget filters (single-config estimates) */,
+       LC_MODE_NO_PLANS = 32 /* disaggregated pools are selected (lc_fetch_pools) but no plans are built:
+                                the per-rank pass of a search sharded across GPUs */ };
 
 /* per-row status codes; the failing entry's label sits in bits 8..15 */
 enum {
@@ -172,7 +174,7 @@ typedef struct {
   double best_thru, best_speed;
   int64_t queries_1d, queries_2d;    /* reference-equivalent query_latency calls (memoised) */
   int32_t n_survivors;               /* rows left for the exact Pareto scan after bucket pruning */
-  int32_t _pad;
+  int32_t n_feasible_plans;          /* of n_feasible, disaggregated plan rows */
 } lc_search_result;
 
 typedef struct {
@@ -232,6 +234,26 @@ int lc_replay_last(lc_ctx* ctx, int32_t iters, lc_batch_totals* totals);
 /* Asynchronous variant: enqueue the last batch's device pipeline (K0..K4) on the
  * context's stream and return immediately (no per-kernel timing). */
 int lc_replay_async(lc_ctx* ctx);
+
+/* Restrict the raw (tp,pp,ep,dp,batch) tuples of the following lc_search_batch
+ * calls (and replays): tuple r of the batch -- searches concatenated, each
+ * n_combos x n_b in enumeration order -- is considered only if lo <= r < hi and
+ * (mask == NULL or mask[r - lo] != 0).  Every other tuple is treated as filtered
+ * out by enumerate_candidates (search.py:82-113).  hi < 0 clears the filter.
+ * A search sharded across GPUs runs each rank on a contiguous block [lo, hi) of
+ * its candidates, then one merge pass on the union mask of the
+ * ranks' local front / best / nearest-miss / pool top-k candidates. */
+int lc_set_raw_filter(lc_ctx* ctx, int64_t lo, int64_t hi, const uint8_t* mask);
+
+/* Disaggregated pool selections of the last batch (search.py:336-339):
+ * pool_units[s*128 + k] (k < 64: prefill, 64 + k: decode) are unit indices in
+ * pool-rank order, pool_counts[2s], [2s+1] the number of each.  Either pointer
+ * may be NULL. */
+int lc_fetch_pools(lc_ctx* ctx, int32_t* pool_units, int32_t* pool_counts);
+
+/* raw[i] = raw tuple index (as in lc_set_raw_filter) of unit units[i] of the last
+ * batch, -1 if out of range: identifies a candidate across ranks and passes. */
+int lc_unit_raw(lc_ctx* ctx, int32_t n, const int32_t* units, int64_t* raw);
 
 /* The context's CUDA stream (cudaStream_t), for callers that order or time work
  * against it (e.g. CUDA events across several contexts). */

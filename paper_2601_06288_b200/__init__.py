@@ -16,6 +16,7 @@ from .engine import (
     run_search_json,
 )
 from .dbgen import GridAxes, generate_synthetic_db, grid_spec_for_model, save_db
+from .sharded import ShardedResult, run_search_sharded
 from .soa import load_soa, save_soa
 from .queries import OperatorQuery, query_latency, query_latency_batch
 from .report import SearchReport, csv_from_doc, export_csv
@@ -39,4 +40,5 @@ __all__ = [
     "enumerate_candidates", "estimate_aggregated", "estimate_static", "export_csv", "get_engine", "load_db", "load_hardware_spec", "load_model_spec",
     "GridAxes", "generate_synthetic_db", "load_soa", "save_soa", "grid_spec_for_model", "save_db",
     "OperatorQuery", "query_latency", "query_latency_batch", "run_search", "run_search_json",
+    "ShardedResult", "run_search_sharded",
 ]

@@ -60,7 +60,7 @@ class LcSearchResult(C.Structure):
                 ("n_front", C.c_int32), ("front_off", C.c_int32), ("n_plans", C.c_int32), ("plan_off", C.c_int32),
                 ("best", C.c_int64), ("nearest", C.c_int64), ("nearest_violation", C.c_double),
                 ("best_thru", C.c_double), ("best_speed", C.c_double), ("queries_1d", C.c_int64),
-                ("queries_2d", C.c_int64), ("n_survivors", C.c_int32), ("_pad", C.c_int32)]
+                ("queries_2d", C.c_int64), ("n_survivors", C.c_int32), ("n_feasible_plans", C.c_int32)]
 
 
 class LcBatchTotals(C.Structure):
@@ -119,7 +119,8 @@ assert QUERY_DTYPE.itemsize == 64
 
 EXPORTED = ("lc_abi_version", "lc_last_error", "lc_open", "lc_close", "lc_db_upload", "lc_db_free",
             "lc_space_upload", "lc_space_free", "lc_search_batch", "lc_fetch", "lc_replay_last", "lc_replay_async",
-            "lc_stream", "lc_query_batch", "lc_dbgen")
+            "lc_stream", "lc_query_batch", "lc_dbgen", "lc_set_raw_filter", "lc_fetch_pools",
+            "lc_unit_raw")
 
 _LIB = None
 
@@ -149,6 +150,9 @@ def load_library(path: str | os.PathLike | None = None):
     lib.lc_stream.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
     lib.lc_dbgen.argtypes = [C.c_void_p, C.POINTER(LcDbgenDesc), F64P, F64P, I32P]
     lib.lc_query_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, F64P, I32P]
+    lib.lc_set_raw_filter.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]
+    lib.lc_fetch_pools.argtypes = [C.c_void_p, I32P, I32P]
+    lib.lc_unit_raw.argtypes = [C.c_void_p, C.c_int32, I32P, I64P]
     if path is None:
         _LIB = lib
     return lib

@@ -202,6 +202,9 @@ struct lc_ctx {
   DBuf pool_key, qt_groups, ds_groups, front_compact, pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   DBuf q_in, q_lat, q_st;  // lc_query_batch
   DBuf sgroups, smembers, sd;  // shared static decode loops
+  DBuf raw_mask;               // lc_set_raw_filter: optional keep-mask over [filt_lo, filt_hi)
+  int64_t filt_lo = 0, filt_hi = -1;  // filt_hi < 0: no raw-tuple filter
+  bool filt_mask = false;
   std::vector<SeriesGroup> hsg;
   std::vector<SeriesMember> hsm;
   int64_t n_series = 0;
@@ -254,6 +257,7 @@ struct EvalParams {
   const SeriesGroup* sgroups; int32_t n_sgroups; const SeriesMember* smembers; SdOut* sd; int64_t n_series;
   // batch
   const lc_search_desc* searches; const SearchMeta* meta; int32_t n_search;
+  int64_t raw_lo, raw_hi; const uint8_t* raw_mask;  // raw-tuple filter (sharded searches)
   const int64_t* batches; const double* loads;
   // units
   const int32_t* u_search; const int32_t* u_combo; const int32_t* u_batch; const uint8_t* u_budget;
@@ -290,6 +294,11 @@ __device__ __forceinline__ int find_search(const SearchMeta* meta, int n, int64_
 // ---- K0: enumeration flags: bit0 keep (unit), bit1 in budget
 __global__ void k_enum_flags(EvalParams P, int64_t n_raw, uint8_t* flags) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_raw; r += (int64_t)gridDim.x * blockDim.x) {
+    // lc_set_raw_filter: a rank's block of a sharded search, or the merge pass's union set
+    if (r < P.raw_lo || r >= P.raw_hi || (P.raw_mask && !P.raw_mask[r - P.raw_lo])) {
+      flags[r] = 0;
+      continue;
+    }
     const int s = find_search(P.meta, P.n_search, r);
     const lc_search_desc& S = P.searches[s];
     const int64_t rel = r - P.meta[s].raw_off;
@@ -476,6 +485,18 @@ __global__ void k_mark_mixed(EvalParams P, int64_t n_items) {
     const int64_t tok = a.chunk_tokens + a.n_mix_gen;
     if (tok <= P.m_tmax) P.m_used[(int64_t)S.load * (P.m_tmax + 1) + tok] = 1;
   }
+}
+
+// lc_unit_raw: unit index -> raw tuple index of the batch (inverse of K0's compaction)
+__global__ void k_unit_raw(const SearchMeta* meta, const lc_search_desc* searches, const int32_t* u_search,
+                           const int32_t* u_combo, const int32_t* u_batch, int32_t n_units, int32_t n,
+                           const int32_t* units, int64_t* raw) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t u = units[i];
+  if (u < 0 || u >= n_units) { raw[i] = -1; return; }
+  const int s = u_search[u];
+  raw[i] = meta[s].raw_off + (int64_t)u_combo[u] * searches[s].n_b + u_batch[u];
 }
 
 // ---- single-operator queries (lc_query_batch): query_latency (perfdb.py:539-580)
@@ -1123,7 +1144,7 @@ __global__ void __launch_bounds__(1024) k_disagg(EvalParams P, SearchMeta* meta,
   __shared__ int npre, ndec;
   __shared__ PlanRec plans[256];
   __shared__ int nplan;
-  if (!(S.modes & 4)) {
+  if (!(S.modes & 4) || (S.modes & LC_MODE_NO_PLANS)) {
     if (threadIdx.x == 0) { meta[s].plan_cap = 0; results[s].n_plans = 0; }
     return;
   }
@@ -1558,7 +1579,7 @@ __global__ void k_pools_final(EvalParams P, SearchMeta* meta, const PoolPartial*
 struct FrontPartial {
   BestKey best;
   unsigned long long smin, smax, q1, q2;
-  int32_t feas, rows, enums, skips;
+  int32_t feas, rows, enums, skips, fplans, _pad;
 };
 
 struct FrontMeta {
@@ -1576,16 +1597,16 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_pass1(EvalParams P, con
   const int64_t nrows_all = 2 * (int64_t)M.n_units + nplan;
   __shared__ BestKey bred[kFrontThreads];
   __shared__ unsigned long long ured[32];
-  __shared__ int cnt[4];
+  __shared__ int cnt[5];
   __shared__ unsigned long long qsum[2];
-  if (tid < 4) cnt[tid] = 0;
+  if (tid < 5) cnt[tid] = 0;
   if (tid < 2) qsum[tid] = 0;
   __syncthreads();
   int64_t lo, hi;
   slice_of(nrows_all, kSplit, bx, &lo, &hi);
   BestKey best{0, 0, 0, 0, -1};
   unsigned long long smin = ~0ull, smax = 0ull, q1 = 0, q2 = 0;
-  int feas = 0, rows = 0, enums = 0, skips = 0;
+  int feas = 0, rows = 0, enums = 0, skips = 0, fplans = 0;
   for (int64_t r = lo + tid; r < hi; r += blockDim.x) {
     if (r < M.n_units) {
       const int64_t u = M.unit_off + r;
@@ -1604,6 +1625,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_pass1(EvalParams P, con
     ++rows;
     if (!feasible(S, v)) continue;
     ++feas;
+    fplans += r >= 2 * (int64_t)M.n_units;
     const double nt = -v.thru, ns = -v.speed;
     if (best.key < 0 || nt < best.nthru || (nt == best.nthru && ns <= best.nspeed)) {
       BestKey k{nt, ns, v.gpus, mode_rank(v.mode), v.key};
@@ -1614,6 +1636,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_pass1(EvalParams P, con
     smax = sb > smax ? sb : smax;
   }
   atomicAdd(&cnt[0], feas); atomicAdd(&cnt[1], rows); atomicAdd(&cnt[2], enums); atomicAdd(&cnt[3], skips);
+  atomicAdd(&cnt[4], fplans);
   atomicAdd(&qsum[0], q1); atomicAdd(&qsum[1], q2);
   bred[tid] = best;
   __syncthreads();
@@ -1626,7 +1649,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_pass1(EvalParams P, con
   if (tid == 0) {
     FrontPartial& o = part[(int64_t)s * kSplit + bx];
     o.best = bred[0]; o.smin = lo_b; o.smax = hi_b; o.q1 = qsum[0]; o.q2 = qsum[1];
-    o.feas = cnt[0]; o.rows = cnt[1]; o.enums = cnt[2]; o.skips = cnt[3];
+    o.feas = cnt[0]; o.rows = cnt[1]; o.enums = cnt[2]; o.skips = cnt[3]; o.fplans = cnt[4]; o._pad = 0;
   }
 }
 
@@ -1644,17 +1667,18 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_mid(EvalParams P, const
   if (tid == 0) {
     BestKey best{0, 0, 0, 0, -1};
     unsigned long long lo = ~0ull, hi = 0ull, q1 = 0, q2 = 0;
-    int feas = 0, rows = 0, enums = 0, skips = 0;
+    int feas = 0, rows = 0, enums = 0, skips = 0, fplans = 0;
     for (int j = 0; j < kSplit; ++j) {
       const FrontPartial& p = part[(int64_t)s * kSplit + j];
       if (best_less(P, M, plan_i, p.best, best)) best = p.best;
       lo = p.smin < lo ? p.smin : lo;
       hi = p.smax > hi ? p.smax : hi;
       q1 += p.q1; q2 += p.q2;
-      feas += p.feas; rows += p.rows; enums += p.enums; skips += p.skips;
+      feas += p.feas; rows += p.rows; enums += p.enums; skips += p.skips; fplans += p.fplans;
     }
     lc_search_result& R = results[s];
     R.n_enumerated = enums; R.n_rows = rows; R.n_feasible = feas; R.n_skipped = skips;
+    R.n_feasible_plans = fplans;
     R.queries_1d = (int64_t)q1; R.queries_2d = (int64_t)q2;
     R.best = best.key;
     R.best_thru = best.key >= 0 ? -best.nthru : 0.0;
@@ -1935,7 +1959,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->pinned_front) cudaFreeHost(c->pinned_front);
@@ -2110,6 +2134,15 @@ static EvalParams make_params(lc_ctx* c) {
   P.searches = (const lc_search_desc*)c->searches.p;
   P.meta = (const SearchMeta*)c->meta.p;
   P.n_search = c->n_search;
+  if (c->filt_hi >= 0) {
+    P.raw_lo = c->filt_lo;
+    P.raw_hi = c->filt_hi;
+    P.raw_mask = c->filt_mask ? (const uint8_t*)c->raw_mask.p : nullptr;
+  } else {
+    P.raw_lo = 0;
+    P.raw_hi = INT64_MAX;
+    P.raw_mask = nullptr;
+  }
   P.batches = (const int64_t*)c->batches.p;
   P.loads = (const double*)c->loads.p;
   P.u_search = (const int32_t*)c->u_search.p; P.u_combo = (const int32_t*)c->u_combo.p;
@@ -2359,7 +2392,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     M.n_steps = ((S.modes & 1) && S.osl > 1) ? (int32_t)((S.osl - 1 + 31) / 32) : 0;
     M.tail_off[0] = M.tail_off[1] = M.tail_off[2] = 0;
     M.plan_off = (int32_t)plans;
-    const int pc = (S.modes & 4) ? S.prefill_cap * S.decode_cap : 0;
+    const int pc = ((S.modes & 4) && !(S.modes & LC_MODE_NO_PLANS)) ? S.prefill_cap * S.decode_cap : 0;
     if (pc > 256) return fail(LC_ERR_ARG, "prefill_cap * decode_cap above 256 is not supported");
     M.plan_cap = pc;
     plans += pc;
@@ -2713,6 +2746,59 @@ int lc_dbgen(lc_ctx* c, const lc_dbgen_desc* g, double* latency_us, double* late
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   cudaFree(dg); cudaFree(dax); cudaFree(dterm); cudaFree(dlogtab); cudaFree(dlat); cudaFree(dlog); cudaFree(dst);
   if (e != cudaSuccess) return fail(LC_ERR_CUDA, std::string("lc_dbgen: ") + cudaGetErrorString(e));
+  return LC_OK;
+}
+
+int lc_set_raw_filter(lc_ctx* c, int64_t lo, int64_t hi, const uint8_t* mask) {
+  if (!c) return fail(LC_ERR_ARG, "lc_set_raw_filter: NULL context");
+  if (hi < 0) {
+    c->filt_lo = 0; c->filt_hi = -1; c->filt_mask = false;
+    return LC_OK;
+  }
+  if (lo < 0 || hi < lo) return fail(LC_ERR_ARG, "lc_set_raw_filter: need 0 <= lo <= hi");
+  CK(cudaSetDevice(c->device));
+  c->filt_lo = lo; c->filt_hi = hi; c->filt_mask = mask != nullptr;
+  if (mask && hi > lo) {
+    cudaError_t e = cudaSuccess;
+    uint8_t* d = c->raw_mask.get<uint8_t>((size_t)(hi - lo), &e);
+    if (e != cudaSuccess) return fail(LC_ERR_CUDA, std::string("lc_set_raw_filter: ") + cudaGetErrorString(e));
+    CK(cudaMemcpyAsync(d, mask, (size_t)(hi - lo), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  return LC_OK;
+}
+
+int lc_fetch_pools(lc_ctx* c, int32_t* pool_units, int32_t* pool_counts) {
+  if (!c || !c->db) return fail(LC_ERR_STATE, "lc_fetch_pools: no previous batch");
+  CK(cudaSetDevice(c->device));
+  if (pool_units && c->n_search)
+    CK(cudaMemcpyAsync(pool_units, c->pool_sel.p, sizeof(int32_t) * 128 * (size_t)c->n_search,
+                       cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (pool_counts)
+    for (int s = 0; s < c->n_search; ++s) {
+      pool_counts[2 * s] = c->hmeta[s].n_pre;
+      pool_counts[2 * s + 1] = c->hmeta[s].n_dec;
+    }
+  return LC_OK;
+}
+
+int lc_unit_raw(lc_ctx* c, int32_t n, const int32_t* units, int64_t* raw) {
+  if (!c || !c->db) return fail(LC_ERR_STATE, "lc_unit_raw: no previous batch");
+  if (n < 0 || (n > 0 && (!units || !raw))) return fail(LC_ERR_ARG, "lc_unit_raw: bad argument");
+  if (n == 0) return LC_OK;
+  CK(cudaSetDevice(c->device));
+  cudaError_t e = cudaSuccess;
+  int32_t* du = c->q_st.get<int32_t>(n, &e);
+  int64_t* dr = (int64_t*)c->q_lat.get<double>(n, &e);
+  if (e != cudaSuccess) return fail(LC_ERR_CUDA, std::string("lc_unit_raw: ") + cudaGetErrorString(e));
+  CK(cudaMemcpyAsync(du, units, sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice, c->stream));
+  k_unit_raw<<<(n + 127) / 128, 128, 0, c->stream>>>((const SearchMeta*)c->meta.p, (const lc_search_desc*)c->searches.p,
+                                                     (const int32_t*)c->u_search.p, (const int32_t*)c->u_combo.p,
+                                                     (const int32_t*)c->u_batch.p, (int32_t)c->n_units, n, du, dr);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(raw, dr, sizeof(int64_t) * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
   return LC_OK;
 }
 

@@ -204,7 +204,7 @@ class Engine:
 
     # ------------------------------------------------------------------ batches
     def run_batch(self, db, model, space, workloads: Sequence, disagg=DEFAULT_DISAGG, mode_override=None,
-                  enforce_budget: bool = True) -> BatchOutput:
+                  enforce_budget: bool = True, mode_extra: int = 0) -> BatchOutput:
         t0 = time.perf_counter()
         sph, plan, flat = self.space_handle(db, model, space)
         dbh, _ = self.db_handle(db)
@@ -235,7 +235,7 @@ class Engine:
                 modes_v.append(mode_override)
             else:
                 modes_v.append((MODE_STATIC if "static" in w.modes else 0) | (MODE_AGG if "aggregated" in w.modes else 0)
-                               | (MODE_DISAGG if "disaggregated" in w.modes else 0))
+                               | (MODE_DISAGG if "disaggregated" in w.modes else 0) | mode_extra)
             if enforce_budget and w.gpu_budgets:
                 budgets = sorted(set(w.gpu_budgets))
                 if len(budgets) > N.LC_MAX_BUDGETS:
@@ -292,6 +292,31 @@ class Engine:
         out.h2d_bytes = searches.nbytes + 8 * len(batches) + (l_arr.nbytes if loads else 0)
         out.d2h_bytes = results.nbytes + 4
         return out
+
+    def set_raw_filter(self, lo: int = 0, hi: int = -1, mask: np.ndarray | None = None) -> None:
+        """Restrict the raw candidate tuples of the following batches (lc_set_raw_filter); hi < 0 clears."""
+        m = None
+        if mask is not None:
+            mask = np.ascontiguousarray(mask, dtype=np.uint8)
+            if len(mask) != hi - lo:
+                raise ValueError("mask length must be hi - lo")
+            m = C.c_void_p(mask.ctypes.data)
+        self._call(self.lib.lc_set_raw_filter, "lc_set_raw_filter", self.ctx, int(lo), int(hi), m)
+
+    def fetch_pools(self, n_search: int) -> tuple[np.ndarray, np.ndarray]:
+        """Pool selections of the last batch: units [n_search, 2, 64] and counts [n_search, 2]."""
+        units = np.zeros((max(n_search, 1), 2, 64), dtype=np.int32)
+        counts = np.zeros((max(n_search, 1), 2), dtype=np.int32)
+        self._call(self.lib.lc_fetch_pools, "lc_fetch_pools", self.ctx, N.ptr(units, C.c_int32),
+                   N.ptr(counts, C.c_int32))
+        return units[:n_search], counts[:n_search]
+
+    def unit_raw(self, units: np.ndarray) -> np.ndarray:
+        """Raw tuple index of each unit of the last batch (lc_unit_raw)."""
+        u = np.ascontiguousarray(units, dtype=np.int32)
+        raw = np.zeros(max(len(u), 1), dtype=np.int64)
+        self._call(self.lib.lc_unit_raw, "lc_unit_raw", self.ctx, len(u), N.ptr(u, C.c_int32), N.ptr(raw, C.c_int64))
+        return raw[: len(u)]
 
     def replay_async(self) -> None:
         """Enqueue the last batch's device pipeline on this engine's stream (no sync)."""

@@ -13,7 +13,7 @@ int main(void) {
   S(lc_search_result); S(lc_batch_totals); S(lc_fetch_req); S(lc_query); S(lc_gen_grid); S(lc_dbgen_desc);
   F(lc_entry, repeat); F(lc_entry, d); F(lc_combo, weight_bytes); F(lc_slot, step); F(lc_slot, pair);
   F(lc_search_desc, budgets); F(lc_search_desc, ctx_capacity); F(lc_search_desc, load);
-  F(lc_search_result, best); F(lc_search_result, n_survivors); F(lc_batch_totals, kernel_ms);
+  F(lc_search_result, best); F(lc_search_result, n_survivors); F(lc_search_result, n_feasible_plans); F(lc_batch_totals, kernel_ms);
   F(lc_batch_totals, n_cells); F(lc_query, d); F(lc_query, kv_len); F(lc_gen_grid, cell_off);
   F(lc_gen_grid, d); F(lc_gen_grid, offset); F(lc_dbgen_desc, amplitude); F(lc_dbgen_desc, compute);
   F(lc_db_desc, compute); F(lc_db_desc, policy); F(lc_space_desc, gclass_of);

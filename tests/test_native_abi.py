@@ -15,7 +15,7 @@ def test_library_exports_header_symbols():
     assert declared == set(_native.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.lc_abi_version() == 1
+    assert lib.lc_abi_version() == 2
 
 
 def test_struct_layouts_match_header_sizes():
@@ -79,6 +79,7 @@ def test_ctypes_and_numpy_layouts_match_the_c_compiler(tmp_path):
         "lc_search_desc.load": off(N.SEARCH_DESC_DTYPE, "load"),
         "lc_search_result.best": N.LcSearchResult.best.offset,
         "lc_search_result.n_survivors": N.LcSearchResult.n_survivors.offset,
+        "lc_search_result.n_feasible_plans": N.LcSearchResult.n_feasible_plans.offset,
         "lc_batch_totals.kernel_ms": N.LcBatchTotals.kernel_ms.offset,
         "lc_batch_totals.n_cells": N.LcBatchTotals.n_cells.offset,
         "lc_query.d": off(N.QUERY_DTYPE, "d"), "lc_query.kv_len": off(N.QUERY_DTYPE, "kv_len"),
