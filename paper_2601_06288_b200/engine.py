@@ -487,6 +487,12 @@ def run_search_json(db, model, workload, space=CandidateSpace(), jobs: int = 1,
     Same bytes as the reference's report JSON (search.py:262-264); rows are
     written from the device's column arrays (fastreport.report_json).
     """
+    return search_json_columns(db, model, workload, space, jobs, disagg_constants, device)[0]
+
+
+def search_json_columns(db, model, workload, space=CandidateSpace(), jobs: int = 1,
+                        disagg_constants=DEFAULT_DISAGG, device: int = 0):
+    """(report JSON text, fastreport.Columns): run_search_json plus the columns it was written from."""
     from .fastreport import columns_from_batch, report_json
 
     if jobs < 1:
@@ -497,7 +503,15 @@ def run_search_json(db, model, workload, space=CandidateSpace(), jobs: int = 1,
         out = eng.run_batch(db, model, space, [workload], disagg_constants)
         cols = columns_from_batch(out, 0, db, model, workload, space, 0.0)
     cols.total_ms = (time.perf_counter() - t0) * 1000.0
-    return report_json(cols)
+    return report_json(cols), cols
+
+
+def count_candidates(model, space, workload, db, enforce_budget: bool = True, device: int = 0) -> int:
+    """len(enumerate_candidates(...)) from K0 alone: no configs are materialised on the host."""
+    eng = get_engine(device)
+    with eng._lock:
+        out = eng.run_batch(db, model, space, [workload], mode_override=0, enforce_budget=enforce_budget)
+        return int(out.results[0]["n_units"])
 
 
 MODE_FORCE = 16  # LC_MODE_FORCE: no memory-fit / budget filter
