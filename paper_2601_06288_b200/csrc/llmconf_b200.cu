@@ -413,9 +413,12 @@ __global__ void k_unit_offsets(SearchMeta* meta, int n_search, const int32_t* po
   meta[s].n_units = b - a;
 }
 
+#ifndef LC_TAIL_MIN_BLOCKS
+#define LC_TAIL_MIN_BLOCKS 4  // 64 registers: 32 warps per SM for the warp-per-tail radix select
+#endif
 // ---- K3: MoE tails table [type P/D/M][tp_i][ep_i][b_i] per search
 template <int PER>
-__global__ void k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
+__global__ void __launch_bounds__(256, LC_TAIL_MIN_BLOCKS) k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
   __shared__ int hist_all[8][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* hist = hist_all[warp];
@@ -678,9 +681,17 @@ __device__ __forceinline__ int64_t tail_tokens(const EvalParams& P, const Search
   return balanced > tail ? balanced : tail;
 }
 
+// Table kernels stage the database in shared memory once per block (~38 KB for
+// DeepSeek-V3), so blocks are wide: 256 threads, 4 blocks (32 warps) per SM.
+#ifndef LC_TABLE_THREADS
+#define LC_TABLE_THREADS 256
+#endif
+#ifndef LC_TABLE_MIN_BLOCKS
+#define LC_TABLE_MIN_BLOCKS 4
+#endif
 // K2a: query tables.  One thread per (search, slot, batch): the latency every
 // template entry of that slot sees in that step (query_latency, perfdb.py:539-580).
-__global__ void __launch_bounds__(128) k_qtables(EvalParams P) {
+__global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_qtables(EvalParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   DbView V;
   stage_db(P, smem, &V);
@@ -728,7 +739,7 @@ __global__ void __launch_bounds__(128) k_qtables(EvalParams P) {
 
 // K2a': generation-attention latency at every sampled KV length of the static
 // decode loop (serving_modes.py:258-265): one thread per (search, grid, batch, sample).
-__global__ void __launch_bounds__(128) k_dstables(EvalParams P) {
+__global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_dstables(EvalParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   DbView V;
   stage_db(P, smem, &V);
@@ -1434,6 +1445,7 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
 // those maxima are real rows that would dominate it -- so only such
 // survivors go through the exact reference scan (search.py:156-176).
 constexpr int kSplit = 64;      // blocks per search for the Pareto passes
+constexpr int kSplit1 = 16;     // blocks per search for the first (counting / best) pass
 constexpr int kPoolSplit = 16;  // blocks per search for the pool top-k
 constexpr int kCompactFront = 2048;  // fixed-stride copy of each front for one-shot D2H (= survivor cap)
 
@@ -1587,23 +1599,31 @@ struct FrontMeta {
   unsigned long long base;
 };
 
+__device__ __forceinline__ BestKey shfl_best(const BestKey& k, int src) {
+  BestKey o;
+  o.nthru = __shfl_sync(0xffffffffu, k.nthru, src);
+  o.nspeed = __shfl_sync(0xffffffffu, k.nspeed, src);
+  o.gpus = __shfl_sync(0xffffffffu, k.gpus, src);
+  o.mode_rank = __shfl_sync(0xffffffffu, k.mode_rank, src);
+  o.key = __shfl_sync(0xffffffffu, k.key, src);
+  return o;
+}
+
 __global__ void __launch_bounds__(kFrontThreads) k_front_pass1(EvalParams P, const SearchMeta* meta,
                                                                const int32_t* plan_i, const double* plan_d,
                                                                const lc_search_result* results, FrontPartial* part) {
   const int s = blockIdx.y, bx = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const lc_search_desc& S = P.searches[s];
   const SearchMeta& M = meta[s];
   const int64_t nplan = results[s].n_plans;
   const int64_t nrows_all = 2 * (int64_t)M.n_units + nplan;
-  __shared__ BestKey bred[kFrontThreads];
-  __shared__ unsigned long long ured[32];
-  __shared__ int cnt[5];
-  __shared__ unsigned long long qsum[2];
-  if (tid < 5) cnt[tid] = 0;
-  if (tid < 2) qsum[tid] = 0;
-  __syncthreads();
+  constexpr int kWarps = kFrontThreads / 32;
+  __shared__ BestKey wbest[kWarps];
+  __shared__ unsigned long long wlo[kWarps], whi[kWarps], wq1[kWarps], wq2[kWarps];
+  __shared__ int wcnt[kWarps][5];
   int64_t lo, hi;
-  slice_of(nrows_all, kSplit, bx, &lo, &hi);
+  slice_of(nrows_all, kSplit1, bx, &lo, &hi);
   BestKey best{0, 0, 0, 0, -1};
   unsigned long long smin = ~0ull, smax = 0ull, q1 = 0, q2 = 0;
   int feas = 0, rows = 0, enums = 0, skips = 0, fplans = 0;
@@ -1635,21 +1655,45 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_pass1(EvalParams P, con
     smin = sb < smin ? sb : smin;
     smax = sb > smax ? sb : smax;
   }
-  atomicAdd(&cnt[0], feas); atomicAdd(&cnt[1], rows); atomicAdd(&cnt[2], enums); atomicAdd(&cnt[3], skips);
-  atomicAdd(&cnt[4], fplans);
-  atomicAdd(&qsum[0], q1); atomicAdd(&qsum[1], q2);
-  bred[tid] = best;
-  __syncthreads();
-  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-    if (tid < w && best_less(P, M, plan_i, bred[tid + w], bred[tid])) bred[tid] = bred[tid + w];
-    __syncthreads();
+  // warp-level reductions, then one shared-memory step (a block covers few rows per thread)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    feas += __shfl_xor_sync(0xffffffffu, feas, o);
+    rows += __shfl_xor_sync(0xffffffffu, rows, o);
+    enums += __shfl_xor_sync(0xffffffffu, enums, o);
+    skips += __shfl_xor_sync(0xffffffffu, skips, o);
+    fplans += __shfl_xor_sync(0xffffffffu, fplans, o);
+    q1 += __shfl_xor_sync(0xffffffffu, q1, o);
+    q2 += __shfl_xor_sync(0xffffffffu, q2, o);
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, smin, o);
+    const unsigned long long b = __shfl_xor_sync(0xffffffffu, smax, o);
+    smin = a < smin ? a : smin;
+    smax = b > smax ? b : smax;
   }
-  const unsigned long long lo_b = block_min_u64(smin, ured);
-  const unsigned long long hi_b = block_max_u64(smax, ured);
+  for (int o = 1; o < 32; o <<= 1) {
+    const BestKey other = shfl_best(best, lane ^ o);
+    if (best_less(P, M, plan_i, other, best)) best = other;
+  }
+  if (lane == 0) {
+    wbest[warp] = best;
+    wlo[warp] = smin; whi[warp] = smax; wq1[warp] = q1; wq2[warp] = q2;
+    wcnt[warp][0] = feas; wcnt[warp][1] = rows; wcnt[warp][2] = enums; wcnt[warp][3] = skips; wcnt[warp][4] = fplans;
+  }
+  __syncthreads();
   if (tid == 0) {
-    FrontPartial& o = part[(int64_t)s * kSplit + bx];
-    o.best = bred[0]; o.smin = lo_b; o.smax = hi_b; o.q1 = qsum[0]; o.q2 = qsum[1];
-    o.feas = cnt[0]; o.rows = cnt[1]; o.enums = cnt[2]; o.skips = cnt[3]; o.fplans = cnt[4]; o._pad = 0;
+    FrontPartial o;
+    o.best = wbest[0]; o.smin = wlo[0]; o.smax = whi[0]; o.q1 = wq1[0]; o.q2 = wq2[0];
+    o.feas = wcnt[0][0]; o.rows = wcnt[0][1]; o.enums = wcnt[0][2]; o.skips = wcnt[0][3]; o.fplans = wcnt[0][4];
+    o._pad = 0;
+    for (int w = 1; w < kWarps; ++w) {
+      if (best_less(P, M, plan_i, wbest[w], o.best)) o.best = wbest[w];
+      o.smin = wlo[w] < o.smin ? wlo[w] : o.smin;
+      o.smax = whi[w] > o.smax ? whi[w] : o.smax;
+      o.q1 += wq1[w]; o.q2 += wq2[w];
+      o.feas += wcnt[w][0]; o.rows += wcnt[w][1]; o.enums += wcnt[w][2]; o.skips += wcnt[w][3];
+      o.fplans += wcnt[w][4];
+    }
+    part[(int64_t)s * kSplit1 + bx] = o;
   }
 }
 
@@ -1668,8 +1712,8 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_mid(EvalParams P, const
     BestKey best{0, 0, 0, 0, -1};
     unsigned long long lo = ~0ull, hi = 0ull, q1 = 0, q2 = 0;
     int feas = 0, rows = 0, enums = 0, skips = 0, fplans = 0;
-    for (int j = 0; j < kSplit; ++j) {
-      const FrontPartial& p = part[(int64_t)s * kSplit + j];
+    for (int j = 0; j < kSplit1; ++j) {
+      const FrontPartial& p = part[(int64_t)s * kSplit1 + j];
       if (best_less(P, M, plan_i, p.best, best)) best = p.best;
       lo = p.smin < lo ? p.smin : lo;
       hi = p.smax > hi ? p.smax : hi;
@@ -2231,13 +2275,13 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   auto launch_tables = [&](auto kern, int64_t n_items) -> int {
     if (n_items <= 0) return LC_OK;
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, LC_TABLE_THREADS, smem));
     if (per_sm < 1) per_sm = 1;
-    int64_t blocks = (n_items + 127) / 128;
+    int64_t blocks = (n_items + LC_TABLE_THREADS - 1) / LC_TABLE_THREADS;
     const int64_t cap = (int64_t)sms * per_sm;
     if (blocks > cap) blocks = cap;
     ++c->launches;
-    kern<<<(int)blocks, 128, smem, c->stream>>>(P);
+    kern<<<(int)blocks, LC_TABLE_THREADS, smem, c->stream>>>(P);
     CK(cudaGetLastError());
     return LC_OK;
   };
@@ -2296,7 +2340,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     lc_search_result* res = (lc_search_result*)c->results.p;
     const dim3 g(kSplit, c->n_search);
     ++c->launches;
-    k_front_pass1<<<g, kFrontThreads, 0, c->stream>>>(P, meta, pi, pd, res, fp);
+    k_front_pass1<<<dim3(kSplit1, c->n_search), kFrontThreads, 0, c->stream>>>(P, meta, pi, pd, res, fp);
     ++c->launches;
     k_front_mid<<<c->n_search, kFrontThreads, 0, c->stream>>>(P, meta, pi, pd, res, fp, fm, bk, ns);
     ++c->launches;
