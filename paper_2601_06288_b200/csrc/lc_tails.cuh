@@ -179,6 +179,24 @@ __device__ int64_t warp_busiest_shard(const double* __restrict__ q, const double
   }
   // busiest contiguous EP block
   const int bs = (int)(E / ep);
+  if (per > 0 && bs % per == 0 && E % 32 == 0 && per * 32 == E) {
+    // every lane's experts lie inside one block of bs / per consecutive lanes:
+    // segmented warp sum over those lanes, then the maximum over the blocks
+    int64_t part = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j)
+      if (j < per) part += cnt[j];
+    const int lanes = bs / per;  // power of two: E and ep are powers of two here
+    if ((lanes & (lanes - 1)) == 0) {
+      for (int o = 1; o < lanes && o < 32; o <<= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const int64_t y = __shfl_xor_sync(0xffffffffu, part, o);
+        part = y > part ? y : part;
+      }
+      return part;
+    }
+  }
   int64_t best = 0;
   for (int r = 0; r < ep; ++r) {
     int64_t part = 0;

@@ -682,12 +682,12 @@ __device__ __forceinline__ int64_t tail_tokens(const EvalParams& P, const Search
 }
 
 // Table kernels stage the database in shared memory once per block (~38 KB for
-// DeepSeek-V3), so blocks are wide: 256 threads, 4 blocks (32 warps) per SM.
+// DeepSeek-V3), so blocks are wide: 512 threads, 2 blocks (32 warps) per SM.
 #ifndef LC_TABLE_THREADS
-#define LC_TABLE_THREADS 256
+#define LC_TABLE_THREADS 512
 #endif
 #ifndef LC_TABLE_MIN_BLOCKS
-#define LC_TABLE_MIN_BLOCKS 4
+#define LC_TABLE_MIN_BLOCKS 2
 #endif
 // K2a: query tables.  One thread per (search, slot, batch): the latency every
 // template entry of that slot sees in that step (query_latency, perfdb.py:539-580).
@@ -1444,9 +1444,18 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
 // front if it beats the best throughput of every strictly faster bucket --
 // those maxima are real rows that would dominate it -- so only such
 // survivors go through the exact reference scan (search.py:156-176).
-constexpr int kSplit = 64;      // blocks per search for the Pareto passes
-constexpr int kSplit1 = 16;     // blocks per search for the first (counting / best) pass
-constexpr int kPoolSplit = 16;  // blocks per search for the pool top-k
+#ifndef LC_FRONT_SPLIT
+#define LC_FRONT_SPLIT 64
+#endif
+#ifndef LC_FRONT_SPLIT1
+#define LC_FRONT_SPLIT1 16
+#endif
+#ifndef LC_POOL_SPLIT
+#define LC_POOL_SPLIT 16
+#endif
+constexpr int kSplit = LC_FRONT_SPLIT;     // blocks per search for the Pareto passes
+constexpr int kSplit1 = LC_FRONT_SPLIT1;   // blocks per search for the first (counting / best) pass
+constexpr int kPoolSplit = LC_POOL_SPLIT;  // blocks per search for the pool top-k
 constexpr int kCompactFront = 2048;  // fixed-stride copy of each front for one-shot D2H (= survivor cap)
 
 struct PoolPartial {
