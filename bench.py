@@ -385,7 +385,7 @@ def main() -> int:
         roof["fp64_peak_gflops_measured"] = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())[
             "fp64_fma_gflops"]
         ncu = {}
-        for name in ("r1_ncu_v9.json", "r1_ncu_v8.json"):  # v9: DeepSeek-V3 batch, v8: k_eval_cells
+        for name in ("r1_ncu_v9.json", "r1_ncu_v10.json"):  # v9: DeepSeek-V3 batch, v10: k_eval_cells
             ncu.update(json.loads((ROOT / "profiles" / name).read_text())["kernels"])
         roof["ncu_fp64_pipe_active_pct"] = {
             k: float(str(ncu[k].get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")).split()[0])
