@@ -222,6 +222,10 @@ struct lc_ctx {
   std::vector<DsGroup> hds;
   int64_t* pinned_front = nullptr;  // page-locked staging for front D2H
   size_t pinned_front_cap = 0;
+  int32_t* pinned_plans_i = nullptr;  // page-locked copies of the plan slots
+  double* pinned_plans_d = nullptr;
+  size_t pinned_plans_cap = 0;
+  bool staged = false;  // fronts + plans of the last batch already copied to the pinned buffers
   std::vector<QtGroup> hqt;
   std::vector<lc_search_result> hres;
 };
@@ -2016,6 +2020,8 @@ int lc_close(lc_ctx* c) {
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->pinned_front) cudaFreeHost(c->pinned_front);
+  if (c->pinned_plans_i) cudaFreeHost(c->pinned_plans_i);
+  if (c->pinned_plans_d) cudaFreeHost(c->pinned_plans_d);
   cudaStreamDestroy(c->stream);
   delete c;
   return LC_OK;
@@ -2421,6 +2427,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   if (!c || !db || !sp || (n_search > 0 && !searches) || n_search < 0)
     return fail(LC_ERR_ARG, "lc_search_batch: bad arguments");
   CK(cudaSetDevice(c->device));
+  c->staged = false;
   c->db = db;
   c->sp = sp;
   c->n_search = n_search;
@@ -2630,6 +2637,38 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   c->n_front_slots = 2 * c->n_cap + c->n_plan_slots;
   rc = run_eval_pipeline(c, totals);
   if (rc) return rc;
+  // compact fronts and plan slots ride the same synchronisation as the summaries
+  // (page-locked staging; lc_fetch then serves them from host memory)
+  c->staged = false;
+  if (n_search) {
+    const size_t need_f = (size_t)n_search * kCompactFront;
+    if (c->pinned_front_cap < need_f) {
+      if (c->pinned_front) cudaFreeHost(c->pinned_front);
+      c->pinned_front = nullptr;
+      c->pinned_front_cap = 0;
+      CK(cudaHostAlloc((void**)&c->pinned_front, need_f * 8, cudaHostAllocDefault));
+      c->pinned_front_cap = need_f;
+    }
+    const size_t need_p = (size_t)(c->n_plan_slots > 0 ? c->n_plan_slots : 1);
+    if (c->pinned_plans_cap < need_p) {
+      if (c->pinned_plans_i) cudaFreeHost(c->pinned_plans_i);
+      if (c->pinned_plans_d) cudaFreeHost(c->pinned_plans_d);
+      c->pinned_plans_i = nullptr;
+      c->pinned_plans_d = nullptr;
+      c->pinned_plans_cap = 0;
+      CK(cudaHostAlloc((void**)&c->pinned_plans_i, need_p * 4 * sizeof(int32_t), cudaHostAllocDefault));
+      CK(cudaHostAlloc((void**)&c->pinned_plans_d, need_p * 6 * sizeof(double), cudaHostAllocDefault));
+      c->pinned_plans_cap = need_p;
+    }
+    CK(cudaMemcpyAsync(c->pinned_front, c->front_compact.p, need_f * 8, cudaMemcpyDeviceToHost, c->stream));
+    if (c->n_plan_slots) {
+      CK(cudaMemcpyAsync(c->pinned_plans_i, c->plans_i.p, (size_t)c->n_plan_slots * 4 * sizeof(int32_t),
+                         cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(c->pinned_plans_d, c->plans_d.p, (size_t)c->n_plan_slots * 6 * sizeof(double),
+                         cudaMemcpyDeviceToHost, c->stream));
+    }
+    c->staged = true;
+  }
   c->hres.resize(n_search);
   if (n_search)
     CK(cudaMemcpyAsync(c->hres.data(), c->results.p, sizeof(lc_search_result) * n_search, cudaMemcpyDeviceToHost,
@@ -2905,11 +2944,16 @@ int lc_fetch(lc_ctx* c, const lc_fetch_req* r) {
   std::vector<double> pd;
   if (c->n_plan_slots && (r->plan_p || r->plan_d || r->plan_x || r->plan_y || r->plan_gpus || r->plan_r_sys ||
                           r->plan_ttft || r->plan_tpot || r->plan_speed || r->plan_thru)) {
-    pi.resize(c->n_plan_slots * 4);
-    pd.resize(c->n_plan_slots * 6);
-    CK(cudaMemcpyAsync(pi.data(), c->plans_i.p, pi.size() * 4, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(pd.data(), c->plans_d.p, pd.size() * 8, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    if (c->staged) {
+      pi.assign(c->pinned_plans_i, c->pinned_plans_i + c->n_plan_slots * 4);
+      pd.assign(c->pinned_plans_d, c->pinned_plans_d + c->n_plan_slots * 6);
+    } else {
+      pi.resize(c->n_plan_slots * 4);
+      pd.resize(c->n_plan_slots * 6);
+      CK(cudaMemcpyAsync(pi.data(), c->plans_i.p, pi.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(pd.data(), c->plans_d.p, pd.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
     int64_t k = 0;
     for (int s = 0; s < c->n_search; ++s) {
       const lc_search_result& R = c->hres[s];
@@ -2941,10 +2985,11 @@ int lc_fetch(lc_ctx* c, const lc_fetch_req* r) {
         CK(cudaHostAlloc((void**)&c->pinned_front, need * 8, cudaHostAllocDefault));
         c->pinned_front_cap = need;
       }
-      if (maxf > 0)
+      if (maxf > 0 && !c->staged) {
         CK(cudaMemcpy2DAsync(c->pinned_front, kCompactFront * 8, c->front_compact.p, kCompactFront * 8,
                              (size_t)maxf * 8, c->n_search, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaStreamSynchronize(c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+      }
       int64_t k = 0;
       for (int s = 0; s < c->n_search; ++s) {
         memcpy(r->front + k, c->pinned_front + (size_t)s * kCompactFront, 8 * (size_t)c->hres[s].n_front);
