@@ -223,6 +223,7 @@ def main() -> int:
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--cpu-steps", type=int, default=6, help="reference-oracle sample steps for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--split", type=int, default=1, help="independent batches (engines / streams) per model")
     args = ap.parse_args()
 
     from paper_2601_06288_b200.sweeps import sweep
@@ -268,24 +269,30 @@ def main() -> int:
     # shard searches across ranks: contiguous blocks of each model's workload list
     from paper_2601_06288_b200.dist import shard_range
 
+    # jobs: each model's block of workloads, cut into --split contiguous batches
+    # (the sweep is ISL-major, so a batch keeps whole ISL groups and their shared tables)
     my_parts = []
     for p in parts:
         lo, hi = shard_range(len(p.workloads), rank, ws)
-        my_parts.append((p, p.workloads[lo:hi]))
-    # one engine (CUDA stream + resident workspace) per model so each keeps its batch resident
-    engines = {p.model_name: Engine(dev) for p, w in my_parts if w}
+        mine = p.workloads[lo:hi]
+        for k in range(args.split):
+            a, b = shard_range(len(mine), k, args.split)
+            if b > a:
+                my_parts.append((f"{p.model_name}/{k}", p, mine[a:b]))
+    # one engine (CUDA stream + resident workspace) per batch so each keeps its inputs resident
+    engines = {key: Engine(dev) for key, p, w in my_parts}
 
     pool = ThreadPoolExecutor(max_workers=max(1, len(engines)))
 
-    def one_model(pw):
-        p, wls = pw
-        out = engines[p.model_name].run_batch(p.db, p.model, p.space, wls)
+    def one_model(job):
+        key, p, wls = job
+        out = engines[key].run_batch(p.db, p.model, p.space, wls)
         front, plans = fetch_fronts(out)
         return (int(out.results["n_enumerated"].sum()), out.h2d_bytes,
                 out.d2h_bytes + front.nbytes + sum(v.nbytes for v in plans.values()), out.results)
 
     def e2e_step():
-        outs = list(pool.map(one_model, [pw for pw in my_parts if pw[1]]))
+        outs = list(pool.map(one_model, my_parts))
         return (sum(o[0] for o in outs), sum(o[1] for o in outs), sum(o[2] for o in outs), [o[3] for o in outs])
 
     clocks = ClockSampler(dev)
@@ -296,9 +303,8 @@ def main() -> int:
 
     # ---- device-resident timing: replay K0..K4 per model on resident inputs
     outs = {}
-    for p, wls in my_parts:
-        if wls:
-            outs[p.model_name] = engines[p.model_name].run_batch(p.db, p.model, p.space, wls)
+    for key, p, wls in my_parts:
+        outs[key] = engines[key].run_batch(p.db, p.model, p.space, wls)
     cands_local = sum(int(o.results["n_enumerated"].sum()) for o in outs.values())
     q1 = sum(int(o.results["queries_1d"].sum()) for o in outs.values())
     q2 = sum(int(o.results["queries_2d"].sum()) for o in outs.values())
@@ -306,14 +312,13 @@ def main() -> int:
     kernel_ms = np.zeros(6)
     launches_per_step = 0
     tq = tq2 = n_cells = 0
-    for p, wls in my_parts:
-        if wls:
-            tot = engines[p.model_name].replay(1)
-            kernel_ms += np.array(list(tot.kernel_ms), dtype=np.float64)
-            launches_per_step += int(tot.n_launches)
-            tq += int(tot.n_table_queries)
-            tq2 += int(tot.n_table_queries_2d)
-            n_cells += int(tot.n_cells)
+    for key, p, wls in my_parts:
+        tot = engines[key].replay(1)
+        kernel_ms += np.array(list(tot.kernel_ms), dtype=np.float64)
+        launches_per_step += int(tot.n_launches)
+        tq += int(tot.n_table_queries)
+        tq2 += int(tot.n_table_queries_2d)
+        n_cells += int(tot.n_cells)
     # timed steps: every model's pipeline enqueued at once on its own stream; one
     # CUDA-event span on the current stream covers all of them
     streams = {m: torch.cuda.ExternalStream(e.stream_ptr()) for m, e in engines.items()}
@@ -413,7 +418,7 @@ def main() -> int:
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": float(np.mean(step_ms)), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(workload_desc, candidates=int(cands_total), parallelism=f"searches sharded over {ws} GPU(s)",
+        "config": dict(workload_desc, candidates=int(cands_total), parallelism=f"searches sharded over {ws} GPU(s), {args.split} batch(es) per model",
                        l2="per-step unit arrays exceed L2 (~2 GB written per step)"),
         "search_wall_ms": {"device": dev_s * 1000 / args.steps, "e2e": e2e_s * 1000 / args.steps,
                            "per_model_sequential_device": float(kernel_ms.sum())},
