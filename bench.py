@@ -402,6 +402,10 @@ def main() -> int:
         try:
             roof["traffic"] = json.loads(prof.read_text()).get("dram_bytes_per_step")
             roof["traffic_source"] = "profiles/ncu_k2_traffic.json"
+            # the stage's measured DRAM bytes over its measured time: its physical HBM utilisation
+            if roof["traffic"] and k2_s > 0:
+                roof["traffic_gbs"] = roof["traffic"] / k2_s / 1e9
+                roof["traffic_frac"] = roof["traffic_gbs"] / peak
         except Exception:
             pass
 
