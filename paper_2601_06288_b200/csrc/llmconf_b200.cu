@@ -226,6 +226,9 @@ struct lc_ctx {
   double* pinned_plans_d = nullptr;
   size_t pinned_plans_cap = 0;
   bool staged = false;  // fronts + plans of the last batch already copied to the pinned buffers
+  bool batches_sorted = false;  // every search's batch list is non-decreasing: K0 in closed form
+  std::vector<int32_t> hsearch_nb;
+  DBuf pair_inb, cmax;          // K0 closed form: per (search, combo) budget flag; per (search, template) fit maxima
   std::vector<QtGroup> hqt;
   std::vector<lc_search_result> hres;
 };
@@ -244,7 +247,7 @@ struct EvalParams {
   int32_t gpn, policy;
   int32_t db_global;                 // database too large to stage: read it from global memory (L1/L2)
   // space
-  const lc_combo* combos; const int32_t* tmpl_n; const lc_entry* entries;
+  const lc_combo* combos; const int32_t* tmpl_n; const lc_entry* entries; int32_t sp_n_combos;
   int64_t hidden, topk, n_experts; int32_t is_moe, n_tp, n_ep;
   const int64_t* tp_vals; const int64_t* ep_vals; const uint8_t* pair_used; const int32_t* pair_canon;
   const TailTable* tail_tables; int32_t n_tail_tables;
@@ -420,6 +423,83 @@ __global__ void k_unit_offsets(SearchMeta* meta, int n_search, const int32_t* po
 #ifndef LC_TAIL_MIN_BLOCKS
 #define LC_TAIL_MIN_BLOCKS 4  // 64 registers: 32 warps per SM for the warp-per-tail radix select
 #endif
+// ---- K0 in closed form.  fits_memory (model.py:440-479) is monotone in the
+// batch size: the activation term grows with it, so the static footprint grows
+// and the KV budget shrinks, while the KV need grows -- and each step is a
+// monotone IEEE operation.  Over a search's sorted batch list the fitting
+// batches of a (tp,pp,ep,dp) combo are therefore a prefix, found by binary
+// search; the budget filter does not depend on the batch.  Units (the kept
+// candidates in the reference's order) are then a concatenation of prefixes.
+__global__ void k_enum_fit(EvalParams P, int64_t n_pairs, int32_t* counts, uint8_t* pair_inb, int32_t* cmax,
+                           int32_t n_tmpl) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n_pairs; p += (int64_t)gridDim.x * blockDim.x) {
+    const int s = (int)(p / P.sp_n_combos);
+    const int ci = (int)(p % P.sp_n_combos);
+    const lc_search_desc& S = P.searches[s];
+    const lc_combo c = P.combos[ci];
+    const bool force = (S.modes & LC_MODE_FORCE) != 0;
+    int nfit = S.n_b;
+    if (!force) {
+      int lo = 0, hi = S.n_b;  // first batch index that does not fit
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (fits_memory(c, S, P.gpu_memory, P.hidden, P.batches[S.b_off + mid])) lo = mid + 1;
+        else hi = mid;
+      }
+      nfit = lo;
+    }
+    const bool inb = force || in_budget(S, c.gpus);
+    const bool kept = inb || (S.modes & 4);  // workers skip the budget (search.py:323)
+    counts[p] = kept ? nfit : 0;
+    pair_inb[p] = inb ? 1 : 0;
+    if (kept && nfit > 0) {
+      int32_t* m = cmax + ((int64_t)s * n_tmpl + c.tmpl) * 2;
+      if (inb) atomicMax(&m[0], nfit);
+      if (S.modes & 4) atomicMax(&m[1], nfit);
+    }
+  }
+}
+
+// cell flags from the per-(search, template) prefix maxima: bit0 some in-budget
+// candidate, bit1 some pool worker (as k_enum_flags sets them tuple by tuple)
+__global__ void k_cell_flags_fit(EvalParams P, const int32_t* cmax, int32_t n_tmpl, uint32_t* cell_flags) {
+  const int s = blockIdx.y;
+  const lc_search_desc& S = P.searches[s];
+  const int64_t n = (int64_t)n_tmpl * S.n_b;
+  const int64_t off = P.meta[s].cell_off;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(x / S.n_b), bi = (int)(x % S.n_b);
+    const int32_t* m = cmax + ((int64_t)s * n_tmpl + t) * 2;
+    cell_flags[off + x] = (bi < m[0] ? 1u : 0u) | (bi < m[1] ? 2u : 0u);
+  }
+}
+
+// one block per (search, combo): its kept prefix of batch indices, in order
+__global__ void k_scatter_fit(EvalParams P, int64_t n_pairs, const int32_t* offs, const uint8_t* pair_inb,
+                              int32_t* u_search, int32_t* u_combo, int32_t* u_batch, uint8_t* u_budget) {
+  for (int64_t p = blockIdx.x; p < n_pairs; p += gridDim.x) {
+    const int32_t o = offs[p], n = offs[p + 1] - o;
+    if (n <= 0) continue;
+    const int s = (int)(p / P.sp_n_combos);
+    const int ci = (int)(p % P.sp_n_combos);
+    const uint8_t inb = pair_inb[p];
+    for (int bi = threadIdx.x; bi < n; bi += blockDim.x) {
+      u_search[o + bi] = s;
+      u_combo[o + bi] = ci;
+      u_batch[o + bi] = bi;
+      u_budget[o + bi] = inb;
+    }
+  }
+}
+
+__global__ void k_unit_offsets_fit(SearchMeta* meta, int n_search, int32_t n_combos, const int32_t* offs) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n_search) return;
+  const int32_t a = offs[(int64_t)s * n_combos], b = offs[(int64_t)(s + 1) * n_combos];
+  meta[s].unit_off = a;
+  meta[s].n_units = b - a;
+}
+
 // ---- K3: MoE tails table [type P/D/M][tp_i][ep_i][b_i] per search
 template <int PER>
 __global__ void __launch_bounds__(256, LC_TAIL_MIN_BLOCKS) k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
@@ -2016,7 +2096,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->pinned_front) cudaFreeHost(c->pinned_front);
@@ -2171,7 +2251,7 @@ static EvalParams make_params(lc_ctx* c) {
   for (int i = 0; i < 4; ++i) P.compute[i] = db->compute[i];
   P.gpn = db->gpn; P.policy = db->policy;
   P.db_global = db->staged ? 0 : 1;
-  P.combos = sp->combos; P.tmpl_n = sp->tmpl_n; P.entries = sp->entries;
+  P.combos = sp->combos; P.tmpl_n = sp->tmpl_n; P.entries = sp->entries; P.sp_n_combos = sp->n_combos;
   P.hidden = sp->hidden; P.topk = sp->topk; P.n_experts = sp->n_experts; P.is_moe = sp->is_moe;
   P.n_tp = sp->n_tp; P.n_ep = sp->n_ep; P.tp_vals = sp->tp_vals; P.ep_vals = sp->ep_vals; P.pair_used = sp->pair_used;
   P.pair_canon = sp->pair_canon;
@@ -2377,7 +2457,56 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   return LC_OK;
 }
 
+static int run_enum_fit(lc_ctx* c) {
+  cudaError_t err = cudaSuccess;
+  const int64_t n_raw = c->n_raw;
+  const int32_t nc = c->sp->n_combos, nt = c->sp->n_tmpl;
+  const int64_t n_pairs = (int64_t)c->n_search * nc;
+  int32_t* bs = c->block_sums.get<int32_t>(n_pairs + 1, &err);
+  uint8_t* inb = c->pair_inb.get<uint8_t>(n_pairs > 0 ? n_pairs : 1, &err);
+  int32_t* cmax = c->cmax.get<int32_t>((size_t)c->n_search * (nt > 0 ? nt : 1) * 2 + 1, &err);
+  uint32_t* cflags = c->cell_flags.get<uint32_t>(c->n_cells, &err);
+  c->n_cap = n_raw;
+  int32_t* us = c->u_search.get<int32_t>(n_raw, &err);
+  int32_t* uc = c->u_combo.get<int32_t>(n_raw, &err);
+  int32_t* ub = c->u_batch.get<int32_t>(n_raw, &err);
+  uint8_t* ubud = c->u_budget.get<uint8_t>(n_raw, &err);
+  if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
+  EvalParams P = make_params(c);
+  const int sms = sm_count(c->device);
+  c->n_total_idx = n_pairs;
+  if (n_pairs == 0) {
+    CK(cudaMemsetAsync(bs, 0, sizeof(int32_t), c->stream));
+  } else {
+    CK(cudaMemsetAsync(cmax, 0, sizeof(int32_t) * (size_t)c->n_search * (nt > 0 ? nt : 1) * 2, c->stream));
+    int blocks = (int)((n_pairs + 127) / 128);
+    if (blocks > sms * 8) blocks = sms * 8;
+    ++c->launches;
+    k_enum_fit<<<blocks, 128, 0, c->stream>>>(P, n_pairs, bs, inb, cmax, nt);
+    if (c->n_cells) {
+      int32_t nbmax = 1;
+      for (int s = 0; s < c->n_search; ++s) nbmax = c->hsearch_nb[s] > nbmax ? c->hsearch_nb[s] : nbmax;
+      const int64_t per = (int64_t)nt * nbmax;
+      int bx = (int)((per + 255) / 256);
+      if (bx > 64) bx = 64;
+      ++c->launches;
+      k_cell_flags_fit<<<dim3(bx, c->n_search), 256, 0, c->stream>>>(P, cmax, nt, cflags);
+    }
+    ++c->launches;
+    k_scan_top<<<1, 1024, 0, c->stream>>>(bs, (int)n_pairs);
+    ++c->launches;
+    int sb = (int)(n_pairs < (int64_t)sms * 32 ? n_pairs : (int64_t)sms * 32);
+    k_scatter_fit<<<sb, 128, 0, c->stream>>>(P, n_pairs, bs, inb, us, uc, ub, ubud);
+    CK(cudaGetLastError());
+  }
+  ++c->launches;
+  k_unit_offsets_fit<<<(c->n_search + 127) / 128, 128, 0, c->stream>>>((SearchMeta*)c->meta.p, c->n_search, nc, bs);
+  CK(cudaGetLastError());
+  return LC_OK;
+}
+
 static int run_enum(lc_ctx* c) {
+  if (c->batches_sorted && c->filt_hi < 0 && !getenv("LC_ENUM_FLAGS")) return run_enum_fit(c);
   cudaError_t err = cudaSuccess;
   const int64_t n_raw = c->n_raw;
   const int64_t nblk = (n_raw + kScanBlock - 1) / kScanBlock;
@@ -2435,6 +2564,15 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   c->n_loads = n_loads;
   // host bookkeeping: raw tuple, tail and plan offsets
   c->hmeta.assign(n_search, SearchMeta{});
+  c->batches_sorted = true;
+  c->hsearch_nb.assign(n_search, 0);
+  for (int s = 0; s < n_search; ++s) {
+    const lc_search_desc& S = searches[s];
+    c->hsearch_nb[s] = S.n_b;
+    if (S.b_off < 0 || S.n_b < 0 || S.b_off + S.n_b > n_batches) continue;  // rejected below
+    for (int j = 1; j < S.n_b; ++j)
+      if (batches[S.b_off + j] < batches[S.b_off + j - 1]) c->batches_sorted = false;
+  }
   int64_t raw = 0, tails = 0, plans = 0, cells = 0, qts = 0, dss = 0;
   for (int s = 0; s < n_search; ++s) {
     const lc_search_desc& S = searches[s];
