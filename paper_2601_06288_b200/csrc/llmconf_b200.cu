@@ -228,6 +228,8 @@ struct lc_ctx {
   bool staged = false;  // fronts + plans of the last batch already copied to the pinned buffers
   bool batches_sorted = false;  // every search's batch list is non-decreasing: K0 in closed form
   std::vector<int32_t> hsearch_nb;
+  unsigned char* arena = nullptr;  // page-locked staging for the batch's inputs and summaries
+  size_t arena_cap = 0, arena_used = 0;
   DBuf pair_inb, cmax;          // K0 closed form: per (search, combo) budget flag; per (search, template) fit maxima
   std::vector<QtGroup> hqt;
   std::vector<lc_search_result> hres;
@@ -2102,6 +2104,7 @@ int lc_close(lc_ctx* c) {
   if (c->pinned_front) cudaFreeHost(c->pinned_front);
   if (c->pinned_plans_i) cudaFreeHost(c->pinned_plans_i);
   if (c->pinned_plans_d) cudaFreeHost(c->pinned_plans_d);
+  if (c->arena) cudaFreeHost(c->arena);
   cudaStreamDestroy(c->stream);
   delete c;
   return LC_OK;
@@ -2751,22 +2754,34 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   c->sd.get<SdOut>(c->n_series ? (size_t)cells : 0, &err);
   c->results.get<lc_search_result>(n_search, &err);
   if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
-  if (n_search) CK(cudaMemcpyAsync(dS, searches, sizeof(lc_search_desc) * n_search, cudaMemcpyHostToDevice, c->stream));
-  if (n_batches) CK(cudaMemcpyAsync(dB, batches, sizeof(int64_t) * n_batches, cudaMemcpyHostToDevice, c->stream));
-  if (n_loads && sp->n_experts)
-    CK(cudaMemcpyAsync(dL, loads, sizeof(double) * n_loads * 2 * sp->n_experts, cudaMemcpyHostToDevice, c->stream));
-  if (n_search)
-    CK(cudaMemcpyAsync(dM, c->hmeta.data(), sizeof(SearchMeta) * n_search, cudaMemcpyHostToDevice, c->stream));
-  if (!c->htables.empty())
-    CK(cudaMemcpyAsync(dT, c->htables.data(), sizeof(TailTable) * c->htables.size(), cudaMemcpyHostToDevice,
-                       c->stream));
-  if (!c->hds.empty())
-    CK(cudaMemcpyAsync(dG, c->hds.data(), sizeof(DsGroup) * c->hds.size(), cudaMemcpyHostToDevice, c->stream));
-  if (!c->hqt.empty())
-    CK(cudaMemcpyAsync(dQ, c->hqt.data(), sizeof(QtGroup) * c->hqt.size(), cudaMemcpyHostToDevice, c->stream));
-  if (!c->hsg.empty()) {
-    CK(cudaMemcpyAsync(dSG, c->hsg.data(), sizeof(SeriesGroup) * c->hsg.size(), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(dSM, c->hsm.data(), sizeof(SeriesMember) * c->hsm.size(), cudaMemcpyHostToDevice, c->stream));
+  // inputs go through one page-locked arena so every H2D copy is asynchronous
+  {
+    const size_t sizes[9] = {sizeof(lc_search_desc) * n_search, sizeof(int64_t) * n_batches,
+                             (n_loads && sp->n_experts) ? sizeof(double) * n_loads * 2 * sp->n_experts : 0,
+                             sizeof(SearchMeta) * n_search, sizeof(TailTable) * c->htables.size(),
+                             sizeof(DsGroup) * c->hds.size(), sizeof(QtGroup) * c->hqt.size(),
+                             sizeof(SeriesGroup) * c->hsg.size(), sizeof(SeriesMember) * c->hsm.size()};
+    const void* srcs[9] = {searches, batches, loads, c->hmeta.data(), c->htables.data(), c->hds.data(),
+                           c->hqt.data(), c->hsg.data(), c->hsm.data()};
+    void* dsts[9] = {dS, dB, dL, dM, dT, dG, dQ, dSG, dSM};
+    size_t need = 0;
+    for (int k = 0; k < 9; ++k) need += (sizes[k] + 255) & ~(size_t)255;
+    need += (sizeof(lc_search_result) + sizeof(SearchMeta)) * (size_t)n_search + 1024;  // summaries coming back
+    if (c->arena_cap < need) {
+      if (c->arena) cudaFreeHost(c->arena);
+      c->arena = nullptr;
+      c->arena_cap = 0;
+      CK(cudaHostAlloc((void**)&c->arena, need, cudaHostAllocDefault));
+      c->arena_cap = need;
+    }
+    size_t off = 0;
+    for (int k = 0; k < 9; ++k) {
+      if (!sizes[k]) continue;
+      memcpy(c->arena + off, srcs[k], sizes[k]);
+      CK(cudaMemcpyAsync(dsts[k], c->arena + off, sizes[k], cudaMemcpyHostToDevice, c->stream));
+      off += (sizes[k] + 255) & ~(size_t)255;
+    }
+    c->arena_used = off;
   }
   CK(cudaEventRecord(c->ev[0], c->stream));
   c->launches = 0;
@@ -2808,15 +2823,22 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     c->staged = true;
   }
   c->hres.resize(n_search);
-  if (n_search)
-    CK(cudaMemcpyAsync(c->hres.data(), c->results.p, sizeof(lc_search_result) * n_search, cudaMemcpyDeviceToHost,
-                       c->stream));
-  if (n_search)
-    CK(cudaMemcpyAsync(c->hmeta.data(), c->meta.p, sizeof(SearchMeta) * n_search, cudaMemcpyDeviceToHost, c->stream));
-  int32_t total_units = 0;
-  CK(cudaMemcpyAsync(&total_units, (const int32_t*)c->block_sums.p + c->n_total_idx, sizeof(int32_t),
+  unsigned char* back = c->arena + c->arena_used;  // page-locked landing zone for the summaries
+  lc_search_result* pres = (lc_search_result*)back;
+  SearchMeta* pmeta = (SearchMeta*)(back + ((sizeof(lc_search_result) * (size_t)n_search + 255) & ~(size_t)255));
+  int32_t* ptotal = (int32_t*)((unsigned char*)pmeta + ((sizeof(SearchMeta) * (size_t)n_search + 255) & ~(size_t)255));
+  if (n_search) {
+    CK(cudaMemcpyAsync(pres, c->results.p, sizeof(lc_search_result) * n_search, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(pmeta, c->meta.p, sizeof(SearchMeta) * n_search, cudaMemcpyDeviceToHost, c->stream));
+  }
+  CK(cudaMemcpyAsync(ptotal, (const int32_t*)c->block_sums.p + c->n_total_idx, sizeof(int32_t),
                      cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  if (n_search) {
+    memcpy(c->hres.data(), pres, sizeof(lc_search_result) * n_search);
+    memcpy(c->hmeta.data(), pmeta, sizeof(SearchMeta) * n_search);
+  }
+  const int32_t total_units = *ptotal;
   c->n_units = total_units;
   int64_t nfront = 0, nplan = 0;
   for (int s = 0; s < n_search; ++s) {
