@@ -216,32 +216,42 @@ class Engine:
         load_ix: dict = {}
         if space.prefill_pool_cap < 0 or space.decode_pool_cap < 0:
             raise SearchError("pool caps must be >= 0")
-        # per-search fields gathered in lists, written column-wise
-        isl, osl, prefix, has_ttft, ttft, has_floor, floor_v, cap_v = [], [], [], [], [], [], [], []
-        modes_v, b_off, n_b, load_v = [], [], [], []
-        budget_rows = np.zeros((n, N.LC_MAX_BUDGETS), dtype=np.int64)
-        n_budgets = np.zeros(n, dtype=np.int32)
-        for i, w in enumerate(workloads):
-            isl.append(w.isl)
-            osl.append(w.osl)
-            prefix.append(w.prefix_len)
-            has_ttft.append(w.ttft_limit_ms is not None)
-            ttft.append(float(w.ttft_limit_ms) if w.ttft_limit_ms is not None else 0.0)
-            fl = w.speed_floor()
-            has_floor.append(fl is not None)
-            floor_v.append(float(fl) if fl is not None else 0.0)
-            cap_v.append(float(w.tpot_ceiling()) if fl is not None else 0.0)
-            if mode_override is not None:
-                modes_v.append(mode_override)
-            else:
-                modes_v.append((MODE_STATIC if "static" in w.modes else 0) | (MODE_AGG if "aggregated" in w.modes else 0)
-                               | (MODE_DISAGG if "disaggregated" in w.modes else 0) | mode_extra)
-            if enforce_budget and w.gpu_budgets:
-                budgets = sorted(set(w.gpu_budgets))
-                if len(budgets) > N.LC_MAX_BUDGETS:
-                    raise SearchError(f"at most {N.LC_MAX_BUDGETS} distinct gpu budgets are supported")
-                n_budgets[i] = len(budgets)
-                budget_rows[i, : len(budgets)] = budgets
+        # per-search fields written column-wise (one comprehension per field)
+        ws = list(workloads)
+        floors = [w.speed_floor() for w in ws]
+        ttfts = [w.ttft_limit_ms for w in ws]
+        searches["isl"] = [w.isl for w in ws]
+        searches["osl"] = [w.osl for w in ws]
+        searches["prefix"] = [w.prefix_len for w in ws]
+        searches["has_ttft"] = [t is not None for t in ttfts]
+        searches["ttft_limit"] = [float(t) if t is not None else 0.0 for t in ttfts]
+        searches["has_floor"] = [f is not None for f in floors]
+        searches["speed_floor"] = [float(f) if f is not None else 0.0 for f in floors]
+        searches["tpot_cap"] = [float(w.tpot_ceiling()) if f is not None else 0.0 for w, f in zip(ws, floors)]
+        if mode_override is not None:
+            searches["modes"] = mode_override
+        else:
+            mode_of: dict = {}
+            modes_v = []
+            for w in ws:
+                m = mode_of.get(w.modes)
+                if m is None:
+                    m = mode_of[w.modes] = ((MODE_STATIC if "static" in w.modes else 0)
+                                            | (MODE_AGG if "aggregated" in w.modes else 0)
+                                            | (MODE_DISAGG if "disaggregated" in w.modes else 0) | mode_extra)
+                modes_v.append(m)
+            searches["modes"] = modes_v
+        if enforce_budget:
+            budget_rows = searches["budgets"]
+            for i, w in enumerate(ws):
+                if w.gpu_budgets:
+                    budgets = sorted(set(w.gpu_budgets))
+                    if len(budgets) > N.LC_MAX_BUDGETS:
+                        raise SearchError(f"at most {N.LC_MAX_BUDGETS} distinct gpu budgets are supported")
+                    searches["n_budgets"][i] = len(budgets)
+                    budget_rows[i, : len(budgets)] = budgets
+        b_off, n_b, load_v = [], [], []
+        for w in ws:
             src = w.batch_sweep or space.batch_values
             key = (id(src), len(src)) if isinstance(src, tuple) else tuple(src)
             off = b_index.get(key)
@@ -255,21 +265,17 @@ class Engine:
                 b_index[key] = off
             b_off.append(off)
             n_b.append(len(src))
-            ld = -1
-            if plan.is_moe:
+        if plan.is_moe:
+            for w in ws:
                 params = w.moe_load if w.moe_load is not None else DEFAULT_MOE_LOAD
                 lk = (params.alpha, params.x_min, params.x_max, params.seed)
-                if lk not in load_ix:
-                    load_ix[lk] = len(loads)
+                ld = load_ix.get(lk)
+                if ld is None:
+                    ld = load_ix[lk] = len(loads)
                     loads.append(_moe_q(params, plan.n_experts))
-                ld = load_ix[lk]
-            load_v.append(ld)
-        searches["isl"], searches["osl"], searches["prefix"] = isl, osl, prefix
-        searches["has_ttft"], searches["ttft_limit"] = has_ttft, ttft
-        searches["has_floor"], searches["speed_floor"], searches["tpot_cap"] = has_floor, floor_v, cap_v
-        searches["modes"] = modes_v
-        searches["n_budgets"] = n_budgets
-        searches["budgets"] = budget_rows
+                load_v.append(ld)
+        else:
+            load_v = -1
         searches["b_off"], searches["n_b"] = b_off, n_b
         searches["has_ctx_capacity"] = space.ctx_capacity is not None
         searches["ctx_capacity"] = space.ctx_capacity or 0
