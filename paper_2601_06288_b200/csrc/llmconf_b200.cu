@@ -894,7 +894,10 @@ __device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta&
 // Non-attention terms come from the decode-step query slots (same tokens at every
 // sample), attention from the decode-series table.  For each member the result is
 // its partial sum after n_steps - 1 samples plus the last sample times its run.
-__global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_dseries(EvalParams P) {
+#ifndef LC_DSERIES_MIN_BLOCKS
+#define LC_DSERIES_MIN_BLOCKS 6  // 80 registers (measured slightly better than 64 / 8 blocks)
+#endif
+__global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalParams P) {
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < P.n_series;
        x += (int64_t)gridDim.x * blockDim.x) {
     int lo = 0, hi = P.n_sgroups - 1;
@@ -1127,7 +1130,10 @@ __global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalPara
 
 // K2b: candidates from their cells -- derive_metrics with the candidate's gpu
 // count (serving_modes.py:161-172) and the pool rates (serving_modes.py:366, 380).
-__global__ void __launch_bounds__(256) k_expand(EvalParams P) {
+#ifndef LC_EXPAND_MIN_BLOCKS
+#define LC_EXPAND_MIN_BLOCKS 4  // 64 registers (measured: 4.11 -> 4.00 ms per step)
+#endif
+__global__ void __launch_bounds__(256, LC_EXPAND_MIN_BLOCKS) k_expand(EvalParams P) {
   const int64_t n = P.n_cap;
   const int64_t total = *P.d_total;
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
@@ -1473,7 +1479,10 @@ struct FrontCand {
 };
 
 constexpr int kSurvivorCap = 2048;  // front candidates kept in shared memory
-constexpr int kFrontThreads = 256;
+#ifndef LC_FRONT_THREADS
+#define LC_FRONT_THREADS 256
+#endif
+constexpr int kFrontThreads = LC_FRONT_THREADS;
 constexpr int kSpeedBuckets = 4096;
 
 // Exact staircase over a row subset sorted by (speed desc, row key asc): the
