@@ -151,6 +151,21 @@ struct SdOut {
   int64_t c0, c1;                 // failing query coordinates
 };
 
+// Prefill steps shared by the searches of one prefill query-table group: the
+// step's inputs (context, batch list, MoE load -> tails, query table) are the
+// group key, so its total is the same for every member (estimator.py:71-110).
+struct PGroup {
+  int64_t off;   // first entry: [template][b_i]
+  int32_t rep;   // representative search
+  int32_t n_b;
+};
+struct PStep {
+  double total;
+  int32_t status;  // code | label << 8
+  int32_t q;       // query counts q1 | q2 << 16
+  int64_t c0, c1;  // failing query coordinates
+};
+
 // one priced query (query tables and decode-series tables)
 struct QVal {
   double lat;
@@ -189,6 +204,7 @@ struct SearchMeta {
   int32_t plan_off, plan_cap;
   int32_t pool_off;  // into pool selection arrays (64 slots per role)
   int32_t n_pre, n_dec;
+  int64_t pstep_off;  // this search's prefill-group table of step totals (PStep), -1 none
 };
 
 struct lc_ctx {
@@ -202,6 +218,9 @@ struct lc_ctx {
   DBuf pool_key, qt_groups, ds_groups, front_compact, pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   DBuf q_in, q_lat, q_st;  // lc_query_batch
   DBuf sgroups, smembers, sd;  // shared static decode loops
+  DBuf pgroups, psteps;        // shared prefill step totals
+  std::vector<PGroup> hpg;
+  int64_t n_pstep = 0;
   DBuf raw_mask;               // lc_set_raw_filter: optional keep-mask over [filt_lo, filt_hi)
   int64_t filt_lo = 0, filt_hi = -1;  // filt_hi < 0: no raw-tuple filter
   bool filt_mask = false;
@@ -264,6 +283,7 @@ struct EvalParams {
   QVal* ds; int64_t n_ds;
   const DsGroup* ds_groups; int32_t n_ds_groups;
   const SeriesGroup* sgroups; int32_t n_sgroups; const SeriesMember* smembers; SdOut* sd; int64_t n_series;
+  const PGroup* pgroups; int32_t n_pgroups; PStep* psteps; int64_t n_pstep;
   // batch
   const lc_search_desc* searches; const SearchMeta* meta; int32_t n_search;
   int64_t raw_lo, raw_hi; const uint8_t* raw_mask;  // raw-tuple filter (sharded searches)
@@ -1011,6 +1031,47 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
   }
 }
 
+// K2a'': prefill step totals, one thread per (prefill group, template, batch);
+// k_eval_cells reads them instead of re-summing the step for every member.
+__global__ void __launch_bounds__(128) k_ptables(EvalParams P) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < P.n_pstep;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    int lo = 0, hi = P.n_pgroups - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.pgroups[mid].off <= x) lo = mid;
+      else hi = mid - 1;
+    }
+    const PGroup G = P.pgroups[lo];
+    const lc_search_desc& S = P.searches[G.rep];
+    const SearchMeta& M = P.meta[G.rep];
+    const int64_t rel = x - G.off;
+    const int tmpl = (int)(rel / G.n_b), bi = (int)(rel % G.n_b);
+    const TmplInfo ti = P.tmpl_info[tmpl];
+    lc_combo c;
+    c.tp = ti.tp; c.pp = ti.pp; c.ep = ti.ep; c.tp_i = ti.tp_i; c.ep_i = ti.ep_i;
+    const lc_entry* E = P.entries + (int64_t)tmpl * LC_MAX_ENTRIES;
+    const int ne = P.tmpl_n[tmpl];
+    const int32_t* so = P.slot_of + (int64_t)tmpl * LC_MAX_ENTRIES * 3;
+    const int64_t b = P.batches[S.b_off + bi];
+    const int64_t mb = b > 1 ? b : 1;
+    const double bubble = (double)(mb + ti.pp - 1) / (double)mb;
+    const int64_t chunk = S.isl - S.prefix;
+    const StepArgs a{PH_PREFILL, b * chunk, 0, chunk, expert_tokens(P, c, M, S, 0, bi, b * chunk)};
+    double total = 0.0;
+    ErrRec err{0, 0, 0, 0};
+    int q1 = 0, q2 = 0;
+    table_step(P, M, E, ne, so + LC_STEP_PREFILL, S.n_b, bi, a, bubble, &total, &err, &q1, &q2);
+    PStep o;
+    o.total = total;
+    o.status = err.code | (err.label << 8);
+    o.q = err.code ? 0 : ((q1 & 0xffff) | (q2 << 16));
+    o.c0 = err.c0;
+    o.c1 = err.c1;
+    P.psteps[x] = o;
+  }
+}
+
 // K2: one thread per cell assembles every step from the tables.
 __global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalParams P) {
   const int64_t ncell = P.n_cells_total;
@@ -1047,9 +1108,16 @@ __global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalPara
     double p_total = 0.0;
     ErrRec p_err{0, 0, 0, 0};
     if (do_st || do_dg) {
-      const StepArgs a{PH_PREFILL, b * chunk, 0, chunk, expert_tokens(P, c, M, S, 0, bi, b * chunk)};
-      table_step(P, M, E, ne, so + LC_STEP_PREFILL, S.n_b, bi, a, bubble, &p_total, &p_err, &q1, &q2);
-      if (!p_err.code) o.qP = (q1 & 0xffff) | (q2 << 16);
+      if (M.pstep_off >= 0) {  // shared with the other searches of the prefill group (k_ptables)
+        const PStep ps = P.psteps[M.pstep_off + rel];
+        p_total = ps.total;
+        p_err.code = ps.status & 0xff; p_err.label = ps.status >> 8; p_err.c0 = ps.c0; p_err.c1 = ps.c1;
+        o.qP = ps.q;
+      } else {
+        const StepArgs a{PH_PREFILL, b * chunk, 0, chunk, expert_tokens(P, c, M, S, 0, bi, b * chunk)};
+        table_step(P, M, E, ne, so + LC_STEP_PREFILL, S.n_b, bi, a, bubble, &p_total, &p_err, &q1, &q2);
+        if (!p_err.code) o.qP = (q1 & 0xffff) | (q2 << 16);
+      }
       o.pf_status = p_err.code | (p_err.label << 8);
       o.pf_lat = p_total;
       if (p_err.code) put_cell_err(P, 2, ci, p_err);
@@ -2107,7 +2175,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->pinned_front) cudaFreeHost(c->pinned_front);
@@ -2282,6 +2350,8 @@ static EvalParams make_params(lc_ctx* c) {
   P.ds_groups = (const DsGroup*)c->ds_groups.p; P.n_ds_groups = (int32_t)c->hds.size();
   P.sgroups = (const SeriesGroup*)c->sgroups.p; P.n_sgroups = (int32_t)c->hsg.size();
   P.smembers = (const SeriesMember*)c->smembers.p; P.sd = (SdOut*)c->sd.p; P.n_series = c->n_series;
+  P.pgroups = (const PGroup*)c->pgroups.p; P.n_pgroups = (int32_t)c->hpg.size();
+  P.psteps = (PStep*)c->psteps.p; P.n_pstep = c->n_pstep;
   P.searches = (const lc_search_desc*)c->searches.p;
   P.meta = (const SearchMeta*)c->meta.p;
   P.n_search = c->n_search;
@@ -2401,6 +2471,13 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
     ++c->launches;
     k_dseries<<<(int)blocks, 128, 0, c->stream>>>(P);
+    CK(cudaGetLastError());
+  }
+  if (c->n_pstep > 0) {
+    int64_t blocks = (c->n_pstep + 127) / 128;
+    if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
+    ++c->launches;
+    k_ptables<<<(int)blocks, 128, 0, c->stream>>>(P);
     CK(cudaGetLastError());
   }
   if (c->n_cells > 0) {
@@ -2665,6 +2742,27 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
       }
     }
   }
+  // prefill step tables: one per class-0 query-table group
+  c->hpg.clear();
+  c->n_pstep = 0;
+  for (int s = 0; s < n_search; ++s) c->hmeta[s].pstep_off = -1;
+  {
+    std::map<int64_t, int64_t> by_table;  // qt offset of the group's table -> pstep offset
+    for (int s = 0; s < n_search; ++s) {
+      const lc_search_desc& S = searches[s];
+      if (!(S.modes & 5) || !sp->class_n[0]) continue;
+      const int64_t key = c->hmeta[s].qt_off[0];
+      auto it = by_table.find(key);
+      if (it == by_table.end()) {
+        by_table[key] = c->n_pstep;
+        c->hpg.push_back(PGroup{c->n_pstep, s, S.n_b});
+        c->hmeta[s].pstep_off = c->n_pstep;
+        c->n_pstep += (int64_t)sp->n_tmpl * S.n_b;
+      } else {
+        c->hmeta[s].pstep_off = it->second;
+      }
+    }
+  }
   // decode-series groups: the KV samples isl + 32k + 1 do not depend on osl
   c->hds.clear();
   {
@@ -2760,21 +2858,24 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   QtGroup* dQ = c->qt_groups.get<QtGroup>(c->hqt.size(), &err);
   SeriesGroup* dSG = c->sgroups.get<SeriesGroup>(c->hsg.size(), &err);
   SeriesMember* dSM = c->smembers.get<SeriesMember>(c->hsm.size(), &err);
+  PGroup* dPG = c->pgroups.get<PGroup>(c->hpg.size(), &err);
+  c->psteps.get<PStep>((size_t)c->n_pstep, &err);
   c->sd.get<SdOut>(c->n_series ? (size_t)cells : 0, &err);
   c->results.get<lc_search_result>(n_search, &err);
   if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
   // inputs go through one page-locked arena so every H2D copy is asynchronous
   {
-    const size_t sizes[9] = {sizeof(lc_search_desc) * n_search, sizeof(int64_t) * n_batches,
+    const size_t sizes[10] = {sizeof(lc_search_desc) * n_search, sizeof(int64_t) * n_batches,
                              (n_loads && sp->n_experts) ? sizeof(double) * n_loads * 2 * sp->n_experts : 0,
                              sizeof(SearchMeta) * n_search, sizeof(TailTable) * c->htables.size(),
                              sizeof(DsGroup) * c->hds.size(), sizeof(QtGroup) * c->hqt.size(),
-                             sizeof(SeriesGroup) * c->hsg.size(), sizeof(SeriesMember) * c->hsm.size()};
-    const void* srcs[9] = {searches, batches, loads, c->hmeta.data(), c->htables.data(), c->hds.data(),
-                           c->hqt.data(), c->hsg.data(), c->hsm.data()};
-    void* dsts[9] = {dS, dB, dL, dM, dT, dG, dQ, dSG, dSM};
+                             sizeof(SeriesGroup) * c->hsg.size(), sizeof(SeriesMember) * c->hsm.size(),
+                             sizeof(PGroup) * c->hpg.size()};
+    const void* srcs[10] = {searches, batches, loads, c->hmeta.data(), c->htables.data(), c->hds.data(),
+                            c->hqt.data(), c->hsg.data(), c->hsm.data(), c->hpg.data()};
+    void* dsts[10] = {dS, dB, dL, dM, dT, dG, dQ, dSG, dSM, dPG};
     size_t need = 0;
-    for (int k = 0; k < 9; ++k) need += (sizes[k] + 255) & ~(size_t)255;
+    for (int k = 0; k < 10; ++k) need += (sizes[k] + 255) & ~(size_t)255;
     need += (sizeof(lc_search_result) + sizeof(SearchMeta)) * (size_t)n_search + 1024;  // summaries coming back
     if (c->arena_cap < need) {
       if (c->arena) cudaFreeHost(c->arena);
@@ -2784,7 +2885,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
       c->arena_cap = need;
     }
     size_t off = 0;
-    for (int k = 0; k < 9; ++k) {
+    for (int k = 0; k < 10; ++k) {
       if (!sizes[k]) continue;
       memcpy(c->arena + off, srcs[k], sizes[k]);
       CK(cudaMemcpyAsync(dsts[k], c->arena + off, sizes[k], cudaMemcpyHostToDevice, c->stream));
