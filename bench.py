@@ -372,7 +372,7 @@ def main() -> int:
     uniq_bytes = 32 * (tq - tq2) + 64 * tq2 + 112 * cands_local
     uniq_achieved = uniq_bytes / k2_s / 1e9 if k2_s > 0 else 0.0
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None, "kernel": "K2 stage (k_qtables + k_dstables + k_dseries + k_eval_cells + k_expand)",
+            "traffic": None, "kernel": "K2 stage (k_qtables + k_dstables + k_dseries + k_ptables + k_eval_cells + k_expand)",
             "peak_source": peak_kind,
             "algorithmic_bytes_per_launch": alg_bytes, "queries_1d": q1, "queries_2d": q2,
             "note": ("achieved uses SURVEY.md 8(d)'s gather model: 32/64 B per reference-equivalent 1-D/2-D "
@@ -390,11 +390,11 @@ def main() -> int:
         roof["fp64_peak_gflops_measured"] = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())[
             "fp64_fma_gflops"]
         ncu = {}
-        for name in ("r1_ncu_v9.json", "r1_ncu_v10.json"):  # v9: DeepSeek-V3 batch, v10: k_eval_cells
+        for name in ("r1_ncu_v9.json", "r1_ncu_v11.json"):  # v9: DeepSeek-V3 batch, v11: k_eval_cells
             ncu.update(json.loads((ROOT / "profiles" / name).read_text())["kernels"])
         roof["ncu_fp64_pipe_active_pct"] = {
             k: float(str(ncu[k].get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")).split()[0])
-            for k in ("k_qtables", "k_dstables", "k_dseries", "k_eval_cells", "k_expand") if k in ncu}
+            for k in ("k_qtables", "k_dstables", "k_dseries", "k_ptables", "k_eval_cells", "k_expand") if k in ncu}
     except Exception:
         pass
     prof = ROOT / "profiles" / "ncu_k2_traffic.json"
