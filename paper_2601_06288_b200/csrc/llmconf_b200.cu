@@ -207,6 +207,15 @@ struct SearchMeta {
   int64_t pstep_off;  // this search's prefill-group table of step totals (PStep), -1 none
 };
 
+// Per-search row accounting, accumulated by k_expand (static / aggregated rows)
+// and k_disagg (plan rows) for K4: counts (search.py:343-358 report counts),
+// query totals and the range of feasible speeds (IEEE bit patterns; the
+// minimum is kept complemented so that a zeroed record is the empty state).
+struct SearchAcc {
+  unsigned long long q1, q2, smin_c, smax;
+  int32_t feas, rows, enums, skips, fplans, _pad;
+};
+
 struct lc_ctx {
   int device;
   cudaStream_t stream;
@@ -219,6 +228,7 @@ struct lc_ctx {
   DBuf q_in, q_lat, q_st;  // lc_query_batch
   DBuf sgroups, smembers, sd;  // shared static decode loops
   DBuf pgroups, psteps;        // shared prefill step totals
+  DBuf acc;                    // SearchAcc per search
   std::vector<PGroup> hpg;
   int64_t n_pstep = 0;
   DBuf raw_mask;               // lc_set_raw_filter: optional keep-mask over [filt_lo, filt_hi)
@@ -308,6 +318,7 @@ struct EvalParams {
   int64_t* cell_err;                 // [cell][8]
   int64_t n_cells_total;
   lc_search_result* results;
+  SearchAcc* acc;                    // [n_search]
 };
 
 __device__ __forceinline__ int find_search(const SearchMeta* meta, int n, int64_t r) {
@@ -1201,11 +1212,45 @@ __global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalPara
 #ifndef LC_EXPAND_MIN_BLOCKS
 #define LC_EXPAND_MIN_BLOCKS 4  // 64 registers (measured: 4.11 -> 4.00 ms per step)
 #endif
+// Warp-aggregated per-search accounting: one set of atomics per warp when all
+// its units belong to one search (the common case), per lane otherwise.
+struct RowAcc {
+  unsigned q1, q2;
+  int feas, rows, enums, skips;
+  unsigned long long smin_c, smax;
+  __device__ __forceinline__ void feasible_speed(double speed) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(speed);
+    smax = b > smax ? b : smax;
+    smin_c = ~b > smin_c ? ~b : smin_c;
+  }
+};
+
+__device__ __forceinline__ void acc_flush(SearchAcc* A, const RowAcc& r) {
+  if (r.q1) atomicAdd(&A->q1, (unsigned long long)r.q1);
+  if (r.q2) atomicAdd(&A->q2, (unsigned long long)r.q2);
+  if (r.feas) atomicAdd(&A->feas, r.feas);
+  if (r.rows) atomicAdd(&A->rows, r.rows);
+  if (r.enums) atomicAdd(&A->enums, r.enums);
+  if (r.skips) atomicAdd(&A->skips, r.skips);
+  if (r.smax) atomicMax(&A->smax, r.smax);
+  if (r.smin_c) atomicMax(&A->smin_c, r.smin_c);
+}
+
 __global__ void __launch_bounds__(256, LC_EXPAND_MIN_BLOCKS) k_expand(EvalParams P) {
   const int64_t n = P.n_cap;
   const int64_t total = *P.d_total;
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += (int64_t)gridDim.x * blockDim.x) {
-    const int s = P.u_search[u];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  __shared__ RowAcc wacc[8];
+  for (int64_t bbase = blockIdx.x * (int64_t)blockDim.x; bbase < total; bbase += stride) {
+    const int64_t u = bbase + threadIdx.x;
+    // units are ordered by search: one set of atomics per block when it lies in one search
+    const int64_t last = (bbase + blockDim.x < total ? bbase + blockDim.x : total) - 1;
+    const bool block_uniform = P.u_search[bbase] == P.u_search[last];
+    RowAcc ra{0, 0, 0, 0, 0, 0, 0ull, 0ull};
+    int s = -1;
+    if (u < total) {
+    s = P.u_search[u];
     const lc_search_desc& S = P.searches[s];
     const int bi = P.u_batch[u];
     const lc_combo c = P.combos[P.u_combo[u]];
@@ -1224,6 +1269,11 @@ __global__ void __launch_bounds__(256, LC_EXPAND_MIN_BLOCKS) k_expand(EvalParams
         double speed, thru;
         derive_metrics(o.st_ttft, o.st_tpot, b, S.osl, c.gpus, &speed, &thru);
         P.st_v[u] = o.st_ttft; P.st_v[n + u] = o.st_tpot; P.st_v[2 * n + u] = speed; P.st_v[3 * n + u] = thru;
+        ++ra.rows;
+        if ((!S.has_ttft || o.st_ttft <= S.ttft_limit) && (!S.has_floor || speed >= S.speed_floor)) {
+          ++ra.feas;
+          ra.feasible_speed(speed);
+        }
         add_q(o.qSD);
       }
     }
@@ -1235,6 +1285,11 @@ __global__ void __launch_bounds__(256, LC_EXPAND_MIN_BLOCKS) k_expand(EvalParams
         double speed, thru;
         derive_metrics(o.ag_ttft, o.ag_tpot, b, S.osl, c.gpus, &speed, &thru);
         P.ag_v[u] = o.ag_ttft; P.ag_v[n + u] = o.ag_tpot; P.ag_v[2 * n + u] = speed; P.ag_v[3 * n + u] = thru;
+        ++ra.rows;
+        if ((!S.has_ttft || o.ag_ttft <= S.ttft_limit) && (!S.has_floor || speed >= S.speed_floor)) {
+          ++ra.feas;
+          ra.feasible_speed(speed);
+        }
       }
       add_q(o.qM);
     }
@@ -1265,6 +1320,55 @@ __global__ void __launch_bounds__(256, LC_EXPAND_MIN_BLOCKS) k_expand(EvalParams
     const bool dup = do_st && o.st_status == 0 && S.osl > 1 && k >= 0 && (k % 32) == 0 && (k / 32) < o.st_steps;
     if (((do_ag && (o.flags & 1)) || do_dg) && !dup) add_q(o.qG);
     P.u_queries[u] = q;
+    ra.q1 = (unsigned)(q & 0xffff);
+    ra.q2 = (unsigned)(q >> 16);
+    if (inb) {
+      ++ra.enums;
+      if ((S.modes & 1) && o.st_status) ++ra.skips;
+      if ((S.modes & 2) && o.ag_status) ++ra.skips;
+    }
+    if (do_dg) ra.skips += (o.pf_status != 0) + (o.dc_status != 0);
+    }
+    // per-search accounting for K4 (search.py:343-358 counts, speed range)
+    int s0 = __shfl_sync(0xffffffffu, s, 0);
+    if (s0 < 0) s0 = P.u_search[bbase];  // a warp entirely past the end of the units
+    if (__all_sync(0xffffffffu, s < 0 || s == s0)) {
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) {
+        ra.q1 += __shfl_xor_sync(0xffffffffu, ra.q1, o2);
+        ra.q2 += __shfl_xor_sync(0xffffffffu, ra.q2, o2);
+        ra.feas += __shfl_xor_sync(0xffffffffu, ra.feas, o2);
+        ra.rows += __shfl_xor_sync(0xffffffffu, ra.rows, o2);
+        ra.enums += __shfl_xor_sync(0xffffffffu, ra.enums, o2);
+        ra.skips += __shfl_xor_sync(0xffffffffu, ra.skips, o2);
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, ra.smax, o2);
+        const unsigned long long m = __shfl_xor_sync(0xffffffffu, ra.smin_c, o2);
+        ra.smax = a > ra.smax ? a : ra.smax;
+        ra.smin_c = m > ra.smin_c ? m : ra.smin_c;
+      }
+      if (block_uniform) {
+        if (lane == 0) wacc[warp] = ra;
+      } else if (lane == 0) {
+        acc_flush(P.acc + s0, ra);
+      }
+    } else if (s >= 0) {
+      acc_flush(P.acc + s, ra);
+    }
+    if (block_uniform) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        RowAcc t = wacc[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+          const RowAcc& o2 = wacc[w];
+          t.q1 += o2.q1; t.q2 += o2.q2; t.feas += o2.feas; t.rows += o2.rows; t.enums += o2.enums;
+          t.skips += o2.skips;
+          t.smax = o2.smax > t.smax ? o2.smax : t.smax;
+          t.smin_c = o2.smin_c > t.smin_c ? o2.smin_c : t.smin_c;
+        }
+        acc_flush(P.acc + P.u_search[bbase], t);
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -1412,8 +1516,20 @@ __global__ void __launch_bounds__(1024) k_disagg(EvalParams P, SearchMeta* meta,
     plan_i[slot * 4 + 0] = a.p; plan_i[slot * 4 + 1] = a.d; plan_i[slot * 4 + 2] = a.x; plan_i[slot * 4 + 3] = a.y;
     plan_d[slot * 6 + 0] = (double)a.gpus; plan_d[slot * 6 + 1] = a.r_sys; plan_d[slot * 6 + 2] = a.ttft;
     plan_d[slot * 6 + 3] = a.tpot; plan_d[slot * 6 + 4] = a.speed; plan_d[slot * 6 + 5] = a.thru;
+    // plan rows in the per-search accounting (k_expand covers the other rows)
+    if ((!S.has_ttft || a.ttft <= S.ttft_limit) && (!S.has_floor || a.speed >= S.speed_floor)) {
+      SearchAcc* A = P.acc + s;
+      atomicAdd(&A->feas, 1);
+      atomicAdd(&A->fplans, 1);
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(a.speed);
+      atomicMax(&A->smax, bits);
+      atomicMax(&A->smin_c, ~bits);
+    }
   }
-  if (threadIdx.x == 0) results[s].n_plans = nplan;
+  if (threadIdx.x == 0) {
+    results[s].n_plans = nplan;
+    if (nplan) atomicAdd(&P.acc[s].rows, nplan);
+  }
 }
 
 // ---- K4: feasibility, Pareto front, best, nearest miss (block per search)
@@ -1610,14 +1726,10 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
 #ifndef LC_FRONT_SPLIT
 #define LC_FRONT_SPLIT 64
 #endif
-#ifndef LC_FRONT_SPLIT1
-#define LC_FRONT_SPLIT1 16
-#endif
 #ifndef LC_POOL_SPLIT
 #define LC_POOL_SPLIT 16
 #endif
 constexpr int kSplit = LC_FRONT_SPLIT;     // blocks per search for the Pareto passes
-constexpr int kSplit1 = LC_FRONT_SPLIT1;   // blocks per search for the first (counting / best) pass
 constexpr int kPoolSplit = LC_POOL_SPLIT;  // blocks per search for the pool top-k
 constexpr int kCompactFront = 2048;  // fixed-stride copy of each front for one-shot D2H (= survivor cap)
 
@@ -1760,118 +1872,15 @@ __global__ void k_pools_final(EvalParams P, SearchMeta* meta, const PoolPartial*
   }
 }
 
-struct FrontPartial {
-  BestKey best;
-  unsigned long long smin, smax, q1, q2;
-  int32_t feas, rows, enums, skips, fplans, _pad;
-};
 
 struct FrontMeta {
   int32_t shift, any;
   unsigned long long base;
 };
 
-__device__ __forceinline__ BestKey shfl_best(const BestKey& k, int src) {
-  BestKey o;
-  o.nthru = __shfl_sync(0xffffffffu, k.nthru, src);
-  o.nspeed = __shfl_sync(0xffffffffu, k.nspeed, src);
-  o.gpus = __shfl_sync(0xffffffffu, k.gpus, src);
-  o.mode_rank = __shfl_sync(0xffffffffu, k.mode_rank, src);
-  o.key = __shfl_sync(0xffffffffu, k.key, src);
-  return o;
-}
-
-__global__ void __launch_bounds__(kFrontThreads) k_front_pass1(EvalParams P, const SearchMeta* meta,
-                                                               const int32_t* plan_i, const double* plan_d,
-                                                               const lc_search_result* results, FrontPartial* part) {
-  const int s = blockIdx.y, bx = blockIdx.x, tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const lc_search_desc& S = P.searches[s];
-  const SearchMeta& M = meta[s];
-  const int64_t nplan = results[s].n_plans;
-  const int64_t nrows_all = 2 * (int64_t)M.n_units + nplan;
-  constexpr int kWarps = kFrontThreads / 32;
-  __shared__ BestKey wbest[kWarps];
-  __shared__ unsigned long long wlo[kWarps], whi[kWarps], wq1[kWarps], wq2[kWarps];
-  __shared__ int wcnt[kWarps][5];
-  int64_t lo, hi;
-  slice_of(nrows_all, kSplit1, bx, &lo, &hi);
-  BestKey best{0, 0, 0, 0, -1};
-  unsigned long long smin = ~0ull, smax = 0ull, q1 = 0, q2 = 0;
-  int feas = 0, rows = 0, enums = 0, skips = 0, fplans = 0;
-  for (int64_t r = lo + tid; r < hi; r += blockDim.x) {
-    if (r < M.n_units) {
-      const int64_t u = M.unit_off + r;
-      const int32_t q = P.u_queries[u];
-      q1 += (unsigned)(q & 0xffff);
-      q2 += (unsigned)(q >> 16);
-      if (P.u_budget[u]) {
-        ++enums;
-        if ((S.modes & 1) && P.st_status[u]) ++skips;
-        if ((S.modes & 2) && P.ag_status[u]) ++skips;
-      }
-      if (S.modes & 4) skips += (P.pf_status[u] != 0) + (P.dc_status[u] != 0);
-    }
-    const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-    FRONT_ROW_FILTER(v)
-    ++rows;
-    if (!feasible(S, v)) continue;
-    ++feas;
-    fplans += r >= 2 * (int64_t)M.n_units;
-    const double nt = -v.thru, ns = -v.speed;
-    if (best.key < 0 || nt < best.nthru || (nt == best.nthru && ns <= best.nspeed)) {
-      BestKey k{nt, ns, v.gpus, mode_rank(v.mode), v.key};
-      if (best_less(P, M, plan_i, k, best)) best = k;
-    }
-    const unsigned long long sb = (unsigned long long)__double_as_longlong(v.speed);
-    smin = sb < smin ? sb : smin;
-    smax = sb > smax ? sb : smax;
-  }
-  // warp-level reductions, then one shared-memory step (a block covers few rows per thread)
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    feas += __shfl_xor_sync(0xffffffffu, feas, o);
-    rows += __shfl_xor_sync(0xffffffffu, rows, o);
-    enums += __shfl_xor_sync(0xffffffffu, enums, o);
-    skips += __shfl_xor_sync(0xffffffffu, skips, o);
-    fplans += __shfl_xor_sync(0xffffffffu, fplans, o);
-    q1 += __shfl_xor_sync(0xffffffffu, q1, o);
-    q2 += __shfl_xor_sync(0xffffffffu, q2, o);
-    const unsigned long long a = __shfl_xor_sync(0xffffffffu, smin, o);
-    const unsigned long long b = __shfl_xor_sync(0xffffffffu, smax, o);
-    smin = a < smin ? a : smin;
-    smax = b > smax ? b : smax;
-  }
-  for (int o = 1; o < 32; o <<= 1) {
-    const BestKey other = shfl_best(best, lane ^ o);
-    if (best_less(P, M, plan_i, other, best)) best = other;
-  }
-  if (lane == 0) {
-    wbest[warp] = best;
-    wlo[warp] = smin; whi[warp] = smax; wq1[warp] = q1; wq2[warp] = q2;
-    wcnt[warp][0] = feas; wcnt[warp][1] = rows; wcnt[warp][2] = enums; wcnt[warp][3] = skips; wcnt[warp][4] = fplans;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    FrontPartial o;
-    o.best = wbest[0]; o.smin = wlo[0]; o.smax = whi[0]; o.q1 = wq1[0]; o.q2 = wq2[0];
-    o.feas = wcnt[0][0]; o.rows = wcnt[0][1]; o.enums = wcnt[0][2]; o.skips = wcnt[0][3]; o.fplans = wcnt[0][4];
-    o._pad = 0;
-    for (int w = 1; w < kWarps; ++w) {
-      if (best_less(P, M, plan_i, wbest[w], o.best)) o.best = wbest[w];
-      o.smin = wlo[w] < o.smin ? wlo[w] : o.smin;
-      o.smax = whi[w] > o.smax ? whi[w] : o.smax;
-      o.q1 += wq1[w]; o.q2 += wq2[w];
-      o.feas += wcnt[w][0]; o.rows += wcnt[w][1]; o.enums += wcnt[w][2]; o.skips += wcnt[w][3];
-      o.fplans += wcnt[w][4];
-    }
-    part[(int64_t)s * kSplit1 + bx] = o;
-  }
-}
-
 __global__ void __launch_bounds__(kFrontThreads) k_front_mid(EvalParams P, const SearchMeta* meta,
                                                              const int32_t* plan_i, const double* plan_d,
-                                                             lc_search_result* results, const FrontPartial* part,
+                                                             lc_search_result* results,
                                                              FrontMeta* fmeta, unsigned long long* buckets,
                                                              int32_t* n_surv) {
   const int s = blockIdx.x, tid = threadIdx.x;
@@ -1881,17 +1890,10 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_mid(EvalParams P, const
   unsigned long long* bk = buckets + (int64_t)s * kSpeedBuckets;
   for (int i = tid; i < kSpeedBuckets; i += blockDim.x) bk[i] = 0ull;
   if (tid == 0) {
-    BestKey best{0, 0, 0, 0, -1};
-    unsigned long long lo = ~0ull, hi = 0ull, q1 = 0, q2 = 0;
-    int feas = 0, rows = 0, enums = 0, skips = 0, fplans = 0;
-    for (int j = 0; j < kSplit1; ++j) {
-      const FrontPartial& p = part[(int64_t)s * kSplit1 + j];
-      if (best_less(P, M, plan_i, p.best, best)) best = p.best;
-      lo = p.smin < lo ? p.smin : lo;
-      hi = p.smax > hi ? p.smax : hi;
-      q1 += p.q1; q2 += p.q2;
-      feas += p.feas; rows += p.rows; enums += p.enums; skips += p.skips; fplans += p.fplans;
-    }
+    const SearchAcc A = P.acc[s];  // k_expand + k_disagg
+    const unsigned long long lo = ~A.smin_c, hi = A.smax, q1 = A.q1, q2 = A.q2;
+    const int feas = A.feas, rows = A.rows, enums = A.enums, skips = A.skips, fplans = A.fplans;
+    const BestKey best{0, 0, 0, 0, -1};  // select_best: from the front, in k_front_final
     lc_search_result& R = results[s];
     R.n_enumerated = enums; R.n_rows = rows; R.n_feasible = feas; R.n_skipped = skips;
     R.n_feasible_plans = fplans;
@@ -2073,18 +2075,28 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, con
     __syncthreads();
     if (tid == 0) {
       int m = 0;
+      BestKey best{0, 0, 0, 0, -1};  // select_best (search.py:179-187): the best row is on the front
       for (int i = 0; i < nsv; ++i) {
         if (!flag[i]) continue;
         const int64_t key = sorted[i].key;
         front[foff + m] = key;
         compact[(int64_t)s * kCompactFront + m] = key;
         ++m;
+        const int mode = (int)(key >> 32);
+        const BestKey k{-sorted[i].thru, -sorted[i].speed,
+                        mode == 2 ? (int64_t)plan_d[(M.plan_off + (key & 0xffffffffll)) * 6 + 0] : -1,
+                        mode_rank(mode), key};
+        if (best_less(P, M, plan_i, k, best)) best = k;
       }
       results[s].n_front = m;
+      results[s].best = best.key;
+      results[s].best_thru = best.key >= 0 ? -best.nthru : 0.0;
+      results[s].best_speed = best.key >= 0 ? -best.nspeed : 0.0;
     }
     return;
   }
   // survivor overflow: iterative staircase over all rows (one block)
+  BestKey obest{0, 0, 0, 0, -1};
   if (tid == 0) nfront = 0;
   __syncthreads();
   double best_thru = -INFINITY;
@@ -2115,13 +2127,20 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, con
         if (v.speed == sp && v.thru == top) {
           if (nfront < kCompactFront) compact[(int64_t)s * kCompactFront + nfront] = v.key;
           front[foff + nfront++] = v.key;
+          const BestKey k{-v.thru, -v.speed, v.gpus, mode_rank(v.mode), v.key};
+          if (best_less(P, M, plan_i, k, obest)) obest = k;
         }
       }
     }
     __syncthreads();
     best_thru = top;
   }
-  if (tid == 0) results[s].n_front = nfront;
+  if (tid == 0) {
+    results[s].n_front = nfront;
+    results[s].best = obest.key;
+    results[s].best_thru = obest.key >= 0 ? -obest.nthru : 0.0;
+    results[s].best_speed = obest.key >= 0 ? -obest.nspeed : 0.0;
+  }
 }
 
 }  // namespace
@@ -2175,7 +2194,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->pinned_front) cudaFreeHost(c->pinned_front);
@@ -2384,6 +2403,7 @@ static EvalParams make_params(lc_ctx* c) {
   P.cell_err = (int64_t*)c->cell_err.p;
   P.n_cells_total = c->n_cells;
   P.results = (lc_search_result*)c->results.p;
+  P.acc = (SearchAcc*)c->acc.p;
   return P;
 }
 
@@ -2421,6 +2441,11 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
   // per-search result accumulators (queries are summed by K4)
   CK(cudaMemsetAsync(c->results.p, 0, sizeof(lc_search_result) * c->n_search, c->stream));
+  {
+    SearchAcc* acc = c->acc.get<SearchAcc>(c->n_search > 0 ? c->n_search : 1, &err);
+    if (err != cudaSuccess) return fail(LC_ERR_CUDA, "accumulator allocation");
+    CK(cudaMemsetAsync(acc, 0, sizeof(SearchAcc) * (c->n_search > 0 ? c->n_search : 1), c->stream));
+  }
   EvalParams P = make_params(c);
   const int sms = sm_count(c->device);
   CK(cudaEventRecord(c->ev[1], c->stream));
@@ -2491,7 +2516,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     int64_t blocks = (n + 255) / 256;
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
     ++c->launches;
-    k_expand<<<(int)blocks, 256, 0, c->stream>>>(P);
+    k_expand<<<(int)blocks, 256, 0, c->stream>>>(P);  // also the per-search accounting (SearchAcc)
     CK(cudaGetLastError());
   }
   CK(cudaEventRecord(c->ev[3], c->stream));
@@ -2512,7 +2537,6 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   CK(cudaGetLastError());
   CK(cudaEventRecord(c->ev[5], c->stream));
   {
-    FrontPartial* fp = c->front_part.get<FrontPartial>((size_t)c->n_search * kSplit, &err);
     FrontMeta* fm = c->front_meta.get<FrontMeta>(c->n_search, &err);
     unsigned long long* bk = c->buckets.get<unsigned long long>((size_t)c->n_search * kSpeedBuckets, &err);
     FrontCand* sv = c->surv.get<FrontCand>((size_t)c->n_search * kSurvivorCap, &err);
@@ -2524,9 +2548,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     lc_search_result* res = (lc_search_result*)c->results.p;
     const dim3 g(kSplit, c->n_search);
     ++c->launches;
-    k_front_pass1<<<dim3(kSplit1, c->n_search), kFrontThreads, 0, c->stream>>>(P, meta, pi, pd, res, fp);
-    ++c->launches;
-    k_front_mid<<<c->n_search, kFrontThreads, 0, c->stream>>>(P, meta, pi, pd, res, fp, fm, bk, ns);
+    k_front_mid<<<c->n_search, kFrontThreads, 0, c->stream>>>(P, meta, pi, pd, res, fm, bk, ns);
     ++c->launches;
     k_front_pass2<<<g, kFrontThreads, 0, c->stream>>>(P, meta, pi, pd, res, fm, bk);
     ++c->launches;
