@@ -2464,6 +2464,10 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     if (blocks > sms * 16) blocks = sms * 16;
     ++c->launches;
     // experts per lane: 8 covers E <= 256 (DeepSeek-V3, GPT-OSS) at a quarter of the registers
+#ifndef LC_NO_TAILS4
+    if (c->sp->n_experts <= 128) k_tails<4><<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
+    else
+#endif
     if (c->sp->n_experts <= 256) k_tails<8><<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
     else k_tails<32><<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
     CK(cudaGetLastError());
