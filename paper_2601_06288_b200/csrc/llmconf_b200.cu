@@ -541,50 +541,61 @@ __global__ void __launch_bounds__(256, LC_TAIL_MIN_BLOCKS) k_tails(EvalParams P,
   int* hist = hist_all[warp];
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int npair = P.n_tp * P.n_ep;
-  for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; t < n_tails; t += nw) {
-    int lo = 0, hi = P.n_tail_tables - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (P.tail_tables[mid].off <= t) lo = mid;
-      else hi = mid - 1;
-    }
-    int64_t result = 0;
-    if (t >= P.n_pd_tails) {
-      // dense mixed region: (load, pair, tokens)
-      int64_t r = t - P.n_pd_tails;
-      const int64_t tok = r % (P.m_tmax + 1);
-      r /= (P.m_tmax + 1);
-      const int pair = (int)(r % npair);
-      const int load = (int)(r / npair);
-      const int tp_i = pair / P.n_ep, ep_i = pair % P.n_ep;
-      const int64_t tp = P.tp_vals[tp_i], ep = P.ep_vals[ep_i];
-      if (ep > 1 && P.pair_used[pair] && P.pair_canon[pair] == pair && P.m_used[(int64_t)load * (P.m_tmax + 1) + tok]) {
-        const int64_t f = ep / tp > 1 ? ep / tp : 1;
-        const int E = (int)P.n_experts;
-        const double* q = P.loads + (int64_t)load * 2 * E;
-        result = warp_busiest_shard<PER>(q, q + E, E, tok * f, P.topk, ep, hist);
-        if (lane == 0) tails[t] = result;
+  const int E = (int)P.n_experts;
+  // each warp takes 32 consecutive table entries: the lanes decide in parallel
+  // which are needed (most of the dense mixed region is not), then the warp
+  // computes the needed ones one after another
+  for (int64_t chunk = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; chunk * 32 < n_tails; chunk += nw) {
+    const int64_t t = chunk * 32 + lane;
+    bool need = false;
+    int64_t pooled = 0, ep = 1;
+    int load = 0;
+    if (t < n_tails) {
+      if (t >= P.n_pd_tails) {
+        // dense mixed region: (load, pair, tokens)
+        int64_t r = t - P.n_pd_tails;
+        const int64_t tok = r % (P.m_tmax + 1);
+        r /= (P.m_tmax + 1);
+        const int pair = (int)(r % npair);
+        load = (int)(r / npair);
+        const int64_t tp = P.tp_vals[pair / P.n_ep];
+        ep = P.ep_vals[pair % P.n_ep];
+        need = ep > 1 && P.pair_used[pair] && P.pair_canon[pair] == pair &&
+               P.m_used[(int64_t)load * (P.m_tmax + 1) + tok];
+        pooled = tok * (ep / tp > 1 ? ep / tp : 1);
+      } else {
+        int lo = 0, hi = P.n_tail_tables - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (P.tail_tables[mid].off <= t) lo = mid;
+          else hi = mid - 1;
+        }
+        const TailTable T = P.tail_tables[lo];
+        const int64_t rel = t - T.off;
+        const int bi = (int)(rel % T.n_b);
+        const int pair = (int)(rel / T.n_b);
+        if (pair < npair) {
+          const int64_t tp = P.tp_vals[pair / P.n_ep];
+          ep = P.ep_vals[pair % P.n_ep];
+          need = ep > 1 && P.pair_used[pair] && P.pair_canon[pair] == pair && T.load >= 0;
+          const int64_t b = P.batches[T.b_off + bi];
+          const int64_t tokens = T.type == 0 ? b * T.chunk : b;
+          pooled = tokens * (ep / tp > 1 ? ep / tp : 1);
+          load = T.load;
+        }
       }
-      continue;
     }
-    const TailTable T = P.tail_tables[lo];
-    const int64_t rel = t - T.off;
-    const int bi = (int)(rel % T.n_b);
-    const int pair = (int)(rel / T.n_b);
-    if (pair >= npair) continue;
-    const int tp_i = pair / P.n_ep, ep_i = pair % P.n_ep;
-    const int64_t tp = P.tp_vals[tp_i], ep = P.ep_vals[ep_i];
-    if (!(ep > 1 && P.pair_used[pair] && P.pair_canon[pair] == pair && T.load >= 0)) continue;
-    const int64_t b = P.batches[T.b_off + bi];
-    const int64_t tokens = T.type == 0 ? b * T.chunk : b;
-    {
-      const int64_t f = ep / tp > 1 ? ep / tp : 1;
-      const int64_t pooled = tokens * f;
-      const int E = (int)P.n_experts;
-      const double* q = P.loads + (int64_t)T.load * 2 * E;
-      result = warp_busiest_shard<PER>(q, q + E, E, pooled, P.topk, ep, hist);
+    unsigned mask = __ballot_sync(0xffffffffu, need);
+    while (mask) {
+      const int src = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const int64_t pl = __shfl_sync(0xffffffffu, pooled, src);
+      const int64_t e = __shfl_sync(0xffffffffu, ep, src);
+      const int ld = __shfl_sync(0xffffffffu, load, src);
+      const double* q = P.loads + (int64_t)ld * 2 * E;
+      const int64_t result = warp_busiest_shard<PER>(q, q + E, E, pl, P.topk, e, hist);
+      if (lane == src) tails[t] = result;
     }
-    if (lane == 0) tails[t] = result;
   }
 }
 
@@ -2459,7 +2470,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     CK(cudaGetLastError());
   }
   if (c->n_tails > 0) {
-    const int64_t warps = c->n_tails;
+    const int64_t warps = (c->n_tails + 31) / 32;  // a warp per 32 consecutive entries
     int blocks = (int)((warps + 7) / 8);
     if (blocks > sms * 16) blocks = sms * 16;
     ++c->launches;
