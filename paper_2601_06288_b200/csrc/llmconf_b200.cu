@@ -229,6 +229,7 @@ struct lc_ctx {
   DBuf sgroups, smembers, sd;  // shared static decode loops
   DBuf pgroups, psteps;        // shared prefill step totals
   DBuf acc;                    // SearchAcc per search
+  DBuf plan_scratch;           // K5b pairing results [search][256]
   std::vector<PGroup> hpg;
   int64_t n_pstep = 0;
   DBuf raw_mask;               // lc_set_raw_filter: optional keep-mask over [filt_lo, filt_hi)
@@ -1422,34 +1423,40 @@ struct PlanRec {
   double r_sys, ttft, tpot, speed, thru;
 };
 
-__global__ void __launch_bounds__(1024) k_disagg(EvalParams P, SearchMeta* meta, const int32_t* pool_sel, int32_t* plan_i, double* plan_d,
-                         lc_search_result* results) {
+// K5b: replica sweep (serving_modes.py:468-488), a warp per pairing; the
+// pairings of a search are spread over kDisSplit blocks
+constexpr int kDisSplit = 16;
+__device__ __forceinline__ void disagg_pools(const EvalParams& P, const lc_search_desc& S, const SearchMeta& M,
+                                             const int32_t* pool_sel, int s, int32_t* pre, int32_t* dec, int* npre,
+                                             int* ndec) {
+  // top-k pools first, then the latency filters (search.py:338-339; serving_modes.py:458-466)
+  int a = 0, d = 0;
+  for (int k = 0; k < M.n_pre; ++k) {
+    const int32_t u = pool_sel[(int64_t)s * 128 + k];
+    if (!S.has_ttft || P.pf_v[u] * S.ttft_headroom <= S.ttft_limit) pre[a++] = u;
+  }
+  for (int k = 0; k < M.n_dec; ++k) {
+    const int32_t u = pool_sel[(int64_t)s * 128 + 64 + k];
+    if (!S.has_floor || P.dc_v[u] <= S.tpot_cap) dec[d++] = u;
+  }
+  *npre = a;
+  *ndec = d;
+}
+
+__global__ void __launch_bounds__(256) k_disagg_pairs(EvalParams P, const SearchMeta* meta, const int32_t* pool_sel,
+                                                      PlanRec* scratch) {
   const int s = blockIdx.x;
   const lc_search_desc& S = P.searches[s];
+  if (!(S.modes & 4) || (S.modes & LC_MODE_NO_PLANS)) return;
   __shared__ int32_t pre[64], dec[64];
   __shared__ int npre, ndec;
-  __shared__ PlanRec plans[256];
-  __shared__ int nplan;
-  if (!(S.modes & 4) || (S.modes & LC_MODE_NO_PLANS)) {
-    if (threadIdx.x == 0) { meta[s].plan_cap = 0; results[s].n_plans = 0; }
-    return;
-  }
-  if (threadIdx.x == 0) {
-    npre = ndec = 0;
-    for (int k = 0; k < meta[s].n_pre; ++k) {
-      const int32_t u = pool_sel[(int64_t)s * 128 + k];
-      if (!S.has_ttft || P.pf_v[u] * S.ttft_headroom <= S.ttft_limit) pre[npre++] = u;
-    }
-    for (int k = 0; k < meta[s].n_dec; ++k) {
-      const int32_t u = pool_sel[(int64_t)s * 128 + 64 + k];
-      if (!S.has_floor || P.dc_v[u] <= S.tpot_cap) dec[ndec++] = u;
-    }
-    nplan = 0;
-  }
+  if (threadIdx.x == 0) disagg_pools(P, S, meta[s], pool_sel, s, pre, dec, &npre, &ndec);
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.y * (blockDim.x >> 5) + warp, nwarp = gridDim.y * (blockDim.x >> 5);
   const int npair = npre * ndec;
-  for (int pi = warp; pi < npair && pi < 256; pi += nwarp) {
+  PlanRec* plans = scratch + (int64_t)s * 256;
+  for (int pi = gw; pi < npair && pi < 256; pi += nwarp) {
     const int32_t up = pre[pi / ndec], ud = dec[pi % ndec];
     const double rp = P.pf_v[P.n_cap + up], rd = P.dc_v[P.n_cap + ud];
     const int64_t gp = P.combos[P.u_combo[up]].gpus, gd = P.combos[P.u_combo[ud]].gpus;
@@ -1497,6 +1504,27 @@ __global__ void __launch_bounds__(1024) k_disagg(EvalParams P, SearchMeta* meta,
     }
     if (lane == 0 && !have) plans[pi].p = -1;
   }
+}
+
+// K5b': compact the pairings' plans in pairing order and rank them stably by
+// (-thru, gpus, ttft, x, y) (serving_modes.py:424-427, 493); block per search
+__global__ void __launch_bounds__(256) k_disagg(EvalParams P, SearchMeta* meta, const int32_t* pool_sel,
+                                                const PlanRec* scratch, int32_t* plan_i, double* plan_d,
+                                                lc_search_result* results) {
+  const int s = blockIdx.x;
+  const lc_search_desc& S = P.searches[s];
+  __shared__ int32_t pre[64], dec[64];
+  __shared__ int npre, ndec;
+  __shared__ int nplan;
+  if (!(S.modes & 4) || (S.modes & LC_MODE_NO_PLANS)) {
+    if (threadIdx.x == 0) { meta[s].plan_cap = 0; results[s].n_plans = 0; }
+    return;
+  }
+  if (threadIdx.x == 0) disagg_pools(P, S, meta[s], pool_sel, s, pre, dec, &npre, &ndec);
+  __syncthreads();
+  const int npair = npre * ndec;
+  __shared__ PlanRec plans[256];
+  for (int i = threadIdx.x; i < npair && i < 256; i += blockDim.x) plans[i] = scratch[(int64_t)s * 256 + i];
   __syncthreads();
   // compact in pairing order, then stable rank by (-thru, gpus, ttft, x, y)
   __shared__ int32_t order[256];
@@ -2205,7 +2233,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->pinned_front) cudaFreeHost(c->pinned_front);
@@ -2546,9 +2574,16 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   }
   CK(cudaEventRecord(c->ev[4], c->stream));
   ++c->launches;
-  k_disagg<<<c->n_search, 1024, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, (const int32_t*)c->pool_sel.p,
-                                                (int32_t*)c->plans_i.p, (double*)c->plans_d.p,
-                                                (lc_search_result*)c->results.p);
+  {
+    PlanRec* scr = c->plan_scratch.get<PlanRec>((size_t)c->n_search * 256, &err);
+    if (err != cudaSuccess) return fail(LC_ERR_CUDA, "plan scratch allocation");
+    k_disagg_pairs<<<dim3(c->n_search, kDisSplit), 256, 0, c->stream>>>(P, (const SearchMeta*)c->meta.p,
+                                                                       (const int32_t*)c->pool_sel.p, scr);
+    ++c->launches;
+    k_disagg<<<c->n_search, 256, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, (const int32_t*)c->pool_sel.p, scr,
+                                                 (int32_t*)c->plans_i.p, (double*)c->plans_d.p,
+                                                 (lc_search_result*)c->results.p);
+  }
   CK(cudaGetLastError());
   CK(cudaEventRecord(c->ev[5], c->stream));
   {
