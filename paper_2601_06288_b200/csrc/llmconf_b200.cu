@@ -2112,15 +2112,26 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, con
       flag[i] = (sorted[i].thru == top && top > faster) ? 1 : 0;
     }
     __syncthreads();
+    // select_best (search.py:179-187) on the front, where the best row always is:
+    // highest throughput, then highest speed (block maxima), then the full key
+    double tmax = -INFINITY;
+    for (int i = tid; i < nsv; i += blockDim.x)
+      if (flag[i]) tmax = fmax(tmax, sorted[i].thru);
+    tmax = block_max(tmax, dred);
+    double smax = -INFINITY;
+    for (int i = tid; i < nsv; i += blockDim.x)
+      if (flag[i] && sorted[i].thru == tmax) smax = fmax(smax, sorted[i].speed);
+    smax = block_max(smax, dred);
     if (tid == 0) {
       int m = 0;
-      BestKey best{0, 0, 0, 0, -1};  // select_best (search.py:179-187): the best row is on the front
+      BestKey best{0, 0, 0, 0, -1};
       for (int i = 0; i < nsv; ++i) {
         if (!flag[i]) continue;
         const int64_t key = sorted[i].key;
         front[foff + m] = key;
         compact[(int64_t)s * kCompactFront + m] = key;
         ++m;
+        if (sorted[i].thru != tmax || sorted[i].speed != smax) continue;
         const int mode = (int)(key >> 32);
         const BestKey k{-sorted[i].thru, -sorted[i].speed,
                         mode == 2 ? (int64_t)plan_d[(M.plan_off + (key & 0xffffffffll)) * 6 + 0] : -1,
