@@ -2122,16 +2122,33 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, con
     for (int i = tid; i < nsv; i += blockDim.x)
       if (flag[i] && sorted[i].thru == tmax) smax = fmax(smax, sorted[i].speed);
     smax = block_max(smax, dred);
+    // ordered compaction of the front rows: contiguous runs per thread + block scan
+    const int per = (nsv + (int)blockDim.x - 1) / (int)blockDim.x;
+    const int i0 = tid * per, i1 = i0 + per < nsv ? i0 + per : nsv;
+    int cnt = 0;
+    for (int i = i0; i < i1; ++i) cnt += flag[i];
+    __shared__ int wsum[kFrontThreads / 32];
+    const int lane = tid & 31, wid = tid >> 5;
+    const int wex = warp_excl_scan(cnt, lane);
+    if (lane == 31) wsum[wid] = wex + cnt;
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < wid; ++w) base += wsum[w];
+    int pos = base + wex;
+    for (int i = i0; i < i1; ++i) {
+      if (!flag[i]) continue;
+      const int64_t key = sorted[i].key;
+      front[foff + pos] = key;
+      compact[(int64_t)s * kCompactFront + pos] = key;
+      ++pos;
+    }
     if (tid == 0) {
       int m = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m += wsum[w];
       BestKey best{0, 0, 0, 0, -1};
       for (int i = 0; i < nsv; ++i) {
-        if (!flag[i]) continue;
+        if (!flag[i] || sorted[i].thru != tmax || sorted[i].speed != smax) continue;
         const int64_t key = sorted[i].key;
-        front[foff + m] = key;
-        compact[(int64_t)s * kCompactFront + m] = key;
-        ++m;
-        if (sorted[i].thru != tmax || sorted[i].speed != smax) continue;
         const int mode = (int)(key >> 32);
         const BestKey k{-sorted[i].thru, -sorted[i].speed,
                         mode == 2 ? (int64_t)plan_d[(M.plan_off + (key & 0xffffffffll)) * 6 + 0] : -1,
