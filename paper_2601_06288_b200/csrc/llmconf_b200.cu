@@ -2045,7 +2045,11 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_pass3(EvalParams P, con
   }
 }
 
-__global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, const SearchMeta* meta,
+#ifndef LC_FINAL_THREADS
+#define LC_FINAL_THREADS 256
+#endif
+constexpr int kFinalThreads = LC_FINAL_THREADS;
+__global__ void __launch_bounds__(kFinalThreads) k_front_final(EvalParams P, const SearchMeta* meta,
                                                                const int32_t* plan_i, const double* plan_d,
                                                                lc_search_result* results, const FrontMeta* fmeta,
                                                                const FrontCand* surv, const int32_t* n_surv,
@@ -2127,7 +2131,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, con
     const int i0 = tid * per, i1 = i0 + per < nsv ? i0 + per : nsv;
     int cnt = 0;
     for (int i = i0; i < i1; ++i) cnt += flag[i];
-    __shared__ int wsum[kFrontThreads / 32];
+    __shared__ int wsum[kFinalThreads / 32];
     const int lane = tid & 31, wid = tid >> 5;
     const int wex = warp_excl_scan(cnt, lane);
     if (lane == 31) wsum[wid] = wex + cnt;
@@ -2135,26 +2139,29 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_final(EvalParams P, con
     int base = 0;
     for (int w = 0; w < wid; ++w) base += wsum[w];
     int pos = base + wex;
+    BestKey best{0, 0, 0, 0, -1};
     for (int i = i0; i < i1; ++i) {
       if (!flag[i]) continue;
       const int64_t key = sorted[i].key;
       front[foff + pos] = key;
       compact[(int64_t)s * kCompactFront + pos] = key;
       ++pos;
+      if (sorted[i].thru != tmax || sorted[i].speed != smax) continue;
+      const int mode = (int)(key >> 32);
+      const BestKey k{-sorted[i].thru, -sorted[i].speed,
+                      mode == 2 ? (int64_t)plan_d[(M.plan_off + (key & 0xffffffffll)) * 6 + 0] : -1,
+                      mode_rank(mode), key};
+      if (best_less(P, M, plan_i, k, best)) best = k;
     }
+    // tied candidates are rare: warp leaders collect, thread 0 picks by the full key
+    __shared__ BestKey wbest[kFinalThreads];
+    wbest[tid] = best;
+    __syncthreads();
     if (tid == 0) {
       int m = 0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m += wsum[w];
-      BestKey best{0, 0, 0, 0, -1};
-      for (int i = 0; i < nsv; ++i) {
-        if (!flag[i] || sorted[i].thru != tmax || sorted[i].speed != smax) continue;
-        const int64_t key = sorted[i].key;
-        const int mode = (int)(key >> 32);
-        const BestKey k{-sorted[i].thru, -sorted[i].speed,
-                        mode == 2 ? (int64_t)plan_d[(M.plan_off + (key & 0xffffffffll)) * 6 + 0] : -1,
-                        mode_rank(mode), key};
-        if (best_less(P, M, plan_i, k, best)) best = k;
-      }
+      for (int t = 0; t < (int)blockDim.x; ++t)
+        if (wbest[t].key >= 0 && best_less(P, M, plan_i, wbest[t], best)) best = wbest[t];
       results[s].n_front = m;
       results[s].best = best.key;
       results[s].best_thru = best.key >= 0 ? -best.nthru : 0.0;
@@ -2637,7 +2644,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     ++c->launches;
     int64_t* fc = c->front_compact.get<int64_t>((size_t)c->n_search * kCompactFront, &err);
     if (err != cudaSuccess) return fail(LC_ERR_CUDA, "front workspace allocation");
-    k_front_final<<<c->n_search, kFrontThreads, fsmem, c->stream>>>(P, meta, pi, pd, res, fm, sv, ns,
+    k_front_final<<<c->n_search, kFinalThreads, fsmem, c->stream>>>(P, meta, pi, pd, res, fm, sv, ns,
                                                                       (int64_t*)c->front.p, fc);
     CK(cudaGetLastError());
   }
