@@ -310,7 +310,6 @@ struct EvalParams {
   int32_t* pf_status; double* pf_v;  // [2][n_units] lat, rate
   int32_t* dc_status; double* dc_v;
   int64_t* err_c;                    // [8][n_units]: (c0,c1) x (st,ag,pf,dc)
-  int32_t* u_queries;                // q1 | q2 << 16 per unit
   double* pool_key;                  // [2][n_cap]: (-rate)/gpus per pool role (search.py:276-277), +inf if skipped
   // cells (search x template x batch)
   const struct TmplInfo* tmpl_info;
@@ -1331,7 +1330,6 @@ __global__ void __launch_bounds__(256, LC_EXPAND_MIN_BLOCKS) k_expand(EvalParams
     const int64_t k = (S.isl + S.osl / 2) - S.isl - 1;
     const bool dup = do_st && o.st_status == 0 && S.osl > 1 && k >= 0 && (k % 32) == 0 && (k / 32) < o.st_steps;
     if (((do_ag && (o.flags & 1)) || do_dg) && !dup) add_q(o.qG);
-    P.u_queries[u] = q;
     ra.q1 = (unsigned)(q & 0xffff);
     ra.q2 = (unsigned)(q >> 16);
     if (inb) {
@@ -2469,7 +2467,6 @@ static EvalParams make_params(lc_ctx* c) {
   P.pf_status = (int32_t*)c->pf_status.p; P.pf_v = (double*)c->pf_v.p;
   P.dc_status = (int32_t*)c->dc_status.p; P.dc_v = (double*)c->dc_v.p;
   P.err_c = (int64_t*)c->err_c.p;
-  P.u_queries = (int32_t*)c->u_queries.p;
   P.pool_key = (double*)c->pool_key.p;
   P.tmpl_info = sp->tmpl_info;
   P.cell_flags = (uint32_t*)c->cell_flags.p;
@@ -2499,7 +2496,6 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   c->pf_status.get<int32_t>(n, &err); c->pf_v.get<double>(2 * n, &err);
   c->dc_status.get<int32_t>(n, &err); c->dc_v.get<double>(2 * n, &err);
   c->err_c.get<int64_t>(8 * n, &err);
-  c->u_queries.get<int32_t>(n, &err);
   c->pool_key.get<double>(2 * n, &err);
   c->cells.get<CellOut>(c->n_cells, &err);
   c->qt.get<QVal>(c->n_qt, &err);
