@@ -224,7 +224,7 @@ struct lc_ctx {
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
-  DBuf pool_key, qt_groups, ds_groups, front_compact, pool_part, front_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
+  DBuf pool_key, qt_groups, ds_groups, front_compact, pool_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   DBuf q_in, q_lat, q_st;  // lc_query_batch
   DBuf sgroups, smembers, sd;  // shared static decode loops
   DBuf pgroups, psteps;        // shared prefill step totals
@@ -1706,47 +1706,6 @@ constexpr int kSurvivorCap = 2048;  // front candidates kept in shared memory
 constexpr int kFrontThreads = LC_FRONT_THREADS;
 constexpr int kSpeedBuckets = 4096;
 
-// Exact staircase over a row subset sorted by (speed desc, row key asc): the
-// reference's group-by-speed / running-max scan (search.py:156-176).
-__device__ void front_of_sorted(const FrontCand* c, int n, int64_t* out, int* n_out) {
-  int m = 0;
-  double best_thru = -INFINITY;
-  for (int a = 0; a < n;) {
-    int b = a;
-    double top = -INFINITY;
-    while (b < n && c[b].speed == c[a].speed) { top = fmax(top, c[b].thru); ++b; }
-    if (top > best_thru) {
-      for (int j = a; j < b; ++j)
-        if (c[j].thru == top) out[m++] = c[j].key;
-      best_thru = top;
-    }
-    a = b;
-  }
-  *n_out = m;
-}
-
-__device__ __forceinline__ unsigned long long block_min_u64(unsigned long long v, unsigned long long* red) {
-  for (int o = 16; o > 0; o >>= 1) { const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o); v = w < v ? w : v; }
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  unsigned long long r = ~0ull;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = red[i] < r ? red[i] : r;
-  __syncthreads();
-  return r;
-}
-
-__device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v, unsigned long long* red) {
-  for (int o = 16; o > 0; o >>= 1) { const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o); v = w > v ? w : v; }
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  unsigned long long r = 0;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) r = red[i] > r ? red[i] : r;
-  __syncthreads();
-  return r;
-}
-
 #define FRONT_ROW_FILTER(v)                                                          \
   if (!v.valid) continue;                                                            \
   if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
@@ -2266,7 +2225,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->pinned_front) cudaFreeHost(c->pinned_front);
