@@ -2711,6 +2711,17 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   c->db = db;
   c->sp = sp;
   c->n_search = n_search;
+  if (n_search == 0) {  // nothing to evaluate: empty results, no launches
+    c->n_batches = n_batches;
+    c->n_loads = n_loads;
+    c->n_raw = c->n_cap = c->n_units = c->n_cells = c->n_plan_slots = c->n_front_slots = 0;
+    c->n_qt = c->n_ds = c->n_tails = c->n_series = c->n_pstep = 0;
+    c->launches = 0;
+    c->hres.clear();
+    c->hmeta.clear();
+    if (totals) memset(totals, 0, sizeof(*totals));
+    return LC_OK;
+  }
   c->n_batches = n_batches;
   c->n_loads = n_loads;
   // host bookkeeping: raw tuple, tail and plan offsets
@@ -3046,6 +3057,10 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
 int lc_replay_last(lc_ctx* c, int32_t iters, lc_batch_totals* totals) {
   if (!c || !c->db || iters < 1) return fail(LC_ERR_STATE, "lc_replay_last: no previous batch");
   CK(cudaSetDevice(c->device));
+  if (c->n_search == 0) {
+    if (totals) memset(totals, 0, sizeof(*totals));
+    return LC_OK;
+  }
   double acc[6] = {0, 0, 0, 0, 0, 0};
   for (int it = 0; it < iters; ++it) {
     // inputs (descriptors, batches, loads, DB, plan) are resident: K0 .. K4 only
@@ -3077,6 +3092,7 @@ int lc_replay_last(lc_ctx* c, int32_t iters, lc_batch_totals* totals) {
 int lc_replay_async(lc_ctx* c) {
   if (!c || !c->db) return fail(LC_ERR_STATE, "lc_replay_async: no previous batch");
   CK(cudaSetDevice(c->device));
+  if (c->n_search == 0) return LC_OK;
   CK(cudaEventRecord(c->ev[0], c->stream));
   c->launches = 0;
   int rc = run_enum(c);
