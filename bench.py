@@ -8,9 +8,12 @@ disaggregated combine -> SLA / Pareto / best).  ``value`` is whole-job
 candidates/s with inputs resident on the GPU (CUDA events on the engine stream,
 max over ranks); ``e2e`` is the same metric through the public API
 (``Engine.run_batch`` with host workload objects, H2D descriptors, D2H
-summaries + fronts + plans).  Multi-GPU: one process per GPU, the searches are
-split across ranks (strong scaling of the fixed sweep) and the per-search
-results are merged with one NCCL all-gather.
+summaries + fronts + plans).  Multi-GPU: one process per GPU, no collective on
+the data path.  ``--scaling weak`` (default): the sweep's ISL grid is densified
+N-fold and rank r owns offset r of it, so every rank evaluates a config-5-sized
+block and the whole job grows with N; ``--scaling strong``: the fixed config-5
+sweep is split across ranks by workload blocks.  The per-search results are
+merged with one NCCL all-gather.
 
 ``--impl reference`` times the reference algorithm on the host cores instead:
 the C restatement in oracle/ (test infrastructure; the Python reference cannot
@@ -224,6 +227,9 @@ def main() -> int:
     ap.add_argument("--cpu-steps", type=int, default=6, help="reference-oracle sample steps for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--split", type=int, default=1, help="independent batches (engines / streams) per model")
+    ap.add_argument("--scaling", default="weak", choices=("weak", "strong"),
+                    help="weak: each rank evaluates its own config-5-sized block of an N-fold sweep (default); "
+                         "strong: the fixed sweep is split across ranks")
     args = ap.parse_args()
 
     from paper_2601_06288_b200.sweeps import sweep
@@ -253,7 +259,7 @@ def main() -> int:
         value = float(np.median(vals))
         line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * float(np.median(secs)),
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": workload_desc,
                 "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": "port",
                                  "sample": r["sample"]},
@@ -273,8 +279,15 @@ def main() -> int:
     # (the sweep is ISL-major, so a batch keeps whole ISL groups and their shared tables)
     my_parts = []
     for p in parts:
-        lo, hi = shard_range(len(p.workloads), rank, ws)
-        mine = p.workloads[lo:hi]
+        if args.scaling == "strong":
+            lo, hi = shard_range(len(p.workloads), rank, ws)
+            mine = p.workloads[lo:hi]
+        else:
+            # weak scaling: the sweep's ISL grid is densified N-fold and each rank owns one
+            # offset of it (rank r: every ISL + r), so per-GPU work stays one config-5 sweep
+            import dataclasses
+
+            mine = [dataclasses.replace(w, isl=w.isl + rank) for w in p.workloads] if rank else list(p.workloads)
         for k in range(args.split):
             a, b = shard_range(len(mine), k, args.split)
             if b > a:
@@ -420,9 +433,13 @@ def main() -> int:
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": float(np.mean(step_ms)), "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": float(np.mean(step_ms)), "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(workload_desc, candidates=int(cands_total), parallelism=f"searches sharded over {ws} GPU(s), {args.split} batch(es) per model",
+        "config": dict(workload_desc, searches=total_searches * (ws if args.scaling == "weak" else 1),
+                       candidates=int(cands_total), parallelism=(f"searches sharded over {ws} GPU(s) ({args.scaling} scaling: "
+                                    + ("each rank owns one ISL offset of an N-fold densified sweep"
+                                       if args.scaling == "weak" else "the fixed sweep split by workload blocks")
+                                    + f"), {args.split} batch(es) per model"),
                        l2="per-step unit arrays exceed L2 (~2 GB written per step)"),
         "search_wall_ms": {"device": dev_s * 1000 / args.steps, "e2e": e2e_s * 1000 / args.steps,
                            "per_model_sequential_device": float(kernel_ms.sum())},
