@@ -279,6 +279,29 @@ typedef struct {
 int lc_query_batch(lc_ctx* ctx, const lc_db* db, int32_t n, const lc_query* queries, double* latency_us,
                    int32_t* status);
 
+/* ------------------------------------------------ report rows (host) */
+/* Column view of a search's report rows (fastreport.Columns). */
+typedef struct {
+  int64_t n;                         /* rows */
+  const int32_t* mode;               /* 0 static, 1 aggregated, 2 disaggregated */
+  const int64_t* cfg;                /* [n*5] tp, pp, ep, dp, batch (static / aggregated rows) */
+  const int64_t* gpus;
+  const double* ttft; const double* tpot; const double* speed; const double* thru;
+  const uint8_t* feasible; const uint8_t* frontier;
+  const int64_t* pcfg; const int64_t* dcfg;  /* [n*5] prefill / decode worker (disaggregated rows) */
+  const int64_t* x; const int64_t* y;        /* replicas */
+  const double* r_sys;
+  const char* model_json;            /* json.dumps(model name) */
+  const char* runtime[6];            /* the runtime object, json.dumps(sort_keys, indent=2), re-indented per depth */
+} lc_report_cols;
+
+/* Write the JSON list of rows (rows[0..n_sel) or, when rows is NULL, all rows)
+ * as SearchReport.to_json() prints the "rows" / "frontier" lists at list depth
+ * `depth` (search.py:224-264): the same bytes as json.dumps(sort_keys=True,
+ * indent=2).  Returns the byte count (writes only if it fits in cap), or < 0. */
+int64_t lc_report_rows(const lc_report_cols* cols, const int64_t* rows, int64_t n_sel, int32_t depth, int32_t flags,
+                       char* out, int64_t cap);
+
 /* ------------------------------------------------ synthetic database generation */
 /* One grid of generate_synthetic_db (perfdb.py:641-666): GridAxes (perfdb.py:586-614)
  * with its per-key hash constants already evaluated by the host. */

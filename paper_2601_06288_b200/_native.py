@@ -113,6 +113,13 @@ class LcDbgenDesc(C.Structure):
                 ("inter_node_bandwidth", C.c_double), ("gpus_per_node", C.c_int32), ("compute", C.c_double * 4)]
 
 
+class LcReportCols(C.Structure):
+    _fields_ = [("n", C.c_int64), ("mode", I32P), ("cfg", I64P), ("gpus", I64P), ("ttft", F64P), ("tpot", F64P),
+                ("speed", F64P), ("thru", F64P), ("feasible", C.POINTER(C.c_uint8)),
+                ("frontier", C.POINTER(C.c_uint8)), ("pcfg", I64P), ("dcfg", I64P), ("x", I64P), ("y", I64P),
+                ("r_sys", F64P), ("model_json", C.c_char_p), ("runtime", C.c_char_p * 6)]
+
+
 QUERY_DTYPE = np.dtype([("grid", "<i4"), ("kind", "<i4"), ("quant", "<i4"), ("policy", "<i4"), ("d", "<i8", (5,)),
                         ("kv_len", "<i8")])
 assert QUERY_DTYPE.itemsize == 64
@@ -120,7 +127,7 @@ assert QUERY_DTYPE.itemsize == 64
 EXPORTED = ("lc_abi_version", "lc_last_error", "lc_open", "lc_close", "lc_db_upload", "lc_db_free",
             "lc_space_upload", "lc_space_free", "lc_search_batch", "lc_fetch", "lc_replay_last", "lc_replay_async",
             "lc_stream", "lc_query_batch", "lc_dbgen", "lc_set_raw_filter", "lc_fetch_pools",
-            "lc_unit_raw")
+            "lc_unit_raw", "lc_report_rows")
 
 _LIB = None
 
@@ -153,6 +160,9 @@ def load_library(path: str | os.PathLike | None = None):
     lib.lc_set_raw_filter.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]
     lib.lc_fetch_pools.argtypes = [C.c_void_p, I32P, I32P]
     lib.lc_unit_raw.argtypes = [C.c_void_p, C.c_int32, I32P, I64P]
+    lib.lc_report_rows.argtypes = [C.POINTER(LcReportCols), I64P, C.c_int64, C.c_int32, C.c_int32, C.c_char_p,
+                                   C.c_int64]
+    lib.lc_report_rows.restype = C.c_int64
     if path is None:
         _LIB = lib
     return lib

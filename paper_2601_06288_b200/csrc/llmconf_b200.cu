@@ -25,6 +25,7 @@
 #include "glibc_libm.cuh"
 #include "lc_eval.cuh"
 #include "lc_tails.cuh"
+#include "lc_report.h"
 
 using namespace lc;
 
@@ -3240,6 +3241,109 @@ int lc_unit_raw(lc_ctx* c, int32_t n, const int32_t* units, int64_t* raw) {
   CK(cudaMemcpyAsync(raw, dr, sizeof(int64_t) * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return LC_OK;
+}
+
+// ---- report rows (host): the "rows" / "frontier" lists of SearchReport.to_json()
+static bool put_row(lcr::Out& o, const lc_report_cols* c, int64_t i, int depth, bool flags) {
+  using lcr::Out;
+  char f[4][40];
+  const double vals[4] = {c->thru[i], c->tpot[i], c->ttft[i], c->mode[i] == 2 ? c->r_sys[i] : 0.0};
+  for (int k = 0; k < 4; ++k) {
+    if (!std::isfinite(vals[k])) return false;
+    lcr::py_repr(vals[k], f[k]);
+  }
+  char sp[40];
+  if (std::isfinite(c->speed[i])) lcr::py_repr(c->speed[i], sp);
+  else strcpy(sp, "null");
+  auto key = [&](const int64_t* g) {
+    o.put("tp"); o.i64(g[0]); o.put("pp"); o.i64(g[1]); o.put("ep"); o.i64(g[2]); o.put("dp"); o.i64(g[3]);
+    o.put("b"); o.i64(g[4]);
+  };
+  auto parallel = [&](const int64_t* g, int d) {  // opening brace at depth d
+    o.put("{\n"); o.pad(d + 1); o.put("\"dp\": "); o.i64(g[3]); o.put(",\n");
+    o.pad(d + 1); o.put("\"ep\": "); o.i64(g[2]); o.put(",\n");
+    o.pad(d + 1); o.put("\"pp\": "); o.i64(g[1]); o.put(",\n");
+    o.pad(d + 1); o.put("\"tp\": "); o.i64(g[0]); o.put("\n"); o.pad(d); o.put("}");
+  };
+  auto flag_lines = [&]() {
+    if (!flags) return;
+    o.pad(depth + 1); o.put(c->feasible[i] ? "\"feasible\": true,\n" : "\"feasible\": false,\n");
+    o.pad(depth + 1); o.put(c->frontier[i] ? "\"frontier\": true,\n" : "\"frontier\": false,\n");
+  };
+  auto tail = [&]() {
+    o.pad(depth + 1); o.put("\"speed\": "); o.puts(sp); o.put(",\n");
+    o.pad(depth + 1); o.put("\"throughput_per_gpu\": "); o.puts(f[0]); o.put(",\n");
+    o.pad(depth + 1); o.put("\"tpot_ms\": "); o.puts(f[1]); o.put(",\n");
+    o.pad(depth + 1); o.put("\"ttft_ms\": "); o.puts(f[2]); o.put("\n");
+    o.pad(depth); o.put("}");
+  };
+  o.put("{\n");
+  if (c->mode[i] < 2) {
+    const int64_t* g = c->cfg + 5 * i;
+    static const char* modes[2] = {"static", "aggregated"};
+    o.pad(depth + 1); o.put("\"batch\": "); o.i64(g[4]); o.put(",\n");
+    o.pad(depth + 1); o.put("\"config\": \""); key(g); o.put("\",\n");
+    flag_lines();
+    o.pad(depth + 1); o.put("\"gpus\": "); o.i64(c->gpus[i]); o.put(",\n");
+    o.pad(depth + 1); o.put("\"mode\": \""); o.puts(modes[c->mode[i]]); o.put("\",\n");
+    o.pad(depth + 1); o.put("\"model\": "); o.puts(c->model_json); o.put(",\n");
+    o.pad(depth + 1); o.put("\"parallel\": "); parallel(g, depth + 1); o.put(",\n");
+    o.pad(depth + 1); o.put("\"runtime\": "); o.puts(c->runtime[depth + 1]); o.put(",\n");
+    tail();
+    return true;
+  }
+  const int64_t* pg = c->pcfg + 5 * i;
+  const int64_t* dg = c->dcfg + 5 * i;
+  auto side = [&](const int64_t* g, int64_t reps) {  // opening brace at depth + 1
+    const int d = depth + 1;
+    o.put("{\n");
+    o.pad(d + 1); o.put("\"batch\": "); o.i64(g[4]); o.put(",\n");
+    o.pad(d + 1); o.put("\"parallel\": "); parallel(g, d + 1); o.put(",\n");
+    o.pad(d + 1); o.put("\"replicas\": "); o.i64(reps); o.put(",\n");
+    o.pad(d + 1); o.put("\"runtime\": "); o.puts(c->runtime[d + 1]); o.put("\n");
+    o.pad(d); o.put("}");
+  };
+  o.pad(depth + 1); o.put("\"config\": \"P:"); o.i64(c->x[i]); o.put("x"); key(pg); o.put("|D:"); o.i64(c->y[i]);
+  o.put("x"); key(dg); o.put("\",\n");
+  o.pad(depth + 1); o.put("\"decode\": "); side(dg, c->y[i]); o.put(",\n");
+  flag_lines();
+  o.pad(depth + 1); o.put("\"gpus\": "); o.i64(c->gpus[i]); o.put(",\n");
+  o.pad(depth + 1); o.put("\"mode\": \"disaggregated\",\n");
+  o.pad(depth + 1); o.put("\"prefill\": "); side(pg, c->x[i]); o.put(",\n");
+  o.pad(depth + 1); o.put("\"r_sys\": "); o.puts(f[3]); o.put(",\n");
+  tail();
+  return true;
+}
+
+int64_t lc_report_rows(const lc_report_cols* c, const int64_t* rows, int64_t n_sel, int32_t depth, int32_t flags,
+                       char* out, int64_t cap) {
+  if (!c || depth < 0 || depth > 3 || n_sel < 0) {
+    fail(LC_ERR_ARG, "lc_report_rows: bad argument");
+    return -1;
+  }
+  lcr::Out o{out, 0, out ? cap : 0};
+  const int64_t n = rows ? n_sel : c->n;
+  if (n == 0) {
+    o.put("[]");
+    return o.n;
+  }
+  o.put("[\n");
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t i = rows ? rows[k] : k;
+    if (i < 0 || i >= c->n) {
+      fail(LC_ERR_ARG, "lc_report_rows: row index out of range");
+      return -1;
+    }
+    o.pad(depth + 1);
+    if (!put_row(o, c, i, depth + 1, flags != 0)) {
+      fail(LC_ERR_ARG, "Out of range float values are not JSON compliant");
+      return -2;
+    }
+    o.put(k + 1 < n ? ",\n" : "\n");
+  }
+  o.pad(depth);
+  o.put("]");
+  return o.n;
 }
 
 int lc_stream(lc_ctx* c, void** stream) {

@@ -88,12 +88,6 @@ class _Writer:
         self.on_front = on_front
         self.model_json = json.dumps(cols.model)
         self.rt = {d: _runtime_block(cols.runtime, d) for d in (2, 3, 4)}
-        # floats rendered once per column
-        self.s_ttft = [_f(v) for v in cols.ttft.tolist()]
-        self.s_tpot = [_f(v) for v in cols.tpot.tolist()]
-        self.s_thru = [_f(v) for v in cols.thru.tolist()]
-        self.s_speed = ["null" if not math.isfinite(v) else _f(v) for v in cols.speed.tolist()]
-        self.s_rsys = [_f(v) for v in cols.r_sys.tolist()] if cols.r_sys is not None else None
 
     def label(self, i: int) -> str:
         c = self.c
@@ -110,8 +104,10 @@ class _Writer:
         if flags:
             fl = (f'{p}"feasible": {"true" if c.feasible[i] else "false"},\n'
                   f'{p}"frontier": {"true" if self.on_front[i] else "false"},\n')
-        tail = (f'{p}"speed": {self.s_speed[i]},\n{p}"throughput_per_gpu": {self.s_thru[i]},\n'
-                f'{p}"tpot_ms": {self.s_tpot[i]},\n{p}"ttft_ms": {self.s_ttft[i]}{extra}\n{e}}}')
+        sp = float(c.speed[i])
+        speed = "null" if not math.isfinite(sp) else _f(sp)
+        tail = (f'{p}"speed": {speed},\n{p}"throughput_per_gpu": {_f(float(c.thru[i]))},\n'
+                f'{p}"tpot_ms": {_f(float(c.tpot[i]))},\n{p}"ttft_ms": {_f(float(c.ttft[i]))}{extra}\n{e}}}')
         if c.mode[i] < 2:
             cfg = c.cfg[i]
             return (f'{{\n{p}"batch": {cfg[4]},\n{p}"config": "{_key(cfg)}",\n{fl}{p}"gpus": {c.gpus[i]},\n'
@@ -126,7 +122,7 @@ class _Writer:
 
         return (f'{{\n{p}"config": "{self.label(i)}",\n{p}"decode": {side(c.dcfg[i], c.y[i])},\n{fl}'
                 f'{p}"gpus": {c.gpus[i]},\n{p}"mode": "disaggregated",\n{p}"prefill": {side(c.pcfg[i], c.x[i])},\n'
-                f'{p}"r_sys": {self.s_rsys[i]},\n{tail}')
+                f'{p}"r_sys": {_f(float(c.r_sys[i]))},\n{tail}')
 
 
 def _list(items: list[str], depth: int) -> str:
@@ -136,12 +132,85 @@ def _list(items: list[str], depth: int) -> str:
     return "[\n" + ",\n".join(p + it for it in items) + "\n" + "  " * depth + "]"
 
 
-def report_json(cols: Columns) -> str:
-    """Bytes of SearchReport.to_json() for these columns."""
+class _NativeRows:
+    """The "rows" / "frontier" lists written by lc_report_rows (C ABI, host code)."""
+
+    def __init__(self, cols: Columns):
+        import ctypes as C
+
+        from . import _native as N
+
+        self.lib = N.load_library()
+        n = len(cols.mode)
+        self.n = n
+
+        def arr(a, dt, shape=None):
+            if a is None:
+                a = np.zeros(shape if shape is not None else max(n, 1), dtype=dt)
+            return np.ascontiguousarray(a, dtype=dt)
+
+        self.keep = {
+            "mode": arr(cols.mode, np.int32), "cfg": arr(cols.cfg, np.int64, (max(n, 1), 5)),
+            "gpus": arr(cols.gpus, np.int64), "ttft": arr(cols.ttft, np.float64), "tpot": arr(cols.tpot, np.float64),
+            "speed": arr(cols.speed, np.float64), "thru": arr(cols.thru, np.float64),
+            "feasible": arr(cols.feasible, np.uint8), "pcfg": arr(cols.pcfg, np.int64, (max(n, 1), 5)),
+            "dcfg": arr(cols.dcfg, np.int64, (max(n, 1), 5)), "x": arr(cols.x, np.int64), "y": arr(cols.y, np.int64),
+            "r_sys": arr(cols.r_sys, np.float64),
+        }
+        front = np.zeros(max(n, 1), dtype=np.uint8)
+        front[list(cols.frontier_rows)] = 1
+        self.keep["frontier"] = front
+        rc = N.LcReportCols()
+        rc.n = n
+        for name, a in self.keep.items():
+            ctype = {np.dtype(np.int32): C.c_int32, np.dtype(np.int64): C.c_int64, np.dtype(np.float64): C.c_double,
+                     np.dtype(np.uint8): C.c_uint8}[a.dtype]
+            setattr(rc, name, a.ctypes.data_as(C.POINTER(ctype)))
+        self.model_json = json.dumps(cols.model).encode()
+        rc.model_json = self.model_json
+        self.rt = [_runtime_block(cols.runtime, d).encode() for d in range(6)]
+        for d in range(6):
+            rc.runtime[d] = self.rt[d]
+        self.rc = rc
+
+    def list(self, rows, depth: int, flags: bool) -> str:
+        import ctypes as C
+
+        idx = None if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
+        n_sel = self.n if idx is None else len(idx)
+        ip = None if idx is None else idx.ctypes.data_as(C.POINTER(C.c_int64))
+        cap = 800 * max(n_sel, 1) + 64
+        for _ in range(2):
+            buf = np.empty(cap, dtype=np.uint8)  # no zero fill
+            got = self.lib.lc_report_rows(C.byref(self.rc), ip, n_sel, depth, int(flags),
+                                          buf.ctypes.data_as(C.c_char_p), cap)
+            if got == -2:
+                raise ValueError("Out of range float values are not JSON compliant")
+            if got < 0:
+                raise RuntimeError(self.lib.lc_last_error().decode())
+            if got <= cap:
+                return buf[:got].tobytes().decode("ascii")
+            cap = got
+        raise RuntimeError("lc_report_rows: size changed between calls")
+
+
+def report_json(cols: Columns, native: bool = True) -> str:
+    """Bytes of SearchReport.to_json() for these columns.
+
+    The row lists (the bulk of a large report) are written by the native
+    writer (``lc_report_rows``); ``native=False`` keeps them in Python, the
+    writer the tests hold it against.
+    """
     w = _Writer(cols)
     n = len(cols.mode)
-    rows = [w.row(i, 2, True) for i in range(n)]
-    frontier = [rows[i] for i in cols.frontier_rows]
+    if native:
+        nat = _NativeRows(cols)
+        rows_list = nat.list(None, 1, True)
+        frontier_list = nat.list(list(cols.frontier_rows), 1, True)
+    else:
+        rows = [w.row(i, 2, True) for i in range(n)]
+        rows_list = _list(rows, 1)
+        frontier_list = _list([rows[i] for i in cols.frontier_rows], 1)
     best = w.row(cols.best, 1, False) if cols.best >= 0 else "null"
     if cols.best < 0 and cols.nearest >= 0:
         v = cols.violation
@@ -158,9 +227,9 @@ def report_json(cols: Columns) -> str:
         '  "best": ' + best,
         '  "counts": ' + _indent(json.dumps(counts, sort_keys=True, indent=2), 1),
         '  "diagnostics": ' + diagnostics,
-        '  "frontier": ' + _list(frontier, 1),
+        '  "frontier": ' + frontier_list,
         '  "model": ' + w.model_json,
-        '  "rows": ' + _list(rows, 1),
+        '  "rows": ' + rows_list,
         '  "schema": ' + json.dumps(REPORT_SCHEMA),
         '  "skipped": ' + _list(skipped, 1),
         '  "timing": ' + _indent(json.dumps(timing, sort_keys=True, indent=2, allow_nan=False), 1),
