@@ -173,7 +173,8 @@ class _NativeRows:
             rc.runtime[d] = self.rt[d]
         self.rc = rc
 
-    def list(self, rows, depth: int, flags: bool) -> str:
+    def write(self, rows, depth: int, flags: bool, head: bytes = b"", tail: bytes = b"") -> str:
+        """head + the JSON list of the rows + tail, decoded once from one buffer."""
         import ctypes as C
 
         idx = None if rows is None else np.ascontiguousarray(rows, dtype=np.int64)
@@ -181,17 +182,23 @@ class _NativeRows:
         ip = None if idx is None else idx.ctypes.data_as(C.POINTER(C.c_int64))
         cap = 800 * max(n_sel, 1) + 64
         for _ in range(2):
-            buf = np.empty(cap, dtype=np.uint8)  # no zero fill
-            got = self.lib.lc_report_rows(C.byref(self.rc), ip, n_sel, depth, int(flags),
-                                          buf.ctypes.data_as(C.c_char_p), cap)
+            buf = np.empty(len(head) + cap + len(tail), dtype=np.uint8)  # no zero fill
+            buf[: len(head)] = np.frombuffer(head, dtype=np.uint8)
+            at = buf[len(head):].ctypes.data_as(C.c_char_p)
+            got = self.lib.lc_report_rows(C.byref(self.rc), ip, n_sel, depth, int(flags), at, cap)
             if got == -2:
                 raise ValueError("Out of range float values are not JSON compliant")
             if got < 0:
                 raise RuntimeError(self.lib.lc_last_error().decode())
             if got <= cap:
-                return buf[:got].tobytes().decode("ascii")
+                end = len(head) + got
+                buf[end: end + len(tail)] = np.frombuffer(tail, dtype=np.uint8)
+                return str(memoryview(buf)[: end + len(tail)], "ascii")
             cap = got
         raise RuntimeError("lc_report_rows: size changed between calls")
+
+    def list(self, rows, depth: int, flags: bool) -> str:
+        return self.write(rows, depth, flags)
 
 
 def report_json(cols: Columns, native: bool = True) -> str:
@@ -203,9 +210,10 @@ def report_json(cols: Columns, native: bool = True) -> str:
     """
     w = _Writer(cols)
     n = len(cols.mode)
+    nat = None
     if native:
         nat = _NativeRows(cols)
-        rows_list = nat.list(None, 1, True)
+        rows_list = None  # written straight into the output buffer below
         frontier_list = nat.list(list(cols.frontier_rows), 1, True)
     else:
         rows = [w.row(i, 2, True) for i in range(n)]
@@ -229,14 +237,18 @@ def report_json(cols: Columns, native: bool = True) -> str:
         '  "diagnostics": ' + diagnostics,
         '  "frontier": ' + frontier_list,
         '  "model": ' + w.model_json,
-        '  "rows": ' + rows_list,
+        '  "rows": ' + (rows_list if rows_list is not None else ""),
         '  "schema": ' + json.dumps(REPORT_SCHEMA),
         '  "skipped": ' + _list(skipped, 1),
         '  "timing": ' + _indent(json.dumps(timing, sort_keys=True, indent=2, allow_nan=False), 1),
         '  "version": ' + json.dumps(REPORT_VERSION),
         '  "workload": ' + _indent(json.dumps(cols.workload_doc, sort_keys=True, indent=2), 1),
     ]
-    return ",\n".join(parts) + "\n}\n"
+    if nat is None:
+        return ",\n".join(parts) + "\n}\n"
+    head = (",\n".join(parts[:7])).encode("ascii")  # ... '  "rows": '
+    tail = (",\n" + ",\n".join(parts[7:]) + "\n}\n").encode("ascii")
+    return nat.write(None, 1, True, head, tail)
 
 
 # ----------------------------------------------------------------------------- builders
