@@ -121,3 +121,21 @@ def test_estimate_matches_drop_in(mode):
     want = fn(db, model, cfg, wl).to_doc()
     want["config"] = cfg.key()
     assert json.loads(r.stdout) == want
+
+
+@pytest.mark.gpu
+def test_dbgen_writes_the_reference_database(tmp_path):
+    out = tmp_path / "db.jsonl"
+    r = _run("dbgen", "--model", str(SPECS / "model-qwen3-32b.json"), "--hardware", str(SPECS / "hw-h100-sxm.json"),
+             "--seed", "11", "-o", str(out))
+    assert r.returncode == 0, r.stderr
+    want = gzip.decompress((ROOT / "tests" / "golden" / "db" / "db-qwen3-32b-h100-sxm-s11.jsonl.gz").read_bytes())
+    assert out.read_bytes() == want
+
+
+@pytest.mark.gpu
+def test_estimate_reports_infeasible_config_with_exit_1():
+    case = BY_NAME["a1_qwen_small"]
+    r = _run("estimate", "--db", str(db_path(case)), "--model", str(SPECS / "model-qwen-small.json"),
+             "--isl", "512", "--osl", "64", "--tp", "3", "--batch", "4")
+    assert r.returncode == 1 and "does not divide" in r.stderr
