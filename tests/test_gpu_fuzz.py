@@ -14,6 +14,7 @@ search against the oracle.
 from __future__ import annotations
 
 import json
+import os
 import random
 
 import pytest
@@ -123,7 +124,11 @@ def _objects(mdoc, wdoc, sdoc, ddoc):
     return model, workload, space, dc
 
 
-@pytest.mark.parametrize("seed", range(200))
+N_SINGLE = int(os.environ.get("LC_FUZZ_N", "200"))      # LC_FUZZ_N=3000 for a long campaign
+N_BATCH = int(os.environ.get("LC_FUZZ_BATCHES", "30"))
+
+
+@pytest.mark.parametrize("seed", range(N_SINGLE))
 def test_random_search_matches_oracle(seed):
     import paper_2601_06288_b200 as pkg
     from oracle import oracle
@@ -139,7 +144,7 @@ def test_random_search_matches_oracle(seed):
     assert not diffs, f"{model_name} {extrapolation} {wdoc} {sdoc} {ddoc}\n" + "\n".join(diffs)
 
 
-@pytest.mark.parametrize("seed", range(1000, 1030))
+@pytest.mark.parametrize("seed", range(100_000, 100_000 + N_BATCH))
 def test_random_batch_matches_oracle(seed):
     from oracle import oracle
     from paper_2601_06288_b200.engine import build_report, get_engine
