@@ -73,63 +73,63 @@ __device__ __forceinline__ int lower_bound_i64(const int64_t* v, int n, int64_t 
   return lo;
 }
 
-// _interp_cells (perfdb.py:509-536) for coordinates inside the box.
+// _interp_cells (perfdb.py:509-536) for coordinates inside the box.  At most
+// two axes, so the corners are spelled out (no dynamically indexed arrays):
+// corner order is axis-major, lo before hi; a corner whose weight factor is
+// exactly zero is skipped (t < 1.0 / t > 0.0); weights are the products of the
+// per-axis factors (x * 1.0 == x, so exact axes need no special case).
+__device__ __forceinline__ void axis_pos(const DbView& D, const DevGrid& G, int a, int64_t x, int* lo, int* hi,
+                                         double* t, bool* exact, int* n_log_calls) {
+  const int64_t* v = D.axv + G.ax_off[a];
+  const double* lv = D.axl + G.ax_off[a];
+  const int i = lower_bound_i64(v, G.ax_len[a], x);
+  if (v[i] == x) {
+    *lo = *hi = i;
+    *t = 0.0;
+    *exact = true;
+  } else {
+    *lo = i - 1;
+    *hi = i;
+    *exact = false;
+    const double lx = glibc::log_fma((double)x, D.logtab);
+    ++*n_log_calls;
+    *t = (lx - lv[i - 1]) / (lv[i] - lv[i - 1]);
+  }
+}
+
 __device__ __noinline__ double interp_cells(const DbView& D, const DevGrid& G, int64_t c0, int64_t c1,
                                                int* n_log_calls) {
-  int lo[2], hi[2];
-  double t[2] = {0.0, 0.0};
-  bool exact = true;
-  const int64_t cs[2] = {c0, c1};
-#pragma unroll
-  for (int a = 0; a < 2; ++a) {
-    if (a >= G.ndim) { lo[a] = hi[a] = 0; continue; }
-    const int64_t* v = D.axv + G.ax_off[a];
-    const double* lv = D.axl + G.ax_off[a];
-    const int i = lower_bound_i64(v, G.ax_len[a], cs[a]);
-    if (v[i] == cs[a]) {
-      lo[a] = hi[a] = i;
-    } else {
-      lo[a] = i - 1;
-      hi[a] = i;
-      exact = false;
-      const double lx = glibc::log_fma((double)cs[a], D.logtab);
-      ++*n_log_calls;
-      t[a] = (lx - lv[i - 1]) / (lv[i] - lv[i - 1]);
-    }
-  }
+  int lo0, hi0, lo1 = 0, hi1 = 0;
+  double t0, t1 = 0.0;
+  bool ex0, ex1 = true;
+  axis_pos(D, G, 0, c0, &lo0, &hi0, &t0, &ex0, n_log_calls);
+  if (G.ndim == 2) axis_pos(D, G, 1, c1, &lo1, &hi1, &t1, &ex1, n_log_calls);
   const int n1 = G.ndim == 2 ? G.ax_len[1] : 1;
   const double* cells = D.cell + G.cell_off;
   const double* clogs = D.clog + G.cell_off;
-  if (exact) return cells[lo[0] * n1 + (G.ndim == 2 ? lo[1] : 0)];
-  // corners: axis-major, lo before hi, zero weights skipped (t < 1.0 / t > 0.0)
-  double w[4];
-  int ci[4];
-  int nc = 1;
-  w[0] = 1.0;
-  ci[0] = 0;
-  for (int a = 0; a < G.ndim; ++a) {
-    double nw[4];
-    int nci[4];
-    int m = 0;
-    const int stride = a == 0 ? n1 : 1;
-    for (int c = 0; c < nc; ++c) {
-      if (lo[a] == hi[a]) {
-        nw[m] = w[c]; nci[m] = ci[c] + lo[a] * stride; ++m;
-      } else {
-        if (t[a] < 1.0) { nw[m] = w[c] * (1.0 - t[a]); nci[m] = ci[c] + lo[a] * stride; ++m; }
-        if (t[a] > 0.0) { nw[m] = w[c] * t[a]; nci[m] = ci[c] + hi[a] * stride; ++m; }
-      }
-    }
-    nc = m;
-    for (int c = 0; c < m; ++c) { w[c] = nw[c]; ci[c] = nci[c]; }
-  }
-  const double v0 = cells[ci[0]];
+  if (ex0 && ex1) return cells[lo0 * n1 + lo1];
+  // corners present per axis: the lo side unless its factor (1 - t) is zero, the hi side if t > 0
+  const bool a_lo = ex0 || t0 < 1.0, a_hi = !ex0 && t0 > 0.0;
+  const bool b_lo = ex1 || t1 < 1.0, b_hi = !ex1 && t1 > 0.0;
+  const double fa_lo = ex0 ? 1.0 : 1.0 - t0, fa_hi = t0;
+  const double fb_lo = ex1 ? 1.0 : 1.0 - t1, fb_hi = t1;
+  const bool p00 = a_lo && b_lo, p01 = a_lo && b_hi, p10 = a_hi && b_lo, p11 = a_hi && b_hi;
+  const int i00 = lo0 * n1 + lo1, i01 = lo0 * n1 + hi1, i10 = hi0 * n1 + lo1, i11 = hi0 * n1 + hi1;
+  const int first = p00 ? i00 : (p01 ? i01 : (p10 ? i10 : i11));
+  const double v0 = cells[first];
+  const int nc = (int)p00 + (int)p01 + (int)p10 + (int)p11;
   if (nc == 1) return v0;
   bool same = true;
-  for (int c = 1; c < nc; ++c) same &= cells[ci[c]] == v0;
+  if (p00) same &= cells[i00] == v0;
+  if (p01) same &= cells[i01] == v0;
+  if (p10) same &= cells[i10] == v0;
+  if (p11) same &= cells[i11] == v0;
   if (same) return v0;  // constant cells stay bit-exact
   NeumaierSum s;
-  for (int c = 0; c < nc; ++c) s.add(w[c] * clogs[ci[c]]);
+  if (p00) s.add((fa_lo * fb_lo) * clogs[i00]);
+  if (p01) s.add((fa_lo * fb_hi) * clogs[i01]);
+  if (p10) s.add((fa_hi * fb_lo) * clogs[i10]);
+  if (p11) s.add((fa_hi * fb_hi) * clogs[i11]);
   return glibc::exp_fma(s.result(), D.exptab);
 }
 
