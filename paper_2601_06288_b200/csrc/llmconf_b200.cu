@@ -1006,6 +1006,12 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
     if (!e.code) {
       NeumaierSum pre;
       for (int i = 0; i < gi; ++i) pre.add(term[i]);
+      // the terms after the attention entry, in registers for the sample loop
+      constexpr int kPostRegs = 10;
+      const int npost = m - gi - 1;
+      double post[kPostRegs];
+#pragma unroll
+      for (int i = 0; i < kPostRegs; ++i) post[i] = i < npost ? term[gi + 1 + i] : 0.0;
       double t_gen = 0.0;
 #ifndef LC_DECODE_CHAINS
 #define LC_DECODE_CHAINS 2
@@ -1029,10 +1035,19 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
           sc[j] = pre;
           sc[j].add(g[j]);
         }
-        for (int i = gi + 1; i < m; ++i) {
-          const double xv = term[i];
+        if (npost <= kPostRegs) {
 #pragma unroll
-          for (int j = 0; j < LC_DECODE_CHAINS; ++j) sc[j].add(xv);
+          for (int i = 0; i < kPostRegs; ++i) {
+            if (i >= npost) break;
+#pragma unroll
+            for (int j = 0; j < LC_DECODE_CHAINS; ++j) sc[j].add(post[i]);
+          }
+        } else {
+          for (int i = gi + 1; i < m; ++i) {
+            const double xv = term[i];
+#pragma unroll
+            for (int j = 0; j < LC_DECODE_CHAINS; ++j) sc[j].add(xv);
+          }
         }
 #pragma unroll
         for (int j = 0; j < LC_DECODE_CHAINS; ++j) {
