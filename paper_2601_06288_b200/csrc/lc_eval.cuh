@@ -97,7 +97,7 @@ __device__ __forceinline__ void axis_pos(const DbView& D, const DevGrid& G, int 
   }
 }
 
-__device__ __noinline__ double interp_cells(const DbView& D, const DevGrid& G, int64_t c0, int64_t c1,
+__device__ __noinline__ double interp_cells(const DbView& D, const DevGrid G, int64_t c0, int64_t c1,
                                                int* n_log_calls) {
   int lo0, hi0, lo1 = 0, hi1 = 0;
   double t0, t1 = 0.0;
@@ -175,29 +175,38 @@ __device__ __noinline__ double sol_us(const DbView& D, int kind, int quant, cons
   return (c > a ? c : a) * 1e6;
 }
 
-// query_latency (perfdb.py:539-580) for one plan entry with coordinates in d[0..1].
-__device__ __noinline__ double query(const DbView& D, const lc_entry& e, int64_t* d, int* st, int* n_logs) {
-  if (e.grid < 0) { *st = LC_ST_MISSING_KEY; return 0.0; }
-  const DevGrid G = D.grids[e.grid];
+// query_latency (perfdb.py:539-580) for one query: grid id, kind, quant and the
+// canonical dims d0..d4 (interpolated axes in d0, d1).  Everything is passed by
+// value so callers keep their operands in registers.
+__device__ __noinline__ double query(const DbView& D, int32_t grid, int32_t kind, int32_t quant, int64_t d0,
+                                    int64_t d1, int64_t d2, int64_t d3, int64_t d4, int* st, int* n_logs) {
+  if (grid < 0) { *st = LC_ST_MISSING_KEY; return 0.0; }
+  const DevGrid G = D.grids[grid];
   bool any_oob = false, any_above = false;
-  int64_t cl[2] = {d[0], d[1]};
-  for (int a = 0; a < G.ndim; ++a) {
-    const int64_t* v = D.axv + G.ax_off[a];
-    const int64_t lo = v[0], hi = v[G.ax_len[a] - 1];
-    if (d[a] < lo) { any_oob = true; cl[a] = lo; }
-    if (d[a] > hi) { any_oob = any_above = true; cl[a] = hi; }
+  int64_t cl0 = d0, cl1 = d1;
+  {
+    const int64_t* v = D.axv + G.ax_off[0];
+    const int64_t lo = v[0], hi = v[G.ax_len[0] - 1];
+    if (d0 < lo) { any_oob = true; cl0 = lo; }
+    if (d0 > hi) { any_oob = any_above = true; cl0 = hi; }
   }
-  if (!any_oob) return interp_cells(D, G, d[0], d[1], n_logs);
+  if (G.ndim == 2) {
+    const int64_t* v = D.axv + G.ax_off[1];
+    const int64_t lo = v[0], hi = v[G.ax_len[1] - 1];
+    if (d1 < lo) { any_oob = true; cl1 = lo; }
+    if (d1 > hi) { any_oob = any_above = true; cl1 = hi; }
+  }
+  if (!any_oob) return interp_cells(D, G, d0, d1, n_logs);
   if (D.policy == LC_POLICY_STRICT) { *st = LC_ST_EXTRAPOLATION; return 0.0; }
   const bool use_sol = D.policy == LC_POLICY_SOL || (D.policy == LC_POLICY_DEFAULT && any_above);
-  if (D.policy == LC_POLICY_CLAMP || !use_sol) return interp_cells(D, G, cl[0], cl[1], n_logs);
-  const double edge = interp_cells(D, G, cl[0], cl[1], n_logs);
-  int64_t de[5] = {d[0], d[1], d[2], d[3], d[4]};
-  for (int a = 0; a < G.ndim; ++a) de[a] = cl[a];
-  const double sol_edge = sol_us(D, e.kind, e.quant, de, st);
+  if (D.policy == LC_POLICY_CLAMP || !use_sol) return interp_cells(D, G, cl0, cl1, n_logs);
+  const double edge = interp_cells(D, G, cl0, cl1, n_logs);
+  const int64_t de[5] = {cl0, G.ndim == 2 ? cl1 : d1, d2, d3, d4};
+  const double sol_edge = sol_us(D, kind, quant, de, st);
   if (*st) return 0.0;
   const double eff = edge / sol_edge;
-  const double sol_q = sol_us(D, e.kind, e.quant, d, st);
+  const int64_t dq[5] = {d0, d1, d2, d3, d4};
+  const double sol_q = sol_us(D, kind, quant, dq, st);
   if (*st) return 0.0;
   return sol_q * eff;
 }
