@@ -97,8 +97,8 @@ __device__ __forceinline__ void axis_pos(const DbView& D, const DevGrid& G, int 
   }
 }
 
-__device__ __noinline__ double interp_cells(const DbView& D, const DevGrid G, int64_t c0, int64_t c1,
-                                               int* n_log_calls) {
+__device__ __forceinline__ double interp_body(const DbView& D, const DevGrid G, int64_t c0, int64_t c1,
+                                              int* n_log_calls) {
   int lo0, hi0, lo1 = 0, hi1 = 0;
   double t0, t1 = 0.0;
   bool ex0, ex1 = true;
@@ -131,6 +131,11 @@ __device__ __noinline__ double interp_cells(const DbView& D, const DevGrid G, in
   if (p10) s.add((fa_hi * fb_lo) * clogs[i10]);
   if (p11) s.add((fa_hi * fb_hi) * clogs[i11]);
   return glibc::exp_fma(s.result(), D.exptab);
+}
+
+__device__ __noinline__ double interp_cells(const DbView& D, const DevGrid G, int64_t c0, int64_t c1,
+                                            int* n_log_calls) {
+  return interp_body(D, G, c0, c1, n_log_calls);
 }
 
 // sol_estimate (perfdb.py:431-484); d is the canonical dim vector.
@@ -178,8 +183,9 @@ __device__ __noinline__ double sol_us(const DbView& D, int kind, int quant, cons
 // query_latency (perfdb.py:539-580) for one query: grid id, kind, quant and the
 // canonical dims d0..d4 (interpolated axes in d0, d1).  Everything is passed by
 // value so callers keep their operands in registers.
-__device__ __noinline__ double query(const DbView& D, int32_t grid, int32_t kind, int32_t quant, int64_t d0,
-                                    int64_t d1, int64_t d2, int64_t d3, int64_t d4, int* st, int* n_logs) {
+template <bool INL>
+__device__ __forceinline__ double query_body(const DbView& D, int32_t grid, int32_t kind, int32_t quant, int64_t d0,
+                                             int64_t d1, int64_t d2, int64_t d3, int64_t d4, int* st, int* n_logs) {
   if (grid < 0) { *st = LC_ST_MISSING_KEY; return 0.0; }
   const DevGrid G = D.grids[grid];
   bool any_oob = false, any_above = false;
@@ -196,7 +202,7 @@ __device__ __noinline__ double query(const DbView& D, int32_t grid, int32_t kind
     if (d1 < lo) { any_oob = true; cl1 = lo; }
     if (d1 > hi) { any_oob = any_above = true; cl1 = hi; }
   }
-  if (!any_oob) return interp_cells(D, G, d0, d1, n_logs);
+  if (!any_oob) return INL ? interp_body(D, G, d0, d1, n_logs) : interp_cells(D, G, d0, d1, n_logs);
   if (D.policy == LC_POLICY_STRICT) { *st = LC_ST_EXTRAPOLATION; return 0.0; }
   const bool use_sol = D.policy == LC_POLICY_SOL || (D.policy == LC_POLICY_DEFAULT && any_above);
   if (D.policy == LC_POLICY_CLAMP || !use_sol) return interp_cells(D, G, cl0, cl1, n_logs);
@@ -210,6 +216,18 @@ __device__ __noinline__ double query(const DbView& D, int32_t grid, int32_t kind
   if (*st) return 0.0;
   return sol_q * eff;
 }
+
+__device__ __noinline__ double query(const DbView& D, int32_t grid, int32_t kind, int32_t quant, int64_t d0,
+                                    int64_t d1, int64_t d2, int64_t d3, int64_t d4, int* st, int* n_logs) {
+  return query_body<false>(D, grid, kind, quant, d0, d1, d2, d3, d4, st, n_logs);
+}
+
+// the table kernels have one query site each: inline the common (inside-the-box) path there
+#ifdef LC_NO_INLINE_TABLES
+#define LC_TABLE_QUERY query
+#else
+#define LC_TABLE_QUERY query_body<true>
+#endif
 
 enum { PH_PREFILL = 0, PH_DECODE = 1, PH_MIXED = 2 };
 

@@ -859,7 +859,7 @@ __global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_qtabl
     int64_t d[5];
     if (need && entry_coords(SL.e, a, P.hidden, d)) {
       int st = 0, nlog = 0;
-      out.lat = query(V, SL.e.grid, SL.e.kind, SL.e.quant, d[0], d[1], d[2], d[3], d[4], &st, &nlog);
+      out.lat = LC_TABLE_QUERY(V, SL.e.grid, SL.e.kind, SL.e.quant, d[0], d[1], d[2], d[3], d[4], &st, &nlog);
       out.status = st;
     }
     P.qt[x] = out;
@@ -888,8 +888,8 @@ __global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_dstab
     const lc_entry e = P.gclasses[g];
     int st = 0, nlog = 0;
     QVal out;
-    out.lat = query(V, e.grid, e.kind, e.quant, P.batches[G.b_off + bi], G.isl + 32ll * k + 1, e.d[2], e.d[3], e.d[4],
-                    &st, &nlog);
+    out.lat = LC_TABLE_QUERY(V, e.grid, e.kind, e.quant, P.batches[G.b_off + bi], G.isl + 32ll * k + 1, e.d[2], e.d[3],
+                             e.d[4], &st, &nlog);
     out.status = st;
     out._pad = 0;
     P.ds[x] = out;
