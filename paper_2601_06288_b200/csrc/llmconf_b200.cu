@@ -455,7 +455,7 @@ __global__ void k_unit_offsets(SearchMeta* meta, int n_search, const int32_t* po
 }
 
 #ifndef LC_TAIL_MIN_BLOCKS
-#define LC_TAIL_MIN_BLOCKS 4  // 64 registers: 32 warps per SM for the warp-per-tail radix select
+#define LC_TAIL_MIN_BLOCKS 3  // 80 registers: no spills of the per-lane expert counts and keys (measured best)
 #endif
 // ---- K0 in closed form.  fits_memory (model.py:440-479) is monotone in the
 // batch size: the activation term grows with it, so the static footprint grows
