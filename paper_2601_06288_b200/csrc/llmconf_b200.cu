@@ -2019,7 +2019,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_pass3(EvalParams P, con
 }
 
 #ifndef LC_FINAL_THREADS
-#define LC_FINAL_THREADS 256
+#define LC_FINAL_THREADS 512
 #endif
 constexpr int kFinalThreads = LC_FINAL_THREADS;
 __global__ void __launch_bounds__(kFinalThreads) k_front_final(EvalParams P, const SearchMeta* meta,
