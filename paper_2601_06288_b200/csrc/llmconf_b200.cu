@@ -1421,7 +1421,10 @@ __device__ __forceinline__ bool pool_less(const EvalParams& P, const PoolKey& a,
 
 // ---- K5a: top-k prefill / decode pool members per search (block per search)
 constexpr int kPoolLocal = 16;  // per-thread top-k list length (caps up to 16 take the fast path)
-constexpr int kPoolThreads = 128;
+#ifndef LC_POOL_THREADS
+#define LC_POOL_THREADS 128
+#endif
+constexpr int kPoolThreads = LC_POOL_THREADS;
 
 __device__ __forceinline__ void local_insert(const EvalParams& P, PoolKey* lst, int& n, int cap, const PoolKey& k) {
   if (n == cap && !pool_less(P, k, lst[n - 1])) return;
