@@ -111,6 +111,8 @@ struct lc_space {
   int32_t class_n[4], class_off[4], class_n2d[4];
   lc_entry* gclasses;
   int32_t* gclass_of;  // [n_tmpl]
+  int32_t* tmpl_cidx_off;  // [n_tmpl + 1] into tmpl_cidx
+  int32_t* tmpl_cidx;      // combo indices of each template
 };
 
 // Query-table sharing.  A slot's inputs are (grid, coordinates); which search
@@ -258,6 +260,7 @@ struct lc_ctx {
   size_t pinned_plans_cap = 0;
   bool staged = false;  // fronts + plans of the last batch already copied to the pinned buffers
   bool batches_sorted = false;  // every search's batch list is non-decreasing: K0 in closed form
+  bool enum_fit = false;        // the last K0 ran in closed form (block_sums = per-(search, combo) unit offsets)
   std::vector<int32_t> hsearch_nb;
   unsigned char* arena = nullptr;  // page-locked staging for the batch's inputs and summaries
   size_t arena_cap = 0, arena_used = 0;
@@ -320,6 +323,10 @@ struct EvalParams {
   int64_t n_cells_total;
   lc_search_result* results;
   SearchAcc* acc;                    // [n_search]
+  // closed-form K0 (fused candidate rows): unit offsets per (search, combo), budget flags, template combos
+  const int32_t* pair_off;           // [n_search * n_combos + 1], nullptr otherwise
+  const uint8_t* pair_inb;
+  const int32_t* tmpl_cidx_off; const int32_t* tmpl_cidx;
 };
 
 __device__ __forceinline__ int find_search(const SearchMeta* meta, int n, int64_t r) {
@@ -1111,134 +1118,6 @@ __global__ void __launch_bounds__(128) k_ptables(EvalParams P) {
 }
 
 // K2: one thread per cell assembles every step from the tables.
-__global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalParams P) {
-  const int64_t ncell = P.n_cells_total;
-  for (int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ci < ncell;
-       ci += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t cf = P.cell_flags[ci];
-    if (!cf) continue;
-    const int s = find_cell_search(P.meta, P.n_search, ci);
-    const lc_search_desc& S = P.searches[s];
-    const SearchMeta& M = P.meta[s];
-    const int64_t rel = ci - M.cell_off;
-    const int tmpl = (int)(rel / S.n_b), bi = (int)(rel % S.n_b);
-    const TmplInfo ti = P.tmpl_info[tmpl];
-    lc_combo c;  // the fields expert_tokens() reads
-    c.tp = ti.tp; c.pp = ti.pp; c.ep = ti.ep; c.tp_i = ti.tp_i; c.ep_i = ti.ep_i;
-    const lc_entry* E = P.entries + (int64_t)tmpl * LC_MAX_ENTRIES;
-    const int ne = P.tmpl_n[tmpl];
-    const int32_t* so = P.slot_of + (int64_t)tmpl * LC_MAX_ENTRIES * 3;
-    const int64_t b = P.batches[S.b_off + bi];
-    const bool do_st = (cf & 1) && (S.modes & 1), do_ag = (cf & 1) && (S.modes & 2), do_dg = (cf & 2) != 0;
-    const int64_t mb = b > 1 ? b : 1;
-    const double bubble = (double)(mb + ti.pp - 1) / (double)mb;
-    const int64_t chunk = S.isl - S.prefix;
-    const int64_t kv_mid = S.isl + S.osl / 2;
-    CellOut o;
-    o.st_status = o.ag_status = o.pf_status = o.dc_status = LC_ST_NOT_EVALUATED;
-    o.st_ttft = o.st_tpot = o.ag_ttft = o.ag_tpot = o.pf_lat = o.dc_lat = 0.0;
-    o.qP = o.qSD = o.qM = o.qG = 0;
-    o.st_steps = 0;
-    o.flags = 0;
-    int q1 = 0, q2 = 0;
-
-    // prefill step: static TTFT and the prefill pool
-    double p_total = 0.0;
-    ErrRec p_err{0, 0, 0, 0};
-    if (do_st || do_dg) {
-      if (M.pstep_off >= 0) {  // shared with the other searches of the prefill group (k_ptables)
-        const PStep ps = P.psteps[M.pstep_off + rel];
-        p_total = ps.total;
-        p_err.code = ps.status & 0xff; p_err.label = ps.status >> 8; p_err.c0 = ps.c0; p_err.c1 = ps.c1;
-        o.qP = ps.q;
-      } else {
-        const StepArgs a{PH_PREFILL, b * chunk, 0, chunk, expert_tokens(P, c, M, S, 0, bi, b * chunk)};
-        table_step(P, M, E, ne, so + LC_STEP_PREFILL, S.n_b, bi, a, bubble, &p_total, &p_err, &q1, &q2);
-        if (!p_err.code) o.qP = (q1 & 0xffff) | (q2 << 16);
-      }
-      o.pf_status = p_err.code | (p_err.label << 8);
-      o.pf_lat = p_total;
-      if (p_err.code) put_cell_err(P, 2, ci, p_err);
-    }
-    const int64_t xt_dec = expert_tokens(P, c, M, S, 1, bi, b);
-    const StepArgs ga{PH_DECODE, 0, b, kv_mid, xt_dec};
-    if (do_st) {
-      double tpot = 0.0;
-      ErrRec e = p_err;
-      if (!e.code && S.osl > 1) {
-        const SdOut sd = P.sd[ci];  // k_dseries
-        if (sd.status) {
-          e.code = sd.status & 0xff; e.label = sd.status >> 8; e.c0 = sd.c0; e.c1 = sd.c1;
-        } else {
-          tpot = sd.t_gen / (double)(S.osl - 1);
-          o.qSD = sd.qsd;
-          o.st_steps = M.n_steps;
-        }
-      }
-      o.st_status = e.code | (e.label << 8);
-      o.st_ttft = p_total;
-      o.st_tpot = tpot;
-      if (e.code) put_cell_err(P, 0, ci, e);
-    }
-    // generation step at the KV midpoint: aggregated l_gen and the decode pool
-    bool g_done = false;
-    double g_total = 0.0;
-    ErrRec g_err{0, 0, 0, 0};
-    if (do_ag) {
-      const AggSched sc = agg_schedule(S, b);
-      ErrRec e{sc.st, 0, 0, 0};
-      double ttft = 0.0, tpot = 0.0;
-      if (!sc.st) {
-        double l_mix = 0.0, l_gen = 0.0;
-        const StepArgs a{PH_MIXED, sc.chunk_tokens, sc.n_mix_gen, kv_mid,
-                         expert_tokens(P, c, M, S, 2, bi, sc.chunk_tokens + sc.n_mix_gen)};
-        table_step(P, M, E, ne, so + LC_STEP_MIXED, S.n_b, bi, a, bubble, &l_mix, &e, &q1, &q2);
-        if (!e.code) o.qM = (q1 & 0xffff) | (q2 << 16);
-        if (!e.code && (sc.t_gen || b == 1)) {
-          table_step(P, M, E, ne, so + LC_STEP_GEN, S.n_b, bi, ga, bubble, &g_total, &g_err, &q1, &q2);
-          g_done = true;
-          if (!g_err.code) o.qG = (q1 & 0xffff) | (q2 << 16);
-          o.flags |= 1;
-          e = g_err;
-          l_gen = g_total;
-        }
-        if (!e.code) {
-          const double raw = 2.0 + (double)(sc.T - 3) * (1.0 / 20.0);
-          double F = raw > 2.0 ? raw : 2.0;
-          F = F < 4.0 ? F : 4.0;
-          ttft = l_mix * (double)sc.cpr * F;
-          if (b == 1) tpot = S.osl > 1 ? l_gen : 0.0;
-          else if (S.osl == 1) tpot = 0.0;
-          else if (sc.t_gen == 0) tpot = l_mix;
-          else {
-            const int64_t ms = sc.t_mix - 3 > 1 ? sc.t_mix - 3 : 1;
-            tpot = (l_mix * (double)ms + l_gen * (double)sc.t_gen) / (double)(ms + sc.t_gen);
-          }
-        }
-      }
-      o.ag_status = e.code | (e.label << 8);
-      o.ag_ttft = ttft;
-      o.ag_tpot = tpot;
-      if (e.code) put_cell_err(P, 1, ci, e);
-    }
-    if (do_dg) {
-      if (!g_done) {
-        table_step(P, M, E, ne, so + LC_STEP_GEN, S.n_b, bi, ga, bubble, &g_total, &g_err, &q1, &q2);
-        if (!g_err.code) o.qG = (q1 & 0xffff) | (q2 << 16);
-      }
-      o.dc_status = g_err.code | (g_err.label << 8);
-      o.dc_lat = g_total;
-      if (g_err.code) put_cell_err(P, 3, ci, g_err);
-    }
-    P.cells[ci] = o;
-  }
-}
-
-// K2b: candidates from their cells -- derive_metrics with the candidate's gpu
-// count (serving_modes.py:161-172) and the pool rates (serving_modes.py:366, 380).
-#ifndef LC_EXPAND_MIN_BLOCKS
-#define LC_EXPAND_MIN_BLOCKS 4  // 64 registers (measured: 4.11 -> 4.00 ms per step)
-#endif
 // Warp-aggregated per-search accounting: one set of atomics per warp when all
 // its units belong to one search (the common case), per lane otherwise.
 struct RowAcc {
@@ -1263,6 +1142,258 @@ __device__ __forceinline__ void acc_flush(SearchAcc* A, const RowAcc& r) {
   if (r.smin_c) atomicMax(&A->smin_c, r.smin_c);
 }
 
+// One candidate's rows from its cell (derive_metrics with its gpu count,
+// serving_modes.py:161-172; pool rates, serving_modes.py:366, 380) plus its
+// contribution to the per-search accounting.
+__device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search_desc& S, const CellOut& o, int64_t ci,
+                                            int64_t u, int64_t b, int64_t gpus, bool inb, RowAcc& ra) {
+  const int64_t n = P.n_cap;
+  const bool do_st = (S.modes & 1) && inb, do_ag = (S.modes & 2) && inb, do_dg = (S.modes & 4) != 0;
+  int32_t q = 0;
+  auto add_q = [&](int32_t x) { q += x; };  // packed halves never overflow 16 bits
+  if (do_st) {
+    P.st_status[u] = o.st_status;
+    if (o.st_status) {
+      P.err_c[u] = P.cell_err[ci * 8 + 0]; P.err_c[n + u] = P.cell_err[ci * 8 + 1];
+    } else {
+      double speed, thru;
+      derive_metrics(o.st_ttft, o.st_tpot, b, S.osl, gpus, &speed, &thru);
+      P.st_v[u] = o.st_ttft; P.st_v[n + u] = o.st_tpot; P.st_v[2 * n + u] = speed; P.st_v[3 * n + u] = thru;
+      ++ra.rows;
+      if ((!S.has_ttft || o.st_ttft <= S.ttft_limit) && (!S.has_floor || speed >= S.speed_floor)) {
+        ++ra.feas;
+        ra.feasible_speed(speed);
+      }
+      add_q(o.qSD);
+    }
+  }
+  if (do_ag) {
+    P.ag_status[u] = o.ag_status;
+    if (o.ag_status) {
+      P.err_c[2 * n + u] = P.cell_err[ci * 8 + 2]; P.err_c[3 * n + u] = P.cell_err[ci * 8 + 3];
+    } else {
+      double speed, thru;
+      derive_metrics(o.ag_ttft, o.ag_tpot, b, S.osl, gpus, &speed, &thru);
+      P.ag_v[u] = o.ag_ttft; P.ag_v[n + u] = o.ag_tpot; P.ag_v[2 * n + u] = speed; P.ag_v[3 * n + u] = thru;
+      ++ra.rows;
+      if ((!S.has_ttft || o.ag_ttft <= S.ttft_limit) && (!S.has_floor || speed >= S.speed_floor)) {
+        ++ra.feas;
+        ra.feasible_speed(speed);
+      }
+    }
+    add_q(o.qM);
+  }
+  if (do_st || do_dg) add_q(o.qP);
+  if (do_dg) {
+    P.pf_status[u] = o.pf_status;
+    if (o.pf_status) {
+      P.err_c[4 * n + u] = P.cell_err[ci * 8 + 4]; P.err_c[5 * n + u] = P.cell_err[ci * 8 + 5];
+      P.pool_key[u] = INFINITY;
+    } else {
+      const double rate = (double)b * 1000.0 / o.pf_lat;
+      P.pf_v[u] = o.pf_lat; P.pf_v[n + u] = rate;
+      P.pool_key[u] = -rate / (double)gpus;
+    }
+    P.dc_status[u] = o.dc_status;
+    if (o.dc_status) {
+      P.err_c[6 * n + u] = P.cell_err[ci * 8 + 6]; P.err_c[7 * n + u] = P.cell_err[ci * 8 + 7];
+      P.pool_key[n + u] = INFINITY;
+    } else {
+      const double rate = S.osl == 1 ? INFINITY : (double)b * 1000.0 / ((double)(S.osl - 1) * o.dc_lat);
+      P.dc_v[u] = o.dc_lat;
+      P.dc_v[n + u] = rate;
+      P.pool_key[n + u] = -rate / (double)gpus;
+    }
+  }
+  // the generation step is a memo hit when a static decode step used the same KV length
+  const int64_t k = (S.isl + S.osl / 2) - S.isl - 1;
+  const bool dup = do_st && o.st_status == 0 && S.osl > 1 && k >= 0 && (k % 32) == 0 && (k / 32) < o.st_steps;
+  if (((do_ag && (o.flags & 1)) || do_dg) && !dup) add_q(o.qG);
+  ra.q1 += (unsigned)(q & 0xffff);
+  ra.q2 += (unsigned)(q >> 16);
+  if (inb) {
+    ++ra.enums;
+    if ((S.modes & 1) && o.st_status) ++ra.skips;
+    if ((S.modes & 2) && o.ag_status) ++ra.skips;
+  }
+  if (do_dg) ra.skips += (o.pf_status != 0) + (o.dc_status != 0);
+}
+
+// One cell: every step from the tables (K2).  With the closed-form K0
+// (P.pair_off) the cell also writes the rows of its dp-variant candidates
+// (expand_unit) -- the cell stays in registers instead of a k_expand re-read.
+__device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, uint32_t cf, RowAcc& ra, int& s_out) {
+  const int s = find_cell_search(P.meta, P.n_search, ci);
+  const lc_search_desc& S = P.searches[s];
+  const SearchMeta& M = P.meta[s];
+  const int64_t rel = ci - M.cell_off;
+  const int tmpl = (int)(rel / S.n_b), bi = (int)(rel % S.n_b);
+  const TmplInfo ti = P.tmpl_info[tmpl];
+  lc_combo c;  // the fields expert_tokens() reads
+  c.tp = ti.tp; c.pp = ti.pp; c.ep = ti.ep; c.tp_i = ti.tp_i; c.ep_i = ti.ep_i;
+  const lc_entry* E = P.entries + (int64_t)tmpl * LC_MAX_ENTRIES;
+  const int ne = P.tmpl_n[tmpl];
+  const int32_t* so = P.slot_of + (int64_t)tmpl * LC_MAX_ENTRIES * 3;
+  const int64_t b = P.batches[S.b_off + bi];
+  const bool do_st = (cf & 1) && (S.modes & 1), do_ag = (cf & 1) && (S.modes & 2), do_dg = (cf & 2) != 0;
+  const int64_t mb = b > 1 ? b : 1;
+  const double bubble = (double)(mb + ti.pp - 1) / (double)mb;
+  const int64_t chunk = S.isl - S.prefix;
+  const int64_t kv_mid = S.isl + S.osl / 2;
+  CellOut o;
+  o.st_status = o.ag_status = o.pf_status = o.dc_status = LC_ST_NOT_EVALUATED;
+  o.st_ttft = o.st_tpot = o.ag_ttft = o.ag_tpot = o.pf_lat = o.dc_lat = 0.0;
+  o.qP = o.qSD = o.qM = o.qG = 0;
+  o.st_steps = 0;
+  o.flags = 0;
+  int q1 = 0, q2 = 0;
+
+  // prefill step: static TTFT and the prefill pool
+  double p_total = 0.0;
+  ErrRec p_err{0, 0, 0, 0};
+  if (do_st || do_dg) {
+    if (M.pstep_off >= 0) {  // shared with the other searches of the prefill group (k_ptables)
+      const PStep ps = P.psteps[M.pstep_off + rel];
+      p_total = ps.total;
+      p_err.code = ps.status & 0xff; p_err.label = ps.status >> 8; p_err.c0 = ps.c0; p_err.c1 = ps.c1;
+      o.qP = ps.q;
+    } else {
+      const StepArgs a{PH_PREFILL, b * chunk, 0, chunk, expert_tokens(P, c, M, S, 0, bi, b * chunk)};
+      table_step(P, M, E, ne, so + LC_STEP_PREFILL, S.n_b, bi, a, bubble, &p_total, &p_err, &q1, &q2);
+      if (!p_err.code) o.qP = (q1 & 0xffff) | (q2 << 16);
+    }
+    o.pf_status = p_err.code | (p_err.label << 8);
+    o.pf_lat = p_total;
+    if (p_err.code) put_cell_err(P, 2, ci, p_err);
+  }
+  const int64_t xt_dec = expert_tokens(P, c, M, S, 1, bi, b);
+  const StepArgs ga{PH_DECODE, 0, b, kv_mid, xt_dec};
+  if (do_st) {
+    double tpot = 0.0;
+    ErrRec e = p_err;
+    if (!e.code && S.osl > 1) {
+      const SdOut sd = P.sd[ci];  // k_dseries
+      if (sd.status) {
+        e.code = sd.status & 0xff; e.label = sd.status >> 8; e.c0 = sd.c0; e.c1 = sd.c1;
+      } else {
+        tpot = sd.t_gen / (double)(S.osl - 1);
+        o.qSD = sd.qsd;
+        o.st_steps = M.n_steps;
+      }
+    }
+    o.st_status = e.code | (e.label << 8);
+    o.st_ttft = p_total;
+    o.st_tpot = tpot;
+    if (e.code) put_cell_err(P, 0, ci, e);
+  }
+  // generation step at the KV midpoint: aggregated l_gen and the decode pool
+  bool g_done = false;
+  double g_total = 0.0;
+  ErrRec g_err{0, 0, 0, 0};
+  if (do_ag) {
+    const AggSched sc = agg_schedule(S, b);
+    ErrRec e{sc.st, 0, 0, 0};
+    double ttft = 0.0, tpot = 0.0;
+    if (!sc.st) {
+      double l_mix = 0.0, l_gen = 0.0;
+      const StepArgs a{PH_MIXED, sc.chunk_tokens, sc.n_mix_gen, kv_mid,
+                       expert_tokens(P, c, M, S, 2, bi, sc.chunk_tokens + sc.n_mix_gen)};
+      table_step(P, M, E, ne, so + LC_STEP_MIXED, S.n_b, bi, a, bubble, &l_mix, &e, &q1, &q2);
+      if (!e.code) o.qM = (q1 & 0xffff) | (q2 << 16);
+      if (!e.code && (sc.t_gen || b == 1)) {
+        table_step(P, M, E, ne, so + LC_STEP_GEN, S.n_b, bi, ga, bubble, &g_total, &g_err, &q1, &q2);
+        g_done = true;
+        if (!g_err.code) o.qG = (q1 & 0xffff) | (q2 << 16);
+        o.flags |= 1;
+        e = g_err;
+        l_gen = g_total;
+      }
+      if (!e.code) {
+        const double raw = 2.0 + (double)(sc.T - 3) * (1.0 / 20.0);
+        double F = raw > 2.0 ? raw : 2.0;
+        F = F < 4.0 ? F : 4.0;
+        ttft = l_mix * (double)sc.cpr * F;
+        if (b == 1) tpot = S.osl > 1 ? l_gen : 0.0;
+        else if (S.osl == 1) tpot = 0.0;
+        else if (sc.t_gen == 0) tpot = l_mix;
+        else {
+          const int64_t ms = sc.t_mix - 3 > 1 ? sc.t_mix - 3 : 1;
+          tpot = (l_mix * (double)ms + l_gen * (double)sc.t_gen) / (double)(ms + sc.t_gen);
+        }
+      }
+    }
+    o.ag_status = e.code | (e.label << 8);
+    o.ag_ttft = ttft;
+    o.ag_tpot = tpot;
+    if (e.code) put_cell_err(P, 1, ci, e);
+  }
+  if (do_dg) {
+    if (!g_done) {
+      table_step(P, M, E, ne, so + LC_STEP_GEN, S.n_b, bi, ga, bubble, &g_total, &g_err, &q1, &q2);
+      if (!g_err.code) o.qG = (q1 & 0xffff) | (q2 << 16);
+    }
+    o.dc_status = g_err.code | (g_err.label << 8);
+    o.dc_lat = g_total;
+    if (g_err.code) put_cell_err(P, 3, ci, g_err);
+  }
+  if (P.pair_off) {
+    s_out = s;
+    const int64_t pbase = (int64_t)s * P.sp_n_combos;
+    const int j1 = P.tmpl_cidx_off[tmpl + 1];
+    for (int j = P.tmpl_cidx_off[tmpl]; j < j1; ++j) {
+      const int cj = P.tmpl_cidx[j];
+      const int64_t pr = pbase + cj;
+      const int32_t off = P.pair_off[pr];
+      if (bi >= P.pair_off[pr + 1] - off) continue;  // this dp variant is not a candidate at this batch
+      expand_unit(P, S, o, ci, (int64_t)off + bi, b, P.combos[cj].gpus, P.pair_inb[pr] != 0, ra);
+    }
+  } else {
+    P.cells[ci] = o;
+  }
+}
+
+__global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalParams P) {
+  const int64_t ncell = P.n_cells_total;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; base < ncell; base += stride) {
+    const int64_t ci = base + lane;
+    RowAcc ra{0, 0, 0, 0, 0, 0, 0ull, 0ull};
+    int s = -1;
+    const uint32_t cf = ci < ncell ? P.cell_flags[ci] : 0u;
+    if (cf) eval_cell(P, ci, cf, ra, s);
+    if (!P.pair_off) continue;  // uniform: k_expand does the accounting
+    // warp-aggregated accounting (cells are ordered by search)
+    int s0 = -1;
+    const unsigned act = __ballot_sync(0xffffffffu, s >= 0);
+    if (!act) continue;
+    s0 = __shfl_sync(0xffffffffu, s, __ffs(act) - 1);
+    if (__all_sync(0xffffffffu, s < 0 || s == s0)) {
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) {
+        ra.q1 += __shfl_xor_sync(0xffffffffu, ra.q1, o2);
+        ra.q2 += __shfl_xor_sync(0xffffffffu, ra.q2, o2);
+        ra.feas += __shfl_xor_sync(0xffffffffu, ra.feas, o2);
+        ra.rows += __shfl_xor_sync(0xffffffffu, ra.rows, o2);
+        ra.enums += __shfl_xor_sync(0xffffffffu, ra.enums, o2);
+        ra.skips += __shfl_xor_sync(0xffffffffu, ra.skips, o2);
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, ra.smax, o2);
+        const unsigned long long m = __shfl_xor_sync(0xffffffffu, ra.smin_c, o2);
+        ra.smax = a > ra.smax ? a : ra.smax;
+        ra.smin_c = m > ra.smin_c ? m : ra.smin_c;
+      }
+      if (lane == 0) acc_flush(P.acc + s0, ra);
+    } else if (s >= 0) {
+      acc_flush(P.acc + s, ra);
+    }
+  }
+}
+
+// K2b: candidates from their cells -- derive_metrics with the candidate's gpu
+// count (serving_modes.py:161-172) and the pool rates (serving_modes.py:366, 380).
+#ifndef LC_EXPAND_MIN_BLOCKS
+#define LC_EXPAND_MIN_BLOCKS 4  // 64 registers (measured: 4.11 -> 4.00 ms per step)
+#endif
 __global__ void __launch_bounds__(256, LC_EXPAND_MIN_BLOCKS) k_expand(EvalParams P) {
   const int64_t n = P.n_cap;
   const int64_t total = *P.d_total;
@@ -1285,75 +1416,7 @@ __global__ void __launch_bounds__(256, LC_EXPAND_MIN_BLOCKS) k_expand(EvalParams
     const CellOut o = P.cells[ci];
     const int64_t b = P.batches[S.b_off + bi];
     const bool inb = P.u_budget[u] != 0;
-    const bool do_st = (S.modes & 1) && inb, do_ag = (S.modes & 2) && inb, do_dg = (S.modes & 4) != 0;
-    int32_t q = 0;
-    auto add_q = [&](int32_t x) { q += x; };  // packed halves never overflow 16 bits
-    if (do_st) {
-      P.st_status[u] = o.st_status;
-      if (o.st_status) {
-        P.err_c[u] = P.cell_err[ci * 8 + 0]; P.err_c[n + u] = P.cell_err[ci * 8 + 1];
-      } else {
-        double speed, thru;
-        derive_metrics(o.st_ttft, o.st_tpot, b, S.osl, c.gpus, &speed, &thru);
-        P.st_v[u] = o.st_ttft; P.st_v[n + u] = o.st_tpot; P.st_v[2 * n + u] = speed; P.st_v[3 * n + u] = thru;
-        ++ra.rows;
-        if ((!S.has_ttft || o.st_ttft <= S.ttft_limit) && (!S.has_floor || speed >= S.speed_floor)) {
-          ++ra.feas;
-          ra.feasible_speed(speed);
-        }
-        add_q(o.qSD);
-      }
-    }
-    if (do_ag) {
-      P.ag_status[u] = o.ag_status;
-      if (o.ag_status) {
-        P.err_c[2 * n + u] = P.cell_err[ci * 8 + 2]; P.err_c[3 * n + u] = P.cell_err[ci * 8 + 3];
-      } else {
-        double speed, thru;
-        derive_metrics(o.ag_ttft, o.ag_tpot, b, S.osl, c.gpus, &speed, &thru);
-        P.ag_v[u] = o.ag_ttft; P.ag_v[n + u] = o.ag_tpot; P.ag_v[2 * n + u] = speed; P.ag_v[3 * n + u] = thru;
-        ++ra.rows;
-        if ((!S.has_ttft || o.ag_ttft <= S.ttft_limit) && (!S.has_floor || speed >= S.speed_floor)) {
-          ++ra.feas;
-          ra.feasible_speed(speed);
-        }
-      }
-      add_q(o.qM);
-    }
-    if (do_st || do_dg) add_q(o.qP);
-    if (do_dg) {
-      P.pf_status[u] = o.pf_status;
-      if (o.pf_status) {
-        P.err_c[4 * n + u] = P.cell_err[ci * 8 + 4]; P.err_c[5 * n + u] = P.cell_err[ci * 8 + 5];
-        P.pool_key[u] = INFINITY;
-      } else {
-        const double rate = (double)b * 1000.0 / o.pf_lat;
-        P.pf_v[u] = o.pf_lat; P.pf_v[n + u] = rate;
-        P.pool_key[u] = -rate / (double)c.gpus;
-      }
-      P.dc_status[u] = o.dc_status;
-      if (o.dc_status) {
-        P.err_c[6 * n + u] = P.cell_err[ci * 8 + 6]; P.err_c[7 * n + u] = P.cell_err[ci * 8 + 7];
-        P.pool_key[n + u] = INFINITY;
-      } else {
-        const double rate = S.osl == 1 ? INFINITY : (double)b * 1000.0 / ((double)(S.osl - 1) * o.dc_lat);
-        P.dc_v[u] = o.dc_lat;
-        P.dc_v[n + u] = rate;
-        P.pool_key[n + u] = -rate / (double)c.gpus;
-      }
-    }
-    // the generation step is a memo hit when a static decode step used the same KV length
-    const int64_t k = (S.isl + S.osl / 2) - S.isl - 1;
-    const bool dup = do_st && o.st_status == 0 && S.osl > 1 && k >= 0 && (k % 32) == 0 && (k / 32) < o.st_steps;
-    if (((do_ag && (o.flags & 1)) || do_dg) && !dup) add_q(o.qG);
-    ra.q1 = (unsigned)(q & 0xffff);
-    ra.q2 = (unsigned)(q >> 16);
-    if (inb) {
-      ++ra.enums;
-      if ((S.modes & 1) && o.st_status) ++ra.skips;
-      if ((S.modes & 2) && o.ag_status) ++ra.skips;
-    }
-    if (do_dg) ra.skips += (o.pf_status != 0) + (o.dc_status != 0);
+    expand_unit(P, S, o, ci, u, b, c.gpus, inb, ra);
     }
     // per-search accounting for K4 (search.py:343-358 counts, speed range)
     int s0 = __shfl_sync(0xffffffffu, s, 0);
@@ -2371,6 +2434,18 @@ int lc_space_upload(lc_ctx* c, const lc_space_desc* d, lc_space** out) {
   }
   if ((rc = upload(&sp->gclasses, d->gen_classes, d->n_gen_classes > 0 ? d->n_gen_classes : 0, c->stream))) return rc;
   if ((rc = upload(&sp->gclass_of, d->gclass_of, d->n_tmpl > 0 ? d->n_tmpl : 1, c->stream))) return rc;
+  {
+    std::vector<int32_t> off((size_t)(d->n_tmpl > 0 ? d->n_tmpl : 0) + 1, 0), idx;
+    for (int t = 0; t < d->n_tmpl; ++t) {
+      off[t] = (int32_t)idx.size();
+      for (int i = 0; i < d->n_combos; ++i)
+        if (d->combos[i].tmpl == t) idx.push_back(i);
+    }
+    off[d->n_tmpl > 0 ? d->n_tmpl : 0] = (int32_t)idx.size();
+    if (idx.empty()) idx.push_back(0);
+    if ((rc = upload(&sp->tmpl_cidx_off, off.data(), off.size(), c->stream))) return rc;
+    if ((rc = upload(&sp->tmpl_cidx, idx.data(), idx.size(), c->stream))) return rc;
+  }
   CK(cudaStreamSynchronize(c->stream));
   *out = sp;
   return LC_OK;
@@ -2384,6 +2459,7 @@ int lc_space_free(lc_space* sp) {
   cudaFree(sp->tmpl_info);
   cudaFree(sp->pair_canon);
   cudaFree(sp->slots); cudaFree(sp->slot_of); cudaFree(sp->class_slots); cudaFree(sp->gclasses); cudaFree(sp->gclass_of);
+  cudaFree(sp->tmpl_cidx_off); cudaFree(sp->tmpl_cidx);
   delete sp;
   return LC_OK;
 }
@@ -2453,6 +2529,13 @@ static EvalParams make_params(lc_ctx* c) {
   P.n_cells_total = c->n_cells;
   P.results = (lc_search_result*)c->results.p;
   P.acc = (SearchAcc*)c->acc.p;
+#ifndef LC_NO_FUSE_EXPAND
+  P.pair_off = c->enum_fit ? (const int32_t*)c->block_sums.p : nullptr;
+#else
+  P.pair_off = nullptr;
+#endif
+  P.pair_inb = (const uint8_t*)c->pair_inb.p;
+  P.tmpl_cidx_off = sp->tmpl_cidx_off; P.tmpl_cidx = sp->tmpl_cidx;
   return P;
 }
 
@@ -2567,8 +2650,10 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   if (n > 0) {
     int64_t blocks = (n + 255) / 256;
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
-    ++c->launches;
-    k_expand<<<(int)blocks, 256, 0, c->stream>>>(P);  // also the per-search accounting (SearchAcc)
+    if (!P.pair_off) {  // otherwise k_eval_cells wrote the candidate rows
+      ++c->launches;
+      k_expand<<<(int)blocks, 256, 0, c->stream>>>(P);  // also the per-search accounting (SearchAcc)
+    }
     CK(cudaGetLastError());
   }
   CK(cudaEventRecord(c->ev[3], c->stream));
@@ -2676,7 +2761,8 @@ static int run_enum_fit(lc_ctx* c) {
 }
 
 static int run_enum(lc_ctx* c) {
-  if (c->batches_sorted && c->filt_hi < 0 && !getenv("LC_ENUM_FLAGS")) return run_enum_fit(c);
+  c->enum_fit = c->batches_sorted && c->filt_hi < 0 && !getenv("LC_ENUM_FLAGS");
+  if (c->enum_fit) return run_enum_fit(c);
   cudaError_t err = cudaSuccess;
   const int64_t n_raw = c->n_raw;
   const int64_t nblk = (n_raw + kScanBlock - 1) / kScanBlock;
