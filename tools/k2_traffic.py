@@ -13,7 +13,7 @@ import json
 import sys
 from collections import defaultdict
 
-K2 = ("k_qtables", "k_dstables", "k_dseries", "k_ptables", "k_eval_cells", "k_expand")
+K2 = ("k_qtables", "k_dstables", "k_dseries", "k_ptables", "k_eval_cells", "k_expand")  # k_expand: filtered path only
 rows = list(csv.reader(open(sys.argv[1])))
 hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
 h = rows[hi]
