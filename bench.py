@@ -398,12 +398,12 @@ def main() -> int:
             "kernel_ms": {"K0_enumerate": kernel_ms[0], "K3_moe_tails": kernel_ms[1], "K2_evaluate": kernel_ms[2],
                           "K5a_pools": kernel_ms[3], "K5b_disagg": kernel_ms[4], "K4_front": kernel_ms[5]}}
     # FP64 context: measured DFMA peak (tools/cuda/fp64_peak.cu) and the ncu FP64-pipe activity of
-    # the K2 kernels (profiles/r1_ncu_v9.json, r1_ncu_v17.json) -- the stage is FP64/latency bound, not HBM bound
+    # the K2 kernels (profiles/r1_ncu_v18.json) -- the stage is FP64/latency bound, not HBM bound
     try:
         roof["fp64_peak_gflops_measured"] = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())[
             "fp64_fma_gflops"]
         ncu = {}
-        for name in ("r1_ncu_v9.json", "r1_ncu_v17.json"):  # v9: DeepSeek-V3 batch, v17: k_eval_cells
+        for name in ("r1_ncu_v18.json",):  # every main kernel, GPT-OSS-120B batch of the current build
             ncu.update(json.loads((ROOT / "profiles" / name).read_text())["kernels"])
         roof["ncu_fp64_pipe_active_pct"] = {
             k: float(str(ncu[k].get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")).split()[0])
