@@ -25,10 +25,11 @@ def test_native_float_repr_matches_cpython():
     the whole exponent range and the fixed / scientific switch points."""
     import numpy as np
 
-    doc = golden_report("cfg4_dsv3")
+    doc = golden_report("cfg4_dsv3")  # static, aggregated and disaggregated rows
     doc.pop("_meta")
     doc["timing"] = {"total_ms": 1.0, "per_candidate_median_ms": 0.5}
     cols = columns_from_doc(doc)
+    assert cols.r_sys is not None and (cols.mode == 2).any()
     rng = np.random.default_rng(7)
     n = len(cols.mode)
     edges = np.array([1e-5, 9.999999999999999e-05, 1e-4, 0.1, 1.0, 5000.0, 1e15, 9.999999999999998e15, 1e16,
@@ -39,6 +40,8 @@ def test_native_float_repr_matches_cpython():
         rng.shuffle(vals, axis=1)
         cols.ttft, cols.tpot, cols.thru = vals[0].copy(), vals[1].copy(), vals[2].copy()
         cols.speed = np.where(rng.random(n) < 0.1, np.inf, vals[3])
+        if cols.r_sys is not None:
+            cols.r_sys = np.exp(rng.uniform(-40, 40, size=n))
         assert report_json(cols, native=True) == report_json(cols, native=False)
 
 
