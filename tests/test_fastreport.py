@@ -25,7 +25,7 @@ def test_native_float_repr_matches_cpython():
     the whole exponent range and the fixed / scientific switch points."""
     import numpy as np
 
-    doc = golden_report("cfg4_dsv3")  # static, aggregated and disaggregated rows
+    doc = golden_report("qwen3_all_default")  # static, aggregated and disaggregated rows
     doc.pop("_meta")
     doc["timing"] = {"total_ms": 1.0, "per_candidate_median_ms": 0.5}
     cols = columns_from_doc(doc)
