@@ -887,11 +887,13 @@ __global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_dstab
       else hi = mid - 1;
     }
     const DsGroup G = P.ds_groups[lo];
+    // layout [gclass][sample][batch]: the batch index is fastest, so the threads
+    // of a warp in k_dseries (consecutive batches) read consecutive entries
     int64_t rel = x - G.off;
-    const int k = (int)(rel % G.n_steps);
-    rel /= G.n_steps;
     const int bi = (int)(rel % G.n_b);
-    const int g = (int)(rel / G.n_b);
+    rel /= G.n_b;
+    const int k = (int)(rel % G.n_steps);
+    const int g = (int)(rel / G.n_steps);
     const lc_entry e = P.gclasses[g];
     int st = 0, nlog = 0;
     QVal out;
@@ -979,7 +981,7 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
     const int64_t mb = b > 1 ? b : 1;
     const double bubble = (double)(mb + ti.pp - 1) / (double)mb;
     const int64_t xt_dec = expert_tokens(P, c, M, S, 1, bi, b);
-    const QVal* ds = P.ds + M.ds_off + ((int64_t)P.gclass_of[tmpl] * S.n_b + bi) * M.ds_stride;
+    const QVal* ds = P.ds + M.ds_off + (int64_t)P.gclass_of[tmpl] * M.ds_stride * S.n_b + bi;  // sample k at ds[k * n_b]
     const StepArgs a0{PH_DECODE, 0, b, S.isl + 1, xt_dec};
     double term[LC_MAX_ENTRIES];
     int m = 0, gi = -1;
@@ -1013,6 +1015,7 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
     if (!e.code) {
       NeumaierSum pre;
       for (int i = 0; i < gi; ++i) pre.add(term[i]);
+      const double g_rep = ge ? (double)ge->repeat : 0.0;  // loop-invariant (ge points into global memory)
       // the terms after the attention entry, in registers for the sample loop
       constexpr int kPostRegs = 10;
       const int npost = m - gi - 1;
@@ -1032,9 +1035,9 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
           g[j] = 0.0;
           if (sj >= K || bad >= 0) continue;
           if (sj == 0) { g[j] = term[gi]; continue; }
-          const QVal q = ds[sj];
+          const QVal q = ds[(int64_t)sj * S.n_b];
           if (q.status) { bad = j; e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + 32ll * sj + 1; continue; }
-          g[j] = 0.0 + (q.lat * (double)ge->repeat / 1000.0) * bubble;
+          g[j] = 0.0 + (q.lat * g_rep / 1000.0) * bubble;
         }
         NeumaierSum sc[LC_DECODE_CHAINS];
 #pragma unroll
