@@ -8,12 +8,15 @@ disaggregated combine -> SLA / Pareto / best).  ``value`` is whole-job
 candidates/s with inputs resident on the GPU (CUDA events on the engine stream,
 max over ranks); ``e2e`` is the same metric through the public API
 (``Engine.run_batch`` with host workload objects, H2D descriptors, D2H
-summaries + fronts + plans).  Multi-GPU: one process per GPU, no collective on
-the data path.  ``--scaling weak`` (default): the sweep's ISL grid is densified
-N-fold and rank r owns offset r of it, so every rank evaluates a config-5-sized
-block and the whole job grows with N; ``--scaling strong``: the fixed config-5
-sweep is split across ranks by workload blocks.  The per-search results are
-merged with one NCCL all-gather.
+summaries + fronts + plans).  The north star's named target sweep
+(``config5_qwen``: Qwen3-32B + DeepSeek-V3) is measured the same way in the
+same run and reported under ``north_star``.
+
+Multi-GPU: one process per GPU.  ``--scaling strong`` (default): the fixed
+sweep is split across ranks by workload blocks, and the per-search summaries
+are merged with ONE packed NCCL all-gather inside the e2e timed region;
+``--scaling weak`` (also reported as ``weak_scaling`` for N > 1): the sweep's
+ISL grid is densified N-fold and rank r owns offset r of it.
 
 ``--impl reference`` times the reference algorithm on the host cores instead:
 the C restatement in oracle/ (test infrastructure; the Python reference cannot
@@ -207,13 +210,203 @@ def _sum_over_ranks(ws, x: float) -> float:
     return float(t.item())
 
 
-def _gather_results(ws, results: np.ndarray) -> np.ndarray:
-    """One NCCL all-gather of the packed per-search summaries (fixed-size records)."""
-    if ws == 1:
-        return results
-    from paper_2601_06288_b200.dist import gather_records
+# --------------------------------------------------------------------------- host facts
+def _cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
-    return np.concatenate(gather_records(results))
+
+def _python_factor() -> dict | None:
+    """Measured pure-Python-reference / C-port time ratio (tools/python_vs_port.py, same host, 1 thread)."""
+    f = ROOT / "profiles" / "r2_python_vs_port.json"
+    try:
+        d = json.loads(f.read_text())
+        return {"python_over_port_time": d["factor_median"], "source": "profiles/r2_python_vs_port.json",
+                "how": d.get("how")}
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------------- one sweep
+def _my_workloads(parts, ws, rank, scaling):
+    """(key, part, workloads) jobs of this rank.
+
+    strong: the FIXED sweep is split across ranks by contiguous workload blocks of
+    each model (the sweep is ISL-major, so a block keeps whole ISL groups and their
+    shared tables); weak: the sweep's ISL grid is densified N-fold and rank r owns
+    offset r (every ISL + r), so every rank evaluates a config-5-sized block."""
+    import dataclasses
+
+    from paper_2601_06288_b200.dist import shard_range
+
+    jobs = []
+    for p in parts:
+        if scaling == "strong":
+            lo, hi = shard_range(len(p.workloads), rank, ws)
+            mine = p.workloads[lo:hi]
+        else:
+            mine = [dataclasses.replace(w, isl=w.isl + rank) for w in p.workloads] if rank else list(p.workloads)
+        if mine:
+            jobs.append((p.model_name, p, mine))
+    return jobs
+
+
+def measure(sweep_name: str, args, ws: int, rank: int, dev: int, scaling: str, with_e2e: bool = True) -> dict:
+    """Device-resident and end-to-end timing of one named sweep on this rank's share.
+
+    device: every model's K0..K4 pipeline re-enqueued on resident inputs
+    (lc_replay_async) on its own stream; one CUDA-event span on the current
+    stream covers them; max over ranks.
+    e2e: Engine.run_batch from host workload objects per model (H2D descriptors,
+    the pipeline, D2H of per-search summaries + Pareto fronts + plans) and, with
+    N > 1, the all-gather of the packed per-search summaries -- all inside the
+    timed region; max over ranks of the wall time.
+    """
+    import torch
+
+    from paper_2601_06288_b200.dist import all_gather_bytes
+    from paper_2601_06288_b200.engine import Engine, fetch_fronts
+    from paper_2601_06288_b200.sweeps import sweep
+
+    parts = sweep(sweep_name)
+    jobs = _my_workloads(parts, ws, rank, scaling)
+    engines = {key: Engine(dev) for key, _, _ in jobs}
+    pool = ThreadPoolExecutor(max_workers=max(1, len(engines)))
+
+    def one_model(job):
+        key, p, wls = job
+        out = engines[key].run_batch(p.db, p.model, p.space, wls)
+        front, plans = fetch_fronts(out)
+        return (int(out.results["n_enumerated"].sum()), out.h2d_bytes,
+                out.d2h_bytes + front.nbytes + sum(v.nbytes for v in plans.values()), out.results)
+
+    def e2e_step():
+        outs = list(pool.map(one_model, jobs))
+        res = np.concatenate([o[3] for o in outs]) if outs else np.zeros(0)
+        gathered = res
+        if ws > 1:  # the merge of per-search summaries is part of the search wall time
+            parts_b = all_gather_bytes(res.tobytes(), cap=max(64 * 1024, 2 * res.nbytes + 4096))
+            gathered = np.concatenate([np.frombuffer(b, dtype=res.dtype) for b in parts_b])
+        return (sum(o[0] for o in outs), sum(o[1] for o in outs), sum(o[2] for o in outs), gathered)
+
+    for _ in range(max(args.warmup, 1)):
+        e2e_step()
+    outs = {key: engines[key].run_batch(p.db, p.model, p.space, wls) for key, p, wls in jobs}
+    cands_local = sum(int(o.results["n_enumerated"].sum()) for o in outs.values())
+    q1 = sum(int(o.results["queries_1d"].sum()) for o in outs.values())
+    q2 = sum(int(o.results["queries_2d"].sum()) for o in outs.values())
+    # per-stage CUDA-event breakdown (each model's pipeline alone, sequential, untimed)
+    kernel_ms = np.zeros(6)
+    launches_per_step = tq = tq2 = n_cells = 0
+    for key in engines:
+        tot = engines[key].replay(1)
+        kernel_ms += np.array(list(tot.kernel_ms), dtype=np.float64)
+        launches_per_step += int(tot.n_launches)
+        tq += int(tot.n_table_queries)
+        tq2 += int(tot.n_table_queries_2d)
+        n_cells += int(tot.n_cells)
+    streams = {m: torch.cuda.ExternalStream(e.stream_ptr()) for m, e in engines.items()}
+    cur = torch.cuda.current_stream()
+    step_ms = []
+    _barrier(ws)
+    for _ in range(args.steps):
+        start = torch.cuda.Event(enable_timing=True)
+        stop = torch.cuda.Event(enable_timing=True)
+        start.record(cur)
+        for st in streams.values():
+            st.wait_event(start)
+        for e in engines.values():
+            e.replay_async()
+        for st in streams.values():
+            done = torch.cuda.Event()
+            done.record(st)
+            cur.wait_event(done)
+        stop.record(cur)
+        stop.synchronize()
+        step_ms.append(start.elapsed_time(stop))
+    _barrier(ws)
+    dev_s = _max_over_ranks(ws, sum(step_ms) / 1000.0)
+    cands_total = _sum_over_ranks(ws, float(cands_local))
+    r = {"sweep": sweep_name, "scaling": scaling, "searches": sum(len(p.workloads) for p in parts),
+         "candidates": int(cands_total), "candidates_local": cands_local, "q1": q1, "q2": q2,
+         "value": cands_total * args.steps / dev_s, "ms_per_step": dev_s * 1000.0 / args.steps,
+         "step_ms": step_ms, "kernel_ms": kernel_ms, "launches_per_step": launches_per_step,
+         "tq": tq, "tq2": tq2, "n_cells": n_cells, "models": [p.model_name for p in parts]}
+    if with_e2e:
+        _barrier(ws)
+        t0 = time.perf_counter()
+        h2d = d2h = 0
+        merged = None
+        for _ in range(args.steps):
+            _, hb, db, merged = e2e_step()
+            h2d += hb
+            d2h += db
+        torch.cuda.synchronize()
+        e2e_s = _max_over_ranks(ws, time.perf_counter() - t0)
+        r["e2e"] = {"value": cands_total * args.steps / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps}
+        r["e2e_ms_per_step"] = e2e_s * 1000.0 / args.steps
+        r["best_found"] = int((merged["best"] >= 0).sum()) if merged is not None and len(merged) else 0
+        r["searches_merged"] = int(len(merged)) if merged is not None else 0
+    for e in engines.values():
+        e.close()
+    pool.shutdown()
+    return r
+
+
+def roofline(r: dict) -> dict:
+    """Roofline of the dominant stage, K2 (k_qtables + k_dstables + k_dseries + k_ptables + k_eval_cells).
+
+    achieved = the bytes of the work the kernels actually perform -- 32 B per
+    1-D and 64 B per 2-D query the engine prices (SURVEY.md §8d's per-query
+    figure: bracket axis values + corner cells) + 112 B of candidate I/O -- over
+    the stage's CUDA-event time (each model's pipeline alone, summed).
+    The reference-equivalent query count (what the reference would have to
+    gather, memoised per step) over the priced count is reported separately as
+    ``work_avoided_factor``: it measures sharing, not bandwidth.
+    """
+    peak, peak_kind = _peaks()
+    cands = r["candidates_local"]
+    k2_s = r["kernel_ms"][2] / 1000.0
+    tq, tq2 = r["tq"], r["tq2"]
+    alg = 32 * (tq - tq2) + 64 * tq2 + 112 * cands
+    achieved = alg / k2_s / 1e9 if k2_s > 0 else 0.0
+    ref_equiv = 32 * r["q1"] + 64 * r["q2"] + 112 * cands
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None,
+            "kernel": "K2 stage (k_qtables + k_dstables + k_dseries + k_ptables + k_eval_cells)",
+            "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+            "algorithmic_bytes_per_launch": alg, "stage_ms": r["kernel_ms"][2],
+            "priced_queries": tq, "priced_queries_2d": tq2, "candidates": cands, "cells": r["n_cells"],
+            "byte_model": "32 B per priced 1-D query + 64 B per priced 2-D query + 112 B per candidate (I/O)",
+            "work_avoided_factor": ref_equiv / alg if alg else None,
+            "reference_equivalent_queries": {"1d": r["q1"], "2d": r["q2"]},
+            "kernel_ms": dict(zip(("K0_enumerate", "K3_moe_tails", "K2_evaluate", "K5a_pools", "K5b_disagg",
+                                   "K4_front"), (float(x) for x in r["kernel_ms"])))}
+    prof = ROOT / "profiles" / "r2_ncu_k2_traffic.json"
+    if prof.exists():
+        try:
+            t = json.loads(prof.read_text())
+            roof["traffic"] = t.get("dram_bytes_per_step")
+            roof["traffic_source"] = "profiles/r2_ncu_k2_traffic.json"
+            if roof["traffic"] and k2_s > 0:
+                roof["traffic_frac"] = roof["traffic"] / k2_s / 1e9 / peak
+                roof["traffic_over_algorithmic"] = roof["traffic"] / alg
+        except Exception:
+            pass
+    kt = ROOT / "profiles" / "r2_ncu_kernels.json"
+    if kt.exists():
+        try:
+            roof["dominant_kernel_ncu"] = json.loads(kt.read_text()).get("k_eval_cells")
+            roof["ncu_source"] = "profiles/r2_ncu_kernels.json"
+        except Exception:
+            pass
+    return roof
 
 
 # --------------------------------------------------------------------------- main
@@ -223,13 +416,14 @@ def main() -> int:
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--sweep", default="config5")
+    ap.add_argument("--north-star", default="config5_qwen",
+                    help="second sweep measured in the same run (the north star's named target); 'none' skips")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--cpu-steps", type=int, default=6, help="reference-oracle sample steps for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--split", type=int, default=1, help="independent batches (engines / streams) per model")
-    ap.add_argument("--scaling", default="weak", choices=("weak", "strong"),
-                    help="weak: each rank evaluates its own config-5-sized block of an N-fold sweep (default); "
-                         "strong: the fixed sweep is split across ranks")
+    ap.add_argument("--scaling", default="strong", choices=("weak", "strong"),
+                    help="strong (default): the fixed sweep is split across ranks; weak: each rank evaluates its "
+                         "own config-5-sized block of an N-fold sweep (also reported as an extra field for N > 1)")
     args = ap.parse_args()
 
     from paper_2601_06288_b200.sweeps import sweep
@@ -262,165 +456,32 @@ def main() -> int:
                 "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": workload_desc,
                 "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": "port",
-                                 "sample": r["sample"]},
+                                 "cpu_model": _cpu_model(), "sample": r["sample"],
+                                 "sampled": "rate over a rotating sample of (sweep workload, 32-batch slice) "
+                                            "searches of the same sweep, not the whole sweep per step",
+                                 "python_reference": _python_factor()},
                 "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return 0
 
-    import torch
-
-    from paper_2601_06288_b200.engine import Engine, fetch_fronts
-
     dev = local if ws > 1 else 0
-    # shard searches across ranks: contiguous blocks of each model's workload list
-    from paper_2601_06288_b200.dist import shard_range
-
-    # jobs: each model's block of workloads, cut into --split contiguous batches
-    # (the sweep is ISL-major, so a batch keeps whole ISL groups and their shared tables)
-    my_parts = []
-    for p in parts:
-        if args.scaling == "strong":
-            lo, hi = shard_range(len(p.workloads), rank, ws)
-            mine = p.workloads[lo:hi]
-        else:
-            # weak scaling: the sweep's ISL grid is densified N-fold and each rank owns one
-            # offset of it (rank r: every ISL + r), so per-GPU work stays one config-5 sweep
-            import dataclasses
-
-            mine = [dataclasses.replace(w, isl=w.isl + rank) for w in p.workloads] if rank else list(p.workloads)
-        for k in range(args.split):
-            a, b = shard_range(len(mine), k, args.split)
-            if b > a:
-                my_parts.append((f"{p.model_name}/{k}", p, mine[a:b]))
-    # one engine (CUDA stream + resident workspace) per batch so each keeps its inputs resident
-    engines = {key: Engine(dev) for key, p, w in my_parts}
-
-    pool = ThreadPoolExecutor(max_workers=max(1, len(engines)))
-
-    def one_model(job):
-        key, p, wls = job
-        out = engines[key].run_batch(p.db, p.model, p.space, wls)
-        front, plans = fetch_fronts(out)
-        return (int(out.results["n_enumerated"].sum()), out.h2d_bytes,
-                out.d2h_bytes + front.nbytes + sum(v.nbytes for v in plans.values()), out.results)
-
-    def e2e_step():
-        outs = list(pool.map(one_model, my_parts))
-        return (sum(o[0] for o in outs), sum(o[1] for o in outs), sum(o[2] for o in outs), [o[3] for o in outs])
-
     clocks = ClockSampler(dev)
     clocks.start()
-    # warm-up (also uploads DBs / plans and sizes the workspace)
-    for _ in range(max(args.warmup, 1)):
-        e2e_step()
-
-    # ---- device-resident timing: replay K0..K4 per model on resident inputs
-    outs = {}
-    for key, p, wls in my_parts:
-        outs[key] = engines[key].run_batch(p.db, p.model, p.space, wls)
-    cands_local = sum(int(o.results["n_enumerated"].sum()) for o in outs.values())
-    q1 = sum(int(o.results["queries_1d"].sum()) for o in outs.values())
-    q2 = sum(int(o.results["queries_2d"].sum()) for o in outs.values())
-    # per-kernel breakdown (sequential, untimed) for the roofline of the dominant kernel
-    kernel_ms = np.zeros(6)
-    launches_per_step = 0
-    tq = tq2 = n_cells = 0
-    for key, p, wls in my_parts:
-        tot = engines[key].replay(1)
-        kernel_ms += np.array(list(tot.kernel_ms), dtype=np.float64)
-        launches_per_step += int(tot.n_launches)
-        tq += int(tot.n_table_queries)
-        tq2 += int(tot.n_table_queries_2d)
-        n_cells += int(tot.n_cells)
-    # timed steps: every model's pipeline enqueued at once on its own stream; one
-    # CUDA-event span on the current stream covers all of them
-    streams = {m: torch.cuda.ExternalStream(e.stream_ptr()) for m, e in engines.items()}
-    cur = torch.cuda.current_stream()
-    step_ms = []
-    _barrier(ws)
-    for step in range(args.steps):
-        start = torch.cuda.Event(enable_timing=True)
-        stop = torch.cuda.Event(enable_timing=True)
-        start.record(cur)
-        for m, st in streams.items():
-            st.wait_event(start)
-        for m, e in engines.items():
-            e.replay_async()
-        for m, st in streams.items():
-            done = torch.cuda.Event()
-            done.record(st)
-            cur.wait_event(done)
-        stop.record(cur)
-        stop.synchronize()
-        step_ms.append(start.elapsed_time(stop))
-    _barrier(ws)
-    launches = launches_per_step * args.steps
-    dev_s_local = sum(step_ms) / 1000.0
-    dev_s = _max_over_ranks(ws, dev_s_local)
-    cands_total = _sum_over_ranks(ws, float(cands_local))
-    value = cands_total * args.steps / dev_s
-
-    # ---- end-to-end through the public API (host objects -> summaries + fronts on host)
-    _barrier(ws)
-    t0 = time.perf_counter()
-    e2e_h2d = e2e_d2h = 0
-    for _ in range(args.steps):
-        c, h2d, d2h, res = e2e_step()
-        e2e_h2d += h2d
-        e2e_d2h += d2h
-    torch.cuda.synchronize()
-    e2e_s = _max_over_ranks(ws, time.perf_counter() - t0)
+    head = measure(args.sweep, args, ws, rank, dev, args.scaling)
+    ns = None
+    if args.north_star and args.north_star != "none" and args.north_star != args.sweep:
+        ns = measure(args.north_star, args, ws, rank, dev, args.scaling)
+    weak = None
+    if ws > 1 and args.scaling == "strong":
+        weak = measure(args.sweep, args, ws, rank, dev, "weak", with_e2e=False)
     clk = clocks.stop()
-    merged = _gather_results(ws, np.concatenate(res) if res else np.zeros(0))
-    e2e_value = cands_total * args.steps / e2e_s
 
     if rank != 0:
-        return 0
+        if ws > 1:
+            import torch.distributed as dist
 
-    # ---- roofline of the dominant stage (K2): gather-model bytes
-    peak, peak_kind = _peaks()
-    alg_bytes = 32 * q1 + 64 * q2 + 112 * cands_local
-    k2_s = kernel_ms[2] / 1000.0
-    achieved = alg_bytes / k2_s / 1e9 if k2_s > 0 else 0.0
-    uniq_bytes = 32 * (tq - tq2) + 64 * tq2 + 112 * cands_local
-    uniq_achieved = uniq_bytes / k2_s / 1e9 if k2_s > 0 else 0.0
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": None, "kernel": "K2 stage (k_qtables + k_dstables + k_dseries + k_ptables + k_eval_cells)",
-            "peak_source": peak_kind,
-            "algorithmic_bytes_per_launch": alg_bytes, "queries_1d": q1, "queries_2d": q2,
-            "note": ("achieved uses SURVEY.md 8(d)'s gather model: 32/64 B per reference-equivalent 1-D/2-D "
-                     "query (memoised per step as the reference would) + 112 B candidate I/O.  The engine prices "
-                     "each distinct query once per shared table, so it does far fewer gathers than the model "
-                     "counts and frac exceeds 1; unique_* applies the same model to the queries actually "
-                     "priced, and traffic is the ncu-measured DRAM bytes of the stage per step."),
-            "unique_queries": tq, "unique_queries_2d": tq2, "cells": n_cells, "unique_bytes": uniq_bytes,
-            "unique_achieved": uniq_achieved, "unique_frac": uniq_achieved / peak,
-            "kernel_ms": {"K0_enumerate": kernel_ms[0], "K3_moe_tails": kernel_ms[1], "K2_evaluate": kernel_ms[2],
-                          "K5a_pools": kernel_ms[3], "K5b_disagg": kernel_ms[4], "K4_front": kernel_ms[5]}}
-    # FP64 context: measured DFMA peak (tools/cuda/fp64_peak.cu) and the ncu FP64-pipe activity of
-    # the K2 kernels (profiles/r1_ncu_v18.json) -- the stage is FP64/latency bound, not HBM bound
-    try:
-        roof["fp64_peak_gflops_measured"] = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())[
-            "fp64_fma_gflops"]
-        ncu = {}
-        for name in ("r1_ncu_v18.json",):  # every main kernel, GPT-OSS-120B batch of the current build
-            ncu.update(json.loads((ROOT / "profiles" / name).read_text())["kernels"])
-        roof["ncu_fp64_pipe_active_pct"] = {
-            k: float(str(ncu[k].get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")).split()[0])
-            for k in ("k_qtables", "k_dstables", "k_dseries", "k_ptables", "k_eval_cells", "k_expand") if k in ncu}
-    except Exception:
-        pass
-    prof = ROOT / "profiles" / "ncu_k2_traffic.json"
-    if prof.exists():
-        try:
-            roof["traffic"] = json.loads(prof.read_text()).get("dram_bytes_per_step")
-            roof["traffic_source"] = "profiles/ncu_k2_traffic.json"
-            # the stage's measured DRAM bytes over its measured time: its physical HBM utilisation
-            if roof["traffic"] and k2_s > 0:
-                roof["traffic_gbs"] = roof["traffic"] / k2_s / 1e9
-                roof["traffic_frac"] = roof["traffic_gbs"] / peak
-        except Exception:
-            pass
+            dist.destroy_process_group()
+        return 0
 
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
@@ -428,29 +489,46 @@ def main() -> int:
         cands = sum(r["candidates"] for r in runs)
         secs = sum(r["seconds"] for r in runs)
         cpu = {"value": cands / secs, "unit": UNIT, "cores": runs[0]["cores"], "kind": "port",
+               "cpu_model": _cpu_model(),
                "sample": f"{args.cpu_steps} steps of: " + runs[0]["sample"].split(", ", 1)[0]
-                         + f"; {cands} candidates in {secs:.2f}s total"}
+                         + f"; {cands} candidates in {secs:.2f}s total (oracle/oracle.c, the C restatement of "
+                           f"the reference, one search per host thread)",
+               "python_reference": _python_factor()}
 
+    par = (f"{args.scaling} scaling over {ws} GPU(s): "
+           + ("the fixed sweep's workloads split into contiguous per-model blocks, one per rank; per-search "
+              "summaries merged with one packed all-gather inside the e2e timing"
+              if args.scaling == "strong" else "each rank owns one ISL offset of an N-fold densified sweep"))
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": float(np.mean(step_ms)), "higher_is_better": True, "scaling": args.scaling,
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(workload_desc, searches=total_searches * (ws if args.scaling == "weak" else 1),
-                       candidates=int(cands_total), parallelism=(f"searches sharded over {ws} GPU(s) ({args.scaling} scaling: "
-                                    + ("each rank owns one ISL offset of an N-fold densified sweep"
-                                       if args.scaling == "weak" else "the fixed sweep split by workload blocks")
-                                    + f"), {args.split} batch(es) per model"),
-                       l2="per-step unit arrays exceed L2 (~2 GB written per step)"),
-        "search_wall_ms": {"device": dev_s * 1000 / args.steps, "e2e": e2e_s * 1000 / args.steps,
-                           "per_model_sequential_device": float(kernel_ms.sum())},
-        "roofline": roof,
+        "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(workload_desc, searches=head["searches"] * (ws if args.scaling == "weak" else 1),
+                       candidates=head["candidates"], parallelism=par,
+                       l2="inputs larger than L2: per-step unit arrays (~1.5 GB written per step) exceed the 126 MB L2"),
+        "search_wall_ms": {"device": head["ms_per_step"], "e2e": head["e2e_ms_per_step"],
+                           "per_model_sequential_device": float(head["kernel_ms"].sum())},
+        "roofline": roofline(head),
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_h2d // args.steps,
-                "d2h_bytes_per_step": e2e_d2h // args.steps},
+        "e2e": head["e2e"],
         "clocks": clk,
-        "gpu_launches": launches,
-        "best_found": int((merged["best"] >= 0).sum()) if len(merged) else 0,
+        "gpu_launches": head["launches_per_step"] * args.steps,
+        "best_found": head["best_found"],
     }
+    if ns is not None:
+        line["north_star"] = {
+            "sweep": ns["sweep"], "models": ns["models"], "searches": ns["searches"],
+            "candidates": ns["candidates"], "value": ns["value"], "unit": UNIT, "ms_per_step": ns["ms_per_step"],
+            "e2e": ns["e2e"], "e2e_ms_per_step": ns["e2e_ms_per_step"], "best_found": ns["best_found"],
+            "gpu_launches": ns["launches_per_step"] * args.steps,
+            "target": "10^7-candidate Qwen3-32B + DeepSeek-V3 search in under 1 s on 8xB200",
+            "roofline": {k: v for k, v in roofline(ns).items() if k in ("achieved", "frac", "stage_ms",
+                                                                          "algorithmic_bytes_per_launch",
+                                                                          "work_avoided_factor", "kernel_ms")}}
+    if weak is not None:
+        line["weak_scaling"] = {"value": weak["value"], "ms_per_step": weak["ms_per_step"],
+                                "candidates": weak["candidates"], "searches": weak["searches"] * ws,
+                                "note": "device-resident; every rank evaluates its own ISL offset of an N-fold sweep"}
     print(json.dumps(line))
     if ws > 1:
         import torch.distributed as dist

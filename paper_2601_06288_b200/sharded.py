@@ -11,7 +11,7 @@ Each rank then reduces its block to the candidates any global answer can
 need -- its local Pareto-front rows, its local best and nearest miss, and its
 local top-k prefill / decode pool members (search.py:336-339) -- identified by
 raw tuple index, plus its counts.  One all-gather of those small records
-(``dist.gather_records``: NCCL over NVLink on a GPU box) gives every rank the
+(``dist.all_gather_bytes``, one fixed-size payload: NCCL over NVLink on a GPU box) gives every rank the
 union S, and every rank runs one *merge pass* of the same pipeline on S
 (``lc_set_raw_filter`` with a mask).  The merge pass's answers are the global
 ones because, for any S with global-front ⊆ S ⊆ all rows,
@@ -38,7 +38,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .dist import gather_records, shard_range
+from .dist import all_gather_bytes, pack_records, shard_range, unpack_records
 from .engine import MODE_DISAGG, BatchOutput, build_report, fetch_fronts, get_engine
 from .specs import DEFAULT_DISAGG, CandidateSpace, SearchError
 
@@ -176,12 +176,12 @@ def merge_pass(eng, db, model, workload, space, disagg, shards: list[LocalShard]
     return res
 
 
-def _default_exchange(arr: np.ndarray) -> list[np.ndarray]:
+def _default_exchange(payload: bytes) -> list[bytes]:
     import torch.distributed as dist
 
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
-        return gather_records(arr)
-    return [arr]
+        return all_gather_bytes(payload)
+    return [payload]
 
 
 def run_search_sharded(db, model, workload, space=CandidateSpace(), disagg_constants=DEFAULT_DISAGG,
@@ -190,8 +190,10 @@ def run_search_sharded(db, model, workload, space=CandidateSpace(), disagg_const
     """run_search's reductions for one search split over ``world`` ranks (one process per GPU).
 
     Every rank calls this with the same inputs; every rank returns the same
-    global result.  ``exchange(records) -> [records of rank 0, 1, ...]`` is the
-    all-gather (default: torch.distributed when initialised, else world = 1).
+    global result.  ``exchange(payload: bytes) -> [payload of rank 0, 1, ...]``
+    is the all-gather (default: one fixed-size torch.distributed all-gather of
+    the packed counts + keep set, ``dist.all_gather_bytes``; world = 1 when
+    torch.distributed is not initialised).
     """
     if rank is None or world is None:
         import torch.distributed as dist
@@ -209,9 +211,9 @@ def run_search_sharded(db, model, workload, space=CandidateSpace(), disagg_const
         lo, hi = shard_range(_n_raw(plan, workload, space), rank, world)
         mine = local_pass(eng, db, model, workload, space, disagg_constants, lo, hi)
     t1 = time.perf_counter()
-    counts = exchange(mine.counts)
-    keeps = exchange(mine.keep)
-    shards = [LocalShard(c, k) for c, k in zip(counts, keeps)]
+    # ONE exchange per search: counts and keep set packed into a single record
+    gathered = exchange(pack_records(mine.counts, mine.keep))
+    shards = [LocalShard(*unpack_records(b, [COUNTS_DTYPE, KEEP_DTYPE])) for b in gathered]
     t2 = time.perf_counter()
     with eng._lock:
         res = merge_pass(eng, db, model, workload, space, disagg_constants, shards)

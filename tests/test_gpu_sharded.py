@@ -114,8 +114,12 @@ def _worker(rank, world, port, name, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         db, model, workload, space, dc = objs(cases[name])
+        from paper_2601_06288_b200.dist import COLLECTIVES
+
+        before = COLLECTIVES["all_gather"]
         res = run_search_sharded(db, model, workload, space, dc)
-        q.put((rank, json.dumps(res.summary_doc(), sort_keys=True), res.front, res.best))
+        n_coll = COLLECTIVES["all_gather"] - before
+        q.put((rank, json.dumps(res.summary_doc(), sort_keys=True), res.front, res.best, n_coll))
     finally:
         dist.destroy_process_group()
 
@@ -137,3 +141,5 @@ def test_two_processes_gloo_match_golden(name):
     want = json.dumps(_golden_summary(name), sort_keys=True)
     assert got[0][1] == want and got[1][1] == want
     assert got[0][2] == got[1][2] and got[0][3] == got[1][3]
+    # one collective per sharded search (counts + keep set in one fixed-size record)
+    assert got[0][4] == 1 and got[1][4] == 1

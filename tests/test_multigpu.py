@@ -18,8 +18,12 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2601_06288_b200.dist import (
+    COLLECTIVES,
     FRONT_DTYPE,
+    all_gather_bytes,
     gather_records,
+    pack_records,
+    unpack_records,
     merge_best,
     merge_fronts,
     merge_topk,
@@ -108,3 +112,51 @@ def test_gloo_world2_merge_matches_global(case_name):
     i = np.lexsort((rows["key"], -rows["speed"], -rows["thru"]))[0]
     assert gbest == (-rows["thru"][i], -rows["speed"][i], int(rows["key"][i]))
     assert gtk == sorted(topk_src)[:4]
+
+
+def _bytes_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a = np.arange(rank * 3, dtype=np.int64)
+        b = np.zeros(rank + 1, dtype=[("x", "<f8"), ("k", "<i4")])
+        b["x"] = rank + 0.5
+        n0 = COLLECTIVES["all_gather"]
+        small = all_gather_bytes(pack_records(a, b), device="cpu")
+        n_small = COLLECTIVES["all_gather"] - n0
+        # rank 1's payload overflows a tiny cap: every rank takes the second gather
+        n0 = COLLECTIVES["all_gather"]
+        big = all_gather_bytes(bytes(range(rank * 40 % 256)) * (1 + rank), cap=16, device="cpu")
+        n_big = COLLECTIVES["all_gather"] - n0
+        if rank == 0:
+            q.put(([[x.tolist() for x in unpack_records(p, [np.int64, b.dtype])] for p in small], n_small,
+                   [len(x) for x in big], n_big))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_packed_gather_one_collective():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bytes_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    small, n_small, big_lens, n_big = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert n_small == 1 and n_big == 2
+    assert small[0][0] == [] and small[1][0] == [0, 1, 2]
+    assert small[0][1] == [(0.5, 0)] and small[1][1] == [(1.5, 0), (1.5, 0)]
+    assert big_lens == [0, 80]
+
+
+def test_pack_roundtrip():
+    a = np.array([3, 1, 2], dtype=np.int64)
+    b = np.zeros(0, dtype=FRONT_DTYPE)
+    got = unpack_records(pack_records(a, b), [np.int64, FRONT_DTYPE])
+    assert got[0].tolist() == [3, 1, 2] and len(got[1]) == 0
+    with pytest.raises(ValueError):
+        unpack_records(pack_records(a), [np.int64, FRONT_DTYPE])
