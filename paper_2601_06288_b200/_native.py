@@ -23,7 +23,15 @@ I32P, I64P, F64P, U8P = (C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C
 
 
 class NativeUnavailable(RuntimeError):
-    """The CUDA engine cannot run here (library not built or no device)."""
+    """The CUDA engine cannot run here (library not built or no device), or a CUDA call failed."""
+
+
+class EngineLimitError(ValueError):
+    """The C ABI rejected its arguments (LC_ERR_ARG): a request beyond the device path's
+    documented limits or a malformed call -- not an unavailable engine."""
+
+
+LC_ERR_ARG = -1
 
 
 class LcDbDesc(C.Structure):
@@ -171,6 +179,8 @@ def load_library(path: str | os.PathLike | None = None):
 def check(rc: int, what: str) -> None:
     if rc != 0:
         msg = load_library().lc_last_error().decode(errors="replace")
+        if rc == LC_ERR_ARG:
+            raise EngineLimitError(f"{what}: {msg}")
         raise NativeUnavailable(f"{what} failed ({rc}): {msg}")
 
 

@@ -2865,6 +2865,10 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     M.plan_cap = pc;
     plans += pc;
   }
+  // unit / cell / plan positions are int32 on the device (K0 scan, unit_off, n_units)
+  if (raw > INT32_MAX || cells > INT32_MAX || plans > INT32_MAX)
+    return fail(LC_ERR_ARG, "batch too large: more than 2^31-1 raw candidate tuples (or cells, plan slots) in one "
+                            "lc_search_batch call; split the workloads over several calls");
   // MoE tail tables, shared between searches with the same inputs
   c->htables.clear();
   if (sp->is_moe) {

@@ -20,6 +20,7 @@ import math
 import threading
 import time
 import weakref
+from collections import OrderedDict
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -126,8 +127,11 @@ class Engine:
         ctx = C.c_void_p()
         N.check(self.lib.lc_open(device, C.byref(ctx)), "lc_open")
         self.ctx = ctx
-        self._dbs: dict[int, tuple] = {}
-        self._spaces: dict[tuple, tuple] = {}
+        # device handle caches, LRU-bounded; evicted / stale entries free their device memory
+        self._dbs: "OrderedDict[int, tuple]" = OrderedDict()
+        self._spaces: "OrderedDict[tuple, tuple]" = OrderedDict()
+        self._pinned: tuple = ()  # handles the last batch uses (lc_replay_* re-runs it)
+        self._deferred: list = []  # evicted while pinned: freed once the next batch no longer uses them
         self._lock = threading.Lock()
 
     def _call(self, fn, name, *args):
@@ -138,17 +142,51 @@ class Engine:
             self.lib.lc_space_free(h)
         for h, _, _ in self._dbs.values():
             self.lib.lc_db_free(h)
+        for h, f in self._deferred:
+            f(h)
         self._spaces.clear()
         self._dbs.clear()
+        self._deferred = []
+        self._pinned = ()
         if self.ctx:
             self.lib.lc_close(self.ctx)
             self.ctx = None
 
     # ------------------------------------------------------------------ handles
+    MAX_DBS = 8
+    MAX_SPACES = 32
+
+    def _release(self, h, free) -> None:
+        """Free a device handle now, or after the next batch when the last batch still uses it."""
+        if any(h is x for x in self._pinned):
+            self._deferred.append((h, free))
+        else:
+            free(h)
+
+    def _free_space(self, key) -> None:
+        self._release(self._spaces.pop(key)[0], self.lib.lc_space_free)
+
+    def _free_db(self, dbid: int) -> None:
+        for key in [k for k in self._spaces if k[0] == dbid]:
+            self._free_space(key)
+        self._release(self._dbs.pop(dbid)[0], self.lib.lc_db_free)
+
+    def _evict(self) -> None:
+        for cache, cap, free in ((self._spaces, self.MAX_SPACES, self._free_space),
+                                 (self._dbs, self.MAX_DBS, self._free_db)):
+            for key in list(cache):  # least recently used first
+                if len(cache) <= cap:
+                    break
+                if key in cache:
+                    free(key)
+
     def db_handle(self, db) -> tuple[C.c_void_p, FlatDb]:
         hit = self._dbs.get(id(db))
         if hit is not None and hit[2]() is db:
+            self._dbs.move_to_end(id(db))
             return hit[0], hit[1]
+        if hit is not None:  # id() reused by a new object: the old image is dead
+            self._free_db(id(db))
         flat = flatten(db)
         hw = db.hardware
         d = N.LcDbDesc()
@@ -174,14 +212,26 @@ class Engine:
         h = C.c_void_p()
         self._call(self.lib.lc_db_upload, "lc_db_upload", self.ctx, C.byref(d), C.byref(h))
         self._dbs[id(db)] = (h, flat, weakref.ref(db))
+        self._evict()
         return h, flat
+
+    @staticmethod
+    def _plan_key(space) -> tuple:
+        """The CandidateSpace fields build_space_plan reads (batch lists, pool caps and the
+        KV fraction's value travel per search, not in the plan)."""
+        return (tuple(space.tp_values), tuple(space.pp_values), tuple(space.ep_values), tuple(space.dp_values),
+                space.ctx_capacity, bool(space.chunked_prefill), float(space.kv_mem_fraction),
+                bool(space.cuda_graph))
 
     def space_handle(self, db, model, space) -> tuple[C.c_void_p, SpacePlan, FlatDb]:
         dbh, flat = self.db_handle(db)
-        key = (id(db), model, space)
+        key = (id(db), model, self._plan_key(space))
         hit = self._spaces.get(key)
         if hit is not None and hit[2]() is db:
+            self._spaces.move_to_end(key)
             return hit[0], hit[1], flat
+        if hit is not None:
+            self._free_space(key)
         plan = build_space_plan(model, space, flat, db.backend)
         d = N.LcSpaceDesc()
         d.hidden, d.topk, d.n_experts, d.is_moe = plan.hidden, plan.topk, plan.n_experts, int(plan.is_moe)
@@ -200,6 +250,7 @@ class Engine:
         h = C.c_void_p()
         self._call(self.lib.lc_space_upload, "lc_space_upload", self.ctx, C.byref(d), C.byref(h))
         self._spaces[key] = (h, plan, weakref.ref(db))
+        self._evict()
         return h, plan, flat
 
     # ------------------------------------------------------------------ batches
@@ -208,6 +259,13 @@ class Engine:
         t0 = time.perf_counter()
         sph, plan, flat = self.space_handle(db, model, space)
         dbh, _ = self.db_handle(db)
+        self._pinned = (sph, dbh)
+        if self._deferred:
+            keep = [(h, f) for h, f in self._deferred if any(h is x for x in self._pinned)]
+            for h, f in self._deferred:
+                if not any(h is x for x in self._pinned):
+                    f(h)
+            self._deferred = keep
         n = len(workloads)
         searches = np.zeros(n, dtype=N.SEARCH_DESC_DTYPE)
         batches: list[int] = []
@@ -254,17 +312,19 @@ class Engine:
         for w in ws:
             src = w.batch_sweep or space.batch_values
             key = (id(src), len(src)) if isinstance(src, tuple) else tuple(src)
-            off = b_index.get(key)
-            if off is None:
-                bs = tuple(sorted(src))
-                off = b_index.get(bs)
-                if off is None:
-                    off = len(batches)
+            hit = b_index.get(key)
+            if hit is None:
+                # batch values < 1 make ParallelConfig raise, and enumerate_candidates skips
+                # them (search.py:101-105; model.py:190-193); duplicates are kept, as there
+                bs = tuple(sorted(b for b in src if b >= 1))
+                hit = b_index.get(bs)
+                if hit is None:
+                    hit = (len(batches), len(bs))
                     batches.extend(bs)
-                    b_index[bs] = off
-                b_index[key] = off
-            b_off.append(off)
-            n_b.append(len(src))
+                    b_index[bs] = hit
+                b_index[key] = hit
+            b_off.append(hit[0])
+            n_b.append(hit[1])
         if plan.is_moe:
             for w in ws:
                 params = w.moe_load if w.moe_load is not None else DEFAULT_MOE_LOAD

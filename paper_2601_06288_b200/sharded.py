@@ -89,7 +89,7 @@ class ShardedResult:
 
 def _n_raw(plan, workload, space) -> int:
     src = workload.batch_sweep or space.batch_values
-    return len(plan.combos) * len(src)
+    return len(plan.combos) * sum(1 for b in src if b >= 1)  # batch values < 1 are skipped (engine.run_batch)
 
 
 def _modes(workload) -> int:

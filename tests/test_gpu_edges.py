@@ -62,3 +62,70 @@ def test_empty_query_batch():
 
     db, *_ = case_objects(BY_NAME["a1_qwen_small"])
     assert list(pkg.query_latency_batch(db, [])) == []
+
+
+@pytest.mark.parametrize("where", ["space", "sweep"])
+def test_nonpositive_batch_values_are_skipped(where):
+    """ParallelConfig(batch<1) raises and enumerate_candidates skips it (search.py:101-105,
+    model.py:190-193): batch values (0, -2, 1, 8) give the report of (1, 8); (0,) gives none."""
+    import dataclasses
+
+    import paper_2601_06288_b200 as pkg
+    from golden_io import canonical, db_path, diff_canonical, model_doc
+    from oracle import oracle
+
+    case = BY_NAME["a1_qwen_small"]
+    db, model, workload, space, dc = case_objects(case)
+    space = dataclasses.replace(space, tp_values=(1, 2), pp_values=(1, 2), dp_values=(1, 2))
+
+    def run(batches):
+        if where == "space":
+            return pkg.run_search(db, model, workload, dataclasses.replace(space, batch_values=batches),
+                                  disagg_constants=dc).to_doc()
+        return pkg.run_search(db, model, dataclasses.replace(workload, batch_sweep=batches), space,
+                              disagg_constants=dc).to_doc()
+
+    got, want = run((0, -2, 1, 8)), run((1, 8))
+    got.pop("timing"), want.pop("timing")
+    assert got == want and got["counts"]["enumerated"] > 0
+    header, recs = oracle.read_db_records(db_path(case))
+    ref = oracle.run_search(header, recs, model_doc(case["model"]), case["workload"],
+                            {"tp_values": [1, 2], "pp_values": [1, 2], "dp_values": [1, 2], "batch_values": [1, 8]},
+                            disagg=case.get("disagg"))
+    if where == "space":
+        assert not diff_canonical(canonical(got), canonical(ref))
+    none = run((0,))
+    assert none["counts"]["enumerated"] == 0 and none["rows"] == [] and none["best"] is None
+
+
+def test_handle_caches_are_bounded_and_keyed_on_plan_fields():
+    """Distinct spaces that share the plan fields reuse one device plan; many distinct
+    plans stay under the LRU bound, evicted handles are freed, and results stay right."""
+    import dataclasses
+
+    import paper_2601_06288_b200 as pkg
+    from paper_2601_06288_b200.engine import Engine, build_report
+
+    db, model, workload, space, dc = case_objects(BY_NAME["a1_qwen_small"])
+    eng = Engine(0)
+    try:
+        base = dataclasses.replace(space, tp_values=(1, 2), pp_values=(1,), dp_values=(1,), batch_values=(1, 8))
+        out = eng.run_batch(db, model, base, [workload], dc)
+        want = build_report(out, 0, db, model, workload, base, 0.0).to_doc()
+        for caps in ((4, 4), (2, 8), (8, 16)):  # pool caps / batches are per search, not per plan
+            sp = dataclasses.replace(base, prefill_pool_cap=caps[0], decode_pool_cap=caps[1], batch_values=(8, 1))
+            eng.run_batch(db, model, sp, [workload], dc)
+        assert len(eng._spaces) == 1
+        for i in range(eng.MAX_SPACES + 8):
+            sp = dataclasses.replace(base, dp_values=(1, 2 + i))
+            eng.run_batch(db, model, sp, [workload], dc)
+        assert len(eng._spaces) <= eng.MAX_SPACES
+        out = eng.run_batch(db, model, base, [workload], dc)
+        got = build_report(out, 0, db, model, workload, base, 0.0).to_doc()
+        got.pop("timing"), want.pop("timing")
+        assert got == want
+        ref = pkg.run_search(db, model, workload, base, disagg_constants=dc).to_doc()
+        ref.pop("timing")
+        assert got == ref
+    finally:
+        eng.close()
