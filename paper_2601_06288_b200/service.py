@@ -28,6 +28,7 @@ from dataclasses import fields
 from pathlib import Path
 from typing import Any, Mapping
 
+from . import _native as N
 from .database import load_db
 from .engine import count_candidates, get_engine, search_json_columns
 from .report import REPORT_VERSION
@@ -39,9 +40,39 @@ from .specs import (
     ModelSpec,
     ParallelConfigError,
     WorkloadError,
+    SearchError,
     WorkloadSpec,
     load_model_spec,
 )
+
+_DATA_DIR = Path(__file__).resolve().parent / "data"
+
+
+def bundled_models() -> dict[str, ModelSpec]:
+    """The reference's bundled desk-scale models, registered before configured ones
+    (service.py:87-92, 143): qwen-small and moe-small."""
+    out = {}
+    for p in sorted((_DATA_DIR / "models").glob("*.json")):
+        spec = load_model_spec(p)
+        out[spec.name] = spec
+    return out
+
+
+def check_device_limits(model: ModelSpec, workload: WorkloadSpec, space: CandidateSpace) -> None:
+    """The device path's size limits as 400s on the offending field.
+
+    The reference has no such limits; requests beyond them are rejected up front
+    rather than failing inside the engine with a 500."""
+    if not 0 <= space.prefill_pool_cap <= 64 or not 0 <= space.decode_pool_cap <= 64:
+        raise ApiError(400, "pool caps must be in [0, 64] on the device engine", field="space")
+    if "disaggregated" in workload.modes and space.prefill_pool_cap * space.decode_pool_cap > 256:
+        raise ApiError(400, "prefill_pool_cap * decode_pool_cap above 256 is not supported on the device engine",
+                       field="space")
+    if len(set(workload.gpu_budgets)) > N.LC_MAX_BUDGETS:
+        raise ApiError(400, f"at most {N.LC_MAX_BUDGETS} distinct gpu_budgets are supported on the device engine",
+                       field="workload")
+    if model.moe is not None and model.moe.num_experts > 1024:
+        raise ApiError(400, "at most 1024 experts are supported on the device engine", field="model")
 
 MAX_CANDIDATES = 10_000  # service.py:34
 MAX_JOBS = 16            # service.py:35
@@ -121,7 +152,7 @@ def _space_from_doc(doc) -> CandidateSpace:
 class SearchService:
     """Device-resident search service state: databases, models and the engine."""
 
-    def __init__(self, config: str | Path | Mapping | None = None, bundled_models: Mapping | None = None,
+    def __init__(self, config: str | Path | Mapping | None = None, bundled: Mapping | None = None,
                  max_candidates: int = MAX_CANDIDATES, device: int = 0, soa_cache: bool = False,
                  upload: bool = True):
         if config is None:
@@ -131,7 +162,7 @@ class SearchService:
         self.config = dict(config)
         self.databases = {name: load_db(path, soa_cache=soa_cache)
                           for name, path in sorted((config.get("databases") or {}).items())}
-        self.models: dict[str, ModelSpec] = dict(bundled_models or {})
+        self.models: dict[str, ModelSpec] = bundled_models() if bundled is None else dict(bundled)
         for name, path in sorted((config.get("models") or {}).items()):
             self.models[name] = load_model_spec(path)
         self.max_candidates = max_candidates
@@ -189,7 +220,11 @@ class SearchService:
         model = _model_from_request(body["model"], self.models)
         workload = _workload_from_doc(body["workload"])
         space = _space_from_doc(body.get("space"))
-        n = count_candidates(model, space, workload, db, device=self.device)
+        check_device_limits(model, workload, space)
+        try:
+            n = count_candidates(model, space, workload, db, device=self.device)
+        except (N.EngineLimitError, SearchError) as e:
+            raise ApiError(400, str(e), field="space")
         if n > self.max_candidates:
             raise ApiError(413, f"{n} candidates exceed the {self.max_candidates} limit", field="space")
         return db, model, workload, space
@@ -198,7 +233,11 @@ class SearchService:
         """POST /api/v1/search (service.py:226-236): the report JSON, or ApiError."""
         body = self.validate(body)
         db, model, workload, space = self.resolve(body)
-        text, cols = search_json_columns(db, model, workload, space, jobs=body.get("jobs", 1), device=self.device)
+        try:
+            text, cols = search_json_columns(db, model, workload, space, jobs=body.get("jobs", 1),
+                                             device=self.device)
+        except (N.EngineLimitError, SearchError) as e:
+            raise ApiError(400, str(e), field="space")
         if cols.best < 0:
             import json
 

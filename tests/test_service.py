@@ -96,6 +96,33 @@ def test_extra_request_field_400(cpu_client):
     assert resp.json()["detail"]["field"] == "surprise"
 
 
+def test_bundled_models_registered_without_config():
+    """create_app registers the reference's bundled models (service.py:87-92, 143)."""
+    from fastapi.testclient import TestClient
+
+    from paper_2601_06288_b200.service import create_app
+
+    client = TestClient(create_app({"databases": {"qwen-h100": str(db_path(BY_NAME["a1_qwen_small"]))}},
+                                   upload=False))
+    assert [m["name"] for m in client.get("/api/v1/meta").json()["models"]] == ["moe-small", "qwen-small"]
+    for name in ("qwen-small", "moe-small"):
+        assert json.loads((ROOT_SPECS / f"model-{name}.json").read_text()) == json.loads(
+            (ROOT_SPECS.parents[2] / "paper_2601_06288_b200" / "data" / "models" / f"{name}.json").read_text())
+
+
+@pytest.mark.parametrize("space,workload_over,field", [
+    ({"prefill_pool_cap": 65}, {}, "space"),
+    ({"prefill_pool_cap": 32, "decode_pool_cap": 16}, {}, "space"),
+    ({}, {"gpu_budgets": list(range(1, 18))}, "workload"),
+])
+def test_device_limits_are_400(cpu_client, space, workload_over, field):
+    body = _body(space=space)
+    body["workload"] = dict(body["workload"], **workload_over)
+    resp = cpu_client.post("/api/v1/search", json=body)
+    assert resp.status_code == 400
+    assert resp.json()["detail"]["field"] == field
+
+
 def test_config_file_rejects_unknown_keys(tmp_path):
     from paper_2601_06288_b200.service import load_config
 
