@@ -5,7 +5,7 @@ Public seam: ``run_search`` -- a drop-in for ``llmconf.search.run_search``
 hand-written sm_100a kernels behind the C ABI in include/llmconf_b200.h.
 """
 
-from .database import PerfDatabase, load_db
+from .database import PerfDatabase, ValidationReport, load_db, validate_db
 from .engine import (
     Engine,
     enumerate_candidates,
@@ -37,7 +37,7 @@ from .specs import (
 __all__ = [
     "CandidateSpace", "DEFAULT_DISAGG", "DisaggConstants", "Engine", "HardwareSpec", "ModelSpec", "MoESpec",
     "ParallelConfig", "PerfDatabase", "PowerLawParams", "SearchReport", "WorkloadSpec", "csv_from_doc",
-    "enumerate_candidates", "estimate_aggregated", "estimate_static", "export_csv", "get_engine", "load_db", "load_hardware_spec", "load_model_spec",
+    "ValidationReport", "validate_db", "enumerate_candidates", "estimate_aggregated", "estimate_static", "export_csv", "get_engine", "load_db", "load_hardware_spec", "load_model_spec",
     "GridAxes", "generate_synthetic_db", "load_soa", "save_soa", "grid_spec_for_model", "save_db",
     "OperatorQuery", "query_latency", "query_latency_batch", "run_search", "run_search_json",
     "ShardedResult", "run_search_sharded",

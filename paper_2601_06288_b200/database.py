@@ -129,13 +129,22 @@ class Grid:
         self.cells = cells
 
 
+def record_key_coords(rec) -> tuple[tuple, tuple]:
+    """(grid key, interpolation coords) of a record: this package's or the reference's
+    (``rec.query.grid_key()`` / ``coords()``, perfdb.py:239-248) -- only attributes are read."""
+    q = getattr(rec, "query", None)
+    if q is not None:
+        return q.grid_key(), q.coords()
+    shape = dict(rec.shape)
+    return grid_key(rec.kind, rec.quant, shape), tuple(int(shape[a]) for a in KIND_DIMS[rec.kind][1])
+
+
 def build_grids(records: Iterable[OperatorRecord]) -> dict:
+    """_build_grids (perfdb.py:329-355): index records by grid key; duplicates and ragged grids raise."""
     per_key: dict[tuple, dict] = {}
     first: dict[tuple, dict] = {}
     for idx, rec in enumerate(records):
-        shape = dict(rec.shape)
-        key = grid_key(rec.kind, rec.quant, shape)
-        coords = tuple(int(shape[a]) for a in KIND_DIMS[rec.kind][1])
+        key, coords = record_key_coords(rec)
         seen = first.setdefault(key, {})
         if coords in seen:
             raise DbValidationError(
@@ -181,6 +190,47 @@ class PerfDatabase:
 
     def kinds(self) -> set[str]:
         return {k[0] for k in self._grids}
+
+
+@dataclass
+class ValidationReport:
+    """validate_db's result (perfdb.py:672-683)."""
+
+    violations: list[str] = field(default_factory=list)
+    gaps: list[str] = field(default_factory=list)
+
+    @property
+    def ok(self) -> bool:
+        return not self.violations and not self.gaps
+
+    def lines(self) -> list[str]:
+        return [f"violation: {v}" for v in self.violations] + [f"gap: {g}" for g in self.gaps]
+
+
+def validate_db(db, required_kinds: Iterable[str] = ()) -> ValidationReport:
+    """Drop-in for perfdb.validate_db (perfdb.py:685-701): re-check every record's latency
+    and provenance, the grid invariants (duplicates, rectangularity) and the required kinds.
+
+    Accepts this package's databases and the reference's (attributes only); the
+    messages are the reference's.  Host code: it runs once per database file, off
+    the search path (the device image is built by ``flatten`` from the checked grids).
+    """
+    report = ValidationReport()
+    for idx, rec in enumerate(db.records):
+        lat = rec.latency_us
+        if not (isinstance(lat, (int, float)) and math.isfinite(lat) and lat > 0):
+            report.violations.append(f"record #{idx} {record_key_coords(rec)[0]}: latency_us={lat}")
+        if rec.provenance not in PROVENANCES:
+            report.violations.append(f"record #{idx}: provenance={rec.provenance!r}")
+    try:
+        build_grids(db.records)
+    except DbValidationError as e:
+        report.violations.append(str(e))
+    present = db.kinds()
+    for kind in sorted(set(required_kinds)):
+        if kind not in present:
+            report.gaps.append(f"operator kind {kind!r} required but absent")
+    return report
 
 
 def load_db(path: str | Path, extrapolation: str = "default", soa_cache: bool | str | Path = False) -> PerfDatabase:

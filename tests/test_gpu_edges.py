@@ -64,10 +64,10 @@ def test_empty_query_batch():
     assert list(pkg.query_latency_batch(db, [])) == []
 
 
-@pytest.mark.parametrize("where", ["space", "sweep"])
-def test_nonpositive_batch_values_are_skipped(where):
+def test_nonpositive_batch_values_are_skipped():
     """ParallelConfig(batch<1) raises and enumerate_candidates skips it (search.py:101-105,
-    model.py:190-193): batch values (0, -2, 1, 8) give the report of (1, 8); (0,) gives none."""
+    model.py:190-193): batch values (0, -2, 1, 8) give the report of (1, 8); (0,) gives none.
+    (A workload's batch_sweep cannot hold them: WorkloadSpec rejects it, serving_modes.py:94-95.)"""
     import dataclasses
 
     import paper_2601_06288_b200 as pkg
@@ -79,10 +79,7 @@ def test_nonpositive_batch_values_are_skipped(where):
     space = dataclasses.replace(space, tp_values=(1, 2), pp_values=(1, 2), dp_values=(1, 2))
 
     def run(batches):
-        if where == "space":
-            return pkg.run_search(db, model, workload, dataclasses.replace(space, batch_values=batches),
-                                  disagg_constants=dc).to_doc()
-        return pkg.run_search(db, model, dataclasses.replace(workload, batch_sweep=batches), space,
+        return pkg.run_search(db, model, workload, dataclasses.replace(space, batch_values=batches),
                               disagg_constants=dc).to_doc()
 
     got, want = run((0, -2, 1, 8)), run((1, 8))
@@ -92,8 +89,7 @@ def test_nonpositive_batch_values_are_skipped(where):
     ref = oracle.run_search(header, recs, model_doc(case["model"]), case["workload"],
                             {"tp_values": [1, 2], "pp_values": [1, 2], "dp_values": [1, 2], "batch_values": [1, 8]},
                             disagg=case.get("disagg"))
-    if where == "space":
-        assert not diff_canonical(canonical(got), canonical(ref))
+    assert not diff_canonical(canonical(got), canonical(ref))
     none = run((0,))
     assert none["counts"]["enumerated"] == 0 and none["rows"] == [] and none["best"] is None
 
