@@ -158,7 +158,7 @@ typedef struct {
   double ttft_headroom, prefill_util, decode_util;
   int32_t max_x, max_y;
   int32_t load;                      /* MoE load vector index (-1 dense) */
-  int32_t _pad;
+  int32_t static_stride;             /* estimate_static's decode stride (serving_modes.py:236); <= 0: 32 */
 } lc_search_desc;
 
 typedef struct {

@@ -656,7 +656,8 @@ static int estimate_static(ctx_t* X, const cfg_t* c, est_t* e, err_t* err) {
     int64_t kv = isl + k + 1;
     double step;
     if (step_latency(X, c, 1, 0, b, kv, &step, err)) return err->st;
-    int64_t run = osl - 1 - k < 32 ? osl - 1 - k : 32;
+    const int64_t stride = s->static_stride > 0 ? s->static_stride : 32; /* STATIC_DECODE_STRIDE */
+    int64_t run = osl - 1 - k < stride ? osl - 1 - k : stride;
     t_gen += step * (double)run;
     k += run;
   }

@@ -74,6 +74,7 @@ typedef struct {
   /* disagg constants */
   double ttft_headroom, prefill_util, decode_util;
   int32_t max_x, max_y;
+  int32_t static_stride;   /* estimate_static's decode stride (serving_modes.py:236); <= 0: 32 */
 } or_search;
 
 /* one evaluated row (static / aggregated estimate or disaggregated plan) */

@@ -84,7 +84,7 @@ class OrSearch(C.Structure):
                 ("chunked_prefill", C.c_int32), ("kv_mem_fraction", C.c_double),
                 ("prefill_pool_cap", C.c_int32), ("decode_pool_cap", C.c_int32),
                 ("ttft_headroom", C.c_double), ("prefill_util", C.c_double), ("decode_util", C.c_double),
-                ("max_x", C.c_int32), ("max_y", C.c_int32)]
+                ("max_x", C.c_int32), ("max_y", C.c_int32), ("static_stride", C.c_int32)]
 
 
 class OrRow(C.Structure):
@@ -344,6 +344,7 @@ def run_search(header: dict, records: list[dict], model: dict, workload: dict, s
     s.max_y = disagg.get("max_decode_replicas", 64)
 
     if _estimate is not None:
+        s.static_stride = _estimate[2] if len(_estimate) > 2 else 32
         cfg = OrCfg(*_estimate[0])
         out = (C.c_double * 4)()
         reason = C.create_string_buffer(512)
@@ -423,7 +424,8 @@ def busiest_shard(weights, total: int, topk: int, ep: int) -> tuple[int, list[in
 
 
 def estimate(header: dict, records: list[dict], model: dict, workload: dict, cfg: tuple, mode: str,
-             space: dict | None = None, extrapolation: str = "default") -> dict:
-    """estimate_static / estimate_aggregated of one (tp, pp, ep, dp, batch) config."""
+             space: dict | None = None, extrapolation: str = "default", stride: int = 32) -> dict:
+    """estimate_static (with its decode ``stride``, serving_modes.py:231-267) / estimate_aggregated
+    of one (tp, pp, ep, dp, batch) config."""
     return run_search(header, records, model, workload, space, None, extrapolation,
-                      _estimate=(cfg, 0 if mode == "static" else 1))
+                      _estimate=(cfg, 0 if mode == "static" else 1, stride))

@@ -59,7 +59,7 @@ class LcSearchDesc(C.Structure):
                 ("has_ctx_capacity", C.c_int32), ("chunked_prefill", C.c_int32), ("ctx_capacity", C.c_int64),
                 ("kv_mem_fraction", C.c_double), ("prefill_cap", C.c_int32), ("decode_cap", C.c_int32),
                 ("ttft_headroom", C.c_double), ("prefill_util", C.c_double), ("decode_util", C.c_double),
-                ("max_x", C.c_int32), ("max_y", C.c_int32), ("load", C.c_int32), ("_pad", C.c_int32)]
+                ("max_x", C.c_int32), ("max_y", C.c_int32), ("load", C.c_int32), ("static_stride", C.c_int32)]
 
 
 class LcSearchResult(C.Structure):
@@ -105,7 +105,7 @@ SEARCH_DESC_DTYPE = np.dtype([("isl", "<i8"), ("osl", "<i8"), ("prefix", "<i8"),
                               ("has_ctx_capacity", "<i4"), ("chunked_prefill", "<i4"), ("ctx_capacity", "<i8"),
                               ("kv_mem_fraction", "<f8"), ("prefill_cap", "<i4"), ("decode_cap", "<i4"),
                               ("ttft_headroom", "<f8"), ("prefill_util", "<f8"), ("decode_util", "<f8"),
-                              ("max_x", "<i4"), ("max_y", "<i4"), ("load", "<i4"), ("_pad", "<i4")])
+                              ("max_x", "<i4"), ("max_y", "<i4"), ("load", "<i4"), ("static_stride", "<i4")])
 assert SEARCH_DESC_DTYPE.itemsize == C.sizeof(LcSearchDesc), (SEARCH_DESC_DTYPE.itemsize, C.sizeof(LcSearchDesc))
 
 GEN_GRID_DTYPE = np.dtype([("kind", "<i4"), ("quant", "<i4"), ("n_axes", "<i4"), ("_pad", "<i4"),

@@ -130,8 +130,13 @@ struct QtGroup {
 // a decode-series table shared by the searches with the same (isl, batch list)
 struct DsGroup {
   int64_t off, isl;
-  int32_t b_off, n_b, n_steps, _pad;
+  int32_t b_off, n_b, n_steps, stride;  // stride: estimate_static's decode stride (32 by default)
 };
+
+// estimate_static's decode stride (serving_modes.py:236, STATIC_DECODE_STRIDE = 32)
+__host__ __device__ __forceinline__ int64_t static_stride(const lc_search_desc& S) {
+  return S.static_stride > 0 ? (int64_t)S.static_stride : 32;
+}
 
 // Static decode loops shared across output lengths.  The KV samples isl + 32k + 1
 // and the decode step terms depend on (isl, batch list, MoE load), not on osl, and
@@ -199,7 +204,7 @@ struct SearchMeta {
   int64_t tail_off[3];  // per tail type
   int64_t qt_off[4];    // query tables per slot class [slot-in-class][b_i] (classes in QtGroup)
   int64_t ds_off;       // decode-series table [gclass][b_i][step], shared by searches with equal (isl, batches)
-  int32_t n_steps;      // static decode samples (ceil((osl-1)/32), 0 without static mode)
+  int32_t n_steps;      // static decode samples (ceil((osl-1)/stride), 0 without static mode)
   int32_t ds_stride;    // steps stored per (gclass, batch) in the shared table (max over its searches)
   int64_t mark_off;     // offset of this search's batches in the mixed-token marking pass
   int32_t _pad2;
@@ -897,7 +902,7 @@ __global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_dstab
     const lc_entry e = P.gclasses[g];
     int st = 0, nlog = 0;
     QVal out;
-    out.lat = LC_TABLE_QUERY(V, e.grid, e.kind, e.quant, P.batches[G.b_off + bi], G.isl + 32ll * k + 1, e.d[2], e.d[3],
+    out.lat = LC_TABLE_QUERY(V, e.grid, e.kind, e.quant, P.batches[G.b_off + bi], G.isl + (int64_t)G.stride * k + 1, e.d[2], e.d[3],
                              e.d[4], &st, &nlog);
     out.status = st;
     out._pad = 0;
@@ -982,6 +987,7 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
     const double bubble = (double)(mb + ti.pp - 1) / (double)mb;
     const int64_t xt_dec = expert_tokens(P, c, M, S, 1, bi, b);
     const QVal* ds = P.ds + M.ds_off + (int64_t)P.gclass_of[tmpl] * M.ds_stride * S.n_b + bi;  // sample k at ds[k * n_b]
+    const int64_t stride = static_stride(S);  // every member of the group shares it (SeriesGroup key)
     const StepArgs a0{PH_DECODE, 0, b, S.isl + 1, xt_dec};
     double term[LC_MAX_ENTRIES];
     int m = 0, gi = -1;
@@ -1036,7 +1042,7 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
           if (sj >= K || bad >= 0) continue;
           if (sj == 0) { g[j] = term[gi]; continue; }
           const QVal q = ds[(int64_t)sj * S.n_b];
-          if (q.status) { bad = j; e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + 32ll * sj + 1; continue; }
+          if (q.status) { bad = j; e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + stride * sj + 1; continue; }
           g[j] = 0.0 + (q.lat * g_rep / 1000.0) * bubble;
         }
         NeumaierSum sc[LC_DECODE_CHAINS];
@@ -1064,13 +1070,13 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
           const int sj = step + j;
           if (sj >= K || (bad >= 0 && j >= bad)) continue;
           const double st = sc[j].result();
-          // members whose last sample is sj: t_gen + st * run, run = osl - 1 - 32 sj
+          // members whose last sample is sj: t_gen + st * run, run = osl - 1 - stride sj
           while (mi < G.n_m && mem[mi].n_steps - 1 == sj) {
-            const int64_t run = P.searches[mem[mi].search].osl - 1 - 32ll * sj;
+            const int64_t run = P.searches[mem[mi].search].osl - 1 - stride * sj;
             put(mi, t_gen + st * (double)run, 0, mem[mi].n_steps, 0, 0);
             ++mi;
           }
-          t_gen += st * 32.0;
+          t_gen += st * (double)stride;
         }
       }
     }
@@ -1210,7 +1216,8 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
   }
   // the generation step is a memo hit when a static decode step used the same KV length
   const int64_t k = (S.isl + S.osl / 2) - S.isl - 1;
-  const bool dup = do_st && o.st_status == 0 && S.osl > 1 && k >= 0 && (k % 32) == 0 && (k / 32) < o.st_steps;
+  const int64_t sstr = static_stride(S);
+  const bool dup = do_st && o.st_status == 0 && S.osl > 1 && k >= 0 && (k % sstr) == 0 && (k / sstr) < o.st_steps;
   if (((do_ag && (o.flags & 1)) || do_dg) && !dup) add_q(o.qG);
   ra.q1 += (unsigned)(q & 0xffff);
   ra.q2 += (unsigned)(q >> 16);
@@ -2857,7 +2864,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     M.cell_off = cells;
     cells += (int64_t)sp->n_tmpl * S.n_b;
     M.qt_off[0] = M.qt_off[1] = M.qt_off[2] = M.qt_off[3] = 0;
-    M.n_steps = ((S.modes & 1) && S.osl > 1) ? (int32_t)((S.osl - 1 + 31) / 32) : 0;
+    M.n_steps = ((S.modes & 1) && S.osl > 1) ? (int32_t)((S.osl - 1 + static_stride(S) - 1) / static_stride(S)) : 0;
     M.tail_off[0] = M.tail_off[1] = M.tail_off[2] = 0;
     M.plan_off = (int32_t)plans;
     const int pc = ((S.modes & 4) && !(S.modes & LC_MODE_NO_PLANS)) ? S.prefill_cap * S.decode_cap : 0;
@@ -2959,12 +2966,12 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
       M.ds_stride = 0;
       if (!M.n_steps || !sp->n_gclass) continue;
       const int32_t cb = S.b_off;
-      const std::vector<int64_t> key = {S.isl, cb, S.n_b};
+      const std::vector<int64_t> key = {S.isl, cb, S.n_b, static_stride(S)};
       auto jt = gidx.find(key);
       int32_t gi;
       if (jt == gidx.end()) {
         gi = gidx[key] = (int32_t)c->hds.size();
-        c->hds.push_back(DsGroup{0, S.isl, cb, S.n_b, 0, 0});
+        c->hds.push_back(DsGroup{0, S.isl, cb, S.n_b, 0, (int32_t)static_stride(S)});
       } else {
         gi = jt->second;
       }
@@ -2992,7 +2999,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     for (int s = 0; s < n_search; ++s) {
       const lc_search_desc& S = searches[s];
       if (!c->hmeta[s].n_steps) continue;
-      std::vector<int64_t> key = {S.isl, S.b_off, S.n_b, S.load};
+      std::vector<int64_t> key = {S.isl, S.b_off, S.n_b, S.load, static_stride(S)};
       auto it = members.find(key);
       if (it == members.end()) { order.push_back(key); members[key] = {s}; }
       else it->second.push_back(s);

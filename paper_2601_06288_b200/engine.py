@@ -255,7 +255,7 @@ class Engine:
 
     # ------------------------------------------------------------------ batches
     def run_batch(self, db, model, space, workloads: Sequence, disagg=DEFAULT_DISAGG, mode_override=None,
-                  enforce_budget: bool = True, mode_extra: int = 0) -> BatchOutput:
+                  enforce_budget: bool = True, mode_extra: int = 0, static_stride: int = 32) -> BatchOutput:
         t0 = time.perf_counter()
         sph, plan, flat = self.space_handle(db, model, space)
         dbh, _ = self.db_handle(db)
@@ -347,6 +347,7 @@ class Engine:
         searches["decode_util"] = float(disagg.decode_utilization)
         searches["max_x"], searches["max_y"] = disagg.max_prefill_replicas, disagg.max_decode_replicas
         searches["load"] = load_v
+        searches["static_stride"] = static_stride  # estimate_static's decode stride (serving_modes.py:236)
         b_arr = np.array(batches if batches else [1], dtype=np.int64)
         l_arr = np.concatenate(loads) if loads else np.zeros(1)
         results = np.zeros(n, dtype=N.SEARCH_RESULT_DTYPE)
@@ -611,7 +612,7 @@ def consistency_problems(model, cfg) -> list[str]:
     return out
 
 
-def _estimate(mode_bit: int, name: str, db, model, cfg, workload, device: int):
+def _estimate(mode_bit: int, name: str, db, model, cfg, workload, device: int, stride: int = 32):
     import dataclasses
 
     from . import specs as S
@@ -626,7 +627,8 @@ def _estimate(mode_bit: int, name: str, db, model, cfg, workload, device: int):
     wl = dataclasses.replace(workload, batch_sweep=())
     eng = get_engine(device)
     with eng._lock:
-        out = eng.run_batch(db, model, space, [wl], mode_override=mode_bit | MODE_FORCE, enforce_budget=False)
+        out = eng.run_batch(db, model, space, [wl], mode_override=mode_bit | MODE_FORCE, enforce_budget=False,
+                            static_stride=stride)
         U = out.fetch_units()
         if int(out.results[0]["n_units"]) != 1:
             raise SearchError("single-config estimate did not produce exactly one unit")
@@ -645,16 +647,18 @@ def _estimate(mode_bit: int, name: str, db, model, cfg, workload, device: int):
 def estimate_static(db, model, cfg, workload, stride: int = 32, device: int = 0) -> PerfEstimate:
     """Drop-in for serving_modes.estimate_static (serving_modes.py:231-267) for one config.
 
-    Raises like the reference (ParallelConfigError, PerfDbError subclasses).  Only
-    the reference's default decode stride (32) is implemented on the device.
+    Raises like the reference (ParallelConfigError, PerfDbError subclasses).  The
+    decode loop samples the KV length every ``stride`` tokens on the device (the
+    decode-series table and loop take the stride per search); stride 1 is the
+    reference's brute-force setting (acceptance A2, tests/test_acceptance.py:96-135).
     """
     from .specs import WorkloadError
 
     if stride < 1:
         raise WorkloadError("stride must be >= 1")
-    if stride != 32:
-        raise NotImplementedError("the device evaluates the default decode stride (32) only")
-    return _estimate(MODE_STATIC, "static", db, model, cfg, workload, device)
+    if stride > 2**31 - 1:
+        stride = 2**31 - 1  # any stride >= osl - 1 samples once; keep it in the descriptor's int32
+    return _estimate(MODE_STATIC, "static", db, model, cfg, workload, device, int(stride))
 
 
 def estimate_aggregated(db, model, cfg, workload, device: int = 0) -> PerfEstimate:

@@ -58,3 +58,42 @@ def test_inconsistent_config_raises_parallel_config_error():
     with pytest.raises(pkg.specs.ParallelConfigError) as ei:
         pkg.estimate_static(db, model, bad, workload)
     assert "tp=3 does not divide num_heads=128" in str(ei.value)
+
+
+STRIDE_CONFIGS = [("cfg4_dsv3", (8, 2, 8, 1, 128)), ("a1_qwen_small", (2, 2, 1, 4, 64)),
+                  ("moe_load_custom", (2, 1, 4, 2, 256)), ("strict_long_isl", (1, 1, 1, 1, 4)),
+                  ("cfg3_llama70b_kv90", (4, 2, 1, 1, 32))]
+
+
+@pytest.mark.parametrize("stride", [1, 3, 7, 31, 33, 100, 10_000])
+@pytest.mark.parametrize("name,cfg", STRIDE_CONFIGS, ids=[n for n, _ in STRIDE_CONFIGS])
+def test_static_estimate_any_stride_matches_oracle(name, cfg, stride):
+    """estimate_static(..., stride) for any stride >= 1 (serving_modes.py:236-265); stride 1 is
+    acceptance A2's brute-force setting (pkg/tests/test_acceptance.py:96-135)."""
+    import paper_2601_06288_b200 as pkg
+    from oracle import oracle
+
+    case = BY_NAME[name]
+    db, model, workload, space, dc = case_objects(case)
+    header, recs = oracle.read_db_records(db_path(case))
+    header, recs = oracle.mutate(header, recs, case.get("mutation"), hw_docs())
+    pc = space.config(*cfg, db.backend)
+    ref = oracle.estimate(header, recs, model_doc(case["model"]), case["workload"], cfg, "static",
+                          case.get("space"), case.get("extrapolation", "default"), stride=stride)
+    if ref["status"]:
+        kind, msg = ref["reason"].split(": ", 1)
+        with pytest.raises(Exception) as ei:
+            pkg.estimate_static(db, model, pc, workload, stride=stride)
+        assert type(ei.value).__name__ == kind and str(ei.value) == msg
+    else:
+        est = pkg.estimate_static(db, model, pc, workload, stride=stride)
+        got = [est.ttft_ms, est.tpot_ms, est.speed, est.throughput_per_gpu]
+        assert [x.hex() for x in got] == [float(x).hex() for x in ref["values"]]
+
+
+def test_stride_must_be_positive():
+    import paper_2601_06288_b200 as pkg
+
+    db, model, workload, space, dc = case_objects(BY_NAME["a1_qwen_small"])
+    with pytest.raises(pkg.specs.WorkloadError):
+        pkg.estimate_static(db, model, space.config(1, 1, 1, 1, 8, db.backend), workload, stride=0)

@@ -212,3 +212,32 @@ def test_integration_patch_imports_cleanly(ref, monkeypatch):
         for m, d in saved.items():
             vars(m).clear()
             vars(m).update(d)
+
+
+@pytest.mark.parametrize("stride", [1, 5, 32, 77, 5000])
+@pytest.mark.parametrize("name,cfg,wl", [
+    ("deepseek-v3", (8, 2, 8, 1, 128), dict(isl=5000, osl=1000)),
+    ("qwen3-32b", (2, 1, 1, 4, 64), dict(isl=4000, osl=500, prefix_len=1000)),
+    ("gpt-oss-120b", (4, 1, 4, 1, 512), dict(isl=512, osl=97)),
+])
+def test_oracle_static_stride_matches_reference(ref, name, cfg, wl, stride, tmp_path):
+    """The oracle's estimate_static at any stride equals the reference's (serving_modes.py:231-267)
+    bit for bit: the oracle that pins the device's stride path (tests/test_gpu_estimate.py)."""
+    from oracle import oracle
+
+    header, recs = oracle.read_db_records(_db_file(name))
+    mdoc = json.loads((GOLDEN / "specs" / f"model-{name}.json").read_text())
+    tmp = tmp_path / "db.jsonl"
+    tmp.write_bytes(gzip.decompress(_db_file(name).read_bytes()))
+    rdb = ref.perfdb.load_db(str(tmp))
+    rmodel = ref.model.ModelSpec.from_doc(mdoc)
+    rwl = ref.serving_modes.WorkloadSpec.from_doc(dict(wl))
+    rcfg = ref.search.CandidateSpace().config(*cfg, rdb.backend)
+    from llmconf import estimator
+
+    estimator.clear_caches()
+    est = ref.serving_modes.estimate_static(rdb, rmodel, rcfg, rwl, stride=stride)
+    got = oracle.estimate(header, recs, mdoc, dict(wl), cfg, "static", stride=stride)
+    assert got["status"] == 0
+    want = [est.ttft_ms, est.tpot_ms, est.speed, est.throughput_per_gpu]
+    assert [float(x).hex() for x in got["values"]] == [x.hex() for x in want]
