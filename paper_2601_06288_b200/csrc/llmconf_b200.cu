@@ -328,6 +328,7 @@ struct EvalParams {
   int64_t n_cells_total;
   lc_search_result* results;
   SearchAcc* acc;                    // [n_search]
+  unsigned long long* fbuckets;      // [n_search][kSpeedBuckets]: K4 speed-bucket maxima of throughput
   // closed-form K0 (fused candidate rows): unit offsets per (search, combo), budget flags, template combos
   const int32_t* pair_off;           // [n_search * n_combos + 1], nullptr otherwise
   const uint8_t* pair_inb;
@@ -1126,6 +1127,27 @@ __global__ void __launch_bounds__(128) k_ptables(EvalParams P) {
   }
 }
 
+// K4 speed buckets (k_front_*): order-preserving buckets of the IEEE bit pattern
+// of a feasible row's speed, holding the best throughput seen in each.  With a
+// speed floor every feasible speed is >= the floor, so the buckets can be fixed
+// before any row exists -- 256 per binade from the floor's binade up, 16 binades,
+// faster rows sharing the top bucket -- and the maxima are accumulated while the
+// rows are written (k_eval_cells / k_expand / k_disagg), saving K4 a pass over
+// every row.  Without a floor the range pass (k_front_mid / k_front_pass2) runs.
+constexpr int kSpeedBuckets = 4096;
+constexpr int kFixedShift = 44;
+__device__ __forceinline__ bool fixed_buckets(const lc_search_desc& S) {
+  return S.has_floor && S.speed_floor > 0.0 && S.speed_floor < INFINITY;
+}
+__device__ __forceinline__ int fixed_bucket(const lc_search_desc& S, double speed) {
+  const unsigned long long base = ((unsigned long long)__double_as_longlong(S.speed_floor)) >> kFixedShift;
+  const unsigned long long d = (((unsigned long long)__double_as_longlong(speed)) >> kFixedShift) - base;
+  return d < (unsigned long long)kSpeedBuckets ? (int)d : kSpeedBuckets - 1;  // speed >= floor: no wrap
+}
+__device__ __forceinline__ void bucket_max(unsigned long long* bk, const lc_search_desc& S, double speed, double thru) {
+  atomicMax(&bk[fixed_bucket(S, speed)], (unsigned long long)__double_as_longlong(thru));
+}
+
 // K2: one thread per cell assembles every step from the tables.
 // Warp-aggregated per-search accounting: one set of atomics per warp when all
 // its units belong to one search (the common case), per lane otherwise.
@@ -1155,7 +1177,8 @@ __device__ __forceinline__ void acc_flush(SearchAcc* A, const RowAcc& r) {
 // serving_modes.py:161-172; pool rates, serving_modes.py:366, 380) plus its
 // contribution to the per-search accounting.
 __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search_desc& S, const CellOut& o, int64_t ci,
-                                            int64_t u, int64_t b, int64_t gpus, bool inb, RowAcc& ra) {
+                                            int64_t u, int64_t b, int64_t gpus, bool inb, RowAcc& ra,
+                                            unsigned long long* bk) {
   const int64_t n = P.n_cap;
   const bool do_st = (S.modes & 1) && inb, do_ag = (S.modes & 2) && inb, do_dg = (S.modes & 4) != 0;
   int32_t q = 0;
@@ -1172,6 +1195,7 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
       if ((!S.has_ttft || o.st_ttft <= S.ttft_limit) && (!S.has_floor || speed >= S.speed_floor)) {
         ++ra.feas;
         ra.feasible_speed(speed);
+        if (bk) bucket_max(bk, S, speed, thru);
       }
       add_q(o.qSD);
     }
@@ -1188,6 +1212,7 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
       if ((!S.has_ttft || o.ag_ttft <= S.ttft_limit) && (!S.has_floor || speed >= S.speed_floor)) {
         ++ra.feas;
         ra.feasible_speed(speed);
+        if (bk) bucket_max(bk, S, speed, thru);
       }
     }
     add_q(o.qM);
@@ -1348,6 +1373,7 @@ __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, uint3
   }
   if (P.pair_off) {
     s_out = s;
+    unsigned long long* bk = fixed_buckets(S) ? P.fbuckets + (int64_t)s * kSpeedBuckets : nullptr;
     const int64_t pbase = (int64_t)s * P.sp_n_combos;
     const int j1 = P.tmpl_cidx_off[tmpl + 1];
     for (int j = P.tmpl_cidx_off[tmpl]; j < j1; ++j) {
@@ -1355,7 +1381,7 @@ __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, uint3
       const int64_t pr = pbase + cj;
       const int32_t off = P.pair_off[pr];
       if (bi >= P.pair_off[pr + 1] - off) continue;  // this dp variant is not a candidate at this batch
-      expand_unit(P, S, o, ci, (int64_t)off + bi, b, P.combos[cj].gpus, P.pair_inb[pr] != 0, ra);
+      expand_unit(P, S, o, ci, (int64_t)off + bi, b, P.combos[cj].gpus, P.pair_inb[pr] != 0, ra, bk);
     }
   } else {
     P.cells[ci] = o;
@@ -1426,7 +1452,8 @@ __global__ void __launch_bounds__(256, LC_EXPAND_MIN_BLOCKS) k_expand(EvalParams
     const CellOut o = P.cells[ci];
     const int64_t b = P.batches[S.b_off + bi];
     const bool inb = P.u_budget[u] != 0;
-    expand_unit(P, S, o, ci, u, b, c.gpus, inb, ra);
+    expand_unit(P, S, o, ci, u, b, c.gpus, inb, ra,
+                fixed_buckets(S) ? P.fbuckets + (int64_t)s * kSpeedBuckets : nullptr);
     }
     // per-search accounting for K4 (search.py:343-358 counts, speed range)
     int s0 = __shfl_sync(0xffffffffu, s, 0);
@@ -1477,7 +1504,9 @@ struct PoolKey {
   int32_t unit; // global unit index, -1 = none
 };
 
-__device__ __forceinline__ int cfg_cmp(const EvalParams& P, int32_t ua, int32_t ub) {
+// Out of line: only reached when two keys tie exactly, and the formatted strings
+// would otherwise bloat every caller with local-memory buffers.
+__device__ __noinline__ int cfg_cmp(const EvalParams& P, int32_t ua, int32_t ub) {
   char a[96], b[96];
   const lc_search_desc& S = P.searches[P.u_search[ua]];
   fmt_cfg_key(a, P.combos[P.u_combo[ua]], P.batches[S.b_off + P.u_batch[ua]]);
@@ -1485,26 +1514,50 @@ __device__ __forceinline__ int cfg_cmp(const EvalParams& P, int32_t ua, int32_t 
   return str_cmp(a, b);
 }
 
-__device__ __forceinline__ bool pool_less(const EvalParams& P, const PoolKey& a, const PoolKey& b) {
-  if (a.unit < 0) return false;
-  if (b.unit < 0) return true;
-  if (a.r != b.r) return a.r < b.r;
-  return cfg_cmp(P, a.unit, b.unit) < 0;
-}
 
-// ---- K5a: top-k prefill / decode pool members per search (block per search)
-constexpr int kPoolLocal = 16;  // per-thread top-k list length (caps up to 16 take the fast path)
+// ---- K5a: top-k prefill / decode pool members per search
+// sorted(pool, key=_pool_rank)[:cap] (search.py:276-277, 338-339): the order is
+// (-rate/gpus, config-key string), and the stable sort keeps unit order for
+// identical keys (duplicate batch values), so the total order is (r, key, unit).
+constexpr int kPoolLocal = 32;  // caps up to 32 take the fast path (one list element per lane)
 #ifndef LC_POOL_THREADS
-#define LC_POOL_THREADS 128
+#define LC_POOL_THREADS 256
 #endif
 constexpr int kPoolThreads = LC_POOL_THREADS;
 
-__device__ __forceinline__ void local_insert(const EvalParams& P, PoolKey* lst, int& n, int cap, const PoolKey& k) {
-  if (n == cap && !pool_less(P, k, lst[n - 1])) return;
-  int j = n < cap ? n++ : cap - 1;
-  while (j > 0 && pool_less(P, k, lst[j - 1])) { lst[j] = lst[j - 1]; --j; }
-  lst[j] = k;
+__device__ __forceinline__ bool pool_before(const EvalParams& P, const PoolKey& a, const PoolKey& b) {
+  if (a.unit < 0) return false;
+  if (b.unit < 0) return true;
+  if (a.r != b.r) return a.r < b.r;
+  if (a.unit == b.unit) return false;
+  const int c = cfg_cmp(P, a.unit, b.unit);
+  return c != 0 ? c < 0 : a.unit < b.unit;
 }
+
+// A sorted top-`cap` list held across a warp's registers: lane j holds element j
+// (j < n).  Insertion is one comparison per lane, a ballot and a shuffle -- no
+// local memory.  `thr` is the last element once the list is full (a candidate
+// not strictly before it cannot enter).
+struct WarpTopK {
+  PoolKey mine;
+  int n;
+  __device__ __forceinline__ void init() { mine = PoolKey{0.0, -1}; n = 0; }
+  __device__ __forceinline__ double thr_r(int cap) const {
+    return n < cap ? INFINITY : __shfl_sync(0xffffffffu, mine.r, cap - 1);
+  }
+  // every lane passes the same x (warp-uniform call)
+  __device__ __forceinline__ void insert(const EvalParams& P, const PoolKey& x, int cap) {
+    const int lane = threadIdx.x & 31;
+    const bool after = lane < n && !pool_before(P, x, mine);  // elements staying ahead of x
+    const int pos = __popc(__ballot_sync(0xffffffffu, after));
+    if (pos >= cap) return;
+    const double ur = __shfl_up_sync(0xffffffffu, mine.r, 1);
+    const int32_t uu = __shfl_up_sync(0xffffffffu, mine.unit, 1);
+    if (lane == pos) mine = x;
+    else if (lane > pos && lane < cap) { mine.r = ur; mine.unit = uu; }
+    n = n < cap ? n + 1 : cap;
+  }
+};
 
 // ---- K5b: replica sweep per pairing and plan sort (block per search)
 struct PlanRec {
@@ -1653,6 +1706,7 @@ __global__ void __launch_bounds__(256) k_disagg(EvalParams P, SearchMeta* meta, 
       const unsigned long long bits = (unsigned long long)__double_as_longlong(a.speed);
       atomicMax(&A->smax, bits);
       atomicMax(&A->smin_c, ~bits);
+      if (fixed_buckets(S)) bucket_max(P.fbuckets + (int64_t)s * kSpeedBuckets, S, a.speed, a.thru);
     }
   }
   if (threadIdx.x == 0) {
@@ -1796,8 +1850,6 @@ constexpr int kSurvivorCap = 2048;  // front candidates kept in shared memory
 #define LC_FRONT_THREADS 256
 #endif
 constexpr int kFrontThreads = LC_FRONT_THREADS;
-constexpr int kSpeedBuckets = 4096;
-
 #define FRONT_ROW_FILTER(v)                                                          \
   if (!v.valid) continue;                                                            \
   if ((v.mode == 0 && !(S.modes & 1)) || (v.mode == 1 && !(S.modes & 2))) continue;
@@ -1831,30 +1883,8 @@ __device__ __forceinline__ void slice_of(int64_t n, int parts, int part, int64_t
   *hi = n * (part + 1) / parts;
 }
 
-// k-way merge across a warp: lane l holds a sorted list lst[0..n) (n <= cap);
-// writes the warp's `cap` smallest keys, in order, to out[] and returns how many.
-__device__ int warp_merge(const EvalParams& P, const PoolKey* lst, int n, int cap, PoolKey* out) {
-  const int lane = threadIdx.x & 31;
-  int head = 0, got = 0;
-  for (int k = 0; k < cap; ++k) {
-    PoolKey best = head < n ? lst[head] : PoolKey{0.0, -1};
-    int src = lane;
-    for (int o = 16; o > 0; o >>= 1) {
-      PoolKey other;
-      other.r = __shfl_xor_sync(0xffffffffu, best.r, o);
-      other.unit = __shfl_xor_sync(0xffffffffu, best.unit, o);
-      const int osrc = __shfl_xor_sync(0xffffffffu, src, o);
-      if (pool_less(P, other, best) || (other.unit == best.unit && osrc < src)) { best = other; src = osrc; }
-    }
-    if (best.unit < 0) break;
-    if (lane == src) ++head;
-    if (lane == 0) out[k] = best;
-    ++got;
-  }
-  return got;
-}
-
-__global__ void k_pools_partial(EvalParams P, const SearchMeta* meta, PoolPartial* part) {
+__global__ void __launch_bounds__(kPoolThreads) k_pools_partial(EvalParams P, const SearchMeta* meta,
+                                                                 PoolPartial* part) {
   const int s = blockIdx.y, bx = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const lc_search_desc& S = P.searches[s];
   if (!(S.modes & 4)) return;
@@ -1869,27 +1899,35 @@ __global__ void k_pools_partial(EvalParams P, const SearchMeta* meta, PoolPartia
     const int cap = role == 0 ? S.prefill_cap : S.decode_cap;
     if (cap > kPoolLocal || cap <= 0) { if (tid == 0) dst->n[role] = 0; continue; }
     const double* keys = P.pool_key + (int64_t)role * P.n_cap;
-    PoolKey lst[kPoolLocal];
-    int n = 0;
-    for (int64_t i = lo + tid; i < hi; i += blockDim.x) {
-      const int32_t u = (int32_t)(u0 + i);
-      const double r = keys[u];
-      if (r == INFINITY) continue;  // pool candidate skipped
-      local_insert(P, lst, n, cap, PoolKey{r, u});
+    WarpTopK tk;
+    tk.init();
+    double thr = INFINITY;
+    // warp-strided chunks of 32 consecutive units (coalesced); candidates must not be
+    // after the current last element (r <= thr; exact order decided on insertion)
+    for (int64_t base = lo + (int64_t)warp * 32; base < hi; base += kPoolThreads) {
+      const int64_t i = base + lane;
+      const double r = i < hi ? keys[u0 + i] : INFINITY;  // INFINITY: pool candidate skipped
+      unsigned m = __ballot_sync(0xffffffffu, r != INFINITY && r <= thr);
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const PoolKey x{__shfl_sync(0xffffffffu, r, src), (int32_t)(u0 + base + src)};
+        if (x.r <= thr) {
+          tk.insert(P, x, cap);
+          thr = tk.thr_r(cap);
+        }
+      }
     }
-    const int got = warp_merge(P, lst, n, cap, wout[warp]);
-    if (lane == 0) wn[warp] = got;
+    if (lane < tk.n) wout[warp][lane] = tk.mine;
+    if (lane == 0) wn[warp] = tk.n;
     __syncthreads();
     if (warp == 0) {
-      PoolKey l2[kPoolLocal];
-      int n2 = 0;
-      if (lane < kWarps) {
-        n2 = wn[lane];
-        for (int j = 0; j < n2; ++j) l2[j] = wout[lane][j];
-      }
-      PoolKey* o = dst->k[role];
-      const int g2 = warp_merge(P, l2, n2, cap, o);
-      if (lane == 0) dst->n[role] = g2;
+      WarpTopK t2;
+      t2.init();
+      for (int w = 0; w < kWarps; ++w)
+        for (int j = 0; j < wn[w]; ++j) t2.insert(P, wout[w][j], cap);
+      if (lane < t2.n) dst->k[role][lane] = t2.mine;
+      if (lane == 0) dst->n[role] = t2.n;
     }
     __syncthreads();
   }
@@ -1900,32 +1938,28 @@ __global__ void k_pools_final(EvalParams P, SearchMeta* meta, const PoolPartial*
   const lc_search_desc& S = P.searches[s];
   if (!(S.modes & 4)) return;
   __shared__ PoolKey red[kPoolThreads];
-  __shared__ PoolKey outk[kPoolLocal];
   for (int role = 0; role < 2; ++role) {
     const int cap = role == 0 ? S.prefill_cap : S.decode_cap;
     int got = 0;
     if (cap <= kPoolLocal) {
       if (tid < 32) {
-        PoolKey l[kPoolLocal];
-        int n = 0;
-        if (tid < kPoolSplit) {
-          const PoolPartial& pp = part[(int64_t)s * kPoolSplit + tid];
-          n = pp.n[role];
-          for (int j = 0; j < n; ++j) l[j] = pp.k[role][j];
+        WarpTopK t;
+        t.init();
+        for (int b = 0; b < kPoolSplit; ++b) {
+          const PoolPartial& pp = part[(int64_t)s * kPoolSplit + b];
+          for (int j = 0; j < pp.n[role]; ++j) t.insert(P, pp.k[role][j], cap);
         }
-        got = warp_merge(P, l, n, cap, outk);
-        __syncwarp();
-        if (tid < got) pool_sel[(int64_t)s * 128 + role * 64 + tid] = outk[tid].unit;
-      }
-      got = __shfl_sync(0xffffffffu, got, 0);  // warp 0's count, broadcast within warp 0 only
-      if (tid == 0) {
-        if (role == 0) meta[s].n_pre = got;
-        else meta[s].n_dec = got;
+        got = t.n;
+        if (tid < got) pool_sel[(int64_t)s * 128 + role * 64 + tid] = t.mine.unit;
+        if (tid == 0) {
+          if (role == 0) meta[s].n_pre = got;
+          else meta[s].n_dec = got;
+        }
       }
       __syncthreads();
       continue;
     }
-    // large caps: rounds over all units (rare)
+    // large caps (33..64): rounds over all units (rare)
     const int32_t u0 = meta[s].unit_off, nu = meta[s].n_units;
     const double* keys = P.pool_key + (int64_t)role * P.n_cap;
     PoolKey prev{0.0, -1};
@@ -1936,13 +1970,13 @@ __global__ void k_pools_final(EvalParams P, SearchMeta* meta, const PoolPartial*
         const double r = keys[u];
         if (r == INFINITY) continue;
         const PoolKey key{r, u};
-        if (prev.unit >= 0 && !pool_less(P, prev, key)) continue;
-        if (pool_less(P, key, best)) best = key;
+        if (prev.unit >= 0 && !pool_before(P, prev, key)) continue;
+        if (pool_before(P, key, best)) best = key;
       }
       red[tid] = best;
       __syncthreads();
       for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (tid < w && pool_less(P, red[tid + w], red[tid])) red[tid] = red[tid + w];
+        if (tid < w && pool_before(P, red[tid + w], red[tid])) red[tid] = red[tid + w];
         __syncthreads();
       }
       const PoolKey sel = red[0];
@@ -1964,6 +1998,7 @@ __global__ void k_pools_final(EvalParams P, SearchMeta* meta, const PoolPartial*
 struct FrontMeta {
   int32_t shift, any;
   unsigned long long base;
+  int32_t fixed, _pad;  // fixed: buckets from the speed floor, filled while the rows were written
 };
 
 __global__ void __launch_bounds__(kFrontThreads) k_front_mid(EvalParams P, const SearchMeta* meta,
@@ -1975,8 +2010,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_mid(EvalParams P, const
   const lc_search_desc& S = P.searches[s];
   const SearchMeta& M = meta[s];
   __shared__ MissKey mred[kFrontThreads];
-  unsigned long long* bk = buckets + (int64_t)s * kSpeedBuckets;
-  for (int i = tid; i < kSpeedBuckets; i += blockDim.x) bk[i] = 0ull;
+  (void)buckets;  // zeroed at the start of the pipeline; fixed-geometry searches are filled by now
   if (tid == 0) {
     const SearchAcc A = P.acc[s];  // k_expand + k_disagg
     const unsigned long long lo = ~A.smin_c, hi = A.smax, q1 = A.q1, q2 = A.q2;
@@ -1993,11 +2027,15 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_mid(EvalParams P, const
     R.nearest_violation = 0.0;
     R.front_off = (int32_t)((int64_t)M.unit_off * 2 + M.plan_off);
     R.n_front = 0;
+    const bool fixed = fixed_buckets(S);
     int shift = 0;
-    if (feas) while (shift < 63 && ((hi >> shift) - (lo >> shift)) >= (unsigned long long)kSpeedBuckets) ++shift;
+    if (fixed) shift = kFixedShift;
+    else if (feas) while (shift < 63 && ((hi >> shift) - (lo >> shift)) >= (unsigned long long)kSpeedBuckets) ++shift;
     fmeta[s].shift = shift;
     fmeta[s].any = feas > 0;
-    fmeta[s].base = feas ? (lo >> shift) : 0ull;
+    fmeta[s].fixed = fixed;
+    fmeta[s].base = fixed ? ((unsigned long long)__double_as_longlong(S.speed_floor)) >> kFixedShift
+                          : (feas ? (lo >> shift) : 0ull);
     n_surv[s] = 0;
   }
   __syncthreads();
@@ -2035,7 +2073,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_pass2(EvalParams P, con
                                                                unsigned long long* buckets) {
   const int s = blockIdx.y, bx = blockIdx.x, tid = threadIdx.x;
   const FrontMeta fm = fmeta[s];
-  if (!fm.any) return;
+  if (!fm.any || fm.fixed) return;  // fixed geometry: filled while the rows were written
   const lc_search_desc& S = P.searches[s];
   const SearchMeta& M = meta[s];
   const int64_t nplan = results[s].n_plans;
@@ -2087,7 +2125,8 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_pass3(EvalParams P, con
     const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
     FRONT_ROW_FILTER(v)
     if (!feasible(S, v)) continue;
-    const int b = (int)((((unsigned long long)__double_as_longlong(v.speed)) >> fm.shift) - fm.base);
+    const int b = fm.fixed ? fixed_bucket(S, v.speed)
+                           : (int)((((unsigned long long)__double_as_longlong(v.speed)) >> fm.shift) - fm.base);
     if (bk[b] != 0ull && v.thru <= __longlong_as_double((long long)bk[b])) continue;
     const int k = atomicAdd(&n_surv[s], 1);
     if (k < kSurvivorCap) surv[(int64_t)s * kSurvivorCap + k] = FrontCand{v.speed, v.thru, v.key};
@@ -2539,6 +2578,7 @@ static EvalParams make_params(lc_ctx* c) {
   P.n_cells_total = c->n_cells;
   P.results = (lc_search_result*)c->results.p;
   P.acc = (SearchAcc*)c->acc.p;
+  P.fbuckets = (unsigned long long*)c->buckets.p;
 #ifndef LC_NO_FUSE_EXPAND
   P.pair_off = c->enum_fit ? (const int32_t*)c->block_sums.p : nullptr;
 #else
@@ -2586,6 +2626,12 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     SearchAcc* acc = c->acc.get<SearchAcc>(c->n_search > 0 ? c->n_search : 1, &err);
     if (err != cudaSuccess) return fail(LC_ERR_CUDA, "accumulator allocation");
     CK(cudaMemsetAsync(acc, 0, sizeof(SearchAcc) * (c->n_search > 0 ? c->n_search : 1), c->stream));
+  }
+  {
+    // K4 speed buckets: zeroed here, filled by K2 / K5b for fixed-geometry searches
+    c->buckets.get<unsigned long long>((size_t)c->n_search * kSpeedBuckets, &err);
+    if (err != cudaSuccess) return fail(LC_ERR_CUDA, "bucket allocation");
+    CK(cudaMemsetAsync(c->buckets.p, 0, sizeof(unsigned long long) * kSpeedBuckets * c->n_search, c->stream));
   }
   EvalParams P = make_params(c);
   const int sms = sm_count(c->device);
