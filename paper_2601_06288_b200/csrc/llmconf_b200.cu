@@ -1504,14 +1504,36 @@ struct PoolKey {
   int32_t unit; // global unit index, -1 = none
 };
 
-// Out of line: only reached when two keys tie exactly, and the formatted strings
-// would otherwise bloat every caller with local-memory buffers.
-__device__ __noinline__ int cfg_cmp(const EvalParams& P, int32_t ua, int32_t ub) {
-  char a[96], b[96];
+// Python string order of two config keys "tp{tp}pp{pp}ep{ep}dp{dp}b{batch}"
+// (ParallelConfig.key, model.py:205-206), without formatting them: the literal
+// parts are equal, so the first difference lies in the first numeric field whose
+// decimal strings differ -- a digit against a digit, or (one string a prefix of
+// the other) a digit against the next literal letter, which sorts after every
+// digit, or against the end of the key (the batch field), which sorts before.
+__device__ __forceinline__ int dec_field_cmp(int64_t x, int64_t y, bool letter_follows) {
+  if (x == y) return 0;
+  int nx = 1, ny = 1;
+  int64_t px = 1, py = 1;  // 10^(digits - 1)
+  while (x / px >= 10) { px *= 10; ++nx; }
+  while (y / py >= 10) { py *= 10; ++ny; }
+  for (; px > 0 && py > 0; px /= 10, py /= 10) {
+    const int dx = (int)((x / px) % 10), dy = (int)((y / py) % 10);
+    if (dx != dy) return dx < dy ? -1 : 1;
+  }
+  // one decimal string is a prefix of the other: compare its terminator with a digit
+  const int shorter_vs_longer = letter_follows ? 1 : -1;
+  return nx < ny ? shorter_vs_longer : -shorter_vs_longer;
+}
+
+__device__ __forceinline__ int cfg_cmp(const EvalParams& P, int32_t ua, int32_t ub) {
   const lc_search_desc& S = P.searches[P.u_search[ua]];
-  fmt_cfg_key(a, P.combos[P.u_combo[ua]], P.batches[S.b_off + P.u_batch[ua]]);
-  fmt_cfg_key(b, P.combos[P.u_combo[ub]], P.batches[S.b_off + P.u_batch[ub]]);
-  return str_cmp(a, b);
+  const lc_combo a = P.combos[P.u_combo[ua]], b = P.combos[P.u_combo[ub]];
+  int c = dec_field_cmp(a.tp, b.tp, true);
+  if (!c) c = dec_field_cmp(a.pp, b.pp, true);
+  if (!c) c = dec_field_cmp(a.ep, b.ep, true);
+  if (!c) c = dec_field_cmp(a.dp, b.dp, true);
+  if (!c) c = dec_field_cmp(P.batches[S.b_off + P.u_batch[ua]], P.batches[S.b_off + P.u_batch[ub]], false);
+  return c;
 }
 
 

@@ -2,7 +2,7 @@
 mkdir -p gpurun_out
 for so in variants/*.so; do
   n=$(basename $so .so)
-  LC_B200_LIB=$so timeout 600 python bench.py --no-cpu-baseline --steps 20 > gpurun_out/var_$n.json 2>/dev/null
+  LC_B200_LIB=$so timeout 600 python bench.py --no-cpu-baseline --north-star none --steps 20 > gpurun_out/var_$n.json 2>/dev/null
   python -c "
 import json,sys; d=json.load(open('gpurun_out/var_$n.json'))
 print('$n', 'ms/step', round(d['ms_per_step'],3), 'seq', round(d['search_wall_ms']['per_model_sequential_device'],3), {k: round(v,3) for k,v in d['roofline']['kernel_ms'].items()})" || echo "$n failed"
