@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define LC_ABI_VERSION 2
+#define LC_ABI_VERSION 3
 #define LC_MAX_ENTRIES 16   /* plan entries per (tp, pp, ep) template */
 #define LC_MAX_BUDGETS 16
 #define LC_MAX_EXPERTS 1024
@@ -278,6 +278,34 @@ typedef struct {
  * _interp_cells (perfdb.py:509-536); sol_estimate (perfdb.py:431-484) above the grid. */
 int lc_query_batch(lc_ctx* ctx, const lc_db* db, int32_t n, const lc_query* queries, double* latency_us,
                    int32_t* status);
+
+/* ------------------------------------------------ step latency with breakdown */
+typedef struct {
+  int32_t tmpl;                      /* (tp, pp, ep) template index of the space plan */
+  int32_t phase;                     /* 0 prefill, 1 decode, 2 mixed (model.py PHASES) */
+  int64_t n_ctx, n_gen, seq;         /* decompose's token arguments (model.py:271-285) */
+  int64_t batch;                     /* cfg.batch: the pipeline bubble's microbatches (estimator.py:83) */
+  int32_t load;                      /* MoE load vector index; -1: no skew (dense model) */
+  int32_t _pad;
+} lc_step_req;                       /* 48 bytes */
+
+typedef struct {
+  double total_ms;                   /* sum(breakdown.values()), CPython float sum (estimator.py:95) */
+  int32_t status;                    /* code | label << 8 of the first failing entry in plan order; 0 ok */
+  int32_t n_entries;                 /* template entries (plan order) */
+  int64_t c0, c1;                    /* the failing query's interpolated coordinates */
+  double entry_ms[LC_MAX_ENTRIES];   /* 0.0 + ms * bubble per entry (estimator.py:93) */
+  int32_t entry_label[LC_MAX_ENTRIES]; /* label id per entry; -1: entry absent from this step */
+} lc_step_out;
+
+/* Step latencies with per-label breakdown for n requests: one warp per request
+ * computes the expert-tail token count (busiest EP shard, moe_load.py:141-147),
+ * every plan entry's coordinates and interpolated latency, and the bubble-scaled
+ * sum in plan order.  Host arrays in and out; returns after the copy back.
+ * Replaces get_step_latency / _step_latency_cached (estimator.py:71-110) and
+ * through them get_mix_latency / get_gen_latency (estimator.py:117-156). */
+int lc_step_latency(lc_ctx* ctx, const lc_db* db, const lc_space* sp, int32_t n, const lc_step_req* reqs,
+                    int32_t n_loads, const double* loads, lc_step_out* out);
 
 /* ------------------------------------------------ report rows (host) */
 /* Column view of a search's report rows (fastreport.Columns). */

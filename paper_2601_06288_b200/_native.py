@@ -128,6 +128,15 @@ class LcReportCols(C.Structure):
                 ("r_sys", F64P), ("model_json", C.c_char_p), ("runtime", C.c_char_p * 6)]
 
 
+LC_MAX_ENTRIES = 16
+STEP_REQ_DTYPE = np.dtype([("tmpl", "<i4"), ("phase", "<i4"), ("n_ctx", "<i8"), ("n_gen", "<i8"), ("seq", "<i8"),
+                           ("batch", "<i8"), ("load", "<i4"), ("_pad", "<i4")])
+assert STEP_REQ_DTYPE.itemsize == 48
+STEP_OUT_DTYPE = np.dtype([("total_ms", "<f8"), ("status", "<i4"), ("n_entries", "<i4"), ("c0", "<i8"),
+                           ("c1", "<i8"), ("entry_ms", "<f8", (LC_MAX_ENTRIES,)),
+                           ("entry_label", "<i4", (LC_MAX_ENTRIES,))])
+assert STEP_OUT_DTYPE.itemsize == 224
+
 QUERY_DTYPE = np.dtype([("grid", "<i4"), ("kind", "<i4"), ("quant", "<i4"), ("policy", "<i4"), ("d", "<i8", (5,)),
                         ("kv_len", "<i8")])
 assert QUERY_DTYPE.itemsize == 64
@@ -135,7 +144,7 @@ assert QUERY_DTYPE.itemsize == 64
 EXPORTED = ("lc_abi_version", "lc_last_error", "lc_open", "lc_close", "lc_db_upload", "lc_db_free",
             "lc_space_upload", "lc_space_free", "lc_search_batch", "lc_fetch", "lc_replay_last", "lc_replay_async",
             "lc_stream", "lc_query_batch", "lc_dbgen", "lc_set_raw_filter", "lc_fetch_pools",
-            "lc_unit_raw", "lc_report_rows")
+            "lc_unit_raw", "lc_report_rows", "lc_step_latency")
 
 _LIB = None
 
@@ -171,6 +180,8 @@ def load_library(path: str | os.PathLike | None = None):
     lib.lc_report_rows.argtypes = [C.POINTER(LcReportCols), I64P, C.c_int64, C.c_int32, C.c_int32, C.c_char_p,
                                    C.c_int64]
     lib.lc_report_rows.restype = C.c_int64
+    lib.lc_step_latency.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, F64P,
+                                    C.c_void_p]
     if path is None:
         _LIB = lib
     return lib

@@ -232,7 +232,7 @@ struct lc_ctx {
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
-  DBuf pool_key, qt_groups, ds_groups, front_compact, pool_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
+  DBuf step_in, step_out, step_loads, pool_key, qt_groups, ds_groups, front_compact, pool_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   DBuf q_in, q_lat, q_st;  // lc_query_batch
   DBuf sgroups, smembers, sd;  // shared static decode loops
   DBuf pgroups, psteps;        // shared prefill step totals
@@ -2337,6 +2337,81 @@ static int upload(T** dst, const T* src, size_t n, cudaStream_t st) {
   return LC_OK;
 }
 
+struct StepView {  // what k_step reads of a space plan
+  const lc_entry* entries;
+  const int32_t* tmpl_n;
+  const TmplInfo* tmpl_info;
+  int64_t hidden, topk, n_experts;
+  int32_t is_moe, n_tmpl;
+};
+
+// get_step_latency (estimator.py:71-110), one warp per request: the expert-tail
+// token count (busiest EP shard, a warp apportionment), then the plan entries
+// across the lanes -- coordinates (decompose, model.py:302-404), latency
+// (query_latency), 0.0 + ms * bubble -- and lane 0 sums them in plan order with
+// CPython's float sum; the first failing entry in plan order decides the error.
+template <int PER>
+__global__ void __launch_bounds__(128) k_step(DbView V, StepView T, int32_t n, const lc_step_req* __restrict__ reqs,
+                                              const double* __restrict__ loads, lc_step_out* __restrict__ out) {
+  __shared__ int hist_all[4][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t r = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; r < n; r += nw) {
+    const lc_step_req R = reqs[r];
+    const TmplInfo ti = T.tmpl_info[R.tmpl];
+    const int64_t tokens = R.n_ctx + R.n_gen;
+    int64_t xt = 0;
+    if (T.is_moe) {  // _skewed_expert_tokens (estimator.py:58-68)
+      const int64_t f = ti.ep / ti.tp > 1 ? ti.ep / ti.tp : 1;
+      const int64_t pooled = tokens * f;
+      xt = ceil_div_f(pooled * T.topk, ti.ep);
+      if (ti.ep > 1 && R.load >= 0) {
+        const int E = (int)T.n_experts;
+        const double* q = loads + (int64_t)R.load * 2 * E;
+        const int64_t tail = warp_busiest_shard<PER>(q, q + E, E, pooled, T.topk, ti.ep, hist_all[warp]);
+        xt = tail > xt ? tail : xt;
+      }
+    }
+    const StepArgs a{R.phase, R.n_ctx, R.n_gen, R.seq, xt};
+    const int ne = T.tmpl_n[R.tmpl];
+    const int64_t mb = R.batch > 1 ? R.batch : 1;
+    const double bubble = (double)(mb + ti.pp - 1) / (double)mb;  // pipeline_bubble (estimator.py:45-48)
+    double val = 0.0;
+    int st = 0, label = -1;
+    int64_t d[5] = {0, 0, 0, 0, 0};
+    if (lane < ne) {
+      const lc_entry e = T.entries[(int64_t)R.tmpl * LC_MAX_ENTRIES + lane];
+      if (entry_coords(e, a, T.hidden, d)) {
+        label = e.label;
+        int nlog = 0;
+        const double lat = query_body<true>(V, e.grid, e.kind, e.quant, d[0], d[1], d[2], d[3], d[4], &st, &nlog);
+        val = 0.0 + (lat * (double)e.repeat / 1000.0) * bubble;
+      }
+    }
+    lc_step_out* o = out + r;
+    if (lane < LC_MAX_ENTRIES) {
+      o->entry_ms[lane] = st ? 0.0 : val;
+      o->entry_label[lane] = lane < ne ? label : -1;
+    }
+    const unsigned bad = __ballot_sync(0xffffffffu, label >= 0 && st != 0);
+    if (bad) {  // the first failing entry in plan order raises (query_latency)
+      const int src = __ffs(bad) - 1;
+      const int bst = __shfl_sync(0xffffffffu, st, src);
+      const int blb = __shfl_sync(0xffffffffu, label, src);
+      const int64_t c0 = __shfl_sync(0xffffffffu, d[0], src), c1 = __shfl_sync(0xffffffffu, d[1], src);
+      if (lane == 0) { o->status = bst | (blb << 8); o->c0 = c0; o->c1 = c1; o->total_ms = 0.0; o->n_entries = ne; }
+      continue;
+    }
+    NeumaierSum sum;
+    for (int i = 0; i < ne; ++i) {
+      const double v = __shfl_sync(0xffffffffu, val, i);
+      const int lb = __shfl_sync(0xffffffffu, label, i);
+      if (lb >= 0) sum.add(v);
+    }
+    if (lane == 0) { o->status = 0; o->c0 = o->c1 = 0; o->total_ms = sum.result(); o->n_entries = ne; }
+  }
+}
+
 // ============================================================================ C ABI
 extern "C" {
 
@@ -2378,7 +2453,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->step_in, &c->step_out, &c->step_loads, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->pinned_front) cudaFreeHost(c->pinned_front);
@@ -3287,6 +3362,16 @@ int lc_replay_async(lc_ctx* c) {
   return run_eval_pipeline(c, nullptr);
 }
 
+static DbView db_view(const lc_db* db) {
+  DbView V;
+  V.grids = db->grids; V.axv = db->axv; V.axl = db->axl; V.cell = db->cell; V.clog = db->clog;
+  V.logtab = db->logtab; V.exptab = db->exptab;
+  V.mem_bw = db->mem_bw; V.intra_bw = db->intra_bw; V.inter_bw = db->inter_bw; V.gpu_memory = db->gpu_memory;
+  for (int i = 0; i < 4; ++i) V.compute[i] = db->compute[i];
+  V.gpn = db->gpn; V.policy = db->policy;
+  return V;
+}
+
 int lc_query_batch(lc_ctx* c, const lc_db* db, int32_t n, const lc_query* queries, double* latency_us,
                    int32_t* status) {
   if (!c || !db || n < 0 || (n > 0 && (!queries || !latency_us || !status)))
@@ -3305,18 +3390,49 @@ int lc_query_batch(lc_ctx* c, const lc_db* db, int32_t n, const lc_query* querie
   int32_t* dst = c->q_st.get<int32_t>(n, &e);
   if (e != cudaSuccess) return fail(LC_ERR_CUDA, std::string("lc_query_batch: ") + cudaGetErrorString(e));
   CK(cudaMemcpyAsync(dq, queries, sizeof(lc_query) * (size_t)n, cudaMemcpyHostToDevice, c->stream));
-  DbView V;
-  V.grids = db->grids; V.axv = db->axv; V.axl = db->axl; V.cell = db->cell; V.clog = db->clog;
-  V.logtab = db->logtab; V.exptab = db->exptab;
-  V.mem_bw = db->mem_bw; V.intra_bw = db->intra_bw; V.inter_bw = db->inter_bw; V.gpu_memory = db->gpu_memory;
-  for (int i = 0; i < 4; ++i) V.compute[i] = db->compute[i];
-  V.gpn = db->gpn; V.policy = db->policy;
+  const DbView V = db_view(db);
   const int threads = 128;
   const int blocks = (int)std::min<int64_t>(((int64_t)n + threads - 1) / threads, 148 * 16);
   k_query<<<blocks, threads, 0, c->stream>>>(V, n, dq, dlat, dst);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(latency_us, dlat, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaMemcpyAsync(status, dst, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return LC_OK;
+}
+
+int lc_step_latency(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n, const lc_step_req* reqs,
+                    int32_t n_loads, const double* loads, lc_step_out* out) {
+  if (!c || !db || !sp || n < 0 || (n > 0 && (!reqs || !out)) || n_loads < 0 || (n_loads > 0 && !loads))
+    return fail(LC_ERR_ARG, "lc_step_latency: bad argument");
+  if (n == 0) return LC_OK;
+  for (int32_t i = 0; i < n; ++i) {
+    const lc_step_req& r = reqs[i];
+    if (r.tmpl < 0 || r.tmpl >= sp->n_tmpl || r.phase < 0 || r.phase > 2 || r.n_ctx < 0 || r.n_gen < 0 ||
+        r.seq < 1 || r.load >= n_loads || (r.phase == PH_PREFILL && r.n_ctx % r.seq))
+      return fail(LC_ERR_ARG, "lc_step_latency: request " + std::to_string(i) + " out of range");
+  }
+  CK(cudaSetDevice(c->device));
+  cudaError_t e = cudaSuccess;
+  lc_step_req* dreq = c->step_in.get<lc_step_req>(n, &e);
+  lc_step_out* dout = c->step_out.get<lc_step_out>(n, &e);
+  double* dload = c->step_loads.get<double>(n_loads > 0 ? (size_t)n_loads * 2 * sp->n_experts : 1, &e);
+  if (e != cudaSuccess) return fail(LC_ERR_CUDA, std::string("lc_step_latency: ") + cudaGetErrorString(e));
+  CK(cudaMemcpyAsync(dreq, reqs, sizeof(lc_step_req) * (size_t)n, cudaMemcpyHostToDevice, c->stream));
+  if (n_loads > 0)
+    CK(cudaMemcpyAsync(dload, loads, sizeof(double) * (size_t)n_loads * 2 * sp->n_experts, cudaMemcpyHostToDevice,
+                       c->stream));
+  StepView T;
+  T.entries = sp->entries; T.tmpl_n = sp->tmpl_n; T.tmpl_info = sp->tmpl_info;
+  T.hidden = sp->hidden; T.topk = sp->topk; T.n_experts = sp->n_experts; T.is_moe = sp->is_moe;
+  T.n_tmpl = sp->n_tmpl;
+  const DbView V = db_view(db);
+  const int blocks = (int)std::min<int64_t>(((int64_t)n + 3) / 4, 148 * 8);
+  if (sp->n_experts <= 128) k_step<4><<<blocks, 128, 0, c->stream>>>(V, T, n, dreq, dload, dout);
+  else if (sp->n_experts <= 256) k_step<8><<<blocks, 128, 0, c->stream>>>(V, T, n, dreq, dload, dout);
+  else k_step<32><<<blocks, 128, 0, c->stream>>>(V, T, n, dreq, dload, dout);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, dout, sizeof(lc_step_out) * (size_t)n, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return LC_OK;
 }

@@ -15,7 +15,7 @@ def test_library_exports_header_symbols():
     assert declared == set(_native.EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.lc_abi_version() == 2
+    assert lib.lc_abi_version() == 3
 
 
 def test_struct_layouts_match_header_sizes():
@@ -68,7 +68,8 @@ def test_ctypes_and_numpy_layouts_match_the_c_compiler(tmp_path):
              "lc_batch_totals": ctypes.sizeof(N.LcBatchTotals), "lc_fetch_req": ctypes.sizeof(N.LcFetchReq),
              "lc_entry": ENTRY_DTYPE.itemsize, "lc_combo": COMBO_DTYPE.itemsize, "lc_slot": SLOT_DTYPE.itemsize,
              "lc_query": N.QUERY_DTYPE.itemsize, "lc_gen_grid": N.GEN_GRID_DTYPE.itemsize,
-             "lc_dbgen_desc": ctypes.sizeof(N.LcDbgenDesc)}
+             "lc_dbgen_desc": ctypes.sizeof(N.LcDbgenDesc), "lc_step_req": N.STEP_REQ_DTYPE.itemsize,
+             "lc_step_out": N.STEP_OUT_DTYPE.itemsize}
     for k, v in sizes.items():
         assert c[k] == v, (k, c[k], v)
     fields = {
@@ -89,6 +90,10 @@ def test_ctypes_and_numpy_layouts_match_the_c_compiler(tmp_path):
         "lc_dbgen_desc.compute": N.LcDbgenDesc.compute.offset,
         "lc_db_desc.compute": N.LcDbDesc.compute.offset, "lc_db_desc.policy": N.LcDbDesc.policy.offset,
         "lc_space_desc.gclass_of": N.LcSpaceDesc.gclass_of.offset,
+        "lc_search_desc.static_stride": off(N.SEARCH_DESC_DTYPE, "static_stride"),
+        "lc_step_req.batch": off(N.STEP_REQ_DTYPE, "batch"), "lc_step_req.load": off(N.STEP_REQ_DTYPE, "load"),
+        "lc_step_out.c1": off(N.STEP_OUT_DTYPE, "c1"), "lc_step_out.entry_ms": off(N.STEP_OUT_DTYPE, "entry_ms"),
+        "lc_step_out.entry_label": off(N.STEP_OUT_DTYPE, "entry_label"),
     }
     for k, v in fields.items():
         assert c[k] == v, (k, c[k], v)

@@ -191,7 +191,10 @@ def test_integration_patch_imports_cleanly(ref, monkeypatch):
     block = re.search(r"## 1\. Python drop-in.*?```python\n(.*?)```", text, re.S).group(1)
     parts = [p for p in re.split(r"\n(?=# llmconf/)", "\n" + block.strip()) if p.strip()]
     monkeypatch.setenv("LLMCONF_ENGINE", "b200")
-    targets = {"search.py": ref.search, "perfdb.py": ref.perfdb, "serving_modes.py": ref.serving_modes}
+    import llmconf.estimator
+
+    targets = {"search.py": ref.search, "perfdb.py": ref.perfdb, "serving_modes.py": ref.serving_modes,
+               "estimator.py": llmconf.estimator}
     done = set()
     saved = {m: dict(vars(m)) for m in targets.values()}
     try:
@@ -208,6 +211,8 @@ def test_integration_patch_imports_cleanly(ref, monkeypatch):
         assert ref.perfdb.query_latency is pkg.query_latency
         assert ref.serving_modes.estimate_static is pkg.estimate_static
         assert ref.serving_modes.estimate_aggregated is pkg.estimate_aggregated
+        assert llmconf.estimator.get_step_latency is pkg.get_step_latency
+        assert llmconf.estimator.get_gen_latency is pkg.get_gen_latency
     finally:
         for m, d in saved.items():
             vars(m).clear()
