@@ -1557,27 +1557,68 @@ __device__ __forceinline__ bool pool_before(const EvalParams& P, const PoolKey& 
 }
 
 // A sorted top-`cap` list held across a warp's registers: lane j holds element j
-// (j < n).  Insertion is one comparison per lane, a ballot and a shuffle -- no
-// local memory.  `thr` is the last element once the list is full (a candidate
-// not strictly before it cannot enter).
+// (absent elements are {0, -1}, which sort last).  A chunk of up to 32 new keys
+// is merged in one step -- a warp bitonic sort of the chunk, then the bitonic
+// merge of the two sorted lists keeping the 32 smallest -- so a long run of
+// improving keys (the pool rate per GPU grows along a combo's batch list) costs
+// one merge per chunk, not one serial insertion per key.  No local memory.
+__device__ __forceinline__ PoolKey shfl_key(const PoolKey& v, int src) {
+  return PoolKey{__shfl_sync(0xffffffffu, v.r, src), __shfl_sync(0xffffffffu, v.unit, src)};
+}
+__device__ __forceinline__ PoolKey shfl_xor_key(const PoolKey& v, int m) {
+  return PoolKey{__shfl_xor_sync(0xffffffffu, v.r, m), __shfl_xor_sync(0xffffffffu, v.unit, m)};
+}
+// compare-exchange with the partner lane (lane ^ j): the lower lane keeps the
+// earlier key when `ascending`, the later one otherwise
+__device__ __forceinline__ void warp_cx(const EvalParams& P, PoolKey& v, int j, bool ascending) {
+  const int lane = threadIdx.x & 31;
+  const PoolKey o = shfl_xor_key(v, j);
+  const bool lower = (lane & j) == 0;
+  if (lower == ascending ? pool_before(P, o, v) : pool_before(P, v, o)) v = o;
+}
+__device__ __forceinline__ void warp_sort32(const EvalParams& P, PoolKey& v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) warp_cx(P, v, j, (lane & k) == 0);
+}
+// v: ascending list; w: ascending list; returns the 32 earliest of both, ascending
+__device__ __forceinline__ PoolKey warp_merge32(const EvalParams& P, const PoolKey& v, const PoolKey& w) {
+  const int lane = threadIdx.x & 31;
+  const PoolKey wr = shfl_key(w, 31 - lane);
+  PoolKey m = pool_before(P, wr, v) ? wr : v;  // bitonic: the 32 earliest of v ++ reverse(w)
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) warp_cx(P, m, j, true);
+  return m;
+}
+
 struct WarpTopK {
   PoolKey mine;
   int n;
   __device__ __forceinline__ void init() { mine = PoolKey{0.0, -1}; n = 0; }
+  // key of the cap-th element once the list is full (INFINITY before): a new key
+  // with a larger r cannot enter
   __device__ __forceinline__ double thr_r(int cap) const {
     return n < cap ? INFINITY : __shfl_sync(0xffffffffu, mine.r, cap - 1);
   }
-  // every lane passes the same x (warp-uniform call)
-  __device__ __forceinline__ void insert(const EvalParams& P, const PoolKey& x, int cap) {
+  // merge one key per lane (unit < 0: none); warp-uniform call
+  __device__ __forceinline__ void merge_chunk(const EvalParams& P, PoolKey x, int cap) {
     const int lane = threadIdx.x & 31;
-    const bool after = lane < n && !pool_before(P, x, mine);  // elements staying ahead of x
-    const int pos = __popc(__ballot_sync(0xffffffffu, after));
-    if (pos >= cap) return;
-    const double ur = __shfl_up_sync(0xffffffffu, mine.r, 1);
-    const int32_t uu = __shfl_up_sync(0xffffffffu, mine.unit, 1);
-    if (lane == pos) mine = x;
-    else if (lane > pos && lane < cap) { mine.r = ur; mine.unit = uu; }
-    n = n < cap ? n + 1 : cap;
+    const int got = __popc(__ballot_sync(0xffffffffu, x.unit >= 0));
+    if (!got) return;
+    warp_sort32(P, x);
+    mine = warp_merge32(P, mine, x);
+    n = n + got < cap ? n + got : cap;
+    if (lane >= cap) mine = PoolKey{0.0, -1};
+  }
+  // merge another warp's sorted list (element j in lane j, `m` elements)
+  __device__ __forceinline__ void merge_sorted(const EvalParams& P, const PoolKey& x, int m, int cap) {
+    const int lane = threadIdx.x & 31;
+    if (!m) return;
+    mine = warp_merge32(P, mine, x);
+    n = n + m < cap ? n + m : cap;
+    if (lane >= cap) mine = PoolKey{0.0, -1};
   }
 };
 
@@ -1924,30 +1965,23 @@ __global__ void __launch_bounds__(kPoolThreads) k_pools_partial(EvalParams P, co
     WarpTopK tk;
     tk.init();
     double thr = INFINITY;
-    // warp-strided chunks of 32 consecutive units (coalesced); candidates must not be
-    // after the current last element (r <= thr; exact order decided on insertion)
+    // warp-strided chunks of 32 consecutive units (coalesced); a key can enter only if
+    // not after the current cap-th element (r <= thr; exact order in the merge)
     for (int64_t base = lo + (int64_t)warp * 32; base < hi; base += kPoolThreads) {
       const int64_t i = base + lane;
       const double r = i < hi ? keys[u0 + i] : INFINITY;  // INFINITY: pool candidate skipped
-      unsigned m = __ballot_sync(0xffffffffu, r != INFINITY && r <= thr);
-      while (m) {
-        const int src = __ffs(m) - 1;
-        m &= m - 1;
-        const PoolKey x{__shfl_sync(0xffffffffu, r, src), (int32_t)(u0 + base + src)};
-        if (x.r <= thr) {
-          tk.insert(P, x, cap);
-          thr = tk.thr_r(cap);
-        }
-      }
+      const bool cand = r != INFINITY && r <= thr;
+      if (!__any_sync(0xffffffffu, cand)) continue;
+      tk.merge_chunk(P, cand ? PoolKey{r, (int32_t)(u0 + i)} : PoolKey{0.0, -1}, cap);
+      thr = tk.thr_r(cap);
     }
-    if (lane < tk.n) wout[warp][lane] = tk.mine;
+    wout[warp][lane] = tk.mine;
     if (lane == 0) wn[warp] = tk.n;
     __syncthreads();
     if (warp == 0) {
       WarpTopK t2;
       t2.init();
-      for (int w = 0; w < kWarps; ++w)
-        for (int j = 0; j < wn[w]; ++j) t2.insert(P, wout[w][j], cap);
+      for (int w = 0; w < kWarps; ++w) t2.merge_sorted(P, wout[w][lane], wn[w], cap);
       if (lane < t2.n) dst->k[role][lane] = t2.mine;
       if (lane == 0) dst->n[role] = t2.n;
     }
@@ -1969,7 +2003,8 @@ __global__ void k_pools_final(EvalParams P, SearchMeta* meta, const PoolPartial*
         t.init();
         for (int b = 0; b < kPoolSplit; ++b) {
           const PoolPartial& pp = part[(int64_t)s * kPoolSplit + b];
-          for (int j = 0; j < pp.n[role]; ++j) t.insert(P, pp.k[role][j], cap);
+          const int m = pp.n[role];
+          t.merge_sorted(P, tid < m ? pp.k[role][tid] : PoolKey{0.0, -1}, m, cap);
         }
         got = t.n;
         if (tid < got) pool_sel[(int64_t)s * 128 + role * 64 + tid] = t.mine.unit;
