@@ -25,6 +25,7 @@
 #include "glibc_libm.cuh"
 #include "lc_eval.cuh"
 #include "lc_tails.cuh"
+#include "lc_keys.h"
 #include "lc_report.h"
 
 using namespace lc;
@@ -113,6 +114,7 @@ struct lc_space {
   int32_t* gclass_of;  // [n_tmpl]
   int32_t* tmpl_cidx_off;  // [n_tmpl + 1] into tmpl_cidx
   int32_t* tmpl_cidx;      // combo indices of each template
+  uint64_t* combo_rank;    // [n_combos] rank of (tp, pp, ep, dp) in config-key string order << 36 (lc_keys.h)
 };
 
 // Query-table sharing.  A slot's inputs are (grid, coordinates); which search
@@ -228,7 +230,7 @@ struct lc_ctx {
   int device;
   cudaStream_t stream;
   cudaEvent_t ev[8];
-  DBuf searches, batches, loads, meta, results;
+  DBuf searches, batches, batch_code, loads, meta, results;
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
@@ -239,6 +241,7 @@ struct lc_ctx {
   DBuf acc;                    // SearchAcc per search
   DBuf plan_scratch;           // K5b pairing results [search][256]
   std::vector<PGroup> hpg;
+  std::vector<uint64_t> hbatch_code;  // config-key batch-field codes of the batches array (lc_keys.h)
   int64_t n_pstep = 0;
   DBuf raw_mask;               // lc_set_raw_filter: optional keep-mask over [filt_lo, filt_hi)
   int64_t filt_lo = 0, filt_hi = -1;  // filt_hi < 0: no raw-tuple filter
@@ -329,6 +332,8 @@ struct EvalParams {
   lc_search_result* results;
   SearchAcc* acc;                    // [n_search]
   unsigned long long* fbuckets;      // [n_search][kSpeedBuckets]: K4 speed-bucket maxima of throughput
+  const uint64_t* combo_rank;        // [n_combos] config-key string rank << 36 (lc_keys.h)
+  const uint64_t* batch_code;        // [n_batches] config-key batch-field code (lc_keys.h)
   // closed-form K0 (fused candidate rows): unit offsets per (search, combo), budget flags, template combos
   const int32_t* pair_off;           // [n_search * n_combos + 1], nullptr otherwise
   const uint8_t* pair_inb;
@@ -1501,41 +1506,13 @@ __global__ void __launch_bounds__(256, LC_EXPAND_MIN_BLOCKS) k_expand(EvalParams
 // ---- comparison helpers for top-k / best / nearest
 struct PoolKey {
   double r;     // -rate / gpus
+  uint64_t sk;  // config-key string order (lc_keys.h): combo rank << 36 | batch code
   int32_t unit; // global unit index, -1 = none
 };
 
-// Python string order of two config keys "tp{tp}pp{pp}ep{ep}dp{dp}b{batch}"
-// (ParallelConfig.key, model.py:205-206), without formatting them: the literal
-// parts are equal, so the first difference lies in the first numeric field whose
-// decimal strings differ -- a digit against a digit, or (one string a prefix of
-// the other) a digit against the next literal letter, which sorts after every
-// digit, or against the end of the key (the batch field), which sorts before.
-__device__ __forceinline__ int dec_field_cmp(int64_t x, int64_t y, bool letter_follows) {
-  if (x == y) return 0;
-  int nx = 1, ny = 1;
-  int64_t px = 1, py = 1;  // 10^(digits - 1)
-  while (x / px >= 10) { px *= 10; ++nx; }
-  while (y / py >= 10) { py *= 10; ++ny; }
-  for (; px > 0 && py > 0; px /= 10, py /= 10) {
-    const int dx = (int)((x / px) % 10), dy = (int)((y / py) % 10);
-    if (dx != dy) return dx < dy ? -1 : 1;
-  }
-  // one decimal string is a prefix of the other: compare its terminator with a digit
-  const int shorter_vs_longer = letter_follows ? 1 : -1;
-  return nx < ny ? shorter_vs_longer : -shorter_vs_longer;
+__device__ __forceinline__ PoolKey pool_key_of(const EvalParams& P, const lc_search_desc& S, double r, int32_t u) {
+  return PoolKey{r, P.combo_rank[P.u_combo[u]] | P.batch_code[S.b_off + P.u_batch[u]], u};
 }
-
-__device__ __forceinline__ int cfg_cmp(const EvalParams& P, int32_t ua, int32_t ub) {
-  const lc_search_desc& S = P.searches[P.u_search[ua]];
-  const lc_combo a = P.combos[P.u_combo[ua]], b = P.combos[P.u_combo[ub]];
-  int c = dec_field_cmp(a.tp, b.tp, true);
-  if (!c) c = dec_field_cmp(a.pp, b.pp, true);
-  if (!c) c = dec_field_cmp(a.ep, b.ep, true);
-  if (!c) c = dec_field_cmp(a.dp, b.dp, true);
-  if (!c) c = dec_field_cmp(P.batches[S.b_off + P.u_batch[ua]], P.batches[S.b_off + P.u_batch[ub]], false);
-  return c;
-}
-
 
 // ---- K5a: top-k prefill / decode pool members per search
 // sorted(pool, key=_pool_rank)[:cap] (search.py:276-277, 338-339): the order is
@@ -1551,9 +1528,8 @@ __device__ __forceinline__ bool pool_before(const EvalParams& P, const PoolKey& 
   if (a.unit < 0) return false;
   if (b.unit < 0) return true;
   if (a.r != b.r) return a.r < b.r;
-  if (a.unit == b.unit) return false;
-  const int c = cfg_cmp(P, a.unit, b.unit);
-  return c != 0 ? c < 0 : a.unit < b.unit;
+  if (a.sk != b.sk) return a.sk < b.sk;
+  return a.unit < b.unit;
 }
 
 // A sorted top-`cap` list held across a warp's registers: lane j holds element j
@@ -1563,10 +1539,13 @@ __device__ __forceinline__ bool pool_before(const EvalParams& P, const PoolKey& 
 // improving keys (the pool rate per GPU grows along a combo's batch list) costs
 // one merge per chunk, not one serial insertion per key.  No local memory.
 __device__ __forceinline__ PoolKey shfl_key(const PoolKey& v, int src) {
-  return PoolKey{__shfl_sync(0xffffffffu, v.r, src), __shfl_sync(0xffffffffu, v.unit, src)};
+  return PoolKey{__shfl_sync(0xffffffffu, v.r, src), (uint64_t)__shfl_sync(0xffffffffu, (unsigned long long)v.sk, src),
+                 __shfl_sync(0xffffffffu, v.unit, src)};
 }
 __device__ __forceinline__ PoolKey shfl_xor_key(const PoolKey& v, int m) {
-  return PoolKey{__shfl_xor_sync(0xffffffffu, v.r, m), __shfl_xor_sync(0xffffffffu, v.unit, m)};
+  return PoolKey{__shfl_xor_sync(0xffffffffu, v.r, m),
+                 (uint64_t)__shfl_xor_sync(0xffffffffu, (unsigned long long)v.sk, m),
+                 __shfl_xor_sync(0xffffffffu, v.unit, m)};
 }
 // compare-exchange with the partner lane (lane ^ j): the lower lane keeps the
 // earlier key when `ascending`, the later one otherwise
@@ -1596,7 +1575,7 @@ __device__ __forceinline__ PoolKey warp_merge32(const EvalParams& P, const PoolK
 struct WarpTopK {
   PoolKey mine;
   int n;
-  __device__ __forceinline__ void init() { mine = PoolKey{0.0, -1}; n = 0; }
+  __device__ __forceinline__ void init() { mine = PoolKey{0.0, 0, -1}; n = 0; }
   // key of the cap-th element once the list is full (INFINITY before): a new key
   // with a larger r cannot enter
   __device__ __forceinline__ double thr_r(int cap) const {
@@ -1610,7 +1589,7 @@ struct WarpTopK {
     warp_sort32(P, x);
     mine = warp_merge32(P, mine, x);
     n = n + got < cap ? n + got : cap;
-    if (lane >= cap) mine = PoolKey{0.0, -1};
+    if (lane >= cap) mine = PoolKey{0.0, 0, -1};
   }
   // merge another warp's sorted list (element j in lane j, `m` elements)
   __device__ __forceinline__ void merge_sorted(const EvalParams& P, const PoolKey& x, int m, int cap) {
@@ -1618,7 +1597,7 @@ struct WarpTopK {
     if (!m) return;
     mine = warp_merge32(P, mine, x);
     n = n + m < cap ? n + m : cap;
-    if (lane >= cap) mine = PoolKey{0.0, -1};
+    if (lane >= cap) mine = PoolKey{0.0, 0, -1};
   }
 };
 
@@ -1972,7 +1951,7 @@ __global__ void __launch_bounds__(kPoolThreads) k_pools_partial(EvalParams P, co
       const double r = i < hi ? keys[u0 + i] : INFINITY;  // INFINITY: pool candidate skipped
       const bool cand = r != INFINITY && r <= thr;
       if (!__any_sync(0xffffffffu, cand)) continue;
-      tk.merge_chunk(P, cand ? PoolKey{r, (int32_t)(u0 + i)} : PoolKey{0.0, -1}, cap);
+      tk.merge_chunk(P, cand ? pool_key_of(P, S, r, (int32_t)(u0 + i)) : PoolKey{0.0, 0, -1}, cap);
       thr = tk.thr_r(cap);
     }
     wout[warp][lane] = tk.mine;
@@ -2004,7 +1983,7 @@ __global__ void k_pools_final(EvalParams P, SearchMeta* meta, const PoolPartial*
         for (int b = 0; b < kPoolSplit; ++b) {
           const PoolPartial& pp = part[(int64_t)s * kPoolSplit + b];
           const int m = pp.n[role];
-          t.merge_sorted(P, tid < m ? pp.k[role][tid] : PoolKey{0.0, -1}, m, cap);
+          t.merge_sorted(P, tid < m ? pp.k[role][tid] : PoolKey{0.0, 0, -1}, m, cap);
         }
         got = t.n;
         if (tid < got) pool_sel[(int64_t)s * 128 + role * 64 + tid] = t.mine.unit;
@@ -2026,7 +2005,7 @@ __global__ void k_pools_final(EvalParams P, SearchMeta* meta, const PoolPartial*
         const int32_t u = u0 + i;
         const double r = keys[u];
         if (r == INFINITY) continue;
-        const PoolKey key{r, u};
+        const PoolKey key = pool_key_of(P, S, r, u);
         if (prev.unit >= 0 && !pool_before(P, prev, key)) continue;
         if (pool_before(P, key, best)) best = key;
       }
@@ -2485,7 +2464,7 @@ int lc_open(int device, lc_ctx** out) {
 int lc_close(lc_ctx* c) {
   if (!c) return LC_OK;
   cudaSetDevice(c->device);
-  DBuf* bufs[] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
+  DBuf* bufs[] = {&c->searches, &c->batches, &c->batch_code, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
                   &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->step_in, &c->step_out, &c->step_loads, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch};
@@ -2627,6 +2606,22 @@ int lc_space_upload(lc_ctx* c, const lc_space_desc* d, lc_space** out) {
     if ((rc = upload(&sp->tmpl_cidx_off, off.data(), off.size(), c->stream))) return rc;
     if ((rc = upload(&sp->tmpl_cidx, idx.data(), idx.size(), c->stream))) return rc;
   }
+  {
+    // string-order rank of each combo's (tp, pp, ep, dp) (lc_keys.h): the pool-rank tie break
+    std::vector<uint64_t> code(d->n_combos > 0 ? d->n_combos : 1, 0), rank(code.size(), 0);
+    for (int i = 0; i < d->n_combos; ++i) {
+      const lc_combo& k = d->combos[i];
+      if (k.tp > LC_KEY_FIELD_MAX || k.pp > LC_KEY_FIELD_MAX || k.ep > LC_KEY_FIELD_MAX || k.dp > LC_KEY_FIELD_MAX)
+        return fail(LC_ERR_ARG, "lc_space_upload: tp/pp/ep/dp values above 9999 are not supported");
+      code[i] = lc_combo_code(k.tp, k.pp, k.ep, k.dp);
+    }
+    std::vector<uint64_t> sorted(code.begin(), code.begin() + (d->n_combos > 0 ? d->n_combos : 0));
+    std::sort(sorted.begin(), sorted.end());
+    sorted.erase(std::unique(sorted.begin(), sorted.end()), sorted.end());
+    for (int i = 0; i < d->n_combos; ++i)
+      rank[i] = (uint64_t)(std::lower_bound(sorted.begin(), sorted.end(), code[i]) - sorted.begin()) << 36;
+    if ((rc = upload(&sp->combo_rank, rank.data(), rank.size(), c->stream))) return rc;
+  }
   CK(cudaStreamSynchronize(c->stream));
   *out = sp;
   return LC_OK;
@@ -2640,7 +2635,7 @@ int lc_space_free(lc_space* sp) {
   cudaFree(sp->tmpl_info);
   cudaFree(sp->pair_canon);
   cudaFree(sp->slots); cudaFree(sp->slot_of); cudaFree(sp->class_slots); cudaFree(sp->gclasses); cudaFree(sp->gclass_of);
-  cudaFree(sp->tmpl_cidx_off); cudaFree(sp->tmpl_cidx);
+  cudaFree(sp->tmpl_cidx_off); cudaFree(sp->tmpl_cidx); cudaFree(sp->combo_rank);
   delete sp;
   return LC_OK;
 }
@@ -2711,6 +2706,8 @@ static EvalParams make_params(lc_ctx* c) {
   P.results = (lc_search_result*)c->results.p;
   P.acc = (SearchAcc*)c->acc.p;
   P.fbuckets = (unsigned long long*)c->buckets.p;
+  P.combo_rank = c->sp ? c->sp->combo_rank : nullptr;
+  P.batch_code = (const uint64_t*)c->batch_code.p;
 #ifndef LC_NO_FUSE_EXPAND
   P.pair_off = c->enum_fit ? (const int32_t*)c->block_sums.p : nullptr;
 #else
@@ -3221,6 +3218,12 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   cudaError_t err = cudaSuccess;
   lc_search_desc* dS = c->searches.get<lc_search_desc>(n_search, &err);
   int64_t* dB = c->batches.get<int64_t>(n_batches, &err);
+  uint64_t* dBC = c->batch_code.get<uint64_t>(n_batches, &err);
+  c->hbatch_code.resize(n_batches > 0 ? n_batches : 1);
+  for (int32_t i = 0; i < n_batches; ++i) {
+    if (batches[i] > LC_KEY_BATCH_MAX) return fail(LC_ERR_ARG, "batch sizes above 9999999999 are not supported");
+    c->hbatch_code[i] = lc_batch_code(batches[i] > 0 ? batches[i] : 1);
+  }
   double* dL = c->loads.get<double>((size_t)n_loads * 2 * (sp->n_experts > 0 ? sp->n_experts : 1), &err);
   SearchMeta* dM = c->meta.get<SearchMeta>(n_search, &err);
   TailTable* dT = c->tail_tables.get<TailTable>(c->htables.size(), &err);
@@ -3235,17 +3238,17 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(err));
   // inputs go through one page-locked arena so every H2D copy is asynchronous
   {
-    const size_t sizes[10] = {sizeof(lc_search_desc) * n_search, sizeof(int64_t) * n_batches,
+    const size_t sizes[11] = {sizeof(lc_search_desc) * n_search, sizeof(int64_t) * n_batches,
                              (n_loads && sp->n_experts) ? sizeof(double) * n_loads * 2 * sp->n_experts : 0,
                              sizeof(SearchMeta) * n_search, sizeof(TailTable) * c->htables.size(),
                              sizeof(DsGroup) * c->hds.size(), sizeof(QtGroup) * c->hqt.size(),
                              sizeof(SeriesGroup) * c->hsg.size(), sizeof(SeriesMember) * c->hsm.size(),
-                             sizeof(PGroup) * c->hpg.size()};
-    const void* srcs[10] = {searches, batches, loads, c->hmeta.data(), c->htables.data(), c->hds.data(),
-                            c->hqt.data(), c->hsg.data(), c->hsm.data(), c->hpg.data()};
-    void* dsts[10] = {dS, dB, dL, dM, dT, dG, dQ, dSG, dSM, dPG};
+                             sizeof(PGroup) * c->hpg.size(), sizeof(uint64_t) * n_batches};
+    const void* srcs[11] = {searches, batches, loads, c->hmeta.data(), c->htables.data(), c->hds.data(),
+                            c->hqt.data(), c->hsg.data(), c->hsm.data(), c->hpg.data(), c->hbatch_code.data()};
+    void* dsts[11] = {dS, dB, dL, dM, dT, dG, dQ, dSG, dSM, dPG, dBC};
     size_t need = 0;
-    for (int k = 0; k < 10; ++k) need += (sizes[k] + 255) & ~(size_t)255;
+    for (int k = 0; k < 11; ++k) need += (sizes[k] + 255) & ~(size_t)255;
     need += (sizeof(lc_search_result) + sizeof(SearchMeta)) * (size_t)n_search + 1024;  // summaries coming back
     if (c->arena_cap < need) {
       if (c->arena) cudaFreeHost(c->arena);
@@ -3255,7 +3258,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
       c->arena_cap = need;
     }
     size_t off = 0;
-    for (int k = 0; k < 10; ++k) {
+    for (int k = 0; k < 11; ++k) {
       if (!sizes[k]) continue;
       memcpy(c->arena + off, srcs[k], sizes[k]);
       CK(cudaMemcpyAsync(dsts[k], c->arena + off, sizes[k], cudaMemcpyHostToDevice, c->stream));

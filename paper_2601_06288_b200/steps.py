@@ -98,24 +98,23 @@ def step_latency_batch(db, model, requests: Sequence[StepRequest], device: int =
         return out
     eng = get_engine(device)
     with eng._lock:
-        # one plan per distinct (tp, pp, ep): the template index of each request
-        plans: dict = {}
+        # one space plan holding a template for every requested (tp, pp, ep): the
+        # cross product of the requested values (each request's own config is
+        # consistent, so its combo and template are in it); one launch
+        cfgs = [requests[i].cfg for i in live]
+        space = CandidateSpace(tp_values=tuple(sorted({c.tp for c in cfgs})),
+                               pp_values=tuple(sorted({c.pp for c in cfgs})),
+                               ep_values=tuple(sorted({c.ep for c in cfgs})),
+                               dp_values=tuple(sorted({c.dp for c in cfgs})))
+        sph, plan, flat = eng.space_handle(db, model, space)
+        tmpl_of = {(int(c["tp"]), int(c["pp"]), int(c["ep"])): int(c["tmpl"]) for c in plan.combos}
         reqs = np.zeros(len(live), dtype=N.STEP_REQ_DTYPE)
         loads: list[np.ndarray] = []
         load_ix: dict = {}
-        handles = []
         for j, i in enumerate(live):
             r = requests[i]
             cfg = r.cfg
-            key = (cfg.tp, cfg.pp, cfg.ep)
-            if key not in plans:
-                space = CandidateSpace(tp_values=(cfg.tp,), pp_values=(cfg.pp,), ep_values=(cfg.ep,),
-                                       dp_values=(cfg.dp,))
-                sph, plan, flat = eng.space_handle(db, model, space)
-                plans[key] = (sph, plan, flat)
-            sph, plan, flat = plans[key]
-            handles.append(plans[key])
-            reqs[j]["tmpl"] = int(plan.combos[0]["tmpl"])
+            reqs[j]["tmpl"] = tmpl_of[(cfg.tp, cfg.pp, cfg.ep)]
             reqs[j]["phase"] = PHASES.index(r.phase)
             reqs[j]["n_ctx"], reqs[j]["n_gen"], reqs[j]["seq"] = r.n_ctx_tokens, r.n_gen_tokens, r.seq_len
             reqs[j]["batch"] = cfg.batch
@@ -131,19 +130,10 @@ def step_latency_batch(db, model, requests: Sequence[StepRequest], device: int =
         dbh, flat = eng.db_handle(db)
         res = np.zeros(len(live), dtype=N.STEP_OUT_DTYPE)
         l_arr = np.concatenate(loads) if loads else np.zeros(1)
-        # requests of different templates share one launch only when they share a plan handle
-        by_plan: dict = {}
-        for j, h in enumerate(handles):
-            by_plan.setdefault(id(h[0]), (h, []))[1].append(j)
-        for (sph, plan, _), idx in by_plan.values():
-            sub = np.ascontiguousarray(reqs[idx])
-            sub_out = np.zeros(len(idx), dtype=N.STEP_OUT_DTYPE)
-            eng._call(eng.lib.lc_step_latency, "lc_step_latency", eng.ctx, dbh, sph, len(idx), N.vptr(sub),
-                      len(loads), N.ptr(l_arr, C.c_double), N.vptr(sub_out))
-            res[idx] = sub_out
+        eng._call(eng.lib.lc_step_latency, "lc_step_latency", eng.ctx, dbh, sph, len(live), N.vptr(reqs),
+                  len(loads), N.ptr(l_arr, C.c_double), N.vptr(res))
     for j, i in enumerate(live):
         o = res[j]
-        plan = handles[j][1]
         if o["status"]:
             cfg = requests[i].cfg
             msg = _reason(int(o["status"]), int(o["c0"]), int(o["c1"]), plan, {"tmpl": int(reqs[j]["tmpl"])}, flat,

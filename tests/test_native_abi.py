@@ -97,3 +97,30 @@ def test_ctypes_and_numpy_layouts_match_the_c_compiler(tmp_path):
     }
     for k, v in fields.items():
         assert c[k] == v, (k, c[k], v)
+
+
+def test_config_key_integer_codes_sort_like_python_strings(tmp_path):
+    """csrc/lc_keys.h: (combo code, batch code) order == ParallelConfig.key() string order
+    (the pool-rank tie break, search.py:276-277), on random configs with many shared prefixes."""
+    import random
+    import subprocess
+
+    exe = tmp_path / "key_order"
+    src = Path(__file__).resolve().parent / "native" / "key_order.c"
+    subprocess.run(["gcc", "-O1", "-o", str(exe), str(src)], check=True)
+    rng = random.Random(7)
+    pool = [1, 2, 3, 4, 5, 8, 9, 10, 11, 12, 16, 19, 20, 32, 64, 99, 100, 101, 128, 256, 512, 999, 1000, 1024, 4096,
+            9999]
+    bpool = pool + [10000, 65536, 99999, 123456, 1000000, 9999999999]
+    cfgs = [tuple(rng.choice(pool) for _ in range(4)) + (rng.choice(bpool),) for _ in range(20000)]
+    cfgs += [(1, 1, 1, 1, b) for b in (1, 10, 100, 2, 20, 9, 99)] + [(t, 1, 1, 1, 8) for t in (1, 10, 16, 2, 100)]
+    text = "\n".join(" ".join(map(str, c)) for c in cfgs) + "\n"
+    out = subprocess.run([str(exe)], input=text, capture_output=True, text=True, check=True).stdout.split("\n")
+    codes = [tuple(int(x) for x in line.split()) for line in out if line]
+    assert len(codes) == len(cfgs)
+    key = [f"tp{a}pp{b}ep{c}dp{d}b{e}" for a, b, c, d, e in cfgs]
+    by_str = sorted(range(len(cfgs)), key=lambda i: (key[i], i))
+    by_code = sorted(range(len(cfgs)), key=lambda i: (codes[i], i))
+    assert [key[i] for i in by_str] == [key[i] for i in by_code]
+    # equal strings <=> equal codes
+    assert len(set(key)) == len(set(codes))
