@@ -9,6 +9,7 @@
 //   K5b k_disagg                           : x*y replica sweep per pairing + plan sort (serving_modes.py:449-494)
 //   K4  k_front                            : SLA, Pareto front, best, nearest miss (search.py:129-208)
 // Build with --fmad=false: bit-exact parity with CPython needs unfused arithmetic.
+#include <cuda_pipeline.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -960,7 +961,12 @@ __device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta&
 #ifndef LC_DSERIES_MIN_BLOCKS
 #define LC_DSERIES_MIN_BLOCKS 6  // 80 registers (measured slightly better than 64 / 8 blocks)
 #endif
+#ifndef LC_DS_RING
+#define LC_DS_RING 8
+#endif
+constexpr int kDsRing = LC_DS_RING;  // decode-series samples in flight per thread
 __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalParams P) {
+  __shared__ QVal ds_ring[kDsRing * 128];  // [slot][thread], 16 KB
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < P.n_series;
        x += (int64_t)gridDim.x * blockDim.x) {
     int lo = 0, hi = P.n_sgroups - 1;
@@ -1035,25 +1041,37 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
 #pragma unroll
       for (int i = 0; i < kPostRegs; ++i) post[i] = i < npost ? term[gi + 1 + i] : 0.0;
       double t_gen = 0.0;
-#ifndef LC_DECODE_CHAINS
-#define LC_DECODE_CHAINS 2
-#endif
-      for (int step = 0; step < K && !e.code; step += LC_DECODE_CHAINS) {
-        double g[LC_DECODE_CHAINS];
+      // The attention latencies of samples 1..K-1 stream from the decode-series
+      // table through a per-thread ring in shared memory, kDsRing samples ahead
+      // (cp.async: LDGSTS), so the L2 latency of sample sj + kDsRing overlaps the
+      // Neumaier chains of sample sj instead of stalling each iteration.
+      QVal* ring = ds_ring + threadIdx.x;  // slot k at ring[k * 128]
+      auto issue = [&](int k) {
+        if (k > 0 && k < K) __pipeline_memcpy_async(ring + (k % kDsRing) * 128, ds + (int64_t)k * S.n_b, sizeof(QVal));
+        __pipeline_commit();
+      };
+#pragma unroll
+      for (int k = 0; k < kDsRing; ++k) issue(k);
+      for (int step = 0; step < K && !e.code; step += 2) {
+        // groups of samples <= step + 1 are complete once at most kDsRing - 2 are pending
+        __pipeline_wait_prior(kDsRing - 2);
+        double g[2];
         int bad = -1;
 #pragma unroll
-        for (int j = 0; j < LC_DECODE_CHAINS; ++j) {
+        for (int j = 0; j < 2; ++j) {
           const int sj = step + j;
           g[j] = 0.0;
           if (sj >= K || bad >= 0) continue;
           if (sj == 0) { g[j] = term[gi]; continue; }
-          const QVal q = ds[(int64_t)sj * S.n_b];
+          const QVal q = ring[(sj % kDsRing) * 128];
           if (q.status) { bad = j; e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + stride * sj + 1; continue; }
           g[j] = 0.0 + (q.lat * g_rep / 1000.0) * bubble;
         }
-        NeumaierSum sc[LC_DECODE_CHAINS];
+        issue(step + kDsRing);
+        issue(step + kDsRing + 1);
+        NeumaierSum sc[2];
 #pragma unroll
-        for (int j = 0; j < LC_DECODE_CHAINS; ++j) {
+        for (int j = 0; j < 2; ++j) {
           sc[j] = pre;
           sc[j].add(g[j]);
         }
@@ -1062,17 +1080,17 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
           for (int i = 0; i < kPostRegs; ++i) {
             if (i >= npost) break;
 #pragma unroll
-            for (int j = 0; j < LC_DECODE_CHAINS; ++j) sc[j].add(post[i]);
+            for (int j = 0; j < 2; ++j) sc[j].add(post[i]);
           }
         } else {
           for (int i = gi + 1; i < m; ++i) {
             const double xv = term[i];
 #pragma unroll
-            for (int j = 0; j < LC_DECODE_CHAINS; ++j) sc[j].add(xv);
+            for (int j = 0; j < 2; ++j) sc[j].add(xv);
           }
         }
 #pragma unroll
-        for (int j = 0; j < LC_DECODE_CHAINS; ++j) {
+        for (int j = 0; j < 2; ++j) {
           const int sj = step + j;
           if (sj >= K || (bad >= 0 && j >= bad)) continue;
           const double st = sc[j].result();
@@ -1085,6 +1103,7 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
           t_gen += st * (double)stride;
         }
       }
+      __pipeline_wait_prior(0);  // the ring is reused by this thread's next series
     }
     // members not reached: the first failing query decides
     for (; mi < G.n_m; ++mi) put(mi, 0.0, e.code | (e.label << 8), 0, e.c0, e.c1);
@@ -1436,7 +1455,6 @@ __global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalPara
 #define LC_EXPAND_MIN_BLOCKS 4  // 64 registers (measured: 4.11 -> 4.00 ms per step)
 #endif
 __global__ void __launch_bounds__(256, LC_EXPAND_MIN_BLOCKS) k_expand(EvalParams P) {
-  const int64_t n = P.n_cap;
   const int64_t total = *P.d_total;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1998,9 +2016,9 @@ __global__ void k_pools_final(EvalParams P, SearchMeta* meta, const PoolPartial*
     // large caps (33..64): rounds over all units (rare)
     const int32_t u0 = meta[s].unit_off, nu = meta[s].n_units;
     const double* keys = P.pool_key + (int64_t)role * P.n_cap;
-    PoolKey prev{0.0, -1};
+    PoolKey prev{0.0, 0, -1};
     for (int k = 0; k < cap && k < 64; ++k) {
-      PoolKey best{0.0, -1};
+      PoolKey best{0.0, 0, -1};
       for (int i = tid; i < nu; i += blockDim.x) {
         const int32_t u = u0 + i;
         const double r = keys[u];

@@ -125,3 +125,27 @@ def test_handle_caches_are_bounded_and_keyed_on_plan_fields():
         assert got == ref
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("caps", [(24, 10), (32, 8), (40, 6), (64, 4), (4, 64), (17, 15)])
+@pytest.mark.parametrize("name", ["a1_qwen_small", "cfg4_dsv3", "flat_ties"])
+def test_large_pool_caps_match_oracle(name, caps):
+    """Pool caps above 16 (the warp top-k fast path holds up to 32, larger caps take the
+    per-search rounds): sorted(pool, key=_pool_rank)[:cap] (search.py:336-339) vs the oracle."""
+    import dataclasses
+
+    import paper_2601_06288_b200 as pkg
+    from golden_io import canonical, db_path, diff_canonical, hw_docs, model_doc
+    from oracle import oracle
+
+    case = BY_NAME[name]
+    db, model, workload, space, dc = case_objects(case)
+    space = dataclasses.replace(space, prefill_pool_cap=caps[0], decode_pool_cap=caps[1])
+    got = pkg.run_search(db, model, workload, space, disagg_constants=dc).to_doc()
+    header, recs = oracle.read_db_records(db_path(case))
+    header, recs = oracle.mutate(header, recs, case.get("mutation"), hw_docs())
+    sp = dict(case.get("space", {}), prefill_pool_cap=caps[0], decode_pool_cap=caps[1])
+    ref = oracle.run_search(header, recs, model_doc(case["model"]), case["workload"], sp, disagg=case.get("disagg"),
+                            extrapolation=case.get("extrapolation", "default"))
+    diffs = diff_canonical(canonical(got), canonical(ref))
+    assert not diffs, "\n".join(diffs)
