@@ -279,6 +279,12 @@ struct lc_ctx {
 };
 
 // ============================================================================ device kernels
+// rel / d and rel % d for an offset inside one search / table group: every such
+// offset is below 2^31 (lc_search_batch bounds the batch), so 32-bit unsigned
+// arithmetic replaces the 64-bit software division.
+__device__ __forceinline__ int div32(int64_t rel, int64_t d) { return (int)((uint32_t)rel / (uint32_t)d); }
+__device__ __forceinline__ int mod32(int64_t rel, int64_t d) { return (int)((uint32_t)rel % (uint32_t)d); }
+
 namespace {
 
 constexpr int kScanBlock = 1024;
@@ -362,7 +368,7 @@ __global__ void k_enum_flags(EvalParams P, int64_t n_raw, uint8_t* flags) {
     const int s = find_search(P.meta, P.n_search, r);
     const lc_search_desc& S = P.searches[s];
     const int64_t rel = r - P.meta[s].raw_off;
-    const int ci = (int)(rel / S.n_b), bi = (int)(rel % S.n_b);
+    const int ci = div32(rel, S.n_b), bi = mod32(rel, S.n_b);
     const lc_combo c = P.combos[ci];
     const int64_t b = P.batches[S.b_off + bi];
     uint8_t f = 0;
@@ -454,8 +460,8 @@ __global__ void k_scatter(EvalParams P, const uint8_t* flags, int64_t n, const i
       const lc_search_desc& S = P.searches[s];
       const int64_t rel = i - P.meta[s].raw_off;
       u_search[p] = s;
-      u_combo[p] = (int32_t)(rel / S.n_b);
-      u_batch[p] = (int32_t)(rel % S.n_b);
+      u_combo[p] = div32(rel, S.n_b);
+      u_batch[p] = mod32(rel, S.n_b);
       u_budget[p] = (f >> 1) & 1;
     }
   }
@@ -592,8 +598,8 @@ __global__ void __launch_bounds__(256, LC_TAIL_MIN_BLOCKS) k_tails(EvalParams P,
         }
         const TailTable T = P.tail_tables[lo];
         const int64_t rel = t - T.off;
-        const int bi = (int)(rel % T.n_b);
-        const int pair = (int)(rel / T.n_b);
+        const int bi = mod32(rel, T.n_b);
+        const int pair = div32(rel, T.n_b);
         if (pair < npair) {
           const int64_t tp = P.tp_vals[pair / P.n_ep];
           ep = P.ep_vals[pair % P.n_ep];
@@ -855,7 +861,7 @@ __global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_qtabl
     const lc_search_desc& S = P.searches[s];
     const SearchMeta& M = P.meta[s];
     const int64_t rel = x - Gq.off;
-    const int j = (int)(rel / S.n_b), bi = (int)(rel % S.n_b);
+    const int j = div32(rel, S.n_b), bi = mod32(rel, S.n_b);
     const lc_slot SL = P.slots[P.class_slots[P.class_off[Gq.cls] + j]];
     QVal out{0.0, LC_ST_NOT_EVALUATED, 0};
     const int64_t b = P.batches[S.b_off + bi];
@@ -902,10 +908,10 @@ __global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_dstab
     // layout [gclass][sample][batch]: the batch index is fastest, so the threads
     // of a warp in k_dseries (consecutive batches) read consecutive entries
     int64_t rel = x - G.off;
-    const int bi = (int)(rel % G.n_b);
-    rel /= G.n_b;
-    const int k = (int)(rel % G.n_steps);
-    const int g = (int)(rel / G.n_steps);
+    const int bi = mod32(rel, G.n_b);
+    rel = div32(rel, G.n_b);
+    const int k = mod32(rel, G.n_steps);
+    const int g = div32(rel, G.n_steps);
     const lc_entry e = P.gclasses[g];
     int st = 0, nlog = 0;
     QVal out;
@@ -964,6 +970,10 @@ __device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta&
 #ifndef LC_DS_RING
 #define LC_DS_RING 8
 #endif
+#ifndef LC_DECODE_CHAINS
+#define LC_DECODE_CHAINS 2  // interleaved Neumaier chains (decode samples) per thread
+#endif
+constexpr int kChains = LC_DECODE_CHAINS;
 constexpr int kDsRing = LC_DS_RING;  // decode-series samples in flight per thread
 __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalParams P) {
   __shared__ QVal ds_ring[kDsRing * 128];  // [slot][thread], 16 KB
@@ -979,7 +989,7 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
     const lc_search_desc& S = P.searches[G.rep];
     const SearchMeta& M = P.meta[G.rep];
     const int64_t rel = x - G.off;
-    const int tmpl = (int)(rel / S.n_b), bi = (int)(rel % S.n_b);
+    const int tmpl = div32(rel, S.n_b), bi = mod32(rel, S.n_b);
     const SeriesMember* mem = P.smembers + G.m_off;
     // samples needed: the longest member whose cell is evaluated
     int K = 0;
@@ -1052,13 +1062,13 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
       };
 #pragma unroll
       for (int k = 0; k < kDsRing; ++k) issue(k);
-      for (int step = 0; step < K && !e.code; step += 2) {
-        // groups of samples <= step + 1 are complete once at most kDsRing - 2 are pending
-        __pipeline_wait_prior(kDsRing - 2);
-        double g[2];
+      for (int step = 0; step < K && !e.code; step += kChains) {
+        // groups of samples < step + kChains are complete once at most kDsRing - kChains are pending
+        __pipeline_wait_prior(kDsRing - kChains);
+        double g[kChains];
         int bad = -1;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < kChains; ++j) {
           const int sj = step + j;
           g[j] = 0.0;
           if (sj >= K || bad >= 0) continue;
@@ -1067,11 +1077,11 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
           if (q.status) { bad = j; e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + stride * sj + 1; continue; }
           g[j] = 0.0 + (q.lat * g_rep / 1000.0) * bubble;
         }
-        issue(step + kDsRing);
-        issue(step + kDsRing + 1);
-        NeumaierSum sc[2];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < kChains; ++j) issue(step + kDsRing + j);
+        NeumaierSum sc[kChains];
+#pragma unroll
+        for (int j = 0; j < kChains; ++j) {
           sc[j] = pre;
           sc[j].add(g[j]);
         }
@@ -1080,17 +1090,17 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
           for (int i = 0; i < kPostRegs; ++i) {
             if (i >= npost) break;
 #pragma unroll
-            for (int j = 0; j < 2; ++j) sc[j].add(post[i]);
+            for (int j = 0; j < kChains; ++j) sc[j].add(post[i]);
           }
         } else {
           for (int i = gi + 1; i < m; ++i) {
             const double xv = term[i];
 #pragma unroll
-            for (int j = 0; j < 2; ++j) sc[j].add(xv);
+            for (int j = 0; j < kChains; ++j) sc[j].add(xv);
           }
         }
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < kChains; ++j) {
           const int sj = step + j;
           if (sj >= K || (bad >= 0 && j >= bad)) continue;
           const double st = sc[j].result();
@@ -1125,7 +1135,7 @@ __global__ void __launch_bounds__(128) k_ptables(EvalParams P) {
     const lc_search_desc& S = P.searches[G.rep];
     const SearchMeta& M = P.meta[G.rep];
     const int64_t rel = x - G.off;
-    const int tmpl = (int)(rel / G.n_b), bi = (int)(rel % G.n_b);
+    const int tmpl = div32(rel, G.n_b), bi = mod32(rel, G.n_b);
     const TmplInfo ti = P.tmpl_info[tmpl];
     lc_combo c;
     c.tp = ti.tp; c.pp = ti.pp; c.ep = ti.ep; c.tp_i = ti.tp_i; c.ep_i = ti.ep_i;
@@ -1281,12 +1291,12 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
 // One cell: every step from the tables (K2).  With the closed-form K0
 // (P.pair_off) the cell also writes the rows of its dp-variant candidates
 // (expand_unit) -- the cell stays in registers instead of a k_expand re-read.
-__device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, uint32_t cf, RowAcc& ra, int& s_out) {
-  const int s = find_cell_search(P.meta, P.n_search, ci);
+__device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, int s, uint32_t cf, RowAcc& ra,
+                                          int& s_out) {
   const lc_search_desc& S = P.searches[s];
   const SearchMeta& M = P.meta[s];
   const int64_t rel = ci - M.cell_off;
-  const int tmpl = (int)(rel / S.n_b), bi = (int)(rel % S.n_b);
+  const int tmpl = div32(rel, S.n_b), bi = mod32(rel, S.n_b);
   const TmplInfo ti = P.tmpl_info[tmpl];
   lc_combo c;  // the fields expert_tokens() reads
   c.tp = ti.tp; c.pp = ti.pp; c.ep = ti.ep; c.tp_i = ti.tp_i; c.ep_i = ti.ep_i;
@@ -1414,14 +1424,22 @@ __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, uint3
 
 __global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalParams P) {
   const int64_t ncell = P.n_cells_total;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int lane = threadIdx.x & 31;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; base < ncell; base += stride) {
+  // each block walks one contiguous range of cells, so a thread's search index only
+  // moves forward (one compare per cell instead of a binary search over the searches)
+  const int64_t per = ((ncell + gridDim.x - 1) / gridDim.x + 127) / 128 * 128;
+  const int64_t beg = (int64_t)blockIdx.x * per, end = beg + per < ncell ? beg + per : ncell;
+  int hint = -1;
+  for (int64_t base = beg + threadIdx.x - lane; base < end; base += blockDim.x) {
     const int64_t ci = base + lane;
     RowAcc ra{0, 0, 0, 0, 0, 0, 0ull, 0ull};
     int s = -1;
-    const uint32_t cf = ci < ncell ? P.cell_flags[ci] : 0u;
-    if (cf) eval_cell(P, ci, cf, ra, s);
+    const uint32_t cf = ci < end ? P.cell_flags[ci] : 0u;
+    if (cf) {
+      if (hint < 0) hint = find_cell_search(P.meta, P.n_search, ci);
+      while (hint + 1 < P.n_search && P.meta[hint + 1].cell_off <= ci) ++hint;
+      eval_cell(P, ci, hint, cf, ra, s);
+    }
     if (!P.pair_off) continue;  // uniform: k_expand does the accounting
     // warp-aggregated accounting (cells are ordered by search)
     int s0 = -1;
