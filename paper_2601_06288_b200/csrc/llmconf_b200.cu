@@ -50,6 +50,11 @@ int fail(int code, const std::string& msg) {
 // largest database image staged into shared memory; larger ones are read from global memory
 constexpr size_t kDbStageMax = 200 * 1024;
 
+// While a pipeline is being captured into a CUDA graph no allocation may happen:
+// a buffer that would have to grow marks the capture as unusable instead, and the
+// caller runs the pipeline directly (which allocates) -- see launch_pipeline.
+static thread_local bool tl_capturing = false, tl_capture_grow = false;
+
 struct DBuf {
   void* p = nullptr;
   size_t cap = 0;
@@ -57,6 +62,10 @@ struct DBuf {
   T* get(size_t n, cudaError_t* err) {
     size_t bytes = n * sizeof(T);
     if (bytes == 0) bytes = 16;
+    if (bytes > cap && tl_capturing) {
+      tl_capture_grow = true;
+      return (T*)p;
+    }
     if (bytes > cap) {
       if (p) cudaFree(p);
       p = nullptr;
@@ -231,6 +240,9 @@ struct lc_ctx {
   int device;
   cudaStream_t stream;
   cudaEvent_t ev[8];
+  cudaGraphExec_t gexec = nullptr;  // the last K0..K4 pipeline as an instantiated CUDA graph
+  bool graph_ok = false;            // gexec holds the pipeline of the current batch
+  bool capturing = false;
   DBuf searches, batches, batch_code, loads, meta, results;
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
@@ -2506,6 +2518,7 @@ int lc_close(lc_ctx* c) {
                   &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->step_in, &c->step_out, &c->step_loads, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->pinned_front) cudaFreeHost(c->pinned_front);
   if (c->pinned_plans_i) cudaFreeHost(c->pinned_plans_i);
   if (c->pinned_plans_d) cudaFreeHost(c->pinned_plans_d);
@@ -2763,6 +2776,11 @@ static int sm_count(int dev) {
   return n;
 }
 
+// stage boundary events: inside a graph capture they become event-record nodes
+static cudaError_t record_ev(lc_ctx* c, int k) {
+  return cudaEventRecordWithFlags(c->ev[k], c->stream, c->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+}
+
 // Everything after the unit list is known: K3, K2, K5a, K5b, K4.
 static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   cudaError_t err = cudaSuccess;
@@ -2800,7 +2818,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   }
   EvalParams P = make_params(c);
   const int sms = sm_count(c->device);
-  CK(cudaEventRecord(c->ev[1], c->stream));
+  CK(record_ev(c, 1));
   if (c->n_tails > c->n_pd_tails) {
     P.m_used = (uint8_t*)c->m_used.p;
     CK(cudaMemsetAsync(c->m_used.p, 0, n_mark_bytes, c->stream));
@@ -2824,7 +2842,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     else k_tails<32><<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
     CK(cudaGetLastError());
   }
-  CK(cudaEventRecord(c->ev[2], c->stream));
+  CK(record_ev(c, 2));
   {
     EvalParams P2 = make_params(c);  // table pointers are valid only after the allocations above
     P = P2;
@@ -2877,7 +2895,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     }
     CK(cudaGetLastError());
   }
-  CK(cudaEventRecord(c->ev[3], c->stream));
+  CK(record_ev(c, 3));
   {
     PoolPartial* pp = c->pool_part.get<PoolPartial>((size_t)c->n_search * kPoolSplit, &err);
     if (err != cudaSuccess) return fail(LC_ERR_CUDA, "pool partial allocation");
@@ -2887,7 +2905,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     k_pools_final<<<c->n_search, kPoolThreads, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, pp, (int32_t*)c->pool_sel.p);
     CK(cudaGetLastError());
   }
-  CK(cudaEventRecord(c->ev[4], c->stream));
+  CK(record_ev(c, 4));
   ++c->launches;
   {
     PlanRec* scr = c->plan_scratch.get<PlanRec>((size_t)c->n_search * 256, &err);
@@ -2900,7 +2918,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
                                                  (lc_search_result*)c->results.p);
   }
   CK(cudaGetLastError());
-  CK(cudaEventRecord(c->ev[5], c->stream));
+  CK(record_ev(c, 5));
   {
     FrontMeta* fm = c->front_meta.get<FrontMeta>(c->n_search, &err);
     unsigned long long* bk = c->buckets.get<unsigned long long>((size_t)c->n_search * kSpeedBuckets, &err);
@@ -2928,7 +2946,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
                                                                       (int64_t*)c->front.p, fc);
     CK(cudaGetLastError());
   }
-  CK(cudaEventRecord(c->ev[6], c->stream));
+  CK(record_ev(c, 6));
   (void)totals;
   return LC_OK;
 }
@@ -3024,6 +3042,68 @@ static int run_enum(lc_ctx* c) {
   k_unit_offsets<<<(c->n_search + 127) / 128, 128, 0, c->stream>>>((SearchMeta*)c->meta.p, c->n_search, pos, n_raw,
                                                                    bs + nblk);
   CK(cudaGetLastError());
+  return LC_OK;
+}
+
+// K0 .. K4 of the current batch.  The launch sequence (~25 kernels and memsets)
+// is captured into a CUDA graph and launched as one unit: the GPU then runs the
+// dependent kernels back to back without per-launch gaps.  A previous graph is
+// updated in place (cudaGraphExecUpdate) when only parameters changed.  A
+// capture that would have to grow a workspace buffer is discarded and the
+// pipeline runs directly once (allocating); LC_NO_GRAPH=1 always runs directly.
+static int run_direct(lc_ctx* c, lc_batch_totals* totals) {
+  CK(cudaEventRecord(c->ev[0], c->stream));
+  c->launches = 0;
+  int rc = run_enum(c);
+  if (rc) return rc;
+  c->n_front_slots = 2 * c->n_cap + c->n_plan_slots;
+  return run_eval_pipeline(c, totals);
+}
+
+static int launch_pipeline(lc_ctx* c, lc_batch_totals* totals) {
+  static const bool no_graph = getenv("LC_NO_GRAPH") != nullptr;
+  c->graph_ok = false;
+  if (no_graph) return run_direct(c, totals);
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  tl_capturing = true;
+  tl_capture_grow = false;
+  c->capturing = true;
+  c->launches = 0;
+  int rc = (int)record_ev(c, 0) == (int)cudaSuccess ? LC_OK : LC_ERR_CUDA;
+  if (!rc) rc = run_enum(c);
+  if (!rc) {
+    c->n_front_slots = 2 * c->n_cap + c->n_plan_slots;
+    rc = run_eval_pipeline(c, totals);
+  }
+  tl_capturing = false;
+  c->capturing = false;
+  const cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+  if (rc || e != cudaSuccess || tl_capture_grow || !g) {
+    if (g) cudaGraphDestroy(g);
+    (void)cudaGetLastError();
+    if (rc && !tl_capture_grow) return rc;
+    return run_direct(c, totals);  // allocates the workspace; the next batch of this shape is captured
+  }
+  if (c->gexec) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(c->gexec, g, &info) != cudaSuccess) {
+      (void)cudaGetLastError();
+      cudaGraphExecDestroy(c->gexec);
+      c->gexec = nullptr;
+    }
+  }
+  if (!c->gexec) {
+    const cudaError_t ie = cudaGraphInstantiate(&c->gexec, g, 0);
+    if (ie != cudaSuccess) {
+      cudaGraphDestroy(g);
+      c->gexec = nullptr;
+      return fail(LC_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie));
+    }
+  }
+  cudaGraphDestroy(g);
+  CK(cudaGraphLaunch(c->gexec, c->stream));
+  c->graph_ok = true;
   return LC_OK;
 }
 
@@ -3302,12 +3382,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     }
     c->arena_used = off;
   }
-  CK(cudaEventRecord(c->ev[0], c->stream));
-  c->launches = 0;
-  int rc = run_enum(c);
-  if (rc) return rc;
-  c->n_front_slots = 2 * c->n_cap + c->n_plan_slots;
-  rc = run_eval_pipeline(c, totals);
+  int rc = launch_pipeline(c, totals);
   if (rc) return rc;
   // compact fronts and plan slots ride the same synchronisation as the summaries
   // (page-locked staging; lc_fetch then serves them from host memory)
@@ -3429,11 +3504,11 @@ int lc_replay_async(lc_ctx* c) {
   if (!c || !c->db) return fail(LC_ERR_STATE, "lc_replay_async: no previous batch");
   CK(cudaSetDevice(c->device));
   if (c->n_search == 0) return LC_OK;
-  CK(cudaEventRecord(c->ev[0], c->stream));
-  c->launches = 0;
-  int rc = run_enum(c);
-  if (rc) return rc;
-  return run_eval_pipeline(c, nullptr);
+  if (c->graph_ok) {  // inputs and workspace are unchanged: relaunch the batch's graph
+    CK(cudaGraphLaunch(c->gexec, c->stream));
+    return LC_OK;
+  }
+  return launch_pipeline(c, nullptr);
 }
 
 static DbView db_view(const lc_db* db) {
@@ -3568,6 +3643,7 @@ int lc_dbgen(lc_ctx* c, const lc_dbgen_desc* g, double* latency_us, double* late
 
 int lc_set_raw_filter(lc_ctx* c, int64_t lo, int64_t hi, const uint8_t* mask) {
   if (!c) return fail(LC_ERR_ARG, "lc_set_raw_filter: NULL context");
+  c->graph_ok = false;  // the next pipeline run enumerates under the new filter
   if (hi < 0) {
     c->filt_lo = 0; c->filt_hi = -1; c->filt_mask = false;
     return LC_OK;

@@ -7,7 +7,7 @@ them the CPU oracle (C restatement, one thread) on this box and the pure-Python
 reference's wall time recorded when the golden report was made
 (tests/golden/reports/*: _meta.reference_wall_s, survey container CPU).
 
-    python tools/configs_timing.py > profiles/r1_configs1to4.json
+    python tools/configs_timing.py > profiles/r2_configs1to4.json
 """
 
 import json
@@ -62,7 +62,25 @@ for name in NAMES:
     t_orc = med(lambda: oracle.run_search(header, recs, model_doc(case["model"]), case["workload"], case.get("space"),
                                           case.get("disagg"), case.get("extrapolation", "default")), reps=3)
     g = golden_report(name)
+    # device time of the K0..K4 pipeline alone: direct launches (lc_replay_last, CUDA events per stage)
+    # and the batch's CUDA graph relaunched (lc_replay_async between events on the engine stream)
+    import torch
+
+    with eng._lock:
+        o = eng.run_batch(db, model, space, [workload], dc)
+        t_direct = statistics.median(float(sum(eng.replay(1).kernel_ms)) for _ in range(REPS))
+        st = torch.cuda.ExternalStream(eng.stream_ptr())
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(3):
+            eng.replay_async()
+        a.record(st)
+        for _ in range(REPS):
+            eng.replay_async()
+        b.record(st)
+        b.synchronize()
+        t_graph = a.elapsed_time(b) / REPS
     out.append({"config": name, "candidates": int(o.results[0]["n_enumerated"]), "rows": g["counts"]["evaluated"],
+                "device_pipeline_direct_ms": t_direct, "device_pipeline_graph_ms": t_graph,
                 "device_search_ms": t_sum, "run_search_json_ms": t_json, "run_search_objects_to_json_ms": t_obj,
                 "cpu_oracle_1thread_ms": t_orc, "python_reference_ms": 1000.0 * g["_meta"]["reference_wall_s"]})
 print(json.dumps({"reps": REPS, "note": "median wall ms; python_reference_ms from the golden generator (CPU, survey "
