@@ -10,6 +10,7 @@
 #include <math.h>
 #include "../../include/llmconf_b200.h"
 #include "glibc_libm.cuh"
+#include "lc_fastdiv.cuh"
 
 namespace lc {
 

@@ -17,6 +17,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <map>
 #include <mutex>
 #include <string>
@@ -186,12 +187,28 @@ struct PStep {
   int64_t c0, c1;  // failing query coordinates
 };
 
-// one priced query (query tables and decode-series tables)
+// one priced query (decode-series tables)
 struct QVal {
   double lat;
   int32_t status;
   int32_t _pad;
 };
+
+// One priced query of the shared query tables in 8 bytes: the latency, or for a
+// failed query a signalling-NaN pattern carrying its status (exponent all ones,
+// quiet bit clear, tag bits 0x7FF4 in the top 16).  Device arithmetic only ever
+// yields the canonical quiet NaN and lc_db_upload quiets any NaN database cell,
+// so no latency can carry the tag.  Half the bytes of a QVal: the K2 cell kernel
+// stages a whole step's values in shared memory per thread.
+constexpr unsigned long long kBoxTag = 0x7FF4000000000000ull;
+__host__ __device__ __forceinline__ bool is_boxed(unsigned long long bits) { return (bits >> 48) == (kBoxTag >> 48); }
+__device__ __forceinline__ double box_status(int st) {
+  return __longlong_as_double((long long)(kBoxTag | (unsigned long long)(unsigned)st));
+}
+__device__ __forceinline__ QVal unbox(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return is_boxed(b) ? QVal{0.0, (int32_t)(b & 0xffffu), 0} : QVal{v, 0, 0};
+}
 
 // One MoE tail table: [tp_i * n_ep + ep_i][b_i].  Prefill-type tables depend on
 // (batch list, load, context length), decode-type on (batch list, load) only,
@@ -253,6 +270,8 @@ struct lc_ctx {
   DBuf pgroups, psteps;        // shared prefill step totals
   DBuf acc;                    // SearchAcc per search
   DBuf plan_scratch;           // K5b pairing results [search][256]
+  DBuf pool_seed;              // K5a seed thresholds [search][2]
+  DBuf pool_sample;            // K5a seed sample [search * combo][2]
   std::vector<PGroup> hpg;
   std::vector<uint64_t> hbatch_code;  // config-key batch-field codes of the batches array (lc_keys.h)
   int64_t n_pstep = 0;
@@ -321,7 +340,7 @@ struct EvalParams {
   const int32_t* class_slots; int32_t class_off[4];
   const QtGroup* qt_groups; int32_t n_qt_groups;
   const lc_entry* gclasses; int32_t n_gclass; const int32_t* gclass_of;
-  QVal* qt; int64_t n_qt;
+  double* qt; int64_t n_qt;           // boxed (box_status)
   QVal* ds; int64_t n_ds;
   const DsGroup* ds_groups; int32_t n_ds_groups;
   const SeriesGroup* sgroups; int32_t n_sgroups; const SeriesMember* smembers; SdOut* sd; int64_t n_series;
@@ -356,6 +375,7 @@ struct EvalParams {
   // closed-form K0 (fused candidate rows): unit offsets per (search, combo), budget flags, template combos
   const int32_t* pair_off;           // [n_search * n_combos + 1], nullptr otherwise
   const uint8_t* pair_inb;
+  double* pool_sample;               // [n_search * n_combos][2]: pool keys of each pair's last unit (K5a seed)
   const int32_t* tmpl_cidx_off; const int32_t* tmpl_cidx;
 };
 
@@ -875,7 +895,7 @@ __global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_qtabl
     const int64_t rel = x - Gq.off;
     const int j = div32(rel, S.n_b), bi = mod32(rel, S.n_b);
     const lc_slot SL = P.slots[P.class_slots[P.class_off[Gq.cls] + j]];
-    QVal out{0.0, LC_ST_NOT_EVALUATED, 0};
+    double out = box_status(LC_ST_NOT_EVALUATED);
     const int64_t b = P.batches[S.b_off + bi];
     const int64_t chunk = S.isl - S.prefix;
     const int64_t kv_mid = S.isl + S.osl / 2;
@@ -896,8 +916,8 @@ __global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_qtabl
     int64_t d[5];
     if (need && entry_coords(SL.e, a, P.hidden, d)) {
       int st = 0, nlog = 0;
-      out.lat = LC_TABLE_QUERY(V, SL.e.grid, SL.e.kind, SL.e.quant, d[0], d[1], d[2], d[3], d[4], &st, &nlog);
-      out.status = st;
+      const double lat = LC_TABLE_QUERY(V, SL.e.grid, SL.e.kind, SL.e.quant, d[0], d[1], d[2], d[3], d[4], &st, &nlog);
+      out = st ? box_status(st) : lat;
     }
     P.qt[x] = out;
   }
@@ -938,8 +958,11 @@ __global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_dstab
 // One step's total from the query table: sum in plan order of
 // ((lat * repeat) / 1000) * bubble, CPython sum() semantics (estimator.py:83-95);
 // the first failing entry in plan order decides the error.
+__device__ __forceinline__ const double* qt_ptr(const EvalParams& P, const SearchMeta& M, int32_t so, int n_b, int bi) {
+  return P.qt + M.qt_off[so >> 16] + (int64_t)(so & 0xffff) * n_b + bi;
+}
 __device__ __forceinline__ QVal qt_at(const EvalParams& P, const SearchMeta& M, int32_t so, int n_b, int bi) {
-  return P.qt[M.qt_off[so >> 16] + (int64_t)(so & 0xffff) * n_b + bi];
+  return unbox(*qt_ptr(P, M, so, n_b, bi));
 }
 
 __device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta& M, const lc_entry* E, int ne,
@@ -959,7 +982,7 @@ __device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta&
       err->code = q.status; err->label = e.label; err->c0 = d[0]; err->c1 = d[1];
       return q.status;
     }
-    const double ms = q.lat * (double)e.repeat / 1000.0;
+    const double ms = div1000(q.lat * (double)e.repeat);
     sum.add(0.0 + ms * bubble);
   }
   *out = sum.result();
@@ -968,9 +991,61 @@ __device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta&
   return 0;
 }
 
+// K2 cells stage a step's query values in shared memory before the plan-order
+// sum: every entry's 8-byte table value is requested at once (cp.async, one
+// column per thread: [entry][thread]), so the ~16 L2 gathers of a step overlap
+// instead of forming a chain of dependent round trips.  The sum itself is
+// unchanged (table_step's order, skips and first-failure rule).
 #ifndef LC_CELL_MIN_BLOCKS
 #define LC_CELL_MIN_BLOCKS 8  // 64 registers: occupancy beats the few spills (measured)
 #endif
+#ifndef LC_CELL_BUFS
+#define LC_CELL_BUFS 0  // staged steps per thread; 0: unstaged (1 measured neutral, 2 slower: K2 1.93 -> 2.08 / 2.43 ms)
+#endif
+constexpr int kCellThreads = 128;
+constexpr int kCellBufs = LC_CELL_BUFS;
+__device__ __forceinline__ void stage_step(const EvalParams& P, const SearchMeta& M, int ne, const int32_t* slot_row,
+                                           int n_b, int bi, double* col) {
+  if (kCellBufs == 0) return;  // unstaged: the sum reads the table directly
+#pragma unroll 4
+  for (int i = 0; i < ne; ++i) {
+    const int32_t so = slot_row[i * 3];
+    if (so >= 0) __pipeline_memcpy_async(col + i * kCellThreads, qt_ptr(P, M, so, n_b, bi), sizeof(double));
+  }
+  __pipeline_commit();
+}
+
+// table_step over a staged column (stage_step, completed)
+// `xt` yields the step's expert-token count, needed only for a failing expert
+// entry's coordinates (the tail lookup stays off the common path)
+template <class XT>
+__device__ __forceinline__ int table_step_staged(const EvalParams& P, const SearchMeta& M, const lc_entry* E, int ne,
+                                                 const int32_t* slot_row, int n_b, int bi, const double* col,
+                                                 StepArgs a, XT xt, double bubble, double* out, ErrRec* err, int* q1,
+                                                 int* q2) {
+  NeumaierSum sum;
+  int c1 = 0, c2 = 0;
+  for (int i = 0; i < ne; ++i) {
+    const lc_entry& e = E[i];
+    if (e.coord == LC_COORD_CTX && !a.n_ctx) continue;
+    if (e.coord == LC_COORD_GEN && !a.n_gen) continue;
+    const QVal q = unbox(kCellBufs ? col[i * kCellThreads] : *qt_ptr(P, M, slot_row[i * 3], n_b, bi));
+    if (e.coord == LC_COORD_CTX || e.coord == LC_COORD_GEN) ++c2; else ++c1;
+    if (q.status) {
+      int64_t d[5];
+      a.expert_tokens = xt();
+      entry_coords(e, a, P.hidden, d);
+      err->code = q.status; err->label = e.label; err->c0 = d[0]; err->c1 = d[1];
+      return q.status;
+    }
+    const double ms = div1000(q.lat * (double)e.repeat);
+    sum.add(0.0 + ms * bubble);
+  }
+  *out = sum.result();
+  *q1 = c1;
+  *q2 = c2;
+  return 0;
+}
 // K2b: static decode loops (serving_modes.py:256-266), one thread per
 // (series group, template, batch) shared by the group's output lengths (SeriesGroup).
 // Non-attention terms come from the decode-step query slots (same tokens at every
@@ -1039,7 +1114,7 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
         e.code = q.status; e.label = en.label; e.c0 = d[0]; e.c1 = d[1];
         break;
       }
-      const double ms = q.lat * (double)en.repeat / 1000.0;
+      const double ms = div1000(q.lat * (double)en.repeat);
       term[m++] = 0.0 + ms * bubble;
     }
     int mi = 0;  // next member to receive its total (members ascend in n_steps)
@@ -1087,7 +1162,7 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
           if (sj == 0) { g[j] = term[gi]; continue; }
           const QVal q = ring[(sj % kDsRing) * 128];
           if (q.status) { bad = j; e.code = q.status; e.label = ge->label; e.c0 = b; e.c1 = S.isl + stride * sj + 1; continue; }
-          g[j] = 0.0 + (q.lat * g_rep / 1000.0) * bubble;
+          g[j] = 0.0 + div1000(q.lat * g_rep) * bubble;
         }
 #pragma unroll
         for (int j = 0; j < kChains; ++j) issue(step + kDsRing + j);
@@ -1224,7 +1299,7 @@ __device__ __forceinline__ void acc_flush(SearchAcc* A, const RowAcc& r) {
 // contribution to the per-search accounting.
 __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search_desc& S, const CellOut& o, int64_t ci,
                                             int64_t u, int64_t b, int64_t gpus, bool inb, RowAcc& ra,
-                                            unsigned long long* bk) {
+                                            unsigned long long* bk, double* seed_at = nullptr) {
   const int64_t n = P.n_cap;
   const bool do_st = (S.modes & 1) && inb, do_ag = (S.modes & 2) && inb, do_dg = (S.modes & 4) != 0;
   int32_t q = 0;
@@ -1269,20 +1344,26 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
     if (o.pf_status) {
       P.err_c[4 * n + u] = P.cell_err[ci * 8 + 4]; P.err_c[5 * n + u] = P.cell_err[ci * 8 + 5];
       P.pool_key[u] = INFINITY;
+      if (seed_at) seed_at[0] = INFINITY;
     } else {
       const double rate = (double)b * 1000.0 / o.pf_lat;
       P.pf_v[u] = o.pf_lat; P.pf_v[n + u] = rate;
-      P.pool_key[u] = -rate / (double)gpus;
+      const double r = -rate / (double)gpus;
+      P.pool_key[u] = r;
+      if (seed_at) seed_at[0] = r;
     }
     P.dc_status[u] = o.dc_status;
     if (o.dc_status) {
       P.err_c[6 * n + u] = P.cell_err[ci * 8 + 6]; P.err_c[7 * n + u] = P.cell_err[ci * 8 + 7];
       P.pool_key[n + u] = INFINITY;
+      if (seed_at) seed_at[1] = INFINITY;
     } else {
       const double rate = S.osl == 1 ? INFINITY : (double)b * 1000.0 / ((double)(S.osl - 1) * o.dc_lat);
       P.dc_v[u] = o.dc_lat;
       P.dc_v[n + u] = rate;
-      P.pool_key[n + u] = -rate / (double)gpus;
+      const double r = -rate / (double)gpus;
+      P.pool_key[n + u] = r;
+      if (seed_at) seed_at[1] = r;
     }
   }
   // the generation step is a memo hit when a static decode step used the same KV length
@@ -1304,7 +1385,7 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
 // (P.pair_off) the cell also writes the rows of its dp-variant candidates
 // (expand_unit) -- the cell stays in registers instead of a k_expand re-read.
 __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, int s, uint32_t cf, RowAcc& ra,
-                                          int& s_out) {
+                                          int& s_out, double* stage) {
   const lc_search_desc& S = P.searches[s];
   const SearchMeta& M = P.meta[s];
   const int64_t rel = ci - M.cell_off;
@@ -1328,6 +1409,16 @@ __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, int s
   o.st_steps = 0;
   o.flags = 0;
   int q1 = 0, q2 = 0;
+  // the mixed and generation steps' table values, requested before anything else
+  double* colM = stage;
+  double* colG = stage + (kCellBufs > 1 ? LC_MAX_ENTRIES * kCellThreads : 0);
+  __pipeline_wait_prior(0);  // the previous cell's copies into these columns have landed
+  if (do_ag) stage_step(P, M, ne, so + LC_STEP_MIXED, S.n_b, bi, colM);
+  bool g_staged = false;
+  if (kCellBufs > 1 && (do_ag || do_dg)) {
+    stage_step(P, M, ne, so + LC_STEP_GEN, S.n_b, bi, colG);
+    g_staged = true;
+  }
 
   // prefill step: static TTFT and the prefill pool
   double p_total = 0.0;
@@ -1347,8 +1438,19 @@ __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, int s
     o.pf_lat = p_total;
     if (p_err.code) put_cell_err(P, 2, ci, p_err);
   }
-  const int64_t xt_dec = expert_tokens(P, c, M, S, 1, bi, b);
-  const StepArgs ga{PH_DECODE, 0, b, kv_mid, xt_dec};
+  bool g_done = false;
+  double g_total = 0.0;
+  ErrRec g_err{0, 0, 0, 0};
+  const StepArgs ga{PH_DECODE, 0, b, kv_mid, 0};
+  auto xt_dec = [&]() { return expert_tokens(P, c, M, S, 1, bi, b); };
+  auto gen_step = [&]() {
+    if (!g_staged) {
+      stage_step(P, M, ne, so + LC_STEP_GEN, S.n_b, bi, colG);
+      g_staged = true;
+    }
+    __pipeline_wait_prior(0);
+    table_step_staged(P, M, E, ne, so + LC_STEP_GEN, S.n_b, bi, colG, ga, xt_dec, bubble, &g_total, &g_err, &q1, &q2);
+  };
   if (do_st) {
     double tpot = 0.0;
     ErrRec e = p_err;
@@ -1368,21 +1470,19 @@ __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, int s
     if (e.code) put_cell_err(P, 0, ci, e);
   }
   // generation step at the KV midpoint: aggregated l_gen and the decode pool
-  bool g_done = false;
-  double g_total = 0.0;
-  ErrRec g_err{0, 0, 0, 0};
   if (do_ag) {
     const AggSched sc = agg_schedule(S, b);
     ErrRec e{sc.st, 0, 0, 0};
     double ttft = 0.0, tpot = 0.0;
     if (!sc.st) {
       double l_mix = 0.0, l_gen = 0.0;
-      const StepArgs a{PH_MIXED, sc.chunk_tokens, sc.n_mix_gen, kv_mid,
-                       expert_tokens(P, c, M, S, 2, bi, sc.chunk_tokens + sc.n_mix_gen)};
-      table_step(P, M, E, ne, so + LC_STEP_MIXED, S.n_b, bi, a, bubble, &l_mix, &e, &q1, &q2);
+      const StepArgs a{PH_MIXED, sc.chunk_tokens, sc.n_mix_gen, kv_mid, 0};
+      auto xt_mix = [&]() { return expert_tokens(P, c, M, S, 2, bi, sc.chunk_tokens + sc.n_mix_gen); };
+      __pipeline_wait_prior(kCellBufs > 1 ? 1 : 0);  // the mixed column (the generation one may still fly)
+      table_step_staged(P, M, E, ne, so + LC_STEP_MIXED, S.n_b, bi, colM, a, xt_mix, bubble, &l_mix, &e, &q1, &q2);
       if (!e.code) o.qM = (q1 & 0xffff) | (q2 << 16);
       if (!e.code && (sc.t_gen || b == 1)) {
-        table_step(P, M, E, ne, so + LC_STEP_GEN, S.n_b, bi, ga, bubble, &g_total, &g_err, &q1, &q2);
+        gen_step();
         g_done = true;
         if (!g_err.code) o.qG = (q1 & 0xffff) | (q2 << 16);
         o.flags |= 1;
@@ -1410,7 +1510,7 @@ __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, int s
   }
   if (do_dg) {
     if (!g_done) {
-      table_step(P, M, E, ne, so + LC_STEP_GEN, S.n_b, bi, ga, bubble, &g_total, &g_err, &q1, &q2);
+      gen_step();
       if (!g_err.code) o.qG = (q1 & 0xffff) | (q2 << 16);
     }
     o.dc_status = g_err.code | (g_err.label << 8);
@@ -1425,16 +1525,19 @@ __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, int s
     for (int j = P.tmpl_cidx_off[tmpl]; j < j1; ++j) {
       const int cj = P.tmpl_cidx[j];
       const int64_t pr = pbase + cj;
-      const int32_t off = P.pair_off[pr];
-      if (bi >= P.pair_off[pr + 1] - off) continue;  // this dp variant is not a candidate at this batch
-      expand_unit(P, S, o, ci, (int64_t)off + bi, b, P.combos[cj].gpus, P.pair_inb[pr] != 0, ra, bk);
+      const int32_t off = P.pair_off[pr], cnt = P.pair_off[pr + 1] - off;
+      if (bi >= cnt) continue;  // this dp variant is not a candidate at this batch
+      // the pair's last unit (largest batch) also goes to the K5a seed sample
+      double* seed_at = P.pool_sample && bi == cnt - 1 ? P.pool_sample + 2 * pr : nullptr;
+      expand_unit(P, S, o, ci, (int64_t)off + bi, b, P.combos[cj].gpus, P.pair_inb[pr] != 0, ra, bk, seed_at);
     }
   } else {
     P.cells[ci] = o;
   }
 }
 
-__global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalParams P) {
+__global__ void __launch_bounds__(kCellThreads, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalParams P) {
+  __shared__ double stage[kCellBufs ? kCellBufs * LC_MAX_ENTRIES * kCellThreads : 1];  // [buffer][entry][thread]
   const int64_t ncell = P.n_cells_total;
   const int lane = threadIdx.x & 31;
   // each block walks one contiguous range of cells, so a thread's search index only
@@ -1450,7 +1553,7 @@ __global__ void __launch_bounds__(128, LC_CELL_MIN_BLOCKS) k_eval_cells(EvalPara
     if (cf) {
       if (hint < 0) hint = find_cell_search(P.meta, P.n_search, ci);
       while (hint + 1 < P.n_search && P.meta[hint + 1].cell_off <= ci) ++hint;
-      eval_cell(P, ci, hint, cf, ra, s);
+      eval_cell(P, ci, hint, cf, ra, s, stage + threadIdx.x);
     }
     if (!P.pair_off) continue;  // uniform: k_expand does the accounting
     // warp-aggregated accounting (cells are ordered by search)
@@ -1973,8 +2076,61 @@ __device__ __forceinline__ void slice_of(int64_t n, int parts, int part, int64_t
   *hi = n * (part + 1) / parts;
 }
 
+// Seed thresholds for K5a: per (search, role), the cap-th smallest key r among
+// the last unit of every (search, combo) pair -- written by k_eval_cells into
+// pool_sample (closed-form K0 only).  The pool rate per GPU grows along a combo's
+// batch list, so these are nearly the search's best keys.  Any cap units with
+// r <= T leave no room in the top-k for a unit with r > T, so the cap-th smallest
+// sampled r bounds the search's cap-th from above (ties are kept: r <= T passes).
+// One warp per (search, role): a sorted 32-list of doubles, bitonic merges.
+__device__ __forceinline__ double warp_sort32_d(double v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, v, j);
+      const bool lower = (lane & j) == 0, asc = (lane & k) == 0;
+      v = (lower == asc) ? fmin(v, o) : fmax(v, o);
+    }
+  return v;
+}
+__global__ void k_pools_seed(EvalParams P, double* seed) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int s = w >> 1, role = w & 1;
+  if (s >= P.n_search) return;
+  const lc_search_desc& S = P.searches[s];
+  const int cap = role == 0 ? S.prefill_cap : S.decode_cap;
+  double t = INFINITY;
+  if ((S.modes & 4) && cap > 0 && cap <= kPoolLocal) {
+    const int32_t* po = P.pair_off + (int64_t)s * P.sp_n_combos;
+    const double* smp = P.pool_sample + (int64_t)s * P.sp_n_combos * 2 + role;
+    double best = INFINITY;  // lane j: the j-th smallest so far (ascending)
+    for (int c0 = 0; c0 < P.sp_n_combos; c0 += 32) {
+      const int c = c0 + lane;
+      double r = INFINITY;
+      if (c < P.sp_n_combos && po[c + 1] > po[c]) {
+        r = smp[2 * c];
+        if (!(r <= INFINITY)) r = INFINITY;  // NaN keys never enter a pool (k_pools_partial)
+      }
+      if (!__any_sync(0xffffffffu, r != INFINITY)) continue;
+      r = warp_sort32_d(r);
+      // the 32 smallest of best ++ r: bitonic merge of ascending best with descending r
+      double m = fmin(best, __shfl_sync(0xffffffffu, r, 31 - lane));
+#pragma unroll
+      for (int j = 16; j > 0; j >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, m, j);
+        m = (lane & j) == 0 ? fmin(m, o) : fmax(m, o);
+      }
+      best = m;
+    }
+    t = __shfl_sync(0xffffffffu, best, cap - 1);
+  }
+  if (lane == 0) seed[2 * s + role] = t;
+}
+
 __global__ void __launch_bounds__(kPoolThreads) k_pools_partial(EvalParams P, const SearchMeta* meta,
-                                                                 PoolPartial* part) {
+                                                                 PoolPartial* part, const double* seed) {
   const int s = blockIdx.y, bx = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const lc_search_desc& S = P.searches[s];
   if (!(S.modes & 4)) return;
@@ -1991,16 +2147,18 @@ __global__ void __launch_bounds__(kPoolThreads) k_pools_partial(EvalParams P, co
     const double* keys = P.pool_key + (int64_t)role * P.n_cap;
     WarpTopK tk;
     tk.init();
-    double thr = INFINITY;
     // warp-strided chunks of 32 consecutive units (coalesced); a key can enter only if
-    // not after the current cap-th element (r <= thr; exact order in the merge)
+    // not after the current cap-th element (r <= thr; exact order in the merge).  The
+    // threshold starts at the search's seed (k_pools_seed): with it most chunks hold
+    // no candidate and cost one coalesced load.
+    double thr = seed ? seed[2 * s + role] : INFINITY;
     for (int64_t base = lo + (int64_t)warp * 32; base < hi; base += kPoolThreads) {
       const int64_t i = base + lane;
       const double r = i < hi ? keys[u0 + i] : INFINITY;  // INFINITY: pool candidate skipped
       const bool cand = r != INFINITY && r <= thr;
       if (!__any_sync(0xffffffffu, cand)) continue;
       tk.merge_chunk(P, cand ? pool_key_of(P, S, r, (int32_t)(u0 + i)) : PoolKey{0.0, 0, -1}, cap);
-      thr = tk.thr_r(cap);
+      thr = fmin(thr, tk.thr_r(cap));
     }
     wout[warp][lane] = tk.mine;
     if (lane == 0) wn[warp] = tk.n;
@@ -2447,7 +2605,7 @@ __global__ void __launch_bounds__(128) k_step(DbView V, StepView T, int32_t n, c
         label = e.label;
         int nlog = 0;
         const double lat = query_body<true>(V, e.grid, e.kind, e.quant, d[0], d[1], d[2], d[3], d[4], &st, &nlog);
-        val = 0.0 + (lat * (double)e.repeat / 1000.0) * bubble;
+        val = 0.0 + div1000(lat * (double)e.repeat) * bubble;
       }
     }
     lc_step_out* o = out + r;
@@ -2515,7 +2673,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->batch_code, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->step_in, &c->step_out, &c->step_loads, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->step_in, &c->step_out, &c->step_loads, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch, &c->pool_seed, &c->pool_sample};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -2545,7 +2703,15 @@ int lc_db_upload(lc_ctx* c, const lc_db_desc* d, lc_db** out) {
   if ((rc = upload(&db->grids, g.data(), g.size(), c->stream))) return rc;
   if ((rc = upload(&db->axv, d->axis_val, d->n_axis, c->stream))) return rc;
   if ((rc = upload(&db->axl, d->axis_log, d->n_axis, c->stream))) return rc;
-  if ((rc = upload(&db->cell, d->cell, d->n_cells, c->stream))) return rc;
+  // NaN cells are quieted (repr / JSON print every NaN alike): the query tables'
+  // status boxes are signalling-NaN patterns no latency may carry (box_status)
+  std::vector<double> cells(d->cell, d->cell + d->n_cells);
+  for (double& x : cells) {
+    uint64_t b;
+    memcpy(&b, &x, 8);
+    if (std::isnan(x) && is_boxed(b)) { b |= 0x0008000000000000ull; memcpy(&x, &b, 8); }
+  }
+  if ((rc = upload(&db->cell, cells.data(), d->n_cells, c->stream))) return rc;
   if ((rc = upload(&db->clog, d->cell_log, d->n_cells, c->stream))) return rc;
   if ((rc = upload(&db->logtab, LOG_TAB_H, 256, c->stream))) return rc;
   if ((rc = upload(&db->exptab, EXP_TAB_H, 256, c->stream))) return rc;
@@ -2715,7 +2881,7 @@ static EvalParams make_params(lc_ctx* c) {
   for (int k = 0; k < 4; ++k) P.class_off[k] = sp->class_off[k];
   P.qt_groups = (const QtGroup*)c->qt_groups.p; P.n_qt_groups = (int32_t)c->hqt.size();
   P.gclasses = sp->gclasses; P.n_gclass = sp->n_gclass; P.gclass_of = sp->gclass_of;
-  P.qt = (QVal*)c->qt.p; P.n_qt = c->n_qt;
+  P.qt = (double*)c->qt.p; P.n_qt = c->n_qt;
   P.ds = (QVal*)c->ds.p; P.n_ds = c->n_ds;
   P.ds_groups = (const DsGroup*)c->ds_groups.p; P.n_ds_groups = (int32_t)c->hds.size();
   P.sgroups = (const SeriesGroup*)c->sgroups.p; P.n_sgroups = (int32_t)c->hsg.size();
@@ -2763,6 +2929,11 @@ static EvalParams make_params(lc_ctx* c) {
   P.pair_off = nullptr;
 #endif
   P.pair_inb = (const uint8_t*)c->pair_inb.p;
+#ifndef LC_NO_POOL_SEED
+  P.pool_sample = P.pair_off ? (double*)c->pool_sample.p : nullptr;
+#else
+  P.pool_sample = nullptr;
+#endif
   P.tmpl_cidx_off = sp->tmpl_cidx_off; P.tmpl_cidx = sp->tmpl_cidx;
   return P;
 }
@@ -2792,7 +2963,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   c->err_c.get<int64_t>(8 * n, &err);
   c->pool_key.get<double>(2 * n, &err);
   c->cells.get<CellOut>(c->n_cells, &err);
-  c->qt.get<QVal>(c->n_qt, &err);
+  c->qt.get<double>(c->n_qt, &err);
   c->ds.get<QVal>(c->n_ds, &err);
   c->cell_err.get<int64_t>(8 * c->n_cells, &err);
   c->pool_sel.get<int32_t>((size_t)c->n_search * 128, &err);
@@ -2900,7 +3071,18 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     PoolPartial* pp = c->pool_part.get<PoolPartial>((size_t)c->n_search * kPoolSplit, &err);
     if (err != cudaSuccess) return fail(LC_ERR_CUDA, "pool partial allocation");
     ++c->launches;
-    k_pools_partial<<<dim3(kPoolSplit, c->n_search), kPoolThreads, 0, c->stream>>>(P, (const SearchMeta*)c->meta.p, pp);
+    const double* seed = nullptr;
+#ifndef LC_NO_POOL_SEED
+    if (P.pool_sample) {
+      double* sd = c->pool_seed.get<double>((size_t)c->n_search * 2, &err);
+      if (err != cudaSuccess) return fail(LC_ERR_CUDA, "pool seed allocation");
+      ++c->launches;
+      k_pools_seed<<<(2 * c->n_search + 3) / 4, 128, 0, c->stream>>>(P, sd);
+      seed = sd;
+    }
+#endif
+    k_pools_partial<<<dim3(kPoolSplit, c->n_search), kPoolThreads, 0, c->stream>>>(P, (const SearchMeta*)c->meta.p, pp,
+                                                                                    seed);
     ++c->launches;
     k_pools_final<<<c->n_search, kPoolThreads, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, pp, (int32_t*)c->pool_sel.p);
     CK(cudaGetLastError());
@@ -2958,6 +3140,7 @@ static int run_enum_fit(lc_ctx* c) {
   const int64_t n_pairs = (int64_t)c->n_search * nc;
   int32_t* bs = c->block_sums.get<int32_t>(n_pairs + 1, &err);
   uint8_t* inb = c->pair_inb.get<uint8_t>(n_pairs > 0 ? n_pairs : 1, &err);
+  c->pool_sample.get<double>((size_t)(n_pairs > 0 ? n_pairs : 1) * 2, &err);  // K5a seed sample (k_eval_cells)
   int32_t* cmax = c->cmax.get<int32_t>((size_t)c->n_search * (nt > 0 ? nt : 1) * 2 + 1, &err);
   uint32_t* cflags = c->cell_flags.get<uint32_t>(c->n_cells, &err);
   c->n_cap = n_raw;

@@ -24,3 +24,15 @@ def test_glibc_log_exp_restatement_is_bit_exact(tmp_path):
     checked, bad = map(int, out.stdout.split())
     assert checked > 10_000_000
     assert bad == 0, out.stderr
+
+
+@pytest.mark.skipif(shutil.which("g++") is None, reason="needs g++")
+def test_div1000_is_correctly_rounded(tmp_path):
+    """lc::div1000 (the step sums' `lat * repeat / 1000.0`, estimator.py:93) is IEEE division."""
+    exe = tmp_path / "div_check"
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-mfma", "-o", str(exe),
+                    str(ROOT / "tests" / "native" / "div_check.cpp")], check=True)
+    out = subprocess.run([str(exe), "40000000", "7"], capture_output=True, text=True)
+    checked, bad = map(int, out.stdout.split())
+    assert checked > 40_000_000
+    assert bad == 0, out.stderr

@@ -1,0 +1,8 @@
+# A/B per kernel: ncu launch lists of every variants/*.so (tools/gpu_kernel_variants.sh),
+# then the GPU tests on the in-tree build unless SKIP_TESTS=1.
+mkdir -p gpurun_out
+bash tools/gpu_kernel_variants.sh
+if [ "${SKIP_TESTS:-0}" != 1 ]; then
+  timeout 2400 python -m pytest tests -m gpu -x -q ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
+  tail -4 gpurun_out/pytest_gpu.log
+fi

@@ -21,7 +21,7 @@ SO = ROOT / "paper_2601_06288_b200" / "_lc_b200.so"
 
 def disassemble(so: Path = SO) -> dict[str, list[str]]:
     with tempfile.TemporaryDirectory() as td:
-        subprocess.run(["cuobjdump", "-xelf", "all", str(so)], cwd=td, check=True, capture_output=True)
+        subprocess.run(["cuobjdump", "-xelf", "all", str(Path(so).resolve())], cwd=td, check=True, capture_output=True)
         cubin = next(Path(td).glob("*.cubin"))
         txt = subprocess.run(["nvdisasm", "-g", "-c", str(cubin)], check=True, capture_output=True,
                              text=True).stdout
