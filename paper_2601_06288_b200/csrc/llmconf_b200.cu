@@ -781,11 +781,15 @@ __global__ void k_dbgen(DbView D, const lc_gen_grid* __restrict__ grids, int32_t
 }
 
 // ---- K2: evaluate every unit
+// GLOBAL: the database is too large to stage and is read through L1/L2.  The
+// staged instantiation derives every view pointer from the shared array alone
+// (no branch to a global pointer), so the inlined query path compiles to LDS.
+template <bool GLOBAL>
 __device__ __forceinline__ void stage_db(const EvalParams& P, unsigned char* smem, DbView* V) {
   V->mem_bw = P.mem_bw; V->intra_bw = P.intra_bw; V->inter_bw = P.inter_bw; V->gpu_memory = P.gpu_memory;
   for (int i = 0; i < 4; ++i) V->compute[i] = P.compute[i];
   V->gpn = P.gpn; V->policy = P.policy;
-  if (P.db_global) {
+  if (GLOBAL) {
     V->grids = P.grids; V->axv = P.axv; V->axl = P.axl; V->cell = P.cell; V->clog = P.clog;
     V->logtab = P.logtab; V->exptab = P.exptab;
     return;
@@ -877,10 +881,11 @@ __device__ __forceinline__ int64_t tail_tokens(const EvalParams& P, const Search
 #endif
 // K2a: query tables.  One thread per (search, slot, batch): the latency every
 // template entry of that slot sees in that step (query_latency, perfdb.py:539-580).
+template <bool GLOBAL>
 __global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_qtables(EvalParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   DbView V;
-  stage_db(P, smem, &V);
+  stage_db<GLOBAL>(P, smem, &V);
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < P.n_qt; x += (int64_t)gridDim.x * blockDim.x) {
     int lo = 0, hi = P.n_qt_groups - 1;
     while (lo < hi) {
@@ -925,10 +930,11 @@ __global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_qtabl
 
 // K2a': generation-attention latency at every sampled KV length of the static
 // decode loop (serving_modes.py:258-265): one thread per (search, grid, batch, sample).
+template <bool GLOBAL>
 __global__ void __launch_bounds__(LC_TABLE_THREADS, LC_TABLE_MIN_BLOCKS) k_dstables(EvalParams P) {
   extern __shared__ __align__(16) unsigned char smem[];
   DbView V;
-  stage_db(P, smem, &V);
+  stage_db<GLOBAL>(P, smem, &V);
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < P.n_ds; x += (int64_t)gridDim.x * blockDim.x) {
     int lo = 0, hi = P.n_ds_groups - 1;
     while (lo < hi) {
@@ -1002,6 +1008,9 @@ __device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta&
 #ifndef LC_CELL_BUFS
 #define LC_CELL_BUFS 0  // staged steps per thread; 0: unstaged (1 measured neutral, 2 slower: K2 1.93 -> 2.08 / 2.43 ms)
 #endif
+#ifndef LC_WARP_STEPS
+#define LC_WARP_STEPS 1  // warp-cooperative mixed / generation steps in k_eval_cells (warp_table_step)
+#endif
 constexpr int kCellThreads = 128;
 constexpr int kCellBufs = LC_CELL_BUFS;
 __device__ __forceinline__ void stage_step(const EvalParams& P, const SearchMeta& M, int ne, const int32_t* slot_row,
@@ -1046,6 +1055,83 @@ __device__ __forceinline__ int table_step_staged(const EvalParams& P, const Sear
   *q2 = c2;
   return 0;
 }
+// table_step_staged for a whole warp of cells.  Lanes are grouped by (search,
+// template) -- one group in the common case, batch lists being long -- and per
+// group lane j loads entry j's plan metadata once (coordinate recipe, label,
+// repeat and the query-table row of its slot); the plan-order loop broadcasts
+// it with shuffles.  Each entry then costs one dependent load (the lane's own
+// table value, prefetched two entries ahead) instead of the chain slot ->
+// class offset -> value.  Lanes with `active` false only take part in the
+// shuffles.  Sum order, skips and the first-failure rule are table_step's.
+template <class XT>
+__device__ __forceinline__ void warp_table_step(const EvalParams& P, int s, int tmpl, int step, int bi, bool active,
+                                                StepArgs a, XT xt, double bubble, double* out, ErrRec* err, int* q1,
+                                                int* q2) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  unsigned pending = __ballot_sync(full, active);
+  NeumaierSum sum;
+  int c1 = 0, c2 = 0;
+  bool live = active;
+  while (pending) {
+    const int leader = __ffs(pending) - 1;
+    const int sg = __shfl_sync(full, s, leader), tg = __shfl_sync(full, tmpl, leader);
+    const bool act = live && s == sg && tmpl == tg;
+    pending &= ~__ballot_sync(full, s == sg && tmpl == tg);
+    const int n_b = P.searches[sg].n_b;
+    const lc_entry* E = P.entries + (int64_t)tg * LC_MAX_ENTRIES;
+    const int ne = P.tmpl_n[tg];
+    int my_cl = 0;
+    double my_rep = 0.0;
+    long long my_base = -1;
+    if (lane < ne) {
+      const lc_entry& e = E[lane];
+      my_cl = e.coord | (e.label << 8);
+      my_rep = (double)e.repeat;
+      const int32_t so = P.slot_of[((int64_t)tg * LC_MAX_ENTRIES + lane) * 3 + step];
+      if (so >= 0) my_base = P.meta[sg].qt_off[so >> 16] + (int64_t)(so & 0xffff) * n_b;
+    }
+    auto fetch = [&](int i) -> double {  // entry i's table value for this lane (0.0 if not needed)
+      const int cl = __shfl_sync(full, my_cl, i & 31);
+      const long long base = __shfl_sync(full, my_base, i & 31);
+      const int coord = cl & 0xff;
+      const bool skip = (coord == LC_COORD_CTX && !a.n_ctx) || (coord == LC_COORD_GEN && !a.n_gen);
+      return (act && i < ne && !skip && base >= 0) ? __ldg(P.qt + base + bi) : 0.0;
+    };
+    bool run = act;
+    double v0 = fetch(0), v1 = fetch(1);
+    for (int i = 0; i < ne; ++i) {
+      const int cl = __shfl_sync(full, my_cl, i);
+      const double rep = __shfl_sync(full, my_rep, i);
+      const double v = v0;
+      v0 = v1;
+      v1 = fetch(i + 2);
+      const int coord = cl & 0xff;
+      if (!run) continue;
+      if (coord == LC_COORD_CTX && !a.n_ctx) continue;
+      if (coord == LC_COORD_GEN && !a.n_gen) continue;
+      const QVal q = unbox(v);
+      if (coord == LC_COORD_CTX || coord == LC_COORD_GEN) ++c2; else ++c1;
+      if (q.status) {
+        int64_t d[5];
+        a.expert_tokens = xt();
+        entry_coords(E[i], a, P.hidden, d);
+        err->code = q.status; err->label = cl >> 8; err->c0 = d[0]; err->c1 = d[1];
+        run = false;
+        live = false;
+        continue;
+      }
+      const double ms = div1000(q.lat * rep);
+      sum.add(0.0 + ms * bubble);
+    }
+  }
+  if (live) {
+    *out = sum.result();
+    *q1 = c1;
+    *q2 = c2;
+  }
+}
+
 // K2b: static decode loops (serving_modes.py:256-266), one thread per
 // (series group, template, batch) shared by the group's output lengths (SeriesGroup).
 // Non-attention terms come from the decode-step query slots (same tokens at every
@@ -1384,6 +1470,9 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
 // One cell: every step from the tables (K2).  With the closed-form K0
 // (P.pair_off) the cell also writes the rows of its dp-variant candidates
 // (expand_unit) -- the cell stays in registers instead of a k_expand re-read.
+// WARP: called by all 32 lanes of a warp whose cells share (search, template)
+// (cells with cf == 0 included: they take part in the shuffles, write nothing).
+template <bool WARP>
 __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, int s, uint32_t cf, RowAcc& ra,
                                           int& s_out, double* stage) {
   const lc_search_desc& S = P.searches[s];
@@ -1469,6 +1558,60 @@ __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, int s
     o.st_tpot = tpot;
     if (e.code) put_cell_err(P, 0, ci, e);
   }
+  if constexpr (WARP) {
+    // the mixed step, then the generation step at the KV midpoint for every lane
+    // that needs it (aggregated l_gen, the decode pool), each one warp loop
+    const AggSched sc = agg_schedule(S, b);
+    const bool need_mix = do_ag && !sc.st;
+    const StepArgs am{PH_MIXED, sc.chunk_tokens, sc.n_mix_gen, kv_mid, 0};
+    auto xt_mix = [&]() { return expert_tokens(P, c, M, S, 2, bi, sc.chunk_tokens + sc.n_mix_gen); };
+    double l_mix = 0.0;
+    ErrRec em{0, 0, 0, 0};
+    int m1 = 0, m2 = 0;
+    warp_table_step(P, s, tmpl, LC_STEP_MIXED, bi, need_mix, am, xt_mix, bubble, &l_mix, &em, &m1, &m2);
+    const bool gen_for_ag = need_mix && !em.code && (sc.t_gen || b == 1);
+    warp_table_step(P, s, tmpl, LC_STEP_GEN, bi, gen_for_ag || do_dg, ga, xt_dec, bubble, &g_total, &g_err, &q1, &q2);
+    const int32_t qg = (q1 & 0xffff) | (q2 << 16);
+    if (do_ag) {
+      ErrRec e{sc.st, 0, 0, 0};
+      double ttft = 0.0, tpot = 0.0;
+      if (!sc.st) {
+        e = em;
+        if (!em.code) o.qM = (m1 & 0xffff) | (m2 << 16);
+        double l_gen = 0.0;
+        if (gen_for_ag) {
+          if (!g_err.code) o.qG = qg;
+          o.flags |= 1;
+          e = g_err;
+          l_gen = g_total;
+        }
+        if (!e.code) {
+          const double raw = 2.0 + (double)(sc.T - 3) * (1.0 / 20.0);
+          double F = raw > 2.0 ? raw : 2.0;
+          F = F < 4.0 ? F : 4.0;
+          ttft = l_mix * (double)sc.cpr * F;
+          if (b == 1) tpot = S.osl > 1 ? l_gen : 0.0;
+          else if (S.osl == 1) tpot = 0.0;
+          else if (sc.t_gen == 0) tpot = l_mix;
+          else {
+            const int64_t ms = sc.t_mix - 3 > 1 ? sc.t_mix - 3 : 1;
+            tpot = (l_mix * (double)ms + l_gen * (double)sc.t_gen) / (double)(ms + sc.t_gen);
+          }
+        }
+      }
+      o.ag_status = e.code | (e.label << 8);
+      o.ag_ttft = ttft;
+      o.ag_tpot = tpot;
+      if (e.code) put_cell_err(P, 1, ci, e);
+    }
+    if (do_dg) {
+      if (!g_err.code) o.qG = qg;
+      o.dc_status = g_err.code | (g_err.label << 8);
+      o.dc_lat = g_total;
+      if (g_err.code) put_cell_err(P, 3, ci, g_err);
+    }
+    if (!cf) return;
+  } else {
   // generation step at the KV midpoint: aggregated l_gen and the decode pool
   if (do_ag) {
     const AggSched sc = agg_schedule(S, b);
@@ -1517,6 +1660,7 @@ __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, int s
     o.dc_lat = g_total;
     if (g_err.code) put_cell_err(P, 3, ci, g_err);
   }
+  }  // !WARP
   if (P.pair_off) {
     s_out = s;
     unsigned long long* bk = fixed_buckets(S) ? P.fbuckets + (int64_t)s * kSpeedBuckets : nullptr;
@@ -1550,10 +1694,18 @@ __global__ void __launch_bounds__(kCellThreads, LC_CELL_MIN_BLOCKS) k_eval_cells
     RowAcc ra{0, 0, 0, 0, 0, 0, 0ull, 0ull};
     int s = -1;
     const uint32_t cf = ci < end ? P.cell_flags[ci] : 0u;
-    if (cf) {
+    if (LC_WARP_STEPS) {
+      // every lane of a warp with work takes part (warp_table_step); lanes past
+      // the range stand in as lane 0's cell with nothing to evaluate
+      if (!__any_sync(0xffffffffu, cf != 0u)) continue;
+      const int64_t cv = ci < end ? ci : base;
+      if (hint < 0) hint = find_cell_search(P.meta, P.n_search, cv);
+      while (hint + 1 < P.n_search && P.meta[hint + 1].cell_off <= cv) ++hint;
+      eval_cell<true>(P, cv, hint, cf, ra, s, stage + threadIdx.x);
+    } else if (cf) {
       if (hint < 0) hint = find_cell_search(P.meta, P.n_search, ci);
       while (hint + 1 < P.n_search && P.meta[hint + 1].cell_off <= ci) ++hint;
-      eval_cell(P, ci, hint, cf, ra, s, stage + threadIdx.x);
+      eval_cell<false>(P, ci, hint, cf, ra, s, stage + threadIdx.x);
     }
     if (!P.pair_off) continue;  // uniform: k_expand does the accounting
     // warp-aggregated accounting (cells are ordered by search)
@@ -2652,8 +2804,8 @@ int lc_open(int device, lc_ctx** out) {
     std::lock_guard<std::mutex> lock(mu);
     if (device < 64 && !done[device]) {
       const int big = (int)kDbStageMax;
-      CK(cudaFuncSetAttribute(k_qtables, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
-      CK(cudaFuncSetAttribute(k_dstables, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+      CK(cudaFuncSetAttribute(k_qtables<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
+      CK(cudaFuncSetAttribute(k_dstables<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big));
       CK(cudaFuncSetAttribute(k_front_final, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)((2 * sizeof(FrontCand) + 8) * kSurvivorCap)));
       done[device] = true;
@@ -3032,9 +3184,10 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     CK(cudaGetLastError());
     return LC_OK;
   };
-  int rc2 = launch_tables(k_qtables, c->n_qt);
+  const bool staged = c->db->staged;
+  int rc2 = launch_tables(staged ? k_qtables<false> : k_qtables<true>, c->n_qt);
   if (rc2) return rc2;
-  rc2 = launch_tables(k_dstables, c->n_ds);
+  rc2 = launch_tables(staged ? k_dstables<false> : k_dstables<true>, c->n_ds);
   if (rc2) return rc2;
   if (c->n_series > 0) {
     int64_t blocks = (c->n_series + 127) / 128;
