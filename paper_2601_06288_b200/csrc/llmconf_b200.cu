@@ -1003,7 +1003,7 @@ __device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta&
 // instead of forming a chain of dependent round trips.  The sum itself is
 // unchanged (table_step's order, skips and first-failure rule).
 #ifndef LC_CELL_MIN_BLOCKS
-#define LC_CELL_MIN_BLOCKS 8  // 64 registers: occupancy beats the few spills (measured)
+#define LC_CELL_MIN_BLOCKS 6  // 80 registers (measured 6 > 7 > 8 blocks/SM since the warp step loops: K2 1.88 -> 1.76 ms)
 #endif
 #ifndef LC_CELL_BUFS
 #define LC_CELL_BUFS 0  // staged steps per thread; 0: unstaged (1 measured neutral, 2 slower: K2 1.93 -> 2.08 / 2.43 ms)
@@ -1380,14 +1380,48 @@ __device__ __forceinline__ void acc_flush(SearchAcc* A, const RowAcc& r) {
   if (r.smin_c) atomicMax(&A->smin_c, r.smin_c);
 }
 
-// One candidate's rows from its cell (derive_metrics with its gpu count,
-// serving_modes.py:161-172; pool rates, serving_modes.py:366, 380) plus its
-// contribution to the per-search accounting.
-__device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search_desc& S, const CellOut& o, int64_t ci,
-                                            int64_t u, int64_t b, int64_t gpus, bool inb, RowAcc& ra,
-                                            unsigned long long* bk, double* seed_at = nullptr) {
+// What a cell's dp variants share: derive_metrics (serving_modes.py:161-172)
+// up to the final division by the gpu count -- speed, and throughput as
+// ((1000 / req) * batch) * osl, the reference's left-to-right order -- the pool
+// rates (serving_modes.py:366, 380) before their division by gpus, and the
+// feasibility tests (speed and TTFT do not depend on gpus).
+struct CellRows {
+  double st_speed, st_tp, ag_speed, ag_tp, pf_rate, dc_rate;
+  bool st_feas, ag_feas, dup;
+};
+__device__ __forceinline__ CellRows cell_rows(const lc_search_desc& S, const CellOut& o, int64_t b) {
+  CellRows R;
+  R.st_speed = R.st_tp = R.ag_speed = R.ag_tp = R.pf_rate = R.dc_rate = 0.0;
+  R.st_feas = R.ag_feas = false;
+  if (o.st_status == 0) {
+    R.st_speed = o.st_tpot == 0.0 ? INFINITY : 1000.0 / o.st_tpot;
+    const double req = o.st_ttft + (double)(S.osl - 1) * o.st_tpot;
+    R.st_tp = 1000.0 / req * (double)b * (double)S.osl;
+    R.st_feas = (!S.has_ttft || o.st_ttft <= S.ttft_limit) && (!S.has_floor || R.st_speed >= S.speed_floor);
+  }
+  if (o.ag_status == 0) {
+    R.ag_speed = o.ag_tpot == 0.0 ? INFINITY : 1000.0 / o.ag_tpot;
+    const double req = o.ag_ttft + (double)(S.osl - 1) * o.ag_tpot;
+    R.ag_tp = 1000.0 / req * (double)b * (double)S.osl;
+    R.ag_feas = (!S.has_ttft || o.ag_ttft <= S.ttft_limit) && (!S.has_floor || R.ag_speed >= S.speed_floor);
+  }
+  if (o.pf_status == 0) R.pf_rate = (double)b * 1000.0 / o.pf_lat;
+  if (o.dc_status == 0) R.dc_rate = S.osl == 1 ? INFINITY : (double)b * 1000.0 / ((double)(S.osl - 1) * o.dc_lat);
+  // the generation step is a memo hit when a static decode step used the same KV length
+  const int64_t k = (S.isl + S.osl / 2) - S.isl - 1;
+  const int64_t sstr = static_stride(S);
+  R.dup = o.st_status == 0 && S.osl > 1 && k >= 0 && (k % sstr) == 0 && (k / sstr) < o.st_steps;
+  return R;
+}
+
+// One candidate's rows from its cell's shared values (CellRows) and its gpu
+// count, plus its contribution to the per-search accounting.
+__device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search_desc& S, const CellOut& o,
+                                            const CellRows& R, int64_t ci, int64_t u, int64_t gpus, bool inb,
+                                            RowAcc& ra, unsigned long long* bk, double* seed_at = nullptr) {
   const int64_t n = P.n_cap;
   const bool do_st = (S.modes & 1) && inb, do_ag = (S.modes & 2) && inb, do_dg = (S.modes & 4) != 0;
+  const double g = (double)gpus;
   int32_t q = 0;
   auto add_q = [&](int32_t x) { q += x; };  // packed halves never overflow 16 bits
   if (do_st) {
@@ -1395,14 +1429,13 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
     if (o.st_status) {
       P.err_c[u] = P.cell_err[ci * 8 + 0]; P.err_c[n + u] = P.cell_err[ci * 8 + 1];
     } else {
-      double speed, thru;
-      derive_metrics(o.st_ttft, o.st_tpot, b, S.osl, gpus, &speed, &thru);
-      P.st_v[u] = o.st_ttft; P.st_v[n + u] = o.st_tpot; P.st_v[2 * n + u] = speed; P.st_v[3 * n + u] = thru;
+      const double thru = R.st_tp / g;
+      P.st_v[u] = o.st_ttft; P.st_v[n + u] = o.st_tpot; P.st_v[2 * n + u] = R.st_speed; P.st_v[3 * n + u] = thru;
       ++ra.rows;
-      if ((!S.has_ttft || o.st_ttft <= S.ttft_limit) && (!S.has_floor || speed >= S.speed_floor)) {
+      if (R.st_feas) {
         ++ra.feas;
-        ra.feasible_speed(speed);
-        if (bk) bucket_max(bk, S, speed, thru);
+        ra.feasible_speed(R.st_speed);
+        if (bk) bucket_max(bk, S, R.st_speed, thru);
       }
       add_q(o.qSD);
     }
@@ -1412,14 +1445,13 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
     if (o.ag_status) {
       P.err_c[2 * n + u] = P.cell_err[ci * 8 + 2]; P.err_c[3 * n + u] = P.cell_err[ci * 8 + 3];
     } else {
-      double speed, thru;
-      derive_metrics(o.ag_ttft, o.ag_tpot, b, S.osl, gpus, &speed, &thru);
-      P.ag_v[u] = o.ag_ttft; P.ag_v[n + u] = o.ag_tpot; P.ag_v[2 * n + u] = speed; P.ag_v[3 * n + u] = thru;
+      const double thru = R.ag_tp / g;
+      P.ag_v[u] = o.ag_ttft; P.ag_v[n + u] = o.ag_tpot; P.ag_v[2 * n + u] = R.ag_speed; P.ag_v[3 * n + u] = thru;
       ++ra.rows;
-      if ((!S.has_ttft || o.ag_ttft <= S.ttft_limit) && (!S.has_floor || speed >= S.speed_floor)) {
+      if (R.ag_feas) {
         ++ra.feas;
-        ra.feasible_speed(speed);
-        if (bk) bucket_max(bk, S, speed, thru);
+        ra.feasible_speed(R.ag_speed);
+        if (bk) bucket_max(bk, S, R.ag_speed, thru);
       }
     }
     add_q(o.qM);
@@ -1432,9 +1464,8 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
       P.pool_key[u] = INFINITY;
       if (seed_at) seed_at[0] = INFINITY;
     } else {
-      const double rate = (double)b * 1000.0 / o.pf_lat;
-      P.pf_v[u] = o.pf_lat; P.pf_v[n + u] = rate;
-      const double r = -rate / (double)gpus;
+      P.pf_v[u] = o.pf_lat; P.pf_v[n + u] = R.pf_rate;
+      const double r = -R.pf_rate / g;
       P.pool_key[u] = r;
       if (seed_at) seed_at[0] = r;
     }
@@ -1444,19 +1475,14 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
       P.pool_key[n + u] = INFINITY;
       if (seed_at) seed_at[1] = INFINITY;
     } else {
-      const double rate = S.osl == 1 ? INFINITY : (double)b * 1000.0 / ((double)(S.osl - 1) * o.dc_lat);
       P.dc_v[u] = o.dc_lat;
-      P.dc_v[n + u] = rate;
-      const double r = -rate / (double)gpus;
+      P.dc_v[n + u] = R.dc_rate;
+      const double r = -R.dc_rate / g;
       P.pool_key[n + u] = r;
       if (seed_at) seed_at[1] = r;
     }
   }
-  // the generation step is a memo hit when a static decode step used the same KV length
-  const int64_t k = (S.isl + S.osl / 2) - S.isl - 1;
-  const int64_t sstr = static_stride(S);
-  const bool dup = do_st && o.st_status == 0 && S.osl > 1 && k >= 0 && (k % sstr) == 0 && (k / sstr) < o.st_steps;
-  if (((do_ag && (o.flags & 1)) || do_dg) && !dup) add_q(o.qG);
+  if (((do_ag && (o.flags & 1)) || do_dg) && !(do_st && R.dup)) add_q(o.qG);
   ra.q1 += (unsigned)(q & 0xffff);
   ra.q2 += (unsigned)(q >> 16);
   if (inb) {
@@ -1666,6 +1692,7 @@ __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, int s
     unsigned long long* bk = fixed_buckets(S) ? P.fbuckets + (int64_t)s * kSpeedBuckets : nullptr;
     const int64_t pbase = (int64_t)s * P.sp_n_combos;
     const int j1 = P.tmpl_cidx_off[tmpl + 1];
+    const CellRows R = cell_rows(S, o, b);
     for (int j = P.tmpl_cidx_off[tmpl]; j < j1; ++j) {
       const int cj = P.tmpl_cidx[j];
       const int64_t pr = pbase + cj;
@@ -1673,7 +1700,7 @@ __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, int s
       if (bi >= cnt) continue;  // this dp variant is not a candidate at this batch
       // the pair's last unit (largest batch) also goes to the K5a seed sample
       double* seed_at = P.pool_sample && bi == cnt - 1 ? P.pool_sample + 2 * pr : nullptr;
-      expand_unit(P, S, o, ci, (int64_t)off + bi, b, P.combos[cj].gpus, P.pair_inb[pr] != 0, ra, bk, seed_at);
+      expand_unit(P, S, o, R, ci, (int64_t)off + bi, P.combos[cj].gpus, P.pair_inb[pr] != 0, ra, bk, seed_at);
     }
   } else {
     P.cells[ci] = o;
@@ -1760,7 +1787,7 @@ __global__ void __launch_bounds__(256, LC_EXPAND_MIN_BLOCKS) k_expand(EvalParams
     const CellOut o = P.cells[ci];
     const int64_t b = P.batches[S.b_off + bi];
     const bool inb = P.u_budget[u] != 0;
-    expand_unit(P, S, o, ci, u, b, c.gpus, inb, ra,
+    expand_unit(P, S, o, cell_rows(S, o, b), ci, u, c.gpus, inb, ra,
                 fixed_buckets(S) ? P.fbuckets + (int64_t)s * kSpeedBuckets : nullptr);
     }
     // per-search accounting for K4 (search.py:343-358 counts, speed range)
@@ -2326,33 +2353,57 @@ __global__ void __launch_bounds__(kPoolThreads) k_pools_partial(EvalParams P, co
   }
 }
 
-__global__ void k_pools_final(EvalParams P, SearchMeta* meta, const PoolPartial* part, int32_t* pool_sel) {
-  const int s = blockIdx.x, tid = threadIdx.x;
+// Per search: the kPoolSplit partial top-k lists of each role merged as a tree
+// (8 warps per role: 2 partials each, then 4 -> 2 -> 1), 5 dependent merges
+// instead of 16 per role; the top-k under the strict total order does not
+// depend on the merge order.
+constexpr int kPoolFinalThreads = 512;
+static_assert(kPoolSplit == 16, "k_pools_final's merge tree assumes 16 partials per search");
+__global__ void __launch_bounds__(kPoolFinalThreads) k_pools_final(EvalParams P, SearchMeta* meta,
+                                                                   const PoolPartial* part, int32_t* pool_sel) {
+  const int s = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const lc_search_desc& S = P.searches[s];
   if (!(S.modes & 4)) return;
-  __shared__ PoolKey red[kPoolThreads];
-  for (int role = 0; role < 2; ++role) {
+  __shared__ PoolKey red[kPoolFinalThreads];
+  __shared__ PoolKey lists[2][8][32];
+  __shared__ int ln[2][8];
+  {
+    const int role = warp >> 3, w = warp & 7;
     const int cap = role == 0 ? S.prefill_cap : S.decode_cap;
-    int got = 0;
-    if (cap <= kPoolLocal) {
-      if (tid < 32) {
-        WarpTopK t;
-        t.init();
-        for (int b = 0; b < kPoolSplit; ++b) {
-          const PoolPartial& pp = part[(int64_t)s * kPoolSplit + b];
-          const int m = pp.n[role];
-          t.merge_sorted(P, tid < m ? pp.k[role][tid] : PoolKey{0.0, 0, -1}, m, cap);
-        }
-        got = t.n;
-        if (tid < got) pool_sel[(int64_t)s * 128 + role * 64 + tid] = t.mine.unit;
-        if (tid == 0) {
-          if (role == 0) meta[s].n_pre = got;
-          else meta[s].n_dec = got;
-        }
+    const bool small = cap <= kPoolLocal;  // uniform per role
+    WarpTopK t;
+    t.init();
+    if (small) {
+      for (int b = 2 * w; b < 2 * w + 2; ++b) {
+        const PoolPartial& pp = part[(int64_t)s * kPoolSplit + b];
+        const int m = pp.n[role];
+        t.merge_sorted(P, lane < m ? pp.k[role][lane] : PoolKey{0.0, 0, -1}, m, cap);
+      }
+      lists[role][w][lane] = t.mine;
+      if (lane == 0) ln[role][w] = t.n;
+    }
+    __syncthreads();
+    for (int width = 4; width >= 1; width >>= 1) {
+      if (small && w < width) t.merge_sorted(P, lists[role][w + width][lane], ln[role][w + width], cap);
+      __syncthreads();
+      if (small && w < width) {
+        lists[role][w][lane] = t.mine;
+        if (lane == 0) ln[role][w] = t.n;
       }
       __syncthreads();
-      continue;
     }
+    if (small && w == 0) {
+      if (lane < t.n) pool_sel[(int64_t)s * 128 + role * 64 + lane] = t.mine.unit;
+      if (lane == 0) {
+        if (role == 0) meta[s].n_pre = t.n;
+        else meta[s].n_dec = t.n;
+      }
+    }
+  }
+  for (int role = 0; role < 2; ++role) {
+    const int cap = role == 0 ? S.prefill_cap : S.decode_cap;
+    if (cap <= kPoolLocal) continue;
+    int got = 0;
     // large caps (33..64): rounds over all units (rare)
     const int32_t u0 = meta[s].unit_off, nu = meta[s].n_units;
     const double* keys = P.pool_key + (int64_t)role * P.n_cap;
@@ -3237,7 +3288,8 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     k_pools_partial<<<dim3(kPoolSplit, c->n_search), kPoolThreads, 0, c->stream>>>(P, (const SearchMeta*)c->meta.p, pp,
                                                                                     seed);
     ++c->launches;
-    k_pools_final<<<c->n_search, kPoolThreads, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, pp, (int32_t*)c->pool_sel.p);
+    k_pools_final<<<c->n_search, kPoolFinalThreads, 0, c->stream>>>(P, (SearchMeta*)c->meta.p, pp,
+                                                                   (int32_t*)c->pool_sel.p);
     CK(cudaGetLastError());
   }
   CK(record_ev(c, 4));
