@@ -263,7 +263,7 @@ struct lc_ctx {
   DBuf searches, batches, batch_code, loads, meta, results;
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
-  DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c;
+  DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c, front_flags;
   DBuf step_in, step_out, step_loads, pool_key, qt_groups, ds_groups, front_compact, pool_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   DBuf q_in, q_lat, q_st;  // lc_query_batch
   DBuf sgroups, smembers, sd;  // shared static decode loops
@@ -360,6 +360,7 @@ struct EvalParams {
   int32_t* pf_status; double* pf_v;  // [2][n_units] lat, rate
   int32_t* dc_status; double* dc_v;
   int64_t* err_c;                    // [8][n_units]: (c0,c1) x (st,ag,pf,dc)
+  uint8_t* front_flags;              // [n_units] bit0 / bit1: the static / aggregated row is SLA-feasible
   double* pool_key;                  // [2][n_cap]: (-rate)/gpus per pool role (search.py:276-277), +inf if skipped
   // cells (search x template x batch)
   const struct TmplInfo* tmpl_info;
@@ -1003,7 +1004,7 @@ __device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta&
 // instead of forming a chain of dependent round trips.  The sum itself is
 // unchanged (table_step's order, skips and first-failure rule).
 #ifndef LC_CELL_MIN_BLOCKS
-#define LC_CELL_MIN_BLOCKS 6  // 80 registers (measured 6 > 7 > 8 blocks/SM since the warp step loops: K2 1.88 -> 1.76 ms)
+#define LC_CELL_MIN_BLOCKS 5  // 96 registers (measured 5 ~ 6 > 7 > 8 > 4 blocks/SM since the warp step loops: K2 1.88 -> 1.71 ms)
 #endif
 #ifndef LC_CELL_BUFS
 #define LC_CELL_BUFS 0  // staged steps per thread; 0: unstaged (1 measured neutral, 2 slower: K2 1.93 -> 2.08 / 2.43 ms)
@@ -1422,6 +1423,7 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
   const int64_t n = P.n_cap;
   const bool do_st = (S.modes & 1) && inb, do_ag = (S.modes & 2) && inb, do_dg = (S.modes & 4) != 0;
   const double g = (double)gpus;
+  int fflags = 0;  // K4 reads these instead of the rows' status / ttft / speed
   int32_t q = 0;
   auto add_q = [&](int32_t x) { q += x; };  // packed halves never overflow 16 bits
   if (do_st) {
@@ -1433,6 +1435,7 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
       P.st_v[u] = o.st_ttft; P.st_v[n + u] = o.st_tpot; P.st_v[2 * n + u] = R.st_speed; P.st_v[3 * n + u] = thru;
       ++ra.rows;
       if (R.st_feas) {
+        fflags |= 1;
         ++ra.feas;
         ra.feasible_speed(R.st_speed);
         if (bk) bucket_max(bk, S, R.st_speed, thru);
@@ -1449,6 +1452,7 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
       P.ag_v[u] = o.ag_ttft; P.ag_v[n + u] = o.ag_tpot; P.ag_v[2 * n + u] = R.ag_speed; P.ag_v[3 * n + u] = thru;
       ++ra.rows;
       if (R.ag_feas) {
+        fflags |= 2;
         ++ra.feas;
         ra.feasible_speed(R.ag_speed);
         if (bk) bucket_max(bk, S, R.ag_speed, thru);
@@ -1483,6 +1487,7 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
     }
   }
   if (((do_ag && (o.flags & 1)) || do_dg) && !(do_st && R.dup)) add_q(o.qG);
+  P.front_flags[u] = (uint8_t)fflags;
   ra.q1 += (unsigned)(q & 0xffff);
   ra.q2 += (unsigned)(q >> 16);
   if (inb) {
@@ -2562,19 +2567,31 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_pass3(EvalParams P, con
   const lc_search_desc& S = P.searches[s];
   const SearchMeta& M = meta[s];
   const int64_t nplan = results[s].n_plans;
-  const int64_t nrows_all = 2 * (int64_t)M.n_units + nplan;
   const unsigned long long* bk = buckets + (int64_t)s * kSpeedBuckets;
-  int64_t lo, hi;
-  slice_of(nrows_all, kSplit, bx, &lo, &hi);
-  for (int64_t r = lo + tid; r < hi; r += blockDim.x) {
-    const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
-    FRONT_ROW_FILTER(v)
-    if (!feasible(S, v)) continue;
-    const int b = fm.fixed ? fixed_bucket(S, v.speed)
-                           : (int)((((unsigned long long)__double_as_longlong(v.speed)) >> fm.shift) - fm.base);
-    if (bk[b] != 0ull && v.thru <= __longlong_as_double((long long)bk[b])) continue;
+  auto test = [&](double speed, double thru, int64_t key) {
+    const int b = fm.fixed ? fixed_bucket(S, speed)
+                           : (int)((((unsigned long long)__double_as_longlong(speed)) >> fm.shift) - fm.base);
+    if (bk[b] != 0ull && thru <= __longlong_as_double((long long)bk[b])) return;
     const int k = atomicAdd(&n_surv[s], 1);
-    if (k < kSurvivorCap) surv[(int64_t)s * kSurvivorCap + k] = FrontCand{v.speed, v.thru, v.key};
+    if (k < kSurvivorCap) surv[(int64_t)s * kSurvivorCap + k] = FrontCand{speed, thru, key};
+  };
+  // unit rows: the feasibility byte written with the rows (expand_unit) -- only the
+  // feasible rows' speed and throughput are read
+  int64_t lo, hi;
+  slice_of(M.n_units, kSplit, bx, &lo, &hi);
+  for (int64_t i = lo + tid; i < hi; i += blockDim.x) {
+    const int64_t u = M.unit_off + i;
+    const int f = P.front_flags[u];
+    if (!f) continue;
+    if (f & 1) test(P.st_v[2 * P.n_cap + u], P.st_v[3 * P.n_cap + u], i);
+    if (f & 2) test(P.ag_v[2 * P.n_cap + u], P.ag_v[3 * P.n_cap + u], ((int64_t)1 << 32) | i);
+  }
+  // plan rows
+  slice_of(nplan, kSplit, bx, &lo, &hi);
+  for (int64_t i = lo + tid; i < hi; i += blockDim.x) {
+    const RowView v = get_row(P, M, plan_i, plan_d, nplan, 2 * (int64_t)M.n_units + i);
+    if (!feasible(S, v)) continue;
+    test(v.speed, v.thru, v.key);
   }
 }
 
@@ -2876,7 +2893,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->batch_code, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->step_in, &c->step_out, &c->step_loads, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch, &c->pool_seed, &c->pool_sample};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->step_in, &c->step_out, &c->step_loads, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch, &c->pool_seed, &c->pool_sample, &c->front_flags};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -3115,6 +3132,7 @@ static EvalParams make_params(lc_ctx* c) {
   P.pf_status = (int32_t*)c->pf_status.p; P.pf_v = (double*)c->pf_v.p;
   P.dc_status = (int32_t*)c->dc_status.p; P.dc_v = (double*)c->dc_v.p;
   P.err_c = (int64_t*)c->err_c.p;
+  P.front_flags = (uint8_t*)c->front_flags.p;
   P.pool_key = (double*)c->pool_key.p;
   P.tmpl_info = sp->tmpl_info;
   P.cell_flags = (uint32_t*)c->cell_flags.p;
@@ -3164,6 +3182,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   c->pf_status.get<int32_t>(n, &err); c->pf_v.get<double>(2 * n, &err);
   c->dc_status.get<int32_t>(n, &err); c->dc_v.get<double>(2 * n, &err);
   c->err_c.get<int64_t>(8 * n, &err);
+  c->front_flags.get<uint8_t>(n, &err);
   c->pool_key.get<double>(2 * n, &err);
   c->cells.get<CellOut>(c->n_cells, &err);
   c->qt.get<double>(c->n_qt, &err);

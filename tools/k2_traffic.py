@@ -34,7 +34,8 @@ for r in rows[hi + 1:]:
         bytes_by[name] += v * scale
 models = 2
 passes = len(launches["k_eval_cells"]) / models
-per_step = sum(bytes_by.values()) / passes * models if passes else None
+# bytes_by sums every launch of both models; one step = one pass of each model
+per_step = sum(bytes_by.values()) / passes if passes else None
 print(json.dumps({"source": sys.argv[1], "kernels": list(K2), "passes_per_model": passes,
                   "dram_bytes_per_step": per_step,
-                  "by_kernel_per_step": {k: v / passes * models for k, v in bytes_by.items()}}, indent=2))
+                  "by_kernel_per_step": {k: v / passes for k, v in bytes_by.items()}}, indent=2))
