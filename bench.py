@@ -251,9 +251,23 @@ def _my_workloads(parts, ws, rank, scaling):
             mine = p.workloads[lo:hi]
         else:
             mine = [dataclasses.replace(w, isl=w.isl + rank) for w in p.workloads] if rank else list(p.workloads)
-        if mine:
-            jobs.append((p.model_name, p, mine))
+        if not mine:
+            continue
+        k = max(1, min(_streams_for(p.model_name), len(mine)))
+        for j in range(k):  # contiguous ISL-major blocks keep the shared tables of an ISL together
+            blk = mine[len(mine) * j // k:len(mine) * (j + 1) // k]
+            if blk:
+                jobs.append((p.model_name if k == 1 else f"{p.model_name}#{j}", p, blk))
     return jobs
+
+
+_STREAMS: dict = {}
+
+
+def _streams_for(model_name: str) -> int:
+    """Pipelines (engines, each on its own stream) per model: the larger model's
+    searches are split into contiguous ISL blocks so the streams finish together."""
+    return int(_STREAMS.get(model_name, _STREAMS.get("*", 1)))
 
 
 def measure(sweep_name: str, args, ws: int, rank: int, dev: int, scaling: str, with_e2e: bool = True) -> dict:
@@ -333,6 +347,7 @@ def measure(sweep_name: str, args, ws: int, rank: int, dev: int, scaling: str, w
     dev_s = _max_over_ranks(ws, sum(step_ms) / 1000.0)
     cands_total = _sum_over_ranks(ws, float(cands_local))
     r = {"sweep": sweep_name, "scaling": scaling, "searches": sum(len(p.workloads) for p in parts),
+         "pipelines": {key: len(wls) for key, _, wls in jobs},
          "candidates": int(cands_total), "candidates_local": cands_local, "q1": q1, "q2": q2,
          "value": cands_total * args.steps / dev_s, "ms_per_step": dev_s * 1000.0 / args.steps,
          "step_ms": step_ms, "kernel_ms": kernel_ms, "launches_per_step": launches_per_step,
@@ -421,10 +436,16 @@ def main() -> int:
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--cpu-steps", type=int, default=6, help="reference-oracle sample steps for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", default="*:2",
+                    help="pipelines per model as name:k[,name:k] ('*:k' for every model); each pipeline is one "
+                         "engine on its own stream over a contiguous ISL block of that model's searches")
     ap.add_argument("--scaling", default="strong", choices=("weak", "strong"),
                     help="strong (default): the fixed sweep is split across ranks; weak: each rank evaluates its "
                          "own config-5-sized block of an N-fold sweep (also reported as an extra field for N > 1)")
     args = ap.parse_args()
+    for item in filter(None, (x.strip() for x in args.streams.split(","))):
+        name, _, k = item.partition(":")
+        _STREAMS[name] = int(k or 1)
 
     from paper_2601_06288_b200.sweeps import sweep
 
@@ -504,7 +525,7 @@ def main() -> int:
         "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": dict(workload_desc, searches=head["searches"] * (ws if args.scaling == "weak" else 1),
-                       candidates=head["candidates"], parallelism=par,
+                       candidates=head["candidates"], parallelism=par, pipelines=head["pipelines"],
                        l2="inputs larger than L2: per-step unit arrays (~1.5 GB written per step) exceed the 126 MB L2"),
         "search_wall_ms": {"device": head["ms_per_step"], "e2e": head["e2e_ms_per_step"],
                            "per_model_sequential_device": float(head["kernel_ms"].sum())},

@@ -54,9 +54,17 @@ struct NeumaierSum {
   __device__ __forceinline__ NeumaierSum() : f(0.0), c(0.0), n(0) {}
   __device__ __forceinline__ void add(double x) {
     if (n++ == 0) { f = 0.0 + x; return; }
+    add_next(x);
+  }
+  // add() once a term has been added: the larger-magnitude operand is selected
+  // before the compensation ((a - t) + b), so the branch costs selects instead
+  // of both arms' subtractions on the FP64 pipe -- the same operations as
+  // CPython's `if fabs(f) >= fabs(x)` arms.
+  __device__ __forceinline__ void add_next(double x) {
     const double t = f + x;
-    if (fabs(f) >= fabs(x)) c += (f - t) + x;
-    else c += (x - t) + f;
+    const bool fx = fabs(f) >= fabs(x);
+    const double a = fx ? f : x, b = fx ? x : f;
+    c += (a - t) + b;
     f = t;
   }
   __device__ __forceinline__ double result() const {

@@ -428,16 +428,28 @@ __global__ void k_scan_blocks(const uint8_t* flags, int64_t n, int32_t* block_su
 }
 
 __global__ void k_scan_top(int32_t* block_sums, int n) {
-  // single block exclusive scan, in place; block_sums[n] = total
-  __shared__ int32_t carry;
+  // single block exclusive scan, in place; block_sums[n] = total.  Tiles of 8
+  // consecutive elements per thread (two coalesced 16-byte loads), a serial scan
+  // in registers, then one block scan of the per-thread totals per tile.
   __shared__ int32_t warp_tot[32];
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int base = 0; base < n; base += blockDim.x) {
-    const int i = base + threadIdx.x;
-    const int v = i < n ? block_sums[i] : 0;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int x = v;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, nw = (int)(blockDim.x >> 5);
+  const bool vec = ((uintptr_t)block_sums & 15) == 0;
+  int carry = 0;
+  for (int base = 0; base < n; base += (int)blockDim.x * 8) {
+    const int i0 = base + tid * 8;
+    int v[8];
+    if (vec && i0 + 8 <= n) {
+      const int4 a = *(const int4*)(block_sums + i0), b = *(const int4*)(block_sums + i0 + 4);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = i0 + k < n ? block_sums[i0 + k] : 0;
+    }
+    int sum = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { const int t = v[k]; v[k] = sum; sum += t; }
+    int x = sum;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
@@ -445,7 +457,8 @@ __global__ void k_scan_top(int32_t* block_sums, int n) {
     if (lane == 31) warp_tot[w] = x;
     __syncthreads();
     if (w == 0) {
-      int t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+      int t = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, t, o);
         if (lane >= o) t += y;
@@ -453,13 +466,19 @@ __global__ void k_scan_top(int32_t* block_sums, int n) {
       warp_tot[lane] = t;
     }
     __syncthreads();
-    const int excl = x - v + (w ? warp_tot[w - 1] : 0) + carry;
-    if (i < n) block_sums[i] = excl;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    const int excl = x - sum + (w ? warp_tot[w - 1] : 0) + carry;
+    if (vec && i0 + 8 <= n) {
+      *(int4*)(block_sums + i0) = make_int4(v[0] + excl, v[1] + excl, v[2] + excl, v[3] + excl);
+      *(int4*)(block_sums + i0 + 4) = make_int4(v[4] + excl, v[5] + excl, v[6] + excl, v[7] + excl);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (i0 + k < n) block_sums[i0 + k] = v[k] + excl;
+    }
+    carry += warp_tot[nw - 1];
     __syncthreads();
   }
-  if (threadIdx.x == 0) block_sums[n] = carry;
+  if (tid == 0) block_sums[n] = carry;
 }
 
 __global__ void k_scatter(EvalParams P, const uint8_t* flags, int64_t n, const int32_t* block_sums, int32_t* pos,
@@ -1264,13 +1283,13 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
           for (int i = 0; i < kPostRegs; ++i) {
             if (i >= npost) break;
 #pragma unroll
-            for (int j = 0; j < kChains; ++j) sc[j].add(post[i]);
+            for (int j = 0; j < kChains; ++j) sc[j].add_next(post[i]);  // the attention term came first
           }
         } else {
           for (int i = gi + 1; i < m; ++i) {
             const double xv = term[i];
 #pragma unroll
-            for (int j = 0; j < kChains; ++j) sc[j].add(xv);
+            for (int j = 0; j < kChains; ++j) sc[j].add_next(xv);
           }
         }
 #pragma unroll
@@ -1949,18 +1968,30 @@ constexpr int kDisSplit = 16;
 __device__ __forceinline__ void disagg_pools(const EvalParams& P, const lc_search_desc& S, const SearchMeta& M,
                                              const int32_t* pool_sel, int s, int32_t* pre, int32_t* dec, int* npre,
                                              int* ndec) {
-  // top-k pools first, then the latency filters (search.py:338-339; serving_modes.py:458-466)
-  int a = 0, d = 0;
-  for (int k = 0; k < M.n_pre; ++k) {
-    const int32_t u = pool_sel[(int64_t)s * 128 + k];
-    if (!S.has_ttft || P.pf_v[u] * S.ttft_headroom <= S.ttft_limit) pre[a++] = u;
+  // top-k pools first, then the latency filters (search.py:338-339; serving_modes.py:458-466).
+  // Called by the whole block: warp 0 filters the prefill pool, warp 1 the decode
+  // pool, 32 candidates at a time, compacted in pool order with a ballot.
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < 2) {
+    const int n = warp == 0 ? M.n_pre : M.n_dec;
+    int32_t* out = warp == 0 ? pre : dec;
+    int cnt = 0;
+    for (int k0 = 0; k0 < n; k0 += 32) {
+      const int k = k0 + lane;
+      bool keep = false;
+      int32_t u = -1;
+      if (k < n) {
+        u = pool_sel[(int64_t)s * 128 + warp * 64 + k];
+        keep = warp == 0 ? (!S.has_ttft || P.pf_v[u] * S.ttft_headroom <= S.ttft_limit)
+                         : (!S.has_floor || P.dc_v[u] <= S.tpot_cap);
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) out[cnt + __popc(m & ((1u << lane) - 1u))] = u;
+      cnt += __popc(m);
+    }
+    if (lane == 0) *(warp == 0 ? npre : ndec) = cnt;
   }
-  for (int k = 0; k < M.n_dec; ++k) {
-    const int32_t u = pool_sel[(int64_t)s * 128 + 64 + k];
-    if (!S.has_floor || P.dc_v[u] <= S.tpot_cap) dec[d++] = u;
-  }
-  *npre = a;
-  *ndec = d;
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(256) k_disagg_pairs(EvalParams P, const SearchMeta* meta, const int32_t* pool_sel,
@@ -1970,8 +2001,7 @@ __global__ void __launch_bounds__(256) k_disagg_pairs(EvalParams P, const Search
   if (!(S.modes & 4) || (S.modes & LC_MODE_NO_PLANS)) return;
   __shared__ int32_t pre[64], dec[64];
   __shared__ int npre, ndec;
-  if (threadIdx.x == 0) disagg_pools(P, S, meta[s], pool_sel, s, pre, dec, &npre, &ndec);
-  __syncthreads();
+  disagg_pools(P, S, meta[s], pool_sel, s, pre, dec, &npre, &ndec);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = blockIdx.y * (blockDim.x >> 5) + warp, nwarp = gridDim.y * (blockDim.x >> 5);
   const int npair = npre * ndec;
@@ -2040,19 +2070,26 @@ __global__ void __launch_bounds__(256) k_disagg(EvalParams P, SearchMeta* meta, 
     if (threadIdx.x == 0) { meta[s].plan_cap = 0; results[s].n_plans = 0; }
     return;
   }
-  if (threadIdx.x == 0) disagg_pools(P, S, meta[s], pool_sel, s, pre, dec, &npre, &ndec);
-  __syncthreads();
+  disagg_pools(P, S, meta[s], pool_sel, s, pre, dec, &npre, &ndec);
   const int npair = npre * ndec;
   __shared__ PlanRec plans[256];
   for (int i = threadIdx.x; i < npair && i < 256; i += blockDim.x) plans[i] = scratch[(int64_t)s * 256 + i];
   __syncthreads();
   // compact in pairing order, then stable rank by (-thru, gpus, ttft, x, y)
   __shared__ int32_t order[256];
-  if (threadIdx.x == 0) {
-    int m = 0;
-    for (int i = 0; i < npair && i < 256; ++i)
-      if (plans[i].p >= 0) order[m++] = i;
-    nplan = m;
+  {
+    // ordered compaction: warp w owns pairings [32w, 32w + 32)
+    __shared__ int wcnt[8];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = threadIdx.x;
+    const bool keep = i < npair && i < 256 && plans[i].p >= 0;
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wcnt[warp] = __popc(m);
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < warp; ++w) base += wcnt[w];
+    if (keep) order[base + __popc(m & ((1u << lane) - 1u))] = i;
+    if (threadIdx.x == 255) nplan = base + __popc(m);
   }
   __syncthreads();
   const int32_t off = meta[s].plan_off;
@@ -2279,18 +2316,32 @@ __device__ __forceinline__ double warp_sort32_d(double v) {
     }
   return v;
 }
-__global__ void k_pools_seed(EvalParams P, double* seed) {
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  const int s = w >> 1, role = w & 1;
-  if (s >= P.n_search) return;
+// 32 smallest of two ascending warp lists (bitonic merge of a with reversed b)
+__device__ __forceinline__ double warp_merge32_d(double a, double b) {
+  const int lane = threadIdx.x & 31;
+  double m = fmin(a, __shfl_sync(0xffffffffu, b, 31 - lane));
+#pragma unroll
+  for (int j = 16; j > 0; j >>= 1) {
+    const double o = __shfl_xor_sync(0xffffffffu, m, j);
+    m = (lane & j) == 0 ? fmin(m, o) : fmax(m, o);
+  }
+  return m;
+}
+// block per (search, role): 8 warps take every 8th chunk of 32 combos, then the
+// warps' ascending 32-lists are merged as a tree in shared memory
+constexpr int kSeedThreads = 256;
+__global__ void __launch_bounds__(kSeedThreads) k_pools_seed(EvalParams P, double* seed) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kSeedThreads / 32;
+  const int s = blockIdx.x >> 1, role = blockIdx.x & 1;
+  __shared__ double lists[kSeedThreads / 32][32];
   const lc_search_desc& S = P.searches[s];
   const int cap = role == 0 ? S.prefill_cap : S.decode_cap;
-  double t = INFINITY;
-  if ((S.modes & 4) && cap > 0 && cap <= kPoolLocal) {
+  const bool on = (S.modes & 4) && cap > 0 && cap <= kPoolLocal;  // block-uniform
+  double best = INFINITY;  // lane j: the j-th smallest so far (ascending)
+  if (on) {
     const int32_t* po = P.pair_off + (int64_t)s * P.sp_n_combos;
     const double* smp = P.pool_sample + (int64_t)s * P.sp_n_combos * 2 + role;
-    double best = INFINITY;  // lane j: the j-th smallest so far (ascending)
-    for (int c0 = 0; c0 < P.sp_n_combos; c0 += 32) {
+    for (int c0 = warp * 32; c0 < P.sp_n_combos; c0 += nw * 32) {
       const int c = c0 + lane;
       double r = INFINITY;
       if (c < P.sp_n_combos && po[c + 1] > po[c]) {
@@ -2298,19 +2349,18 @@ __global__ void k_pools_seed(EvalParams P, double* seed) {
         if (!(r <= INFINITY)) r = INFINITY;  // NaN keys never enter a pool (k_pools_partial)
       }
       if (!__any_sync(0xffffffffu, r != INFINITY)) continue;
-      r = warp_sort32_d(r);
-      // the 32 smallest of best ++ r: bitonic merge of ascending best with descending r
-      double m = fmin(best, __shfl_sync(0xffffffffu, r, 31 - lane));
-#pragma unroll
-      for (int j = 16; j > 0; j >>= 1) {
-        const double o = __shfl_xor_sync(0xffffffffu, m, j);
-        m = (lane & j) == 0 ? fmin(m, o) : fmax(m, o);
-      }
-      best = m;
+      best = warp_merge32_d(best, warp_sort32_d(r));
     }
-    t = __shfl_sync(0xffffffffu, best, cap - 1);
   }
-  if (lane == 0) seed[2 * s + role] = t;
+  lists[warp][lane] = best;
+  __syncthreads();
+  for (int width = nw / 2; width >= 1; width >>= 1) {
+    if (warp < width) best = warp_merge32_d(best, lists[warp + width][lane]);
+    __syncthreads();
+    if (warp < width) lists[warp][lane] = best;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) seed[2 * s + role] = on ? lists[0][cap - 1] : INFINITY;
 }
 
 __global__ void __launch_bounds__(kPoolThreads) k_pools_partial(EvalParams P, const SearchMeta* meta,
@@ -2544,15 +2594,27 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_suffix(const FrontMeta*
   const int s = blockIdx.x, tid = threadIdx.x;
   if (!fmeta[s].any) return;
   unsigned long long* bk = buckets + (int64_t)s * kSpeedBuckets;
-  __shared__ unsigned long long tsuf[kFrontThreads];
+  // exclusive suffix maximum: per-thread runs of `per` buckets, then a warp
+  // shuffle scan and a scan over the warps' maxima for the part above
+  __shared__ unsigned long long wmax[kFrontThreads / 32];
   constexpr int per = kSpeedBuckets / kFrontThreads;
+  const int lane = tid & 31, w = tid >> 5;
   unsigned long long loc[per];
   unsigned long long run = 0;
+#pragma unroll
   for (int j = per - 1; j >= 0; --j) { loc[j] = run; const unsigned long long x = bk[tid * per + j]; run = x > run ? x : run; }
-  tsuf[tid] = run;
+  unsigned long long inc = run;  // inclusive suffix max over lanes >= lane
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_down_sync(0xffffffffu, inc, o);
+    if (lane + o < 32) inc = y > inc ? y : inc;
+  }
+  if (lane == 0) wmax[w] = inc;
+  unsigned long long above = __shfl_down_sync(0xffffffffu, inc, 1);
+  if (lane == 31) above = 0;
   __syncthreads();
-  unsigned long long above = 0;
-  for (int t = tid + 1; t < kFrontThreads; ++t) above = tsuf[t] > above ? tsuf[t] : above;
+  for (int v = w + 1; v < kFrontThreads / 32; ++v) above = wmax[v] > above ? wmax[v] : above;
+#pragma unroll
   for (int j = 0; j < per; ++j) bk[tid * per + j] = loc[j] > above ? loc[j] : above;
 }
 
@@ -3300,7 +3362,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
       double* sd = c->pool_seed.get<double>((size_t)c->n_search * 2, &err);
       if (err != cudaSuccess) return fail(LC_ERR_CUDA, "pool seed allocation");
       ++c->launches;
-      k_pools_seed<<<(2 * c->n_search + 3) / 4, 128, 0, c->stream>>>(P, sd);
+      k_pools_seed<<<2 * c->n_search, kSeedThreads, 0, c->stream>>>(P, sd);
       seed = sd;
     }
 #endif
