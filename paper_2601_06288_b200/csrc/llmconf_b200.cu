@@ -20,6 +20,7 @@
 #include <cmath>
 #include <map>
 #include <mutex>
+#include <chrono>
 #include <string>
 #include <vector>
 
@@ -263,7 +264,7 @@ struct lc_ctx {
   DBuf searches, batches, batch_code, loads, meta, results;
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
-  DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c, front_flags;
+  DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c, front_flags, cell_ctr;
   DBuf step_in, step_out, step_loads, pool_key, qt_groups, ds_groups, front_compact, pool_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   DBuf q_in, q_lat, q_st;  // lc_query_batch
   DBuf sgroups, smembers, sd;  // shared static decode loops
@@ -328,6 +329,8 @@ struct EvalParams {
   double mem_bw, intra_bw, inter_bw, gpu_memory, compute[4];
   int32_t gpn, policy;
   int32_t db_global;                 // database too large to stage: read it from global memory (L1/L2)
+  int32_t surv_cap;                  // K4 survivors kept for the sorted front scan (kSurvivorCap; lower only in tests)
+  unsigned long long* cell_ctr;      // k_eval_cells' chunk counter (zeroed before each launch)
   // space
   const lc_combo* combos; const int32_t* tmpl_n; const lc_entry* entries; int32_t sp_n_combos;
   int64_t hidden, topk, n_experts; int32_t is_moe, n_tp, n_ep;
@@ -534,6 +537,9 @@ __global__ void k_unit_offsets(SearchMeta* meta, int n_search, const int32_t* po
 #ifndef LC_TAIL_MIN_BLOCKS
 #define LC_TAIL_MIN_BLOCKS 3  // 80 registers: no spills of the per-lane expert counts and keys (measured best)
 #endif
+#ifndef LC_TAIL8_MIN_BLOCKS
+#define LC_TAIL8_MIN_BLOCKS 3  // k_tails<8> and up (8 experts per lane)
+#endif
 // ---- K0 in closed form.  fits_memory (model.py:440-479) is monotone in the
 // batch size: the activation term grows with it, so the static footprint grows
 // and the KV budget shrinks, while the KV need grows -- and each step is a
@@ -613,7 +619,8 @@ __global__ void k_unit_offsets_fit(SearchMeta* meta, int n_search, int32_t n_com
 
 // ---- K3: MoE tails table [type P/D/M][tp_i][ep_i][b_i] per search
 template <int PER>
-__global__ void __launch_bounds__(256, LC_TAIL_MIN_BLOCKS) k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
+__global__ void __launch_bounds__(256, PER <= 4 ? LC_TAIL_MIN_BLOCKS : LC_TAIL8_MIN_BLOCKS)
+    k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
   __shared__ int hist_all[8][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* hist = hist_all[warp];
@@ -640,7 +647,8 @@ __global__ void __launch_bounds__(256, LC_TAIL_MIN_BLOCKS) k_tails(EvalParams P,
         ep = P.ep_vals[pair % P.n_ep];
         need = ep > 1 && P.pair_used[pair] && P.pair_canon[pair] == pair &&
                P.m_used[(int64_t)load * (P.m_tmax + 1) + tok];
-        pooled = tok * (ep / tp > 1 ? ep / tp : 1);
+        const int f = (int)ep / (int)tp;  // tp, ep: small positive parallel degrees
+        pooled = tok * (f > 1 ? f : 1);
       } else {
         int lo = 0, hi = P.n_tail_tables - 1;
         while (lo < hi) {
@@ -658,7 +666,8 @@ __global__ void __launch_bounds__(256, LC_TAIL_MIN_BLOCKS) k_tails(EvalParams P,
           need = ep > 1 && P.pair_used[pair] && P.pair_canon[pair] == pair && T.load >= 0;
           const int64_t b = P.batches[T.b_off + bi];
           const int64_t tokens = T.type == 0 ? b * T.chunk : b;
-          pooled = tokens * (ep / tp > 1 ? ep / tp : 1);
+          const int f = (int)ep / (int)tp;
+          pooled = tokens * (f > 1 ? f : 1);
           load = T.load;
         }
       }
@@ -1028,6 +1037,13 @@ __device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta&
 #ifndef LC_CELL_BUFS
 #define LC_CELL_BUFS 0  // staged steps per thread; 0: unstaged (1 measured neutral, 2 slower: K2 1.93 -> 2.08 / 2.43 ms)
 #endif
+#ifndef LC_FUSED_STEPS
+#define LC_FUSED_STEPS 1  // mixed + generation steps in one warp pass (warp_table_step2)
+#endif
+#ifndef LC_CELL_DYNAMIC
+#define LC_CELL_DYNAMIC 1
+#endif
+constexpr int kCellChunk = 512;  // cells per dynamically scheduled chunk of k_eval_cells
 #ifndef LC_WARP_STEPS
 #define LC_WARP_STEPS 1  // warp-cooperative mixed / generation steps in k_eval_cells (warp_table_step)
 #endif
@@ -1101,46 +1117,49 @@ __device__ __forceinline__ void warp_table_step(const EvalParams& P, int s, int 
     const int n_b = P.searches[sg].n_b;
     const lc_entry* E = P.entries + (int64_t)tg * LC_MAX_ENTRIES;
     const int ne = P.tmpl_n[tg];
-    int my_cl = 0;
-    double my_rep = 0.0;
-    long long my_base = -1;
+    // lane j: entry j packed in two words -- coordinate recipe (bits 0-3), a flag
+    // for a repeat count above 2^24 - 1 (bit 4; read from the entry then) and the
+    // repeat (bits 8-31); the query-table index of its slot (int32: n_qt is bounded
+    // at batch set-up) -- so an entry costs three shuffles
+    int my_pk = 0, my_base = -1;
     if (lane < ne) {
       const lc_entry& e = E[lane];
-      my_cl = e.coord | (e.label << 8);
-      my_rep = (double)e.repeat;
+      const bool big = e.repeat < 0 || e.repeat >= (1ll << 24);
+      my_pk = e.coord | (big ? 16 : 0) | (big ? 0 : (int)((uint32_t)e.repeat << 8));
       const int32_t so = P.slot_of[((int64_t)tg * LC_MAX_ENTRIES + lane) * 3 + step];
-      if (so >= 0) my_base = P.meta[sg].qt_off[so >> 16] + (int64_t)(so & 0xffff) * n_b;
+      if (so >= 0) my_base = (int)(P.meta[sg].qt_off[so >> 16] + (int64_t)(so & 0xffff) * n_b);
     }
-    auto fetch = [&](int i) -> double {  // entry i's table value for this lane (0.0 if not needed)
-      const int cl = __shfl_sync(full, my_cl, i & 31);
-      const long long base = __shfl_sync(full, my_base, i & 31);
-      const int coord = cl & 0xff;
+    auto fetch = [&](int i, bool& pres) -> double {  // entry i's table value for this lane
+      const int pk = __shfl_sync(full, my_pk, i & 31);
+      const int base = __shfl_sync(full, my_base, i & 31);
+      const int coord = pk & 15;
       const bool skip = (coord == LC_COORD_CTX && !a.n_ctx) || (coord == LC_COORD_GEN && !a.n_gen);
-      return (act && i < ne && !skip && base >= 0) ? __ldg(P.qt + base + bi) : 0.0;
+      pres = act && i < ne && !skip && base >= 0;
+      return pres ? __ldg(P.qt + base + bi) : 0.0;
     };
-    bool run = act;
-    double v0 = fetch(0), v1 = fetch(1);
+    bool run = act, p0, p1;
+    double v0 = fetch(0, p0), v1 = fetch(1, p1);
     for (int i = 0; i < ne; ++i) {
-      const int cl = __shfl_sync(full, my_cl, i);
-      const double rep = __shfl_sync(full, my_rep, i);
+      const int pk = __shfl_sync(full, my_pk, i);
       const double v = v0;
+      const bool pres = p0;
       v0 = v1;
-      v1 = fetch(i + 2);
-      const int coord = cl & 0xff;
-      if (!run) continue;
-      if (coord == LC_COORD_CTX && !a.n_ctx) continue;
-      if (coord == LC_COORD_GEN && !a.n_gen) continue;
+      p0 = p1;
+      v1 = fetch(i + 2, p1);
+      if (!run || !pres) continue;
+      const int coord = pk & 15;
       const QVal q = unbox(v);
       if (coord == LC_COORD_CTX || coord == LC_COORD_GEN) ++c2; else ++c1;
       if (q.status) {
         int64_t d[5];
         a.expert_tokens = xt();
         entry_coords(E[i], a, P.hidden, d);
-        err->code = q.status; err->label = cl >> 8; err->c0 = d[0]; err->c1 = d[1];
+        err->code = q.status; err->label = E[i].label; err->c0 = d[0]; err->c1 = d[1];
         run = false;
         live = false;
         continue;
       }
+      const double rep = (pk & 16) ? (double)E[i].repeat : (double)((uint32_t)pk >> 8);
       const double ms = div1000(q.lat * rep);
       sum.add(0.0 + ms * bubble);
     }
@@ -1150,6 +1169,106 @@ __device__ __forceinline__ void warp_table_step(const EvalParams& P, int s, int 
     *q1 = c1;
     *q2 = c2;
   }
+}
+
+// The mixed and generation steps of a warp of cells in one pass over the plan
+// entries (warp_table_step for two steps): the two plan-order sums are
+// independent dependency chains, so interleaving them hides each other's FP64
+// latency, and the entry metadata is broadcast once for both.  A lane's
+// generation step may be computed when its result is not used (its mixed step
+// failed): the step is a pure function of the tables, so nothing changes.
+struct StepRes {
+  double total;
+  ErrRec err;
+  int q1, q2;
+};
+template <class XM, class XG>
+__device__ __forceinline__ void warp_table_step2(const EvalParams& P, int s, int tmpl, int bi, bool act_m,
+                                                 StepArgs am, XM xtm, bool act_g, StepArgs ag, XG xtg,
+                                                 double bubble, StepRes& rm, StepRes& rg) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  unsigned pending = __ballot_sync(full, act_m || act_g);
+  NeumaierSum sm, sg;
+  int m1 = 0, m2 = 0, g1 = 0, g2 = 0;
+  bool live_m = act_m, live_g = act_g;
+  auto present = [](int coord, const StepArgs& a) {
+    return !((coord == LC_COORD_CTX && !a.n_ctx) || (coord == LC_COORD_GEN && !a.n_gen));
+  };
+  while (pending) {
+    const int leader = __ffs(pending) - 1;
+    const int sgi = __shfl_sync(full, s, leader), tg = __shfl_sync(full, tmpl, leader);
+    const bool in = s == sgi && tmpl == tg;
+    pending &= ~__ballot_sync(full, in);
+    const int n_b = P.searches[sgi].n_b;
+    const lc_entry* E = P.entries + (int64_t)tg * LC_MAX_ENTRIES;
+    const int ne = P.tmpl_n[tg];
+    const SearchMeta& M = P.meta[sgi];
+    // lane j: entry j as in warp_table_step, with the query-table index of its
+    // slot in each of the two steps
+    int my_pk = 0, my_bm = -1, my_bg = -1;
+    if (lane < ne) {
+      const lc_entry& e = E[lane];
+      const bool big = e.repeat < 0 || e.repeat >= (1ll << 24);
+      my_pk = e.coord | (big ? 16 : 0) | (big ? 0 : (int)((uint32_t)e.repeat << 8));
+      const int32_t* so = P.slot_of + ((int64_t)tg * LC_MAX_ENTRIES + lane) * 3;
+      const int32_t sm_ = so[LC_STEP_MIXED], sg_ = so[LC_STEP_GEN];
+      if (sm_ >= 0) my_bm = (int)(M.qt_off[sm_ >> 16] + (int64_t)(sm_ & 0xffff) * n_b);
+      if (sg_ >= 0) my_bg = (int)(M.qt_off[sg_ >> 16] + (int64_t)(sg_ & 0xffff) * n_b);
+    }
+    bool run_m = live_m && in, run_g = live_g && in;
+    const bool go_m = run_m, go_g = run_g;
+    // entry i's two table values, one entry ahead
+    auto fetch = [&](int i, bool& pm, bool& pg, double& vm, double& vg) {
+      const int pk = __shfl_sync(full, my_pk, i & 31);
+      const int bm = __shfl_sync(full, my_bm, i & 31), bg = __shfl_sync(full, my_bg, i & 31);
+      const int coord = pk & 15;
+      pm = go_m && i < ne && present(coord, am) && bm >= 0;
+      pg = go_g && i < ne && present(coord, ag) && bg >= 0;
+      vm = pm ? __ldg(P.qt + bm + bi) : 0.0;
+      vg = pg ? __ldg(P.qt + bg + bi) : 0.0;
+    };
+    bool pm0, pg0;
+    double vm0, vg0;
+    fetch(0, pm0, pg0, vm0, vg0);
+    for (int i = 0; i < ne; ++i) {
+      const int pk = __shfl_sync(full, my_pk, i);
+      const double vm = vm0, vg = vg0;
+      const bool pm = pm0, pg = pg0;
+      fetch(i + 1, pm0, pg0, vm0, vg0);
+      const int coord = pk & 15;
+      const bool c2d = coord == LC_COORD_CTX || coord == LC_COORD_GEN;
+      const double rep = (pk & 16) ? (double)E[i].repeat : (double)((uint32_t)pk >> 8);
+      if (run_m && pm) {
+        const QVal q = unbox(vm);
+        if (c2d) ++m2; else ++m1;
+        if (q.status) {
+          int64_t d[5];
+          am.expert_tokens = xtm();
+          entry_coords(E[i], am, P.hidden, d);
+          rm.err.code = q.status; rm.err.label = E[i].label; rm.err.c0 = d[0]; rm.err.c1 = d[1];
+          run_m = live_m = false;
+        } else {
+          sm.add(0.0 + div1000(q.lat * rep) * bubble);
+        }
+      }
+      if (run_g && pg) {
+        const QVal q = unbox(vg);
+        if (c2d) ++g2; else ++g1;
+        if (q.status) {
+          int64_t d[5];
+          ag.expert_tokens = xtg();
+          entry_coords(E[i], ag, P.hidden, d);
+          rg.err.code = q.status; rg.err.label = E[i].label; rg.err.c0 = d[0]; rg.err.c1 = d[1];
+          run_g = live_g = false;
+        } else {
+          sg.add(0.0 + div1000(q.lat * rep) * bubble);
+        }
+      }
+    }
+  }
+  if (live_m) { rm.total = sm.result(); rm.q1 = m1; rm.q2 = m2; }
+  if (live_g) { rg.total = sg.result(); rg.q1 = g1; rg.q2 = g2; }
 }
 
 // K2b: static decode loops (serving_modes.py:256-266), one thread per
@@ -1224,6 +1343,7 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
       term[m++] = 0.0 + ms * bubble;
     }
     int mi = 0;  // next member to receive its total (members ascend in n_steps)
+    int trig = G.n_m > 0 ? mem[0].n_steps - 1 : -1;  // ... at this sample
     auto put = [&](int j, double t_gen, int32_t status, int steps, int64_t c0, int64_t c1) {
       const int64_t ci = P.meta[mem[j].search].cell_off + (int64_t)tmpl * S.n_b + bi;
       SdOut o;
@@ -1298,10 +1418,11 @@ __global__ void __launch_bounds__(128, LC_DSERIES_MIN_BLOCKS) k_dseries(EvalPara
           if (sj >= K || (bad >= 0 && j >= bad)) continue;
           const double st = sc[j].result();
           // members whose last sample is sj: t_gen + st * run, run = osl - 1 - stride sj
-          while (mi < G.n_m && mem[mi].n_steps - 1 == sj) {
+          while (sj == trig) {  // the next member's last sample (members ascend in n_steps)
             const int64_t run = P.searches[mem[mi].search].osl - 1 - stride * sj;
             put(mi, t_gen + st * (double)run, 0, mem[mi].n_steps, 0, 0);
             ++mi;
+            trig = mi < G.n_m ? mem[mi].n_steps - 1 : -1;
           }
           t_gen += st * (double)stride;
         }
@@ -1361,6 +1482,9 @@ __global__ void __launch_bounds__(128) k_ptables(EvalParams P) {
 // faster rows sharing the top bucket -- and the maxima are accumulated while the
 // rows are written (k_eval_cells / k_expand / k_disagg), saving K4 a pass over
 // every row.  Without a floor the range pass (k_front_mid / k_front_pass2) runs.
+#ifndef LC_BUCKET_PRECHECK
+#define LC_BUCKET_PRECHECK 0  // 1: a plain read before the atomic -- measured no gain
+#endif
 constexpr int kSpeedBuckets = 4096;
 constexpr int kFixedShift = 44;
 __device__ __forceinline__ bool fixed_buckets(const lc_search_desc& S) {
@@ -1372,7 +1496,12 @@ __device__ __forceinline__ int fixed_bucket(const lc_search_desc& S, double spee
   return d < (unsigned long long)kSpeedBuckets ? (int)d : kSpeedBuckets - 1;  // speed >= floor: no wrap
 }
 __device__ __forceinline__ void bucket_max(unsigned long long* bk, const lc_search_desc& S, double speed, double thru) {
-  atomicMax(&bk[fixed_bucket(S, speed)], (unsigned long long)__double_as_longlong(thru));
+  // most rows do not raise their bucket's maximum once it has settled: a plain
+  // read first keeps them off the (same-address, serialising) L2 atomics
+  unsigned long long* at = &bk[fixed_bucket(S, speed)];
+  const unsigned long long v = (unsigned long long)__double_as_longlong(thru);
+  if (LC_BUCKET_PRECHECK && *(volatile unsigned long long*)at >= v) return;
+  atomicMax(at, v);
 }
 
 // K2: one thread per cell assembles every step from the tables.
@@ -1618,9 +1747,19 @@ __device__ __forceinline__ void eval_cell(const EvalParams& P, int64_t ci, int s
     double l_mix = 0.0;
     ErrRec em{0, 0, 0, 0};
     int m1 = 0, m2 = 0;
+#if LC_FUSED_STEPS
+    // both steps in one pass; the generation step for every lane that may use it
+    StepRes rm{0.0, {0, 0, 0, 0}, 0, 0}, rg{0.0, {0, 0, 0, 0}, 0, 0};
+    warp_table_step2(P, s, tmpl, bi, need_mix, am, xt_mix, (need_mix && (sc.t_gen || b == 1)) || do_dg, ga, xt_dec,
+                     bubble, rm, rg);
+    l_mix = rm.total; em = rm.err; m1 = rm.q1; m2 = rm.q2;
+    g_total = rg.total; g_err = rg.err; q1 = rg.q1; q2 = rg.q2;
+    const bool gen_for_ag = need_mix && !em.code && (sc.t_gen || b == 1);
+#else
     warp_table_step(P, s, tmpl, LC_STEP_MIXED, bi, need_mix, am, xt_mix, bubble, &l_mix, &em, &m1, &m2);
     const bool gen_for_ag = need_mix && !em.code && (sc.t_gen || b == 1);
     warp_table_step(P, s, tmpl, LC_STEP_GEN, bi, gen_for_ag || do_dg, ga, xt_dec, bubble, &g_total, &g_err, &q1, &q2);
+#endif
     const int32_t qg = (q1 & 0xffff) | (q2 << 16);
     if (do_ag) {
       ErrRec e{sc.st, 0, 0, 0};
@@ -1735,11 +1874,10 @@ __global__ void __launch_bounds__(kCellThreads, LC_CELL_MIN_BLOCKS) k_eval_cells
   __shared__ double stage[kCellBufs ? kCellBufs * LC_MAX_ENTRIES * kCellThreads : 1];  // [buffer][entry][thread]
   const int64_t ncell = P.n_cells_total;
   const int lane = threadIdx.x & 31;
-  // each block walks one contiguous range of cells, so a thread's search index only
-  // moves forward (one compare per cell instead of a binary search over the searches)
-  const int64_t per = ((ncell + gridDim.x - 1) / gridDim.x + 127) / 128 * 128;
-  const int64_t beg = (int64_t)blockIdx.x * per, end = beg + per < ncell ? beg + per : ncell;
+  // a thread's search index only moves forward (one compare per cell instead of
+  // a binary search over the searches)
   int hint = -1;
+  auto run_range = [&](int64_t beg, int64_t end) {
   for (int64_t base = beg + threadIdx.x - lane; base < end; base += blockDim.x) {
     const int64_t ci = base + lane;
     RowAcc ra{0, 0, 0, 0, 0, 0, 0ull, 0ull};
@@ -1783,6 +1921,26 @@ __global__ void __launch_bounds__(kCellThreads, LC_CELL_MIN_BLOCKS) k_eval_cells
       acc_flush(P.acc + s, ra);
     }
   }
+  };
+#if LC_CELL_DYNAMIC
+  // chunks of kCellChunk cells handed out in order by a counter (the per-cell
+  // cost varies with the cell flags, so static ranges leave a tail); a block's
+  // chunks ascend, so its search index still only moves forward
+  __shared__ long long next;
+  for (;;) {
+    if (threadIdx.x == 0) next = (long long)atomicAdd(P.cell_ctr, 1ull);
+    __syncthreads();
+    const int64_t beg = (int64_t)next * kCellChunk;
+    __syncthreads();
+    if (beg >= ncell) break;
+    run_range(beg, beg + kCellChunk < ncell ? beg + kCellChunk : ncell);
+  }
+#else
+  // each block walks one contiguous range of cells
+  const int64_t per = ((ncell + gridDim.x - 1) / gridDim.x + 127) / 128 * 128;
+  const int64_t beg = (int64_t)blockIdx.x * per;
+  run_range(beg, beg + per < ncell ? beg + per : ncell);
+#endif
 }
 
 // K2b: candidates from their cells -- derive_metrics with the candidate's gpu
@@ -1877,6 +2035,10 @@ constexpr int kPoolLocal = 32;  // caps up to 32 take the fast path (one list el
 #define LC_POOL_THREADS 256
 #endif
 constexpr int kPoolThreads = LC_POOL_THREADS;
+#ifndef LC_POOL_UNROLL
+#define LC_POOL_UNROLL 1  // 4: slower (K5a 0.22 -> 0.28 ms): the merges, not the loads, bound the pass
+#endif
+constexpr int kPoolUnroll = LC_POOL_UNROLL;  // key chunks in flight per warp in k_pools_partial
 
 __device__ __forceinline__ bool pool_before(const EvalParams& P, const PoolKey& a, const PoolKey& b) {
   if (a.unit < 0) return false;
@@ -2385,24 +2547,41 @@ __global__ void __launch_bounds__(kPoolThreads) k_pools_partial(EvalParams P, co
     // not after the current cap-th element (r <= thr; exact order in the merge).  The
     // threshold starts at the search's seed (k_pools_seed): with it most chunks hold
     // no candidate and cost one coalesced load.
+    // Each warp takes kPoolUnroll consecutive chunks per step and issues their
+    // loads together (memory-level parallelism; the test needs only the key).
     double thr = seed ? seed[2 * s + role] : INFINITY;
-    for (int64_t base = lo + (int64_t)warp * 32; base < hi; base += kPoolThreads) {
-      const int64_t i = base + lane;
-      const double r = i < hi ? keys[u0 + i] : INFINITY;  // INFINITY: pool candidate skipped
-      const bool cand = r != INFINITY && r <= thr;
-      if (!__any_sync(0xffffffffu, cand)) continue;
-      tk.merge_chunk(P, cand ? pool_key_of(P, S, r, (int32_t)(u0 + i)) : PoolKey{0.0, 0, -1}, cap);
-      thr = fmin(thr, tk.thr_r(cap));
+    for (int64_t base = lo + (int64_t)warp * 32 * kPoolUnroll; base < hi; base += kPoolThreads * kPoolUnroll) {
+      double r[kPoolUnroll];
+#pragma unroll
+      for (int k = 0; k < kPoolUnroll; ++k) {
+        const int64_t i = base + 32 * k + lane;
+        r[k] = i < hi ? keys[u0 + i] : INFINITY;  // INFINITY: pool candidate skipped
+      }
+#pragma unroll
+      for (int k = 0; k < kPoolUnroll; ++k) {
+        const bool cand = r[k] != INFINITY && r[k] <= thr;
+        if (!__any_sync(0xffffffffu, cand)) continue;
+        const int64_t i = base + 32 * k + lane;
+        tk.merge_chunk(P, cand ? pool_key_of(P, S, r[k], (int32_t)(u0 + i)) : PoolKey{0.0, 0, -1}, cap);
+        thr = fmin(thr, tk.thr_r(cap));
+      }
     }
     wout[warp][lane] = tk.mine;
     if (lane == 0) wn[warp] = tk.n;
     __syncthreads();
+    // the warps' lists merged as a tree
+    for (int width = kWarps / 2; width >= 1; width >>= 1) {
+      if (warp < width) tk.merge_sorted(P, wout[warp + width][lane], wn[warp + width], cap);
+      __syncthreads();
+      if (warp < width) {
+        wout[warp][lane] = tk.mine;
+        if (lane == 0) wn[warp] = tk.n;
+      }
+      __syncthreads();
+    }
     if (warp == 0) {
-      WarpTopK t2;
-      t2.init();
-      for (int w = 0; w < kWarps; ++w) t2.merge_sorted(P, wout[w][lane], wn[w], cap);
-      if (lane < t2.n) dst->k[role][lane] = t2.mine;
-      if (lane == 0) dst->n[role] = t2.n;
+      if (lane < tk.n) dst->k[role][lane] = tk.mine;
+      if (lane == 0) dst->n[role] = tk.n;
     }
     __syncthreads();
   }
@@ -2635,7 +2814,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_pass3(EvalParams P, con
                            : (int)((((unsigned long long)__double_as_longlong(speed)) >> fm.shift) - fm.base);
     if (bk[b] != 0ull && thru <= __longlong_as_double((long long)bk[b])) return;
     const int k = atomicAdd(&n_surv[s], 1);
-    if (k < kSurvivorCap) surv[(int64_t)s * kSurvivorCap + k] = FrontCand{speed, thru, key};
+    if (k < P.surv_cap) surv[(int64_t)s * kSurvivorCap + k] = FrontCand{speed, thru, key};
   };
   // unit rows: the feasibility byte written with the rows (expand_unit) -- only the
   // feasible rows' speed and throughput are read
@@ -2673,7 +2852,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_front_final(EvalParams P, con
   FrontCand* staged = sorted + kSurvivorCap;                // kSurvivorCap
   int64_t* keys_out = (int64_t*)(staged + kSurvivorCap);    // kSurvivorCap
   __shared__ double dred[32];
-  __shared__ int nfront;
+  __shared__ int nfront, nlvl;
   const lc_search_desc& S = P.searches[s];
   const SearchMeta& M = meta[s];
   const int64_t nplan = results[s].n_plans;
@@ -2681,7 +2860,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_front_final(EvalParams P, con
   const int64_t foff = (int64_t)M.unit_off * 2 + M.plan_off;
   const int nsv = n_surv[s];
   if (tid == 0) results[s].n_survivors = nsv;
-  if (nsv <= kSurvivorCap) {
+  if (nsv <= P.surv_cap) {
     // bitonic sort of the survivors by (speed desc, row key asc), padded to a power of two
     const FrontCand* svg = surv + (int64_t)s * kSurvivorCap;
     int np2 = 1;
@@ -2700,20 +2879,40 @@ __global__ void __launch_bounds__(kFinalThreads) k_front_final(EvalParams P, con
             if (up != a_first) { sorted[i] = b; sorted[l] = a; }
           }
         }
-        __syncthreads();
+        // a distance below 32 pairs elements of one warp (i = tid + r * blockDim):
+        // a warp barrier suffices unless this or the next substep crosses warps
+        const int jn = j > 1 ? j >> 1 : k;  // the next substep's distance
+        if (j >= 32 || jn >= 32) __syncthreads();
+        else __syncwarp();
       }
     }
-    // group maxima and the running maximum of all faster rows, in parallel
-    double* pm = (double*)staged;  // inclusive prefix max of thru over sorted order
-    for (int i = tid; i < nsv; i += blockDim.x) pm[i] = sorted[i].thru;
     __syncthreads();
-    for (int off = 1; off < nsv; off <<= 1) {
-      double v[8];
-      int c = 0;
-      for (int i = tid; i < nsv; i += blockDim.x, ++c) v[c & 7] = (i >= off) ? fmax(pm[i], pm[i - off]) : pm[i];
+    // group maxima and the running maximum of all faster rows, in parallel
+    // inclusive prefix max of thru over sorted order: runs of consecutive elements
+    // per thread, a warp shuffle scan and a scan over the warps' maxima
+    double* pm = (double*)staged;
+    {
+      __shared__ double wmx[kFinalThreads / 32];
+      const int lane = tid & 31, wid = tid >> 5;
+      const int per = (nsv + (int)blockDim.x - 1) / (int)blockDim.x;
+      const int a0 = tid * per, a1 = a0 + per < nsv ? a0 + per : nsv;
+      double run = -INFINITY;
+      for (int i = a0; i < a1; ++i) run = fmax(run, sorted[i].thru);
+      double inc = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc = fmax(inc, y);
+      }
+      if (lane == 31) wmx[wid] = inc;
+      double ex = __shfl_up_sync(0xffffffffu, inc, 1);
+      if (lane == 0) ex = -INFINITY;
       __syncthreads();
-      c = 0;
-      for (int i = tid; i < nsv; i += blockDim.x, ++c) pm[i] = v[c & 7];
+      for (int w = 0; w < wid; ++w) ex = fmax(ex, wmx[w]);
+      for (int i = a0; i < a1; ++i) {
+        ex = fmax(ex, sorted[i].thru);
+        pm[i] = ex;
+      }
       __syncthreads();
     }
     int* flag = (int*)keys_out;  // front membership, then output positions
@@ -2769,11 +2968,22 @@ __global__ void __launch_bounds__(kFinalThreads) k_front_final(EvalParams P, con
     __shared__ BestKey wbest[kFinalThreads];
     wbest[tid] = best;
     __syncthreads();
+    if (tid < 32) {
+      // warp 0 finds the threads holding a candidate by ballots; lane 0 compares them
+      for (int base = 0; base < (int)blockDim.x; base += 32) {
+        unsigned m = __ballot_sync(0xffffffffu, wbest[base + tid].key >= 0);
+        if (tid == 0) {
+          while (m) {
+            const int t = base + __ffs(m) - 1;
+            m &= m - 1;
+            if (best_less(P, M, plan_i, wbest[t], best)) best = wbest[t];
+          }
+        }
+      }
+    }
     if (tid == 0) {
       int m = 0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m += wsum[w];
-      for (int t = 0; t < (int)blockDim.x; ++t)
-        if (wbest[t].key >= 0 && best_less(P, M, plan_i, wbest[t], best)) best = wbest[t];
       results[s].n_front = m;
       results[s].best = best.key;
       results[s].best_thru = best.key >= 0 ? -best.nthru : 0.0;
@@ -2805,7 +3015,53 @@ __global__ void __launch_bounds__(kFinalThreads) k_front_final(EvalParams P, con
       if (v.speed == sp) tmax = fmax(tmax, v.thru);
     }
     const double top = block_max(tmax, dred);
-    if (tid == 0) {
+    // this level's rows (speed sp, throughput top), collected in parallel and
+    // emitted in row order (row order is key order); a level with more ties
+    // than the buffer holds is emitted by one thread scanning the rows
+    int64_t* lvl = (int64_t*)fsm2;  // the fast path's sort buffers are free here
+    constexpr int kLevelCap = 8192;  // a power of two (the sort pads to one) within the 112 KB buffer
+    static_assert(kLevelCap * sizeof(int64_t) <= (2 * sizeof(FrontCand) + 8) * kSurvivorCap, "level buffer");
+    if (tid == 0) nlvl = 0;
+    __syncthreads();
+    for (int64_t r = tid; r < nrows_all; r += blockDim.x) {
+      const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
+      FRONT_ROW_FILTER(v)
+      if (!feasible(S, v)) continue;
+      if (v.speed == sp && v.thru == top) {
+        const int k = atomicAdd(&nlvl, 1);
+        if (k < kLevelCap) lvl[k] = v.key;
+      }
+    }
+    __syncthreads();
+    const int nl = nlvl;
+    if (nl <= kLevelCap) {
+      int np2 = 1;
+      while (np2 < nl) np2 <<= 1;
+      for (int i = nl + tid; i < np2; i += blockDim.x) lvl[i] = INT64_MAX;
+      __syncthreads();
+      for (int k = 2; k <= np2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int i = tid; i < np2; i += blockDim.x) {
+            const int l = i ^ j;
+            if (l > i) {
+              const int64_t a = lvl[i], b = lvl[l];
+              if (((i & k) == 0) == (a > b)) { lvl[i] = b; lvl[l] = a; }
+            }
+          }
+          __syncthreads();
+        }
+      if (tid == 0) {
+        for (int i = 0; i < nl; ++i) {
+          const int64_t key = lvl[i];
+          const int mode = (int)(key >> 32);
+          if (nfront < kCompactFront) compact[(int64_t)s * kCompactFront + nfront] = key;
+          front[foff + nfront++] = key;
+          const int64_t g = mode == 2 ? (int64_t)plan_d[(M.plan_off + (key & 0xffffffffll)) * 6 + 0] : -1;
+          const BestKey k{-top, -sp, g, mode_rank(mode), key};
+          if (best_less(P, M, plan_i, k, obest)) obest = k;
+        }
+      }
+    } else if (tid == 0) {
       for (int64_t r = 0; r < nrows_all; ++r) {
         const RowView v = get_row(P, M, plan_i, plan_d, nplan, r);
         FRONT_ROW_FILTER(v)
@@ -2955,7 +3211,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->batch_code, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->step_in, &c->step_out, &c->step_loads, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch, &c->pool_seed, &c->pool_sample, &c->front_flags};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->step_in, &c->step_out, &c->step_loads, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch, &c->pool_seed, &c->pool_sample, &c->front_flags, &c->cell_ctr};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -3149,6 +3405,11 @@ static EvalParams make_params(lc_ctx* c) {
   for (int i = 0; i < 4; ++i) P.compute[i] = db->compute[i];
   P.gpn = db->gpn; P.policy = db->policy;
   P.db_global = db->staged ? 0 : 1;
+  {
+    // LC_SURVIVOR_CAP (tests only) lowers the cap so small searches take K4's overflow path
+    static const int cap_env = getenv("LC_SURVIVOR_CAP") ? atoi(getenv("LC_SURVIVOR_CAP")) : 0;
+    P.surv_cap = cap_env > 0 && cap_env < kSurvivorCap ? cap_env : kSurvivorCap;
+  }
   P.combos = sp->combos; P.tmpl_n = sp->tmpl_n; P.entries = sp->entries; P.sp_n_combos = sp->n_combos;
   P.hidden = sp->hidden; P.topk = sp->topk; P.n_experts = sp->n_experts; P.is_moe = sp->is_moe;
   P.n_tp = sp->n_tp; P.n_ep = sp->n_ep; P.tp_vals = sp->tp_vals; P.ep_vals = sp->ep_vals; P.pair_used = sp->pair_used;
@@ -3195,6 +3456,7 @@ static EvalParams make_params(lc_ctx* c) {
   P.dc_status = (int32_t*)c->dc_status.p; P.dc_v = (double*)c->dc_v.p;
   P.err_c = (int64_t*)c->err_c.p;
   P.front_flags = (uint8_t*)c->front_flags.p;
+  P.cell_ctr = (unsigned long long*)c->cell_ctr.p;
   P.pool_key = (double*)c->pool_key.p;
   P.tmpl_info = sp->tmpl_info;
   P.cell_flags = (uint32_t*)c->cell_flags.p;
@@ -3245,6 +3507,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
   c->dc_status.get<int32_t>(n, &err); c->dc_v.get<double>(2 * n, &err);
   c->err_c.get<int64_t>(8 * n, &err);
   c->front_flags.get<uint8_t>(n, &err);
+  c->cell_ctr.get<unsigned long long>(1, &err);
   c->pool_key.get<double>(2 * n, &err);
   c->cells.get<CellOut>(c->n_cells, &err);
   c->qt.get<double>(c->n_qt, &err);
@@ -3339,6 +3602,7 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     int64_t blocks = (c->n_cells + 127) / 128;
     if (blocks > (int64_t)sms * 16) blocks = (int64_t)sms * 16;
     ++c->launches;
+    CK(cudaMemsetAsync(c->cell_ctr.p, 0, sizeof(unsigned long long), c->stream));
     k_eval_cells<<<(int)blocks, 128, 0, c->stream>>>(P);
     CK(cudaGetLastError());
   }
@@ -3581,6 +3845,12 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
                     const double* loads, lc_search_result* results, lc_batch_totals* totals) {
   if (!c || !db || !sp || (n_search > 0 && !searches) || n_search < 0)
     return fail(LC_ERR_ARG, "lc_search_batch: bad arguments");
+  // LC_HOST_TIMING=1: host-side phases of the call on stderr (plan / launch / wait)
+  static const bool host_timing = getenv("LC_HOST_TIMING") != nullptr;
+  const auto t_in = std::chrono::steady_clock::now();
+  auto ms_since = [](std::chrono::steady_clock::time_point a) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+  };
   CK(cudaSetDevice(c->device));
   c->staged = false;
   c->db = db;
@@ -3796,6 +4066,9 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   if (sp->is_moe && n_loads > 0 && c->m_tmax > 0) tails += (int64_t)n_loads * sp->n_tp * sp->n_ep * (c->m_tmax + 1);
   c->n_raw = raw;
   c->n_cells = cells;
+  if (qts > INT32_MAX || dss > INT32_MAX)
+    return fail(LC_ERR_ARG, "batch too large: more than 2^31-1 query-table entries in one lc_search_batch call; "
+                            "split the workloads over several calls");
   c->n_qt = qts;
   c->n_ds = dss;
   c->n_tails = tails;
@@ -3851,8 +4124,10 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     }
     c->arena_used = off;
   }
+  const double t_plan = host_timing ? ms_since(t_in) : 0.0;
   int rc = launch_pipeline(c, totals);
   if (rc) return rc;
+  const double t_launch = host_timing ? ms_since(t_in) : 0.0;
   // compact fronts and plan slots ride the same synchronisation as the summaries
   // (page-locked staging; lc_fetch then serves them from host memory)
   c->staged = false;
@@ -3897,6 +4172,9 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   CK(cudaMemcpyAsync(ptotal, (const int32_t*)c->block_sums.p + c->n_total_idx, sizeof(int32_t),
                      cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  if (host_timing)
+    fprintf(stderr, "lc_search_batch: %d searches, planned %.3f ms, launched %.3f ms, synchronised %.3f ms\n",
+            n_search, t_plan, t_launch, ms_since(t_in));
   if (n_search) {
     memcpy(c->hres.data(), pres, sizeof(lc_search_result) * n_search);
     memcpy(c->hmeta.data(), pmeta, sizeof(SearchMeta) * n_search);
