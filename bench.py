@@ -436,7 +436,7 @@ def main() -> int:
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--cpu-steps", type=int, default=6, help="reference-oracle sample steps for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--streams", default="*:2",
+    ap.add_argument("--streams", default="*:1",
                     help="pipelines per model as name:k[,name:k] ('*:k' for every model); each pipeline is one "
                          "engine on its own stream over a contiguous ISL block of that model's searches")
     ap.add_argument("--scaling", default="strong", choices=("weak", "strong"),

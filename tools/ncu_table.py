@@ -12,8 +12,10 @@ import io
 import subprocess
 import sys
 
-rep = sys.argv[1]
-peak = float(sys.argv[2]) if len(sys.argv) > 2 else 6650.0
+args = [a for a in sys.argv[1:] if not a.startswith("--json=")]
+json_out = next((a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--json=")), None)
+rep = args[0]
+peak = float(args[1]) if len(args) > 1 else 6553.6
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
@@ -42,6 +44,7 @@ def unit_scale(name, to):
 
 stall_cols = [n for n in hdr if n.startswith("smsp__average_warps_issue_stalled_") and n.endswith(".ratio")]
 seen = set()
+table = {}
 print(f"# Per-kernel ncu evidence ({rep.split('/')[-1]}; first launch of each kernel; HBM peak {peak:.0f} GB/s)\n")
 print("| kernel | µs | DRAM GB/s | % HBM peak | L2 GB/s | SM % | FP64 pipe % | occupancy % | warp eff. (of 32) | top stall (cycles per issue) |")
 print("|---|---|---|---|---|---|---|---|---|---|")
@@ -62,6 +65,18 @@ for r in data:
         v = val(r, n)
         if v is not None and v > best and "selected" not in n:
             best, bname = v, n.split("stalled_")[-1].replace("_per_issue_active.ratio", "") + f" ({v:.1f})"
+    issue = val(r, "smsp__issue_active.avg.pct_of_peak_sustained_active")
+    table[name] = {"us": dur, "dram_gbs": dram, "dram_frac_of_peak": None if dram is None else dram / peak,
+                   "l2_gbs": l2, "sm_pct": sm, "fp64_pipe_pct": fp64, "warps_active_pct": occ,
+                   "issue_active_pct": issue, "active_threads_per_warp": eff, "top_stall": bname,
+                   "dram_bytes": sum((val(r, n) or 0) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(
+                       units[col[n]] if n in col else "byte", 1) for n in ("dram__bytes_read.sum", "dram__bytes_write.sum"))}
     f = lambda x, d=1: "–" if x is None else f"{x:.{d}f}"
     print(f"| {name} | {f(dur)} | {f(dram, 0)} | {f(None if dram is None else 100 * dram / peak)} | {f(l2, 0)} | "
           f"{f(sm)} | {f(fp64)} | {f(occ)} | {f(eff)} | {bname} |")
+
+if json_out:
+    import json
+
+    with open(json_out, "w") as fh:
+        json.dump({"source": rep.split("/")[-1], "hbm_peak_gbs": peak, "kernels": table}, fh, indent=1)
