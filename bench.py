@@ -310,6 +310,15 @@ def measure(sweep_name: str, args, ws: int, rank: int, dev: int, scaling: str, w
 
     for _ in range(max(args.warmup, 1)):
         e2e_step()
+    if args.priority == "auto" and len(engines) > 1:
+        # the pipeline with the most candidates gets the highest stream priority, so
+        # the longest chain claims free SMs first and the others fill around it
+        sizes = {key: int(engines[key].run_batch(p.db, p.model, p.space, wls).results["n_enumerated"].sum())
+                 for key, p, wls in jobs}
+        for rank_i, key in enumerate(sorted(sizes, key=lambda k: -sizes[k])):
+            engines[key].set_priority(-(len(sizes) - 1 - rank_i))
+        for _ in range(max(args.warmup, 1)):
+            e2e_step()
     outs = {key: engines[key].run_batch(p.db, p.model, p.space, wls) for key, p, wls in jobs}
     cands_local = sum(int(o.results["n_enumerated"].sum()) for o in outs.values())
     q1 = sum(int(o.results["queries_1d"].sum()) for o in outs.values())
@@ -436,6 +445,12 @@ def main() -> int:
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--cpu-steps", type=int, default=6, help="reference-oracle sample steps for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--priority", default="none", choices=("auto", "none"),
+                    help="auto: stream priority by pipeline size (largest highest, lc_set_priority); measured no "
+                         "gain on config 5, so off by default")
+    ap.add_argument("--ns-streams", default="*:2",
+                    help="--streams for the north-star sweep (2 per model measured 2.31 -> 2.27 ms device, "
+                         "3.50 -> 3.27 ms e2e; on config 5 one per model is best)")
     ap.add_argument("--streams", default="*:1",
                     help="pipelines per model as name:k[,name:k] ('*:k' for every model); each pipeline is one "
                          "engine on its own stream over a contiguous ISL block of that model's searches")
@@ -443,9 +458,11 @@ def main() -> int:
                     help="strong (default): the fixed sweep is split across ranks; weak: each rank evaluates its "
                          "own config-5-sized block of an N-fold sweep (also reported as an extra field for N > 1)")
     args = ap.parse_args()
-    for item in filter(None, (x.strip() for x in args.streams.split(","))):
-        name, _, k = item.partition(":")
-        _STREAMS[name] = int(k or 1)
+    def set_streams(spec: str) -> None:
+        _STREAMS.clear()
+        for item in filter(None, (x.strip() for x in spec.split(","))):
+            name, _, k = item.partition(":")
+            _STREAMS[name] = int(k or 1)
 
     from paper_2601_06288_b200.sweeps import sweep
 
@@ -488,10 +505,13 @@ def main() -> int:
     dev = local if ws > 1 else 0
     clocks = ClockSampler(dev)
     clocks.start()
+    set_streams(args.streams)
     head = measure(args.sweep, args, ws, rank, dev, args.scaling)
     ns = None
     if args.north_star and args.north_star != "none" and args.north_star != args.sweep:
+        set_streams(args.ns_streams)
         ns = measure(args.north_star, args, ws, rank, dev, args.scaling)
+        set_streams(args.streams)
     weak = None
     if ws > 1 and args.scaling == "strong":
         weak = measure(args.sweep, args, ws, rank, dev, "weak", with_e2e=False)
@@ -541,7 +561,7 @@ def main() -> int:
             "sweep": ns["sweep"], "models": ns["models"], "searches": ns["searches"],
             "candidates": ns["candidates"], "value": ns["value"], "unit": UNIT, "ms_per_step": ns["ms_per_step"],
             "e2e": ns["e2e"], "e2e_ms_per_step": ns["e2e_ms_per_step"], "best_found": ns["best_found"],
-            "gpu_launches": ns["launches_per_step"] * args.steps,
+            "gpu_launches": ns["launches_per_step"] * args.steps, "pipelines": ns["pipelines"],
             "target": "10^7-candidate Qwen3-32B + DeepSeek-V3 search in under 1 s on 8xB200",
             "roofline": {k: v for k, v in roofline(ns).items() if k in ("achieved", "frac", "stage_ms",
                                                                           "algorithmic_bytes_per_launch",

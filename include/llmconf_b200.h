@@ -259,6 +259,12 @@ int lc_unit_raw(lc_ctx* ctx, int32_t n, const int32_t* units, int64_t* raw);
  * against it (e.g. CUDA events across several contexts). */
 int lc_stream(lc_ctx* ctx, void** stream);
 
+/* Scheduling priority of the context's stream (and of the kernels of the batch
+ * graphs captured on it from now on): 0 is the default, negative values are
+ * higher priority, clamped to the device's range.  Several contexts sharing one
+ * GPU can so give the longest pipeline first claim on free SMs. */
+int lc_set_priority(lc_ctx* ctx, int priority);
+
 /* ------------------------------------------------ single-operator queries */
 /* One query_latency(db, query, policy) call (perfdb.py:539-580).  The host
  * resolves the query's grid key (OperatorQuery.grid_key, perfdb.py:239-244) to a

@@ -144,7 +144,7 @@ assert QUERY_DTYPE.itemsize == 64
 EXPORTED = ("lc_abi_version", "lc_last_error", "lc_open", "lc_close", "lc_db_upload", "lc_db_free",
             "lc_space_upload", "lc_space_free", "lc_search_batch", "lc_fetch", "lc_replay_last", "lc_replay_async",
             "lc_stream", "lc_query_batch", "lc_dbgen", "lc_set_raw_filter", "lc_fetch_pools",
-            "lc_unit_raw", "lc_report_rows", "lc_step_latency")
+            "lc_unit_raw", "lc_report_rows", "lc_step_latency", "lc_set_priority")
 
 _LIB = None
 
@@ -172,6 +172,7 @@ def load_library(path: str | os.PathLike | None = None):
     lib.lc_replay_last.argtypes = [C.c_void_p, C.c_int32, C.POINTER(LcBatchTotals)]
     lib.lc_replay_async.argtypes = [C.c_void_p]
     lib.lc_stream.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+    lib.lc_set_priority.argtypes = [C.c_void_p, C.c_int]
     lib.lc_dbgen.argtypes = [C.c_void_p, C.POINTER(LcDbgenDesc), F64P, F64P, I32P]
     lib.lc_query_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, F64P, I32P]
     lib.lc_set_raw_filter.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p]

@@ -276,7 +276,13 @@ __device__ __forceinline__ void derive_metrics(double ttft, double tpot, int64_t
   *thru = 1000.0 / req * (double)batch * (double)osl / (double)gpus;
 }
 
-__device__ __forceinline__ int64_t ceil_div_f(int64_t a, int64_t b) { return (int64_t)ceil((double)a / (double)b); }
+// math.ceil(a / b) with float division (the reference's ceil(x / y) on ints);
+// a power-of-two b divides by an exact multiply (the same correctly rounded value)
+__device__ __forceinline__ int64_t ceil_div_f(int64_t a, int64_t b) {
+  if (b > 0 && (b & (b - 1)) == 0 && b < (1ll << 52))
+    return (int64_t)ceil((double)a * __longlong_as_double((long long)(1023 - (__ffsll(b) - 1)) << 52));
+  return (int64_t)ceil((double)a / (double)b);
+}
 
 // Aggregated-mode schedule (serving_modes.py:292-320): returns status and the
 // mixed-step shape.

@@ -20,6 +20,7 @@
 #include <cmath>
 #include <map>
 #include <mutex>
+#include <array>
 #include <chrono>
 #include <string>
 #include <vector>
@@ -253,6 +254,9 @@ struct SearchAcc {
   unsigned long long q1, q2, smin_c, smax;
   int32_t feas, rows, enums, skips, fplans, _pad;
 };
+
+// fixed-size keys of the host-side table grouping (lc_search_batch)
+using Key5 = std::array<int64_t, 5>;
 
 struct lc_ctx {
   int device;
@@ -1563,6 +1567,20 @@ __device__ __forceinline__ CellRows cell_rows(const lc_search_desc& S, const Cel
   return R;
 }
 
+// x / g for a gpu count g: when g is a power of two, x * 2^-k is the same single
+// correctly rounded operation on the same exact value as x / 2^k (subnormal
+// results included), without the division sequence.
+struct GpuDiv {
+  double g, inv;
+  bool p2;
+  __device__ __forceinline__ explicit GpuDiv(int64_t gpus) {
+    g = (double)gpus;
+    p2 = gpus > 0 && (gpus & (gpus - 1)) == 0 && gpus < (1ll << 52);
+    inv = p2 ? __longlong_as_double((long long)(1023 - (__ffsll(gpus) - 1)) << 52) : 0.0;
+  }
+  __device__ __forceinline__ double operator()(double x) const { return p2 ? x * inv : x / g; }
+};
+
 // One candidate's rows from its cell's shared values (CellRows) and its gpu
 // count, plus its contribution to the per-search accounting.
 __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search_desc& S, const CellOut& o,
@@ -1570,7 +1588,7 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
                                             RowAcc& ra, unsigned long long* bk, double* seed_at = nullptr) {
   const int64_t n = P.n_cap;
   const bool do_st = (S.modes & 1) && inb, do_ag = (S.modes & 2) && inb, do_dg = (S.modes & 4) != 0;
-  const double g = (double)gpus;
+  const GpuDiv div_g(gpus);
   int fflags = 0;  // K4 reads these instead of the rows' status / ttft / speed
   int32_t q = 0;
   auto add_q = [&](int32_t x) { q += x; };  // packed halves never overflow 16 bits
@@ -1579,7 +1597,7 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
     if (o.st_status) {
       P.err_c[u] = P.cell_err[ci * 8 + 0]; P.err_c[n + u] = P.cell_err[ci * 8 + 1];
     } else {
-      const double thru = R.st_tp / g;
+      const double thru = div_g(R.st_tp);
       P.st_v[u] = o.st_ttft; P.st_v[n + u] = o.st_tpot; P.st_v[2 * n + u] = R.st_speed; P.st_v[3 * n + u] = thru;
       ++ra.rows;
       if (R.st_feas) {
@@ -1596,7 +1614,7 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
     if (o.ag_status) {
       P.err_c[2 * n + u] = P.cell_err[ci * 8 + 2]; P.err_c[3 * n + u] = P.cell_err[ci * 8 + 3];
     } else {
-      const double thru = R.ag_tp / g;
+      const double thru = div_g(R.ag_tp);
       P.ag_v[u] = o.ag_ttft; P.ag_v[n + u] = o.ag_tpot; P.ag_v[2 * n + u] = R.ag_speed; P.ag_v[3 * n + u] = thru;
       ++ra.rows;
       if (R.ag_feas) {
@@ -1617,7 +1635,7 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
       if (seed_at) seed_at[0] = INFINITY;
     } else {
       P.pf_v[u] = o.pf_lat; P.pf_v[n + u] = R.pf_rate;
-      const double r = -R.pf_rate / g;
+      const double r = div_g(-R.pf_rate);
       P.pool_key[u] = r;
       if (seed_at) seed_at[0] = r;
     }
@@ -1629,7 +1647,7 @@ __device__ __forceinline__ void expand_unit(const EvalParams& P, const lc_search
     } else {
       P.dc_v[u] = o.dc_lat;
       P.dc_v[n + u] = R.dc_rate;
-      const double r = -R.dc_rate / g;
+      const double r = div_g(-R.dc_rate);
       P.pool_key[n + u] = r;
       if (seed_at) seed_at[1] = r;
     }
@@ -3911,13 +3929,13 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   if (sp->is_moe) {
     // batch lists are identified by (b_off, n_b): callers that pass one copy per
     // distinct list (the Python engine does) get full sharing
-    std::map<std::vector<int64_t>, int32_t> tindex;  // (type, b_off, n_b, load, chunk) -> table
+    std::map<Key5, int32_t> tindex;  // (type, b_off, n_b, load, chunk) -> table
     const int64_t per_b = (int64_t)sp->n_tp * sp->n_ep;
     for (int s = 0; s < n_search; ++s) {
       const lc_search_desc& S = searches[s];
       const int32_t cb = S.b_off;
       for (int type = 0; type < 2; ++type) {
-        std::vector<int64_t> key = {type, cb, S.n_b, S.load, type == 0 ? S.isl - S.prefix : 0};
+        const Key5 key = {type, cb, S.n_b, S.load, type == 0 ? S.isl - S.prefix : 0};
         auto jt = tindex.find(key);
         int32_t ti;
         if (jt == tindex.end()) {
@@ -3939,18 +3957,18 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   c->hqt.clear();
   c->n_qt_2d = 0;
   {
-    std::map<std::vector<int64_t>, int32_t> gidx;
+    std::map<Key5, int32_t> gidx;
     for (int s = 0; s < n_search; ++s) {
       const lc_search_desc& S = searches[s];
       const int64_t cb = S.b_off;
       const bool need[4] = {(S.modes & 5) != 0, (S.modes & 7) != 0, (S.modes & 6) != 0, (S.modes & 2) != 0};
       for (int cl = 0; cl < 4; ++cl) {
         if (!need[cl] || !sp->class_n[cl]) continue;
-        std::vector<int64_t> key;
+        Key5 key;
         if (cl == 0) key = {0, S.isl - S.prefix, cb, S.n_b, S.load};
-        else if (cl == 1) key = {1, cb, S.n_b, S.load};
-        else if (cl == 2) key = {2, S.isl + S.osl / 2, cb, S.n_b};
-        else key = {3, s};
+        else if (cl == 1) key = {1, cb, S.n_b, S.load, 0};
+        else if (cl == 2) key = {2, S.isl + S.osl / 2, cb, S.n_b, 0};
+        else key = {3, s, 0, 0, 0};
         auto jt = gidx.find(key);
         if (jt == gidx.end()) {
           gidx[key] = (int32_t)c->hqt.size();
@@ -3988,7 +4006,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   // decode-series groups: the KV samples isl + 32k + 1 do not depend on osl
   c->hds.clear();
   {
-    std::map<std::vector<int64_t>, int32_t> gidx;
+    std::map<Key5, int32_t> gidx;
     for (int s = 0; s < n_search; ++s) {
       const lc_search_desc& S = searches[s];
       SearchMeta& M = c->hmeta[s];
@@ -3996,7 +4014,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
       M.ds_stride = 0;
       if (!M.n_steps || !sp->n_gclass) continue;
       const int32_t cb = S.b_off;
-      const std::vector<int64_t> key = {S.isl, cb, S.n_b, static_stride(S)};
+      const Key5 key = {S.isl, cb, S.n_b, static_stride(S), 0};
       auto jt = gidx.find(key);
       int32_t gi;
       if (jt == gidx.end()) {
@@ -4024,12 +4042,12 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   c->hsm.clear();
   c->n_series = 0;
   if (sp->n_gclass) {
-    std::map<std::vector<int64_t>, std::vector<int32_t>> members;
-    std::vector<std::vector<int64_t>> order;
+    std::map<Key5, std::vector<int32_t>> members;
+    std::vector<Key5> order;
     for (int s = 0; s < n_search; ++s) {
       const lc_search_desc& S = searches[s];
       if (!c->hmeta[s].n_steps) continue;
-      std::vector<int64_t> key = {S.isl, S.b_off, S.n_b, S.load, static_stride(S)};
+      const Key5 key = {S.isl, S.b_off, S.n_b, S.load, static_stride(S)};
       auto it = members.find(key);
       if (it == members.end()) { order.push_back(key); members[key] = {s}; }
       else it->second.push_back(s);
@@ -4548,6 +4566,24 @@ int64_t lc_report_rows(const lc_report_cols* c, const int64_t* rows, int64_t n_s
 int lc_stream(lc_ctx* c, void** stream) {
   if (!c || !stream) return fail(LC_ERR_ARG, "lc_stream: NULL argument");
   *stream = (void*)c->stream;
+  return LC_OK;
+}
+
+int lc_set_priority(lc_ctx* c, int priority) {
+  if (!c) return fail(LC_ERR_ARG, "lc_set_priority: NULL context");
+  CK(cudaSetDevice(c->device));
+  int least = 0, greatest = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  const int p = priority < greatest ? greatest : (priority > least ? least : priority);
+  CK(cudaStreamSynchronize(c->stream));
+  cudaStream_t s = nullptr;
+  CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, p));
+  CK(cudaStreamDestroy(c->stream));
+  c->stream = s;
+  // kernel nodes take their priority from the capturing stream: recapture
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  c->gexec = nullptr;
+  c->graph_ok = false;
   return LC_OK;
 }
 

@@ -389,6 +389,10 @@ class Engine:
         """Enqueue the last batch's device pipeline on this engine's stream (no sync)."""
         self._call(self.lib.lc_replay_async, "lc_replay_async", self.ctx)
 
+    def set_priority(self, priority: int) -> None:
+        """Stream priority of this engine (lc_set_priority): negative = higher, 0 = default."""
+        self._call(self.lib.lc_set_priority, "lc_set_priority", self.ctx, int(priority))
+
     def stream_ptr(self) -> int:
         """cudaStream_t of this engine (for torch.cuda.ExternalStream)."""
         h = C.c_void_p()
