@@ -1044,6 +1044,9 @@ __device__ __forceinline__ int table_step(const EvalParams& P, const SearchMeta&
 #ifndef LC_FUSED_STEPS
 #define LC_FUSED_STEPS 1  // mixed + generation steps in one warp pass (warp_table_step2)
 #endif
+#ifndef LC_CELL_PREFETCH
+#define LC_CELL_PREFETCH 1
+#endif
 #ifndef LC_CELL_DYNAMIC
 #define LC_CELL_DYNAMIC 1
 #endif
@@ -1901,6 +1904,14 @@ __global__ void __launch_bounds__(kCellThreads, LC_CELL_MIN_BLOCKS) k_eval_cells
     RowAcc ra{0, 0, 0, 0, 0, 0, 0ull, 0ull};
     int s = -1;
     const uint32_t cf = ci < end ? P.cell_flags[ci] : 0u;
+#if LC_CELL_PREFETCH
+    // the next iteration's per-cell inputs start moving now (L1 prefetch): the
+    // chain flags -> search -> step totals otherwise starts cold every iteration
+    if (ci + (int64_t)blockDim.x < end) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(P.cell_flags + ci + blockDim.x));
+      if (P.sd) asm volatile("prefetch.global.L1 [%0];" ::"l"(P.sd + ci + blockDim.x));
+    }
+#endif
     if (LC_WARP_STEPS) {
       // every lane of a warp with work takes part (warp_table_step); lanes past
       // the range stand in as lane 0's cell with nothing to evaluate
