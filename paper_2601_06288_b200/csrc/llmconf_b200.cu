@@ -2588,9 +2588,15 @@ __global__ void __launch_bounds__(kPoolThreads) k_pools_partial(EvalParams P, co
       }
 #pragma unroll
       for (int k = 0; k < kPoolUnroll; ++k) {
+#ifdef LC_COUNT_MERGES
+        if ((threadIdx.x & 31) == 0) atomicAdd(P.cell_ctr, 1ull);
+#endif
         const bool cand = r[k] != INFINITY && r[k] <= thr;
         if (!__any_sync(0xffffffffu, cand)) continue;
         const int64_t i = base + 32 * k + lane;
+#ifdef LC_COUNT_MERGES  // diagnostics build: merges and chunks scanned
+        if ((threadIdx.x & 31) == 0) atomicAdd(P.cell_ctr, 1ull << 32);
+#endif
         tk.merge_chunk(P, cand ? pool_key_of(P, S, r[k], (int32_t)(u0 + i)) : PoolKey{0.0, 0, -1}, cap);
         thr = fmin(thr, tk.thr_r(cap));
       }
@@ -2625,6 +2631,11 @@ static_assert(kPoolSplit == 16, "k_pools_final's merge tree assumes 16 partials 
 __global__ void __launch_bounds__(kPoolFinalThreads) k_pools_final(EvalParams P, SearchMeta* meta,
                                                                    const PoolPartial* part, int32_t* pool_sel) {
   const int s = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef LC_COUNT_MERGES
+  if (s == 0 && tid == 0)
+    printf("k_pools_partial: %llu chunk merges of %llu chunks scanned\n", *P.cell_ctr >> 32,
+           *P.cell_ctr & 0xffffffffull);
+#endif
   const lc_search_desc& S = P.searches[s];
   if (!(S.modes & 4)) return;
   __shared__ PoolKey red[kPoolFinalThreads];

@@ -128,3 +128,22 @@ def test_spec_validation_mirrors_reference():
         pkg.ModelSpec.from_doc(dict(model_doc("qwen-small"), kv_heads=7))
     with pytest.raises(pkg.specs.SearchError):
         pkg.run_search(None, None, None, jobs=0)
+
+
+def test_power_of_two_division_is_an_exact_multiply():
+    """The device divides by power-of-two gpu counts (and ceil_div_f divisors) with
+    a multiply by 2^-k (GpuDiv, lc_eval.cuh ceil_div_f): both are one correctly
+    rounded operation on the same exact value, subnormal results included."""
+    import numpy as np
+
+    rng = np.random.default_rng(7)
+    bits = rng.integers(0, 2**63 - 1, size=200_000, dtype=np.int64)
+    x = bits.view(np.float64)
+    x = np.concatenate([x[np.isfinite(x)], -x[np.isfinite(x)][:1000],
+                        np.array([0.0, -0.0, 5e-324, 2.2250738585072014e-308, 1.7976931348623157e308])])
+    for k in (0, 1, 2, 3, 5, 8, 10, 20, 40, 51):
+        g = float(2**k)
+        inv = float(2.0**-k)
+        a = x / g
+        b = x * inv
+        assert np.array_equal(a.view(np.int64), b.view(np.int64)), k
