@@ -589,7 +589,7 @@ __global__ void k_cell_flags_fit(EvalParams P, const int32_t* cmax, int32_t n_tm
   const int64_t n = (int64_t)n_tmpl * S.n_b;
   const int64_t off = P.meta[s].cell_off;
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
-    const int t = (int)(x / S.n_b), bi = (int)(x % S.n_b);
+    const int t = div32(x, S.n_b), bi = mod32(x, S.n_b);  // x < n_tmpl * n_b < 2^31
     const int32_t* m = cmax + ((int64_t)s * n_tmpl + t) * 2;
     cell_flags[off + x] = (bi < m[0] ? 1u : 0u) | (bi < m[1] ? 2u : 0u);
   }
@@ -2064,10 +2064,6 @@ constexpr int kPoolLocal = 32;  // caps up to 32 take the fast path (one list el
 #define LC_POOL_THREADS 256
 #endif
 constexpr int kPoolThreads = LC_POOL_THREADS;
-#ifndef LC_POOL_UNROLL
-#define LC_POOL_UNROLL 1  // 4: slower (K5a 0.22 -> 0.28 ms): the merges, not the loads, bound the pass
-#endif
-constexpr int kPoolUnroll = LC_POOL_UNROLL;  // key chunks in flight per warp in k_pools_partial
 
 __device__ __forceinline__ bool pool_before(const EvalParams& P, const PoolKey& a, const PoolKey& b) {
   if (a.unit < 0) return false;
@@ -2521,7 +2517,16 @@ __device__ __forceinline__ double warp_merge32_d(double a, double b) {
 // block per (search, role): 8 warps take every 8th chunk of 32 combos, then the
 // warps' ascending 32-lists are merged as a tree in shared memory
 constexpr int kSeedThreads = 256;
-__global__ void __launch_bounds__(kSeedThreads) k_pools_seed(EvalParams P, double* seed) {
+// doubles as order-preserving unsigned keys (k_pools_seed / k_pools_partial share
+// each search's pool threshold through atomicMin on these)
+__device__ __forceinline__ unsigned long long ord_key(double x) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_val(unsigned long long o) {
+  return __longlong_as_double((long long)((o >> 63) ? (o & 0x7fffffffffffffffull) : ~o));
+}
+__global__ void __launch_bounds__(kSeedThreads) k_pools_seed(EvalParams P, unsigned long long* seed) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = kSeedThreads / 32;
   const int s = blockIdx.x >> 1, role = blockIdx.x & 1;
   __shared__ double lists[kSeedThreads / 32][32];
@@ -2551,11 +2556,11 @@ __global__ void __launch_bounds__(kSeedThreads) k_pools_seed(EvalParams P, doubl
     if (warp < width) lists[warp][lane] = best;
     __syncthreads();
   }
-  if (threadIdx.x == 0) seed[2 * s + role] = on ? lists[0][cap - 1] : INFINITY;
+  if (threadIdx.x == 0) seed[2 * s + role] = ord_key(on ? lists[0][cap - 1] : INFINITY);
 }
 
 __global__ void __launch_bounds__(kPoolThreads) k_pools_partial(EvalParams P, const SearchMeta* meta,
-                                                                 PoolPartial* part, const double* seed) {
+                                                                 PoolPartial* part, unsigned long long* seed) {
   const int s = blockIdx.y, bx = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const lc_search_desc& S = P.searches[s];
   if (!(S.modes & 4)) return;
@@ -2576,29 +2581,39 @@ __global__ void __launch_bounds__(kPoolThreads) k_pools_partial(EvalParams P, co
     // not after the current cap-th element (r <= thr; exact order in the merge).  The
     // threshold starts at the search's seed (k_pools_seed): with it most chunks hold
     // no candidate and cost one coalesced load.
-    // Each warp takes kPoolUnroll consecutive chunks per step and issues their
-    // loads together (memory-level parallelism; the test needs only the key).
-    double thr = seed ? seed[2 * s + role] : INFINITY;
-    for (int64_t base = lo + (int64_t)warp * 32 * kPoolUnroll; base < hi; base += kPoolThreads * kPoolUnroll) {
-      double r[kPoolUnroll];
-#pragma unroll
-      for (int k = 0; k < kPoolUnroll; ++k) {
-        const int64_t i = base + 32 * k + lane;
-        r[k] = i < hi ? keys[u0 + i] : INFINITY;  // INFINITY: pool candidate skipped
-      }
-#pragma unroll
-      for (int k = 0; k < kPoolUnroll; ++k) {
+    // Any block's cap-th smallest key bounds the search's cap-th from above (cap
+    // units are at or before it), so the blocks of a search share their
+    // thresholds: atomicMin after each merge, re-read every few chunks.
+    unsigned long long* shared_thr = seed ? seed + 2 * s + role : nullptr;
+    double thr = shared_thr ? ord_val(*shared_thr) : INFINITY;
+    int since = 0;
+    // the next chunk's keys are loaded before this chunk is tested (one merge site:
+    // unrolled copies of the merge code measured slower)
+    const int64_t step = kPoolThreads;
+    int64_t base = lo + (int64_t)warp * 32;
+    double r_next = base + lane < hi ? keys[u0 + base + lane] : INFINITY;
+    for (; base < hi; base += step) {
+      const double r = r_next;  // INFINITY: pool candidate skipped
+      const int64_t nb = base + step + lane;
+      r_next = nb < hi ? keys[u0 + nb] : INFINITY;
 #ifdef LC_COUNT_MERGES
-        if ((threadIdx.x & 31) == 0) atomicAdd(P.cell_ctr, 1ull);
+      if ((threadIdx.x & 31) == 0) atomicAdd(P.cell_ctr, 1ull);
 #endif
-        const bool cand = r[k] != INFINITY && r[k] <= thr;
-        if (!__any_sync(0xffffffffu, cand)) continue;
-        const int64_t i = base + 32 * k + lane;
+      if (shared_thr && ++since == 8) {
+        since = 0;
+        thr = fmin(thr, ord_val(*(volatile unsigned long long*)shared_thr));
+      }
+      const bool cand = r != INFINITY && r <= thr;
+      if (!__any_sync(0xffffffffu, cand)) continue;
+      const int64_t i = base + lane;
 #ifdef LC_COUNT_MERGES  // diagnostics build: merges and chunks scanned
-        if ((threadIdx.x & 31) == 0) atomicAdd(P.cell_ctr, 1ull << 32);
+      if ((threadIdx.x & 31) == 0) atomicAdd(P.cell_ctr, 1ull << 32);
 #endif
-        tk.merge_chunk(P, cand ? pool_key_of(P, S, r[k], (int32_t)(u0 + i)) : PoolKey{0.0, 0, -1}, cap);
-        thr = fmin(thr, tk.thr_r(cap));
+      tk.merge_chunk(P, cand ? pool_key_of(P, S, r, (int32_t)(u0 + i)) : PoolKey{0.0, 0, -1}, cap);
+      const double mine = tk.thr_r(cap);
+      if (mine < thr) {
+        thr = mine;
+        if (shared_thr && lane == 0) atomicMin(shared_thr, ord_key(mine));
       }
     }
     wout[warp][lane] = tk.mine;
@@ -2860,9 +2875,11 @@ __global__ void __launch_bounds__(kFrontThreads) k_front_pass3(EvalParams P, con
   // feasible rows' speed and throughput are read
   int64_t lo, hi;
   slice_of(M.n_units, kSplit, bx, &lo, &hi);
+  int f_next = lo + tid < hi ? P.front_flags[M.unit_off + lo + tid] : 0;
   for (int64_t i = lo + tid; i < hi; i += blockDim.x) {
     const int64_t u = M.unit_off + i;
-    const int f = P.front_flags[u];
+    const int f = f_next;  // loaded one iteration ahead
+    f_next = i + blockDim.x < hi ? P.front_flags[u + blockDim.x] : 0;
     if (!f) continue;
     if (f & 1) test(P.st_v[2 * P.n_cap + u], P.st_v[3 * P.n_cap + u], i);
     if (f & 2) test(P.ag_v[2 * P.n_cap + u], P.ag_v[3 * P.n_cap + u], ((int64_t)1 << 32) | i);
@@ -3660,10 +3677,10 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     PoolPartial* pp = c->pool_part.get<PoolPartial>((size_t)c->n_search * kPoolSplit, &err);
     if (err != cudaSuccess) return fail(LC_ERR_CUDA, "pool partial allocation");
     ++c->launches;
-    const double* seed = nullptr;
+    unsigned long long* seed = nullptr;
 #ifndef LC_NO_POOL_SEED
     if (P.pool_sample) {
-      double* sd = c->pool_seed.get<double>((size_t)c->n_search * 2, &err);
+      unsigned long long* sd = c->pool_seed.get<unsigned long long>((size_t)c->n_search * 2, &err);
       if (err != cudaSuccess) return fail(LC_ERR_CUDA, "pool seed allocation");
       ++c->launches;
       k_pools_seed<<<2 * c->n_search, kSeedThreads, 0, c->stream>>>(P, sd);
