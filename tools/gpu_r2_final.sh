@@ -14,3 +14,6 @@ done
 timeout 1200 ncu --set full --clock-control none --import-source on \
   -k "regex:k_eval_cells|k_pools_partial|k_front_pass3|k_front_final|k_qtables|k_dstables|k_dseries|k_ptables|k_tails|k_disagg|k_scatter_fit|k_front_mid" \
   -c 24 -o gpurun_out/prof_${tag} python tools/profile_run.py gpt-oss-120b 100 > gpurun_out/ncu_${tag}.log 2>&1; echo ncu_full_rc=$?
+LC_NO_GRAPH=1 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 \
+  --csv --log-file gpurun_out/launches_bench_${tag}.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --north-star none \
+  > gpurun_out/bench_under_ncu_${tag}.log 2>&1; echo ncu_launch_rc=$?
