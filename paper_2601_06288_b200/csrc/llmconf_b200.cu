@@ -61,6 +61,7 @@ static thread_local bool tl_capturing = false, tl_capture_grow = false;
 struct DBuf {
   void* p = nullptr;
   size_t cap = 0;
+  bool view = false;  // p points into another buffer (not owned)
   template <class T>
   T* get(size_t n, cudaError_t* err) {
     size_t bytes = n * sizeof(T);
@@ -70,9 +71,10 @@ struct DBuf {
       return (T*)p;
     }
     if (bytes > cap) {
-      if (p) cudaFree(p);
+      if (p && !view) cudaFree(p);
       p = nullptr;
       cap = 0;
+      view = false;
       cudaError_t e = cudaMalloc(&p, bytes);
       if (e != cudaSuccess) { *err = e; return nullptr; }
       cap = bytes;
@@ -80,9 +82,16 @@ struct DBuf {
     return (T*)p;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p && !view) cudaFree(p);
     p = nullptr;
     cap = 0;
+    view = false;
+  }
+  void set_view(void* q, size_t bytes) {
+    if (p && !view) cudaFree(p);
+    p = q;
+    cap = bytes;
+    view = true;
   }
 };
 
@@ -269,6 +278,7 @@ struct lc_ctx {
   DBuf flags, pos, block_sums;
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c, front_flags, cell_ctr;
+  DBuf inputs;  // one block holding the batch's host inputs (searches .. batch codes are views into it)
   DBuf step_in, step_out, step_loads, pool_key, qt_groups, ds_groups, front_compact, pool_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   DBuf q_in, q_lat, q_st;  // lc_query_batch
   DBuf sgroups, smembers, sd;  // shared static decode loops
@@ -3268,7 +3278,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->batch_code, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->step_in, &c->step_out, &c->step_loads, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch, &c->pool_seed, &c->pool_sample, &c->front_flags, &c->cell_ctr};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->step_in, &c->step_out, &c->step_loads, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch, &c->pool_seed, &c->pool_sample, &c->front_flags, &c->cell_ctr, &c->inputs};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -4131,22 +4141,11 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   c->n_tails = tails;
   c->n_plan_slots = plans;
   cudaError_t err = cudaSuccess;
-  lc_search_desc* dS = c->searches.get<lc_search_desc>(n_search, &err);
-  int64_t* dB = c->batches.get<int64_t>(n_batches, &err);
-  uint64_t* dBC = c->batch_code.get<uint64_t>(n_batches, &err);
   c->hbatch_code.resize(n_batches > 0 ? n_batches : 1);
   for (int32_t i = 0; i < n_batches; ++i) {
     if (batches[i] > LC_KEY_BATCH_MAX) return fail(LC_ERR_ARG, "batch sizes above 9999999999 are not supported");
     c->hbatch_code[i] = lc_batch_code(batches[i] > 0 ? batches[i] : 1);
   }
-  double* dL = c->loads.get<double>((size_t)n_loads * 2 * (sp->n_experts > 0 ? sp->n_experts : 1), &err);
-  SearchMeta* dM = c->meta.get<SearchMeta>(n_search, &err);
-  TailTable* dT = c->tail_tables.get<TailTable>(c->htables.size(), &err);
-  DsGroup* dG = c->ds_groups.get<DsGroup>(c->hds.size(), &err);
-  QtGroup* dQ = c->qt_groups.get<QtGroup>(c->hqt.size(), &err);
-  SeriesGroup* dSG = c->sgroups.get<SeriesGroup>(c->hsg.size(), &err);
-  SeriesMember* dSM = c->smembers.get<SeriesMember>(c->hsm.size(), &err);
-  PGroup* dPG = c->pgroups.get<PGroup>(c->hpg.size(), &err);
   c->psteps.get<PStep>((size_t)c->n_pstep, &err);
   c->sd.get<SdOut>(c->n_series ? (size_t)cells : 0, &err);
   c->results.get<lc_search_result>(n_search, &err);
@@ -4161,9 +4160,20 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
                              sizeof(PGroup) * c->hpg.size(), sizeof(uint64_t) * n_batches};
     const void* srcs[11] = {searches, batches, loads, c->hmeta.data(), c->htables.data(), c->hds.data(),
                             c->hqt.data(), c->hsg.data(), c->hsm.data(), c->hpg.data(), c->hbatch_code.data()};
-    void* dsts[11] = {dS, dB, dL, dM, dT, dG, dQ, dSG, dSM, dPG, dBC};
-    size_t need = 0;
-    for (int k = 0; k < 11; ++k) need += (sizes[k] + 255) & ~(size_t)255;
+    // one device block holds all eleven inputs at the arena's offsets, so a single
+    // H2D copy moves them (the buffers are views into it)
+    DBuf* bufs[11] = {&c->searches, &c->batches, &c->loads, &c->meta, &c->tail_tables, &c->ds_groups,
+                      &c->qt_groups, &c->sgroups, &c->smembers, &c->pgroups, &c->batch_code};
+    size_t offs[11], tot = 0;
+    for (int k = 0; k < 11; ++k) {
+      offs[k] = tot;
+      const size_t a = (sizes[k] + 255) & ~(size_t)255;
+      tot += a ? a : 256;  // an empty input still gets a valid (unused) address
+    }
+    unsigned char* base = c->inputs.get<unsigned char>(tot, &err);
+    if (err != cudaSuccess) return fail(LC_ERR_CUDA, std::string("input allocation: ") + cudaGetErrorString(err));
+    for (int k = 0; k < 11; ++k) bufs[k]->set_view(base + offs[k], (sizes[k] + 255) & ~(size_t)255);
+    size_t need = tot;
     need += (sizeof(lc_search_result) + sizeof(SearchMeta)) * (size_t)n_search + 1024;  // summaries coming back
     if (c->arena_cap < need) {
       if (c->arena) cudaFreeHost(c->arena);
@@ -4172,14 +4182,10 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
       CK(cudaHostAlloc((void**)&c->arena, need, cudaHostAllocDefault));
       c->arena_cap = need;
     }
-    size_t off = 0;
-    for (int k = 0; k < 11; ++k) {
-      if (!sizes[k]) continue;
-      memcpy(c->arena + off, srcs[k], sizes[k]);
-      CK(cudaMemcpyAsync(dsts[k], c->arena + off, sizes[k], cudaMemcpyHostToDevice, c->stream));
-      off += (sizes[k] + 255) & ~(size_t)255;
-    }
-    c->arena_used = off;
+    for (int k = 0; k < 11; ++k)
+      if (sizes[k]) memcpy(c->arena + offs[k], srcs[k], sizes[k]);
+    CK(cudaMemcpyAsync(base, c->arena, tot, cudaMemcpyHostToDevice, c->stream));
+    c->arena_used = tot;
   }
   const double t_plan = host_timing ? ms_since(t_in) : 0.0;
   int rc = launch_pipeline(c, totals);

@@ -42,6 +42,15 @@ MODE_STATIC, MODE_AGG, MODE_DISAGG = 1, 2, 4
 ST_OK, ST_MISSING, ST_EXTRAP, ST_UNSUPPORTED, ST_CHUNK_OFF, ST_NO_SLOT = range(6)
 
 
+@functools.lru_cache(maxsize=64)
+def _batch_list(src: tuple) -> tuple:
+    """A search's batch list as the device takes it: sorted, values < 1 dropped
+    (they make ParallelConfig raise, so enumerate_candidates skips them,
+    search.py:101-105; model.py:190-193), duplicates kept as there.  A pure
+    function of the (immutable) candidate-space tuple, cached like the plans."""
+    return tuple(sorted(b for b in src if b >= 1))
+
+
 @functools.lru_cache(maxsize=256)
 def _moe_q(params, num_experts: int) -> np.ndarray:
     """[q_i = w_i / sum(w)] + by-weight order, numpy exactly as moe_load.py:51-57, 84, 97."""
@@ -314,9 +323,7 @@ class Engine:
             key = (id(src), len(src)) if isinstance(src, tuple) else tuple(src)
             hit = b_index.get(key)
             if hit is None:
-                # batch values < 1 make ParallelConfig raise, and enumerate_candidates skips
-                # them (search.py:101-105; model.py:190-193); duplicates are kept, as there
-                bs = tuple(sorted(b for b in src if b >= 1))
+                bs = _batch_list(src if isinstance(src, tuple) else tuple(src))
                 hit = b_index.get(bs)
                 if hit is None:
                     hit = (len(batches), len(bs))
