@@ -294,7 +294,8 @@ class Engine:
         searches["ttft_limit"] = [float(t) if t is not None else 0.0 for t in ttfts]
         searches["has_floor"] = [f is not None for f in floors]
         searches["speed_floor"] = [float(f) if f is not None else 0.0 for f in floors]
-        searches["tpot_cap"] = [float(w.tpot_ceiling()) if f is not None else 0.0 for w, f in zip(ws, floors)]
+        # tpot_ceiling() = 1000 / speed_floor() (specs.py), from the floors already read
+        searches["tpot_cap"] = [float(1000.0 / f) if f is not None else 0.0 for f in floors]
         if mode_override is not None:
             searches["modes"] = mode_override
         else:
