@@ -283,32 +283,70 @@ class Engine:
         load_ix: dict = {}
         if space.prefill_pool_cap < 0 or space.decode_pool_cap < 0:
             raise SearchError("pool caps must be >= 0")
-        # per-search fields written column-wise (one comprehension per field)
+        # one pass over the workloads collects every per-search field (runs of
+        # workloads sharing the batch list / modes / load model reuse the last
+        # lookup), then each column is written with one conversion
         ws = list(workloads)
-        floors = [w.speed_floor() for w in ws]
-        ttfts = [w.ttft_limit_ms for w in ws]
-        searches["isl"] = [w.isl for w in ws]
-        searches["osl"] = [w.osl for w in ws]
-        searches["prefix"] = [w.prefix_len for w in ws]
-        searches["has_ttft"] = [t is not None for t in ttfts]
-        searches["ttft_limit"] = [float(t) if t is not None else 0.0 for t in ttfts]
-        searches["has_floor"] = [f is not None for f in floors]
-        searches["speed_floor"] = [float(f) if f is not None else 0.0 for f in floors]
-        # tpot_ceiling() = 1000 / speed_floor() (specs.py), from the floors already read
-        searches["tpot_cap"] = [float(1000.0 / f) if f is not None else 0.0 for f in floors]
-        if mode_override is not None:
-            searches["modes"] = mode_override
-        else:
-            mode_of: dict = {}
-            modes_v = []
-            for w in ws:
-                m = mode_of.get(w.modes)
+        isl, osl, prefix, ttft_v, floor_v, cap_v, modes_v, b_off, n_b, load_v = ([] for _ in range(10))
+        mode_of: dict = {}
+        last_src = last_modes = last_params = None
+        hit = m = ld = None
+        is_moe = plan.is_moe
+        for w in ws:
+            isl.append(w.isl)
+            osl.append(w.osl)
+            prefix.append(w.prefix_len)
+            t = w.ttft_limit_ms
+            ttft_v.append(float(t) if t is not None else None)
+            f = w.speed_floor()
+            if f is not None:
+                floor_v.append(float(f))
+                cap_v.append(float(1000.0 / f))  # tpot_ceiling() = 1000 / speed_floor() (specs.py)
+            else:
+                floor_v.append(None)
+                cap_v.append(0.0)
+            if mode_override is None and w.modes is not last_modes:
+                last_modes = w.modes
+                m = mode_of.get(last_modes)
                 if m is None:
-                    m = mode_of[w.modes] = ((MODE_STATIC if "static" in w.modes else 0)
-                                            | (MODE_AGG if "aggregated" in w.modes else 0)
-                                            | (MODE_DISAGG if "disaggregated" in w.modes else 0) | mode_extra)
-                modes_v.append(m)
-            searches["modes"] = modes_v
+                    m = mode_of[last_modes] = ((MODE_STATIC if "static" in last_modes else 0)
+                                               | (MODE_AGG if "aggregated" in last_modes else 0)
+                                               | (MODE_DISAGG if "disaggregated" in last_modes else 0) | mode_extra)
+            modes_v.append(m)
+            src = w.batch_sweep or space.batch_values
+            if src is not last_src:
+                last_src = src
+                key = (id(src), len(src)) if isinstance(src, tuple) else tuple(src)
+                hit = b_index.get(key)
+                if hit is None:
+                    bs = _batch_list(src if isinstance(src, tuple) else tuple(src))
+                    hit = b_index.get(bs)
+                    if hit is None:
+                        hit = (len(batches), len(bs))
+                        batches.extend(bs)
+                        b_index[bs] = hit
+                    b_index[key] = hit
+            b_off.append(hit[0])
+            n_b.append(hit[1])
+            if is_moe:
+                params = w.moe_load if w.moe_load is not None else DEFAULT_MOE_LOAD
+                if params is not last_params:
+                    last_params = params
+                    lk = (params.alpha, params.x_min, params.x_max, params.seed)
+                    ld = load_ix.get(lk)
+                    if ld is None:
+                        ld = load_ix[lk] = len(loads)
+                        loads.append(_moe_q(params, plan.n_experts))
+                load_v.append(ld)
+        searches["isl"] = isl
+        searches["osl"] = osl
+        searches["prefix"] = prefix
+        searches["has_ttft"] = [t is not None for t in ttft_v]
+        searches["ttft_limit"] = [t if t is not None else 0.0 for t in ttft_v]
+        searches["has_floor"] = [f is not None for f in floor_v]
+        searches["speed_floor"] = [f if f is not None else 0.0 for f in floor_v]
+        searches["tpot_cap"] = cap_v
+        searches["modes"] = mode_override if mode_override is not None else modes_v
         if enforce_budget:
             budget_rows = searches["budgets"]
             for i, w in enumerate(ws):
@@ -318,33 +356,8 @@ class Engine:
                         raise SearchError(f"at most {N.LC_MAX_BUDGETS} distinct gpu budgets are supported")
                     searches["n_budgets"][i] = len(budgets)
                     budget_rows[i, : len(budgets)] = budgets
-        b_off, n_b, load_v = [], [], []
-        for w in ws:
-            src = w.batch_sweep or space.batch_values
-            key = (id(src), len(src)) if isinstance(src, tuple) else tuple(src)
-            hit = b_index.get(key)
-            if hit is None:
-                bs = _batch_list(src if isinstance(src, tuple) else tuple(src))
-                hit = b_index.get(bs)
-                if hit is None:
-                    hit = (len(batches), len(bs))
-                    batches.extend(bs)
-                    b_index[bs] = hit
-                b_index[key] = hit
-            b_off.append(hit[0])
-            n_b.append(hit[1])
-        if plan.is_moe:
-            for w in ws:
-                params = w.moe_load if w.moe_load is not None else DEFAULT_MOE_LOAD
-                lk = (params.alpha, params.x_min, params.x_max, params.seed)
-                ld = load_ix.get(lk)
-                if ld is None:
-                    ld = load_ix[lk] = len(loads)
-                    loads.append(_moe_q(params, plan.n_experts))
-                load_v.append(ld)
-        else:
-            load_v = -1
         searches["b_off"], searches["n_b"] = b_off, n_b
+        searches["load"] = load_v if is_moe else -1
         searches["has_ctx_capacity"] = space.ctx_capacity is not None
         searches["ctx_capacity"] = space.ctx_capacity or 0
         searches["chunked_prefill"] = int(bool(space.chunked_prefill))
@@ -354,7 +367,6 @@ class Engine:
         searches["prefill_util"] = float(disagg.prefill_utilization)
         searches["decode_util"] = float(disagg.decode_utilization)
         searches["max_x"], searches["max_y"] = disagg.max_prefill_replicas, disagg.max_decode_replicas
-        searches["load"] = load_v
         searches["static_stride"] = static_stride  # estimate_static's decode stride (serving_modes.py:236)
         b_arr = np.array(batches if batches else [1], dtype=np.int64)
         l_arr = np.concatenate(loads) if loads else np.zeros(1)

@@ -147,3 +147,63 @@ def test_power_of_two_division_is_an_exact_multiply():
         a = x / g
         b = x * inv
         assert np.array_equal(a.view(np.int64), b.view(np.int64)), k
+
+
+def test_search_descriptors_one_pass_matches_per_field():
+    """Engine.run_batch's one-pass descriptor builder (reusing the last batch-list /
+    modes / load lookup across runs of workloads) equals a per-field restatement on
+    interleaved workloads: batch lists, modes and MoE load models alternating, limits
+    unset or set, duplicated and out-of-order batch sweeps."""
+    import types
+
+    from paper_2601_06288_b200 import _native as N
+    from paper_2601_06288_b200 import engine as E
+    from paper_2601_06288_b200.specs import DEFAULT_MOE_LOAD
+
+    model, space, db = None, pkg.CandidateSpace(batch_values=(8, 1, 32, 0, 2)), None
+    L1 = pkg.PowerLawParams(alpha=1.5, x_min=1.0, x_max=50.0, seed=3)
+    L2 = pkg.PowerLawParams()
+    sw = (64, 4, 4, 1)
+    wls = [pkg.WorkloadSpec(isl=4000, osl=500, ttft_limit_ms=5000.0, min_speed=20.0),
+           pkg.WorkloadSpec(isl=512, osl=64, tpot_limit_ms=40.0, batch_sweep=sw, moe_load=L1,
+                            modes=("aggregated", "disaggregated"), gpu_budgets=(16, 8, 8)),
+           pkg.WorkloadSpec(isl=300, osl=7, prefix_len=10),
+           pkg.WorkloadSpec(isl=512, osl=64, min_speed=3, batch_sweep=sw, moe_load=L1, modes=("static",)),
+           pkg.WorkloadSpec(isl=100, osl=9, batch_sweep=(2, 1), moe_load=L2, modes=("static",)),
+           pkg.WorkloadSpec(isl=100, osl=9, ttft_limit_ms=7, batch_sweep=(64, 4, 4, 1), moe_load=L1)]
+
+    class Plan:
+        is_moe, n_experts = True, 16
+
+    eng = E.Engine.__new__(E.Engine)
+    eng.lib = types.SimpleNamespace(lc_search_batch=None)
+    eng.ctx, eng._pinned, eng._deferred = None, (), []
+    eng._call = lambda *a: None
+    eng.space_handle = lambda d, m, s: (None, Plan, None)
+    eng.db_handle = lambda d: (None, None)
+    out = eng.run_batch(db, model, space, wls)
+    s, batches = out.searches, out.batches.tolist()
+    loads_seen: list = []
+    for i, w in enumerate(wls):
+        bl = tuple(sorted(b for b in (w.batch_sweep or space.batch_values) if b >= 1))
+        assert tuple(batches[s["b_off"][i]: s["b_off"][i] + s["n_b"][i]]) == bl
+        f = w.speed_floor()
+        assert (s["isl"][i], s["osl"][i], s["prefix"][i]) == (w.isl, w.osl, w.prefix_len)
+        assert bool(s["has_ttft"][i]) == (w.ttft_limit_ms is not None)
+        assert s["ttft_limit"][i] == (float(w.ttft_limit_ms) if w.ttft_limit_ms is not None else 0.0)
+        assert bool(s["has_floor"][i]) == (f is not None)
+        assert s["speed_floor"][i] == (float(f) if f is not None else 0.0)
+        assert s["tpot_cap"][i] == (w.tpot_ceiling() if f is not None else 0.0)
+        modes = ((E.MODE_STATIC if "static" in w.modes else 0) | (E.MODE_AGG if "aggregated" in w.modes else 0)
+                 | (E.MODE_DISAGG if "disaggregated" in w.modes else 0))
+        assert s["modes"][i] == modes
+        bud = sorted(set(w.gpu_budgets))
+        assert s["n_budgets"][i] == len(bud) and list(s["budgets"][i][: len(bud)]) == bud
+        p = w.moe_load if w.moe_load is not None else DEFAULT_MOE_LOAD
+        key = (p.alpha, p.x_min, p.x_max, p.seed)
+        if key not in loads_seen:
+            loads_seen.append(key)
+        assert s["load"][i] == loads_seen.index(key)
+    # equal batch lists share one copy: (1, 2, 8, 32), (1, 4, 4, 64), (1, 2)
+    assert len(batches) == 4 + 4 + 2
+    assert s.dtype == N.SEARCH_DESC_DTYPE
