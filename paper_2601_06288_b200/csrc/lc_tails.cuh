@@ -46,12 +46,13 @@ __device__ __forceinline__ int warp_excl_scan(int v, int lane) {
 }
 
 // hist: 256 ints of shared memory private to this warp.
+// Per-lane expert counts (experts lane*per .. lane*per+per-1) of
+// tokens_per_expert: they depend on (q, total, topk) only, not on ep.
 template <int PER>
-__device__ int64_t warp_busiest_shard(const double* __restrict__ q, const double* __restrict__ order, int E,
-                                      int64_t total, int64_t topk, int64_t ep, int* hist) {
+__device__ __forceinline__ void warp_expert_counts(const double* __restrict__ q, const double* __restrict__ order,
+                                                   int E, int64_t total, int64_t topk, int* hist, int64_t (&cnt)[PER]) {
   const int lane = threadIdx.x & 31;
   const int per = (E + 31) >> 5;  // experts per lane, contiguous
-  int64_t cnt[PER];
   uint64_t key[PER];
   const int64_t target = total * topk;
   const double tgt = (double)target;
@@ -177,6 +178,13 @@ __device__ int64_t warp_busiest_shard(const double* __restrict__ q, const double
       surplus -= take;
     }
   }
+}
+
+// busiest contiguous EP block of the counts (expert_shard_tokens + max)
+template <int PER>
+__device__ __forceinline__ int64_t warp_block_max(const int64_t (&cnt)[PER], int E, int64_t ep) {
+  const int lane = threadIdx.x & 31;
+  const int per = (E + 31) >> 5;
   // busiest contiguous EP block
   const int bs = (int)(E / ep);
   if (per > 0 && bs % per == 0 && E % 32 == 0 && per * 32 == E) {
@@ -209,6 +217,15 @@ __device__ int64_t warp_busiest_shard(const double* __restrict__ q, const double
     if (r == 0 || s > best) best = s;
   }
   return best;
+}
+
+
+template <int PER>
+__device__ int64_t warp_busiest_shard(const double* __restrict__ q, const double* __restrict__ order, int E,
+                                      int64_t total, int64_t topk, int64_t ep, int* hist) {
+  int64_t cnt[PER];
+  warp_expert_counts<PER>(q, order, E, total, topk, hist, cnt);
+  return warp_block_max<PER>(cnt, E, ep);
 }
 
 }  // namespace lc

@@ -124,6 +124,7 @@ struct lc_space {
   lc_entry* entries;
   int64_t* tp_vals;  // [n_tp] from combos
   int64_t* ep_vals;  // [n_ep]
+  int64_t max_ep_h;  // host copy: largest ep value
   uint8_t* pair_used;  // [n_tp*n_ep]
   int32_t* pair_canon; // [n_tp*n_ep] first pair with the same (max(1, ep/tp), ep): identical tails
   struct TmplInfo* tmpl_info;  // [n_tmpl]
@@ -279,7 +280,7 @@ struct lc_ctx {
   DBuf u_search, u_combo, u_batch, u_budget;
   DBuf st_status, st_v, ag_status, ag_v, pf_status, pf_v, dc_status, dc_v, err_c, front_flags, cell_ctr;
   DBuf inputs;  // one block holding the batch's host inputs (searches .. batch codes are views into it)
-  DBuf step_in, step_out, step_loads, pool_key, qt_groups, ds_groups, front_compact, pool_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
+  DBuf step_in, step_out, step_loads, pool_key, qt_groups, ds_groups, front_compact, pool_part, front_meta, buckets, surv, n_surv, qt, ds, m_used, tail_tables, tails, tail_hash, pool_sel, plans_i, plans_d, front, u_queries, cell_flags, cells, cell_err;
   DBuf q_in, q_lat, q_st;  // lc_query_batch
   DBuf sgroups, smembers, sd;  // shared static decode loops
   DBuf pgroups, psteps;        // shared prefill step totals
@@ -302,6 +303,7 @@ struct lc_ctx {
   int32_t n_search = 0, n_batches = 0, n_loads = 0;
   int64_t n_raw = 0, n_cap = 0, n_units = 0, n_tails = 0, n_plan_slots = 0, n_front_slots = 0, n_cells = 0;
   int64_t n_qt = 0, n_ds = 0, n_pd_tails = 0, m_tmax = 0, n_marks = 0;
+  bool tails_dedup_ok = false;  // K3 keys (load << 48 | pooled tokens) fit: see k_tails_keys
   int64_t launches = 0;  // kernels launched by the last pipeline run
   int64_t n_qt_2d = 0;   // 2-D entries among the query tables
   int64_t n_total_idx = 0;  // index of the unit total inside block_sums
@@ -632,6 +634,57 @@ __global__ void k_unit_offsets_fit(SearchMeta* meta, int n_search, int32_t n_com
 }
 
 // ---- K3: MoE tails table [type P/D/M][tp_i][ep_i][b_i] per search
+// entry t of the tails table: whether some candidate reads it, and its
+// (pooled tokens, ep index, load model)
+__device__ __forceinline__ bool tail_entry(const EvalParams& P, int64_t t, int64_t& pooled, int& ep_i, int& load) {
+  const int npair = P.n_tp * P.n_ep;
+  bool need = false;
+  pooled = 0;
+  ep_i = 0;
+  load = 0;
+  if (t >= P.n_pd_tails) {
+    // dense mixed region: (load, pair, tokens)
+    int64_t r = t - P.n_pd_tails;
+    const int64_t tok = r % (P.m_tmax + 1);
+    r /= (P.m_tmax + 1);
+    const int pair = (int)(r % npair);
+    load = (int)(r / npair);
+    const int64_t tp = P.tp_vals[pair / P.n_ep];
+    ep_i = pair % P.n_ep;
+    const int64_t ep = P.ep_vals[ep_i];
+    need = ep > 1 && P.pair_used[pair] && P.pair_canon[pair] == pair &&
+           P.m_used[(int64_t)load * (P.m_tmax + 1) + tok];
+    const int f = (int)ep / (int)tp;  // tp, ep: small positive parallel degrees
+    pooled = tok * (f > 1 ? f : 1);
+  } else {
+    int lo = 0, hi = P.n_tail_tables - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (P.tail_tables[mid].off <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    const TailTable T = P.tail_tables[lo];
+    const int64_t rel = t - T.off;
+    const int bi = mod32(rel, T.n_b);
+    const int pair = div32(rel, T.n_b);
+    if (pair < npair) {
+      const int64_t tp = P.tp_vals[pair / P.n_ep];
+      ep_i = pair % P.n_ep;
+      const int64_t ep = P.ep_vals[ep_i];
+      need = ep > 1 && P.pair_used[pair] && P.pair_canon[pair] == pair && T.load >= 0;
+      const int64_t b = P.batches[T.b_off + bi];
+      const int64_t tokens = T.type == 0 ? b * T.chunk : b;
+      const int f = (int)ep / (int)tp;
+      pooled = tokens * (f > 1 ? f : 1);
+      load = T.load;
+    }
+  }
+  return need;
+}
+
+// General path (any number of ep values): each warp takes 32 consecutive table
+// entries, the lanes decide in parallel which are needed, then the warp
+// computes the needed ones one after another.
 template <int PER>
 __global__ void __launch_bounds__(256, PER <= 4 ? LC_TAIL_MIN_BLOCKS : LC_TAIL8_MIN_BLOCKS)
     k_tails(EvalParams P, int64_t n_tails, int64_t* tails) {
@@ -639,64 +692,108 @@ __global__ void __launch_bounds__(256, PER <= 4 ? LC_TAIL_MIN_BLOCKS : LC_TAIL8_
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int* hist = hist_all[warp];
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  const int npair = P.n_tp * P.n_ep;
   const int E = (int)P.n_experts;
-  // each warp takes 32 consecutive table entries: the lanes decide in parallel
-  // which are needed (most of the dense mixed region is not), then the warp
-  // computes the needed ones one after another
   for (int64_t chunk = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; chunk * 32 < n_tails; chunk += nw) {
     const int64_t t = chunk * 32 + lane;
-    bool need = false;
-    int64_t pooled = 0, ep = 1;
-    int load = 0;
-    if (t < n_tails) {
-      if (t >= P.n_pd_tails) {
-        // dense mixed region: (load, pair, tokens)
-        int64_t r = t - P.n_pd_tails;
-        const int64_t tok = r % (P.m_tmax + 1);
-        r /= (P.m_tmax + 1);
-        const int pair = (int)(r % npair);
-        load = (int)(r / npair);
-        const int64_t tp = P.tp_vals[pair / P.n_ep];
-        ep = P.ep_vals[pair % P.n_ep];
-        need = ep > 1 && P.pair_used[pair] && P.pair_canon[pair] == pair &&
-               P.m_used[(int64_t)load * (P.m_tmax + 1) + tok];
-        const int f = (int)ep / (int)tp;  // tp, ep: small positive parallel degrees
-        pooled = tok * (f > 1 ? f : 1);
-      } else {
-        int lo = 0, hi = P.n_tail_tables - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (P.tail_tables[mid].off <= t) lo = mid;
-          else hi = mid - 1;
-        }
-        const TailTable T = P.tail_tables[lo];
-        const int64_t rel = t - T.off;
-        const int bi = mod32(rel, T.n_b);
-        const int pair = div32(rel, T.n_b);
-        if (pair < npair) {
-          const int64_t tp = P.tp_vals[pair / P.n_ep];
-          ep = P.ep_vals[pair % P.n_ep];
-          need = ep > 1 && P.pair_used[pair] && P.pair_canon[pair] == pair && T.load >= 0;
-          const int64_t b = P.batches[T.b_off + bi];
-          const int64_t tokens = T.type == 0 ? b * T.chunk : b;
-          const int f = (int)ep / (int)tp;
-          pooled = tokens * (f > 1 ? f : 1);
-          load = T.load;
-        }
-      }
-    }
+    int64_t pooled = 0;
+    int ep_i = 0, load = 0;
+    const bool need = t < n_tails && tail_entry(P, t, pooled, ep_i, load);
     unsigned mask = __ballot_sync(0xffffffffu, need);
     while (mask) {
       const int src = __ffs(mask) - 1;
       mask &= mask - 1;
       const int64_t pl = __shfl_sync(0xffffffffu, pooled, src);
-      const int64_t e = __shfl_sync(0xffffffffu, ep, src);
+      const int64_t e = P.ep_vals[__shfl_sync(0xffffffffu, ep_i, src)];
       const int ld = __shfl_sync(0xffffffffu, load, src);
       const double* q = P.loads + (int64_t)ld * 2 * E;
       const int64_t result = warp_busiest_shard<PER>(q, q + E, E, pl, P.topk, e, hist);
       if (lane == src) tails[t] = result;
     }
+  }
+}
+
+// Deduplicated path (n_ep <= 64).  The expert counts depend on (load, pooled
+// tokens) only, and many entries share them: (tp, ep) pairs with the same
+// max(1, ep/tp), and batch b at ratio 2f pools what batch 2b pools at f.
+// K3a inserts every needed entry's (load, pooled) key into an open-addressing
+// table (one job per distinct key, with the mask of ep values wanted), K3b
+// computes each job's counts once and the busiest block for each wanted ep,
+// K3c copies the job results into the tails table.
+struct TailHash {
+  unsigned long long* keys;      // [cap], ~0 empty; key = load << 48 | pooled
+  unsigned long long* epmask;    // [cap] ep indices wanted
+  int32_t* job_of_slot;          // [cap] written by the inserting entry
+  int32_t* jobs;                 // [1 + cap]: count, then slot per job
+  int32_t* slot_of;              // [n_tails] slot << 6 | ep index of each entry, -1 not needed
+  int64_t* res;                  // [cap_jobs * n_ep] busiest-block tokens per (job, ep index)
+  int64_t cap;                   // power of two
+};
+
+__device__ __forceinline__ uint64_t tail_hash(uint64_t k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  return k;
+}
+
+__global__ void k_tails_keys(EvalParams P, int64_t n_tails, TailHash H) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_tails; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t pooled;
+    int ep_i, load;
+    int32_t slot = -1;
+    if (tail_entry(P, t, pooled, ep_i, load)) {
+      const unsigned long long key = ((unsigned long long)load << 48) | (unsigned long long)pooled;
+      int64_t h = (int64_t)(tail_hash(key) & (uint64_t)(H.cap - 1));
+      for (;;) {
+        const unsigned long long prev = atomicCAS(&H.keys[h], ~0ull, key);
+        if (prev == ~0ull) {  // first entry with this key: a new job
+          const int j = atomicAdd(&H.jobs[0], 1);
+          H.jobs[1 + j] = (int32_t)h;
+          H.job_of_slot[h] = j;
+          break;
+        }
+        if (prev == key) break;
+        h = (h + 1) & (H.cap - 1);
+      }
+      atomicOr(&H.epmask[h], 1ull << ep_i);
+      slot = (int32_t)((h << 6) | ep_i);  // cap <= 2^25 (host check)
+    }
+    H.slot_of[t] = slot;
+  }
+}
+
+template <int PER>
+__global__ void __launch_bounds__(256, PER <= 4 ? LC_TAIL_MIN_BLOCKS : LC_TAIL8_MIN_BLOCKS)
+    k_tails_jobs(EvalParams P, TailHash H) {
+  __shared__ int hist_all[8][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int* hist = hist_all[warp];
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const int E = (int)P.n_experts;
+  const int n = H.jobs[0];
+  for (int j = blockIdx.x * (blockDim.x >> 5) + warp; j < n; j += nw) {
+    const int32_t h = H.jobs[1 + j];
+    const unsigned long long key = H.keys[h];
+    const int load = (int)(key >> 48);
+    const int64_t pooled = (int64_t)(key & ((1ull << 48) - 1));
+    const double* q = P.loads + (int64_t)load * 2 * E;
+    int64_t cnt[PER];
+    warp_expert_counts<PER>(q, q + E, E, pooled, P.topk, hist, cnt);
+    unsigned long long m = H.epmask[h];
+    while (m) {
+      const int ei = __ffsll((long long)m) - 1;
+      m &= m - 1;
+      const int64_t r = warp_block_max<PER>(cnt, E, P.ep_vals[ei]);
+      if (lane == 0) H.res[(int64_t)j * P.n_ep + ei] = r;
+    }
+  }
+}
+
+__global__ void k_tails_put(EvalParams P, int64_t n_tails, TailHash H, int64_t* tails) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_tails; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = H.slot_of[t];
+    if (v < 0) continue;
+    tails[t] = H.res[(int64_t)H.job_of_slot[v >> 6] * P.n_ep + (v & 63)];
   }
 }
 
@@ -3278,7 +3375,7 @@ int lc_close(lc_ctx* c) {
   DBuf* bufs[] = {&c->searches, &c->batches, &c->batch_code, &c->loads, &c->meta, &c->results, &c->flags, &c->pos,
                   &c->block_sums, &c->u_search, &c->u_combo, &c->u_batch, &c->u_budget, &c->st_status,
                   &c->st_v, &c->ag_status, &c->ag_v, &c->pf_status, &c->pf_v, &c->dc_status, &c->dc_v,
-                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->step_in, &c->step_out, &c->step_loads, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch, &c->pool_seed, &c->pool_sample, &c->front_flags, &c->cell_ctr, &c->inputs};
+                  &c->err_c, &c->u_queries, &c->cell_flags, &c->cells, &c->cell_err, &c->step_in, &c->step_out, &c->step_loads, &c->pool_key, &c->qt_groups, &c->ds_groups, &c->front_compact, &c->pool_part, &c->front_meta, &c->buckets, &c->surv, &c->n_surv, &c->qt, &c->ds, &c->m_used, &c->tail_tables, &c->tails, &c->tail_hash, &c->pool_sel, &c->plans_i, &c->plans_d, &c->front, &c->q_in, &c->q_lat, &c->q_st, &c->sgroups, &c->smembers, &c->sd, &c->raw_mask, &c->pair_inb, &c->cmax, &c->pgroups, &c->psteps, &c->acc, &c->plan_scratch, &c->pool_seed, &c->pool_sample, &c->front_flags, &c->cell_ctr, &c->inputs};
   for (DBuf* b : bufs) b->release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
@@ -3367,6 +3464,8 @@ int lc_space_upload(lc_ctx* c, const lc_space_desc* d, lc_space** out) {
   if ((rc = upload(&sp->entries, d->entries, (size_t)d->n_tmpl * LC_MAX_ENTRIES, c->stream))) return rc;
   if ((rc = upload(&sp->tp_vals, tpv.data(), tpv.size(), c->stream))) return rc;
   if ((rc = upload(&sp->ep_vals, epv.data(), epv.size(), c->stream))) return rc;
+  sp->max_ep_h = 1;
+  for (int64_t v : epv) sp->max_ep_h = v > sp->max_ep_h ? v : sp->max_ep_h;
   if ((rc = upload(&sp->pair_used, used.data(), used.size(), c->stream))) return rc;
   if ((rc = upload(&sp->tmpl_info, tinfo.data(), tinfo.size(), c->stream))) return rc;
   std::vector<int32_t> canon(used.size(), 0);
@@ -3614,17 +3713,57 @@ static int run_eval_pipeline(lc_ctx* c, lc_batch_totals* totals) {
     CK(cudaGetLastError());
   }
   if (c->n_tails > 0) {
-    const int64_t warps = (c->n_tails + 31) / 32;  // a warp per 32 consecutive entries
-    int blocks = (int)((warps + 7) / 8);
-    if (blocks > sms * 16) blocks = sms * 16;
-    ++c->launches;
-    // experts per lane: 8 covers E <= 256 (DeepSeek-V3, GPT-OSS) at a quarter of the registers
-#ifndef LC_NO_TAILS4
-    if (c->sp->n_experts <= 128) k_tails<4><<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
-    else
+#ifndef LC_TAILS_NODEDUP
+    const bool dedup = c->tails_dedup_ok;
+#else
+    const bool dedup = false;
 #endif
-    if (c->sp->n_experts <= 256) k_tails<8><<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
-    else k_tails<32><<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
+    const int res_blocks = sms * (c->sp->n_experts <= 128 ? LC_TAIL_MIN_BLOCKS : LC_TAIL8_MIN_BLOCKS);
+    if (dedup) {
+      TailHash H;
+      H.cap = 1;
+      while (H.cap < 2 * c->n_tails) H.cap <<= 1;
+      const size_t n_jobs_cap = (size_t)c->n_tails;
+      const size_t b_keys = 8 * H.cap, b_mask = 8 * H.cap, b_jos = 4 * H.cap, b_jobs = 4 * (1 + n_jobs_cap),
+                   b_slot = 4 * (size_t)c->n_tails, b_res = 8 * n_jobs_cap * c->sp->n_ep;
+      auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+      cudaError_t err2 = cudaSuccess;
+      unsigned char* base = c->tail_hash.get<unsigned char>(al(b_keys) + al(b_mask) + al(b_jos) + al(b_jobs) +
+                                                                 al(b_slot) + al(b_res), &err2);
+      if (err2 != cudaSuccess) return fail(LC_ERR_CUDA, "tail hash allocation");
+      size_t o = 0;
+      H.keys = (unsigned long long*)(base + o); o += al(b_keys);
+      H.epmask = (unsigned long long*)(base + o); o += al(b_mask);
+      H.job_of_slot = (int32_t*)(base + o); o += al(b_jos);
+      H.jobs = (int32_t*)(base + o); o += al(b_jobs);
+      H.slot_of = (int32_t*)(base + o); o += al(b_slot);
+      H.res = (int64_t*)(base + o);
+      CK(cudaMemsetAsync(H.keys, 0xff, b_keys, c->stream));
+      CK(cudaMemsetAsync(H.epmask, 0, b_mask, c->stream));
+      CK(cudaMemsetAsync(H.jobs, 0, sizeof(int32_t), c->stream));
+      int eblocks = (int)((c->n_tails + 255) / 256);
+      if (eblocks > sms * 8) eblocks = sms * 8;
+      ++c->launches;
+      k_tails_keys<<<eblocks, 256, 0, c->stream>>>(P, c->n_tails, H);
+      CK(cudaGetLastError());
+      ++c->launches;
+      // persistent: the resident warps take the jobs in turn (their count is on the device)
+      if (c->sp->n_experts <= 128) k_tails_jobs<4><<<res_blocks, 256, 0, c->stream>>>(P, H);
+      else if (c->sp->n_experts <= 256) k_tails_jobs<8><<<res_blocks, 256, 0, c->stream>>>(P, H);
+      else k_tails_jobs<32><<<res_blocks, 256, 0, c->stream>>>(P, H);
+      CK(cudaGetLastError());
+      ++c->launches;
+      k_tails_put<<<eblocks, 256, 0, c->stream>>>(P, c->n_tails, H, (int64_t*)c->tails.p);
+    } else {
+      const int64_t warps = (c->n_tails + 31) / 32;  // a warp per 32 consecutive entries
+      int blocks = (int)((warps + 7) / 8);
+      if (blocks > sms * 16) blocks = sms * 16;
+      ++c->launches;
+      // experts per lane: 8 covers E <= 256 (DeepSeek-V3, GPT-OSS) at a quarter of the registers
+      if (c->sp->n_experts <= 128) k_tails<4><<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
+      else if (c->sp->n_experts <= 256) k_tails<8><<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
+      else k_tails<32><<<blocks, 256, 0, c->stream>>>(P, c->n_tails, (int64_t*)c->tails.p);
+    }
     CK(cudaGetLastError());
   }
   CK(record_ev(c, 2));
@@ -4139,6 +4278,18 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   c->n_qt = qts;
   c->n_ds = dss;
   c->n_tails = tails;
+  {
+    // the deduplicated K3 packs (load, pooled tokens) into 64 bits: loads < 2^16,
+    // pooled = tokens * max(1, ep / tp) < 2^48 (bounded in doubles: no overflow)
+    double max_b = 1.0, max_chunk = 1.0;
+    const double max_ep = (double)sp->max_ep_h;
+    for (int32_t i = 0; i < n_batches; ++i) max_b = std::max(max_b, (double)batches[i]);
+    for (int s = 0; s < n_search; ++s) max_chunk = std::max(max_chunk, (double)(searches[s].isl - searches[s].prefix));
+    const double max_tok = std::max(max_b * max_chunk, (double)c->m_tmax);
+    static const bool general = getenv("LC_TAILS_GENERAL") != nullptr;  // tests: force the general K3
+    c->tails_dedup_ok = !general && n_loads < 65536 && max_tok * max_ep < 1e14 && sp->n_ep <= 64 &&
+                        tails <= (1 << 24);
+  }
   c->n_plan_slots = plans;
   cudaError_t err = cudaSuccess;
   c->hbatch_code.resize(n_batches > 0 ? n_batches : 1);
