@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <array>
 #include <chrono>
@@ -4214,6 +4215,40 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
       if (M.n_steps > c->hds[gi].n_steps) c->hds[gi].n_steps = M.n_steps;
       M._pad2 = gi;  // group index until offsets are known
     }
+    // The attention latency depends on (batch, kv) only, so input lengths whose
+    // KV samples continue one another (same batch list and stride, isl equal
+    // modulo the stride, next first sample at most one stride past the last)
+    // share one merged table: a search starts k0 samples into it.
+    const size_t n_g = c->hds.size();
+    std::vector<int32_t> ord(n_g), to(n_g);
+    std::vector<int64_t> k0(n_g, 0);
+    for (size_t i = 0; i < n_g; ++i) ord[i] = (int32_t)i;
+    auto gkey = [&](const DsGroup& g) {
+      return std::make_tuple(g.b_off, g.n_b, g.stride, g.isl % g.stride, g.isl);
+    };
+    std::sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return gkey(c->hds[a]) < gkey(c->hds[b]); });
+    std::vector<DsGroup> merged;
+    for (int32_t i : ord) {
+      const DsGroup& g = c->hds[i];
+#ifndef LC_DS_NOMERGE
+      if (!merged.empty()) {
+#else
+      if (false) {
+#endif
+        DsGroup& m = merged.back();
+        if (m.b_off == g.b_off && m.n_b == g.n_b && m.stride == g.stride && m.isl % m.stride == g.isl % g.stride &&
+            g.isl <= m.isl + (int64_t)m.stride * m.n_steps) {
+          const int64_t k = (g.isl - m.isl) / m.stride;
+          if (k + g.n_steps > m.n_steps) m.n_steps = (int32_t)(k + g.n_steps);
+          to[i] = (int32_t)merged.size() - 1;
+          k0[i] = k;
+          continue;
+        }
+      }
+      to[i] = (int32_t)merged.size();
+      merged.push_back(g);
+    }
+    c->hds.swap(merged);
     for (auto& g : c->hds) {
       g.off = dss;
       dss += (int64_t)sp->n_gclass * g.n_b * g.n_steps;
@@ -4221,8 +4256,9 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     for (int s = 0; s < n_search; ++s) {
       SearchMeta& M = c->hmeta[s];
       if (!M.n_steps || !sp->n_gclass) continue;
-      M.ds_off = c->hds[M._pad2].off;
-      M.ds_stride = c->hds[M._pad2].n_steps;
+      const DsGroup& G = c->hds[to[M._pad2]];
+      M.ds_off = G.off + k0[M._pad2] * G.n_b;
+      M.ds_stride = G.n_steps;
     }
   }
   // static decode series: searches that differ only in osl share one loop (SeriesGroup)
