@@ -4859,19 +4859,21 @@ int lc_fetch(lc_ctx* c, const lc_fetch_req* r) {
       }
   }
   // plans and fronts are copied compactly per search
-  std::vector<int32_t> pi;
-  std::vector<double> pd;
+  std::vector<int32_t> pi_v;
+  std::vector<double> pd_v;
   if (c->n_plan_slots && (r->plan_p || r->plan_d || r->plan_x || r->plan_y || r->plan_gpus || r->plan_r_sys ||
                           r->plan_ttft || r->plan_tpot || r->plan_speed || r->plan_thru)) {
-    if (c->staged) {
-      pi.assign(c->pinned_plans_i, c->pinned_plans_i + c->n_plan_slots * 4);
-      pd.assign(c->pinned_plans_d, c->pinned_plans_d + c->n_plan_slots * 6);
-    } else {
-      pi.resize(c->n_plan_slots * 4);
-      pd.resize(c->n_plan_slots * 6);
-      CK(cudaMemcpyAsync(pi.data(), c->plans_i.p, pi.size() * 4, cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(pd.data(), c->plans_d.p, pd.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    // staged: read the page-locked copies in place (only the used slots are touched)
+    const int32_t* pi = c->pinned_plans_i;
+    const double* pd = c->pinned_plans_d;
+    if (!c->staged) {
+      pi_v.resize(c->n_plan_slots * 4);
+      pd_v.resize(c->n_plan_slots * 6);
+      CK(cudaMemcpyAsync(pi_v.data(), c->plans_i.p, pi_v.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(pd_v.data(), c->plans_d.p, pd_v.size() * 8, cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
+      pi = pi_v.data();
+      pd = pd_v.data();
     }
     int64_t k = 0;
     for (int s = 0; s < c->n_search; ++s) {
