@@ -4084,6 +4084,7 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
     const lc_search_desc& S = searches[s];
     c->hsearch_nb[s] = S.n_b;
     if (S.b_off < 0 || S.n_b < 0 || S.b_off + S.n_b > n_batches) continue;  // rejected below
+    if (s > 0 && S.b_off == searches[s - 1].b_off && S.n_b == searches[s - 1].n_b) continue;  // same list as the last
     for (int j = 1; j < S.n_b; ++j)
       if (batches[S.b_off + j] < batches[S.b_off + j - 1]) c->batches_sorted = false;
   }
@@ -4294,13 +4295,20 @@ int lc_search_batch(lc_ctx* c, const lc_db* db, const lc_space* sp, int32_t n_se
   c->n_pd_tails = tails;
   c->m_tmax = 0;
   int64_t marks = 0;
+  int32_t last_boff = -1, last_nb = -1;
+  int64_t last_bmax = 0;
   for (int s = 0; s < n_search; ++s) {
     const lc_search_desc& S = searches[s];
     c->hmeta[s].mark_off = marks;
     marks += S.n_b;
     if (!sp->is_moe || !(S.modes & 2) || S.n_b == 0) continue;
-    int64_t bmax = 0;
-    for (int j = 0; j < S.n_b; ++j) bmax = batches[S.b_off + j] > bmax ? batches[S.b_off + j] : bmax;
+    if (S.b_off != last_boff || S.n_b != last_nb) {  // searches sharing a batch list share its maximum
+      last_bmax = 0;
+      for (int j = 0; j < S.n_b; ++j) last_bmax = batches[S.b_off + j] > last_bmax ? batches[S.b_off + j] : last_bmax;
+      last_boff = S.b_off;
+      last_nb = S.n_b;
+    }
+    const int64_t bmax = last_bmax;
     const int64_t t = (S.isl - S.prefix) + bmax;
     c->m_tmax = t > c->m_tmax ? t : c->m_tmax;
   }
